@@ -1,0 +1,23 @@
+# Builds the product library (sm_100a only), the synthetic-input helper and
+# the test oracle. `python -c "import __graft_entry__ as g; g.build()"` runs this.
+NVCC ?= /usr/local/cuda/bin/nvcc
+PKG := paper_1710_07193_b200
+CSRC := $(PKG)/csrc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-O3 -Xptxas -v --expt-relaxed-constexpr
+
+all: $(PKG)/libdctf_b200.so $(PKG)/libdctf_synth.so oracle
+
+$(PKG)/libdctf_b200.so: $(CSRC)/kernels.cu $(CSRC)/plan.cc $(CSRC)/internal.h include/dctf.h
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/kernels.cu $(CSRC)/plan.cc 2> build_ptxas.log || (cat build_ptxas.log; false)
+
+$(PKG)/libdctf_synth.so: $(CSRC)/synth.cc
+	g++ -O3 -std=c++17 -fPIC -shared -pthread -o $@ $<
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(PKG)/*.so oracle/*.so oracle/_ref/*.so
+
+.PHONY: all oracle clean

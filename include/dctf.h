@@ -1,0 +1,154 @@
+/*
+ * dctf.h — C ABI of the B200-native DCT-domain block filter
+ * (libdctf_b200.so, built from paper_1710_07193_b200/csrc).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (arXiv 1710.07193, reference library /root/reference/proj/include/dctfilter).
+ * Plain pointers and sizes only. Every entry point is batched: one call
+ * covers a whole image or a whole range of blocks, where the reference works
+ * one BlockMatrix at a time.
+ *
+ * Data layouts
+ *   image    : u8, row-major, `pitch` bytes between rows (pitch >= width).
+ *   coeffs   : FP64, block-major. Block b = by * bw + bx (row-major block grid,
+ *              the order of tile(), image.hpp:164-184); within a block,
+ *              coefficient (u, v) at u * n + v (BlockMatrix row-major,
+ *              block_matrix.hpp:46). bw = ceil(w/n), bh = ceil(h/n).
+ *   blocks   : FP64 spatial samples, same layout as coeffs.
+ *   operator : FP64 n^2 x n^2 row-major; row (u*n+v), column (a*n+b).
+ *
+ * Device pointers: every `d_` argument is device memory (cudaMalloc'd,
+ * 16-byte aligned for the fast paths); `stream` is a cudaStream_t (NULL =
+ * legacy default stream). Calls are asynchronous with respect to the host
+ * unless stated. `h_` arguments are host memory.
+ *
+ * Errors: every call returns a dctf_status; the reference throws instead
+ * (std::invalid_argument, filter.hpp / spatial.hpp / mask.hpp). A
+ * thread-local message describes the last failure.
+ *
+ * Thread-safety: a plan is immutable after dctf_plan_create; concurrent calls
+ * on one plan from several host threads / streams are allowed, as for the
+ * reference FilterPlan (filter.hpp:47-51).
+ */
+#ifndef DCTF_H
+#define DCTF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DCTF_OK = 0,
+  DCTF_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument           */
+  DCTF_CUDA_ERROR = 2,       /* CUDA runtime / launch failure              */
+  DCTF_NAN_ENCOUNTERED = 3,  /* reference: quantize_sample throws on NaN   */
+  DCTF_UNSUPPORTED = 4       /* valid request this build does not provide  */
+} dctf_status;
+
+typedef enum { DCTF_PAD_ZERO = 0, DCTF_PAD_REPLICATE = 1 } dctf_padding; /* spatial.hpp:29-32 */
+
+typedef enum {
+  DCTF_PREC_FP64 = 0,    /* FP64 DMMA tensor pipe; coefficients within 1e-9 rel. */
+  DCTF_PREC_TF32X3 = 1,  /* split-precision tcgen05 kind::tf32, 3 passes          */
+  DCTF_PREC_BF16X3 = 2   /* split-precision tcgen05 kind::f16 (bf16), 3 passes     */
+} dctf_precision;
+
+typedef struct dctf_plan dctf_plan;
+
+/* Replaces FilterPlan(const Mask&, int n, PaddingMode) (filter.hpp:54-56)
+ * together with Mask(int k, std::vector<double>) (mask.hpp:29-41).
+ * weights: kr x kc row-major, kr and kc odd, finite. The reference accepts
+ * square masks with k <= n only (operators.hpp:84,106); those compile exactly
+ * like the reference (shift/band pairs, merge_symmetric, to_dct_domain). This
+ * build also accepts kr != kc and masks wider than the block (convolve
+ * formula, spatial.hpp:36-37, with the k <= n guard lifted).
+ * n: block side, 8 or 16. device: CUDA ordinal the plan's operator lives on. */
+dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int padding,
+                             int precision, int device, dctf_plan** out);
+dctf_status dctf_plan_destroy(dctf_plan* plan);
+
+/* Plan metadata: block side, sandwich pair count and whether mirrored rows
+ * were merged (OperatorSet::pairs.size(), ::symmetric_merged). */
+dctf_status dctf_plan_info(const dctf_plan* plan, int* n, int* npairs, int* symmetric_merged);
+
+/* Host-only operator compile (no device needed): the same compile
+ * dctf_plan_create performs, returning C (n*n) and H (n^4) into host buffers
+ * (either may be NULL) plus the pair count / merge flag. */
+dctf_status dctf_compile_operator(const double* h_weights, int kr, int kc, int n, int padding,
+                                  double* h_c, double* h_op, int* npairs, int* symmetric_merged);
+
+/* Host FP64 copies: the DCT basis C (n*n; DctBasis::c(), dct.hpp:37) and the
+ * dense DCT-domain operator H (n^4), H = sum_p L_p (x) R_p^T of the plan's
+ * sandwich pairs (FilterPlan::dct_set(), filter.hpp:62). */
+dctf_status dctf_plan_basis(const dctf_plan* plan, double* h_c);
+dctf_status dctf_plan_operator(const dctf_plan* plan, double* h_op);
+
+/* forward_2d over a u8 image: tile() (edge replication of ragged edges) then
+ * C X C^t per block (dct.hpp:59-62). d_coeffs: bw*bh*n*n doubles. */
+dctf_status dctf_forward(const dctf_plan* plan, const uint8_t* d_img, int width, int height,
+                         size_t pitch, double* d_coeffs, void* stream);
+
+/* forward_2d / inverse_2d over FP64 blocks (dct.hpp:59-68). */
+dctf_status dctf_forward_blocks(const dctf_plan* plan, const double* d_blocks, double* d_coeffs,
+                                size_t nblocks, void* stream);
+dctf_status dctf_inverse_blocks(const dctf_plan* plan, const double* d_coeffs, double* d_blocks,
+                                size_t nblocks, void* stream);
+
+/* FilterPlan::filter_coeffs (filter.hpp:65-67) over nblocks coefficient
+ * blocks: out_b = H * in_b. In-place (d_in == d_out) is not allowed. */
+dctf_status dctf_filter_coeffs(const dctf_plan* plan, const double* d_in, double* d_out,
+                               size_t nblocks, void* stream);
+
+/* inverse_2d + assemble() (image.hpp:188-203): C^t Y C per block, round half
+ * away from zero, clamp to [0,255], crop to width x height. A NaN sample sets
+ * the plan's NaN flag (see dctf_plan_nan_check). */
+dctf_status dctf_inverse_u8(const dctf_plan* plan, const double* d_coeffs, uint8_t* d_img,
+                            int width, int height, size_t pitch, void* stream);
+
+/* filter_image(img, mask, padding, Domain::kDct, n) (image.hpp:210-218),
+ * fused on the device: u8 -> forward DCT -> H -> inverse DCT -> round/clamp
+ * -> u8 in one HBM pass. d_in and d_out may not alias. If d_coeffs_out is not
+ * NULL the filtered coefficients (bw*bh*n*n doubles) are also written
+ * (parity mode). */
+dctf_status dctf_filter_image_u8(const dctf_plan* plan, const uint8_t* d_in, uint8_t* d_out,
+                                 int width, int height, size_t pitch, double* d_coeffs_out,
+                                 void* stream);
+
+/* Frame batch (video): frame f (0..nframes-1) of the d_in batch is filtered
+ * with plans[plan_of_frame[f]]; frames are frame_stride bytes apart, all
+ * width x height with the same pitch. All plans must share n and device. */
+dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
+                                  const int* h_plan_of_frame, const uint8_t* d_in, uint8_t* d_out,
+                                  int nframes, int width, int height, size_t pitch,
+                                  size_t frame_stride, void* stream);
+
+/* End-to-end host-buffer entry (the reference's filter_image signature):
+ * copies h_in to the device, filters, copies back into h_out, in chunks of
+ * block rows pipelined over two streams so PCIe transfers overlap the
+ * kernel. Synchronous. Pinned (cudaHostAlloc'd) buffers run at full PCIe
+ * speed; pageable ones work. Returns DCTF_NAN_ENCOUNTERED like
+ * quantize_sample would throw. */
+dctf_status dctf_filter_image_host(const dctf_plan* plan, const uint8_t* h_in, uint8_t* h_out,
+                                   int width, int height, size_t pitch);
+
+/* Synchronises `stream`, reads and clears the plan's NaN flag; *nan_seen is
+ * 1 if any quantised sample was NaN since the last check. */
+dctf_status dctf_plan_nan_check(const dctf_plan* plan, void* stream, int* nan_seen);
+
+/* Number of kernels the last call on this host thread launched (bench
+ * accounting of gpu_launches). */
+int dctf_last_launch_count(void);
+
+/* Thread-local description of the last non-OK status. */
+const char* dctf_last_error_message(void);
+
+/* Library version string. */
+const char* dctf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCTF_H */

@@ -1,0 +1,53 @@
+// Internal declarations shared by plan.cc (host operator compiler) and
+// kernels.cu (sm_100a kernels + C-ABI launchers).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dctf.h"
+
+struct dctf_plan {
+  int n = 0, kr = 0, kc = 0, padding = 0, precision = 0, device = 0;
+  int npairs = 0, merged = 0;
+  bool reference_domain = true;  // square k <= n mask, compiled like FilterPlan
+  std::vector<double> weights;   // kr*kc row-major
+  std::vector<double> basis;     // C, n*n row-major (DctBasis::c())
+  std::vector<double> op;        // H, n^4 row-major (natural coefficient order)
+
+  // Device-resident copies (owned). Layouts: see kernels.cu.
+  double* d_basis = nullptr;     // C, n*n
+  double* d_hcoef = nullptr;     // H in coefficient-kernel fragment order
+  double* d_hfused = nullptr;    // H in fused-kernel fragment order (n = 8)
+  int* d_nan = nullptr;          // NaN flag
+
+  // Scratch for multi-kernel paths and the host-buffer entry (guarded).
+  mutable std::mutex scratch_mu;
+  mutable void* scratch = nullptr;
+  mutable size_t scratch_bytes = 0;
+  mutable void* io_in = nullptr;
+  mutable void* io_out = nullptr;
+  mutable size_t io_bytes = 0;
+  mutable void* streams[2] = {nullptr, nullptr};
+};
+
+namespace dctf {
+
+// Thread-local error / launch bookkeeping (kernels.cu).
+dctf_status set_error(dctf_status s, const std::string& msg);
+void add_launches(int k);
+void reset_launches();
+
+// Host operator compiler (plan.cc).
+// Builds C and the dense DCT-domain operator H for the mask.
+// Returns DCTF_INVALID_ARGUMENT with a message on bad input.
+dctf_status compile_operator(dctf_plan& p);
+
+// Fragment-order permutations of H for the kernels (plan.cc).
+void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out);
+void layout_hfused8(const std::vector<double>& op, std::vector<double>& out);
+
+}  // namespace dctf

@@ -1,0 +1,1192 @@
+// sm_100a kernels and C-ABI launchers of the DCT-domain block filter.
+//
+// Kernels (all FP64; the contraction stages run on the FP64 tensor pipe via
+// mma.sync.m8n8k4.f64 -> DMMA.8x8x4):
+//   k_forward<N,U8>   forward_2d (dct.hpp:59-62) per block, reference
+//                     operation order (mul then add, no FMA, zero-skip), so
+//                     coefficients are bit-identical to the reference.
+//   k_inverse<N,U8>   inverse_2d (dct.hpp:65-68) [+ quantize_sample +
+//                     assemble crop (spatial.hpp:71-75, image.hpp:188-203)].
+//   k_coef8           FilterPlan::filter_coeffs (filter.hpp:65-67) for n=8:
+//                     Y^T = X^T H^T, blocks on the MMA M axis; X tiles are
+//                     TMA-staged (cp.async.bulk.tensor.2d, 128B swizzle)
+//                     through a per-warp mbarrier ring; H (32 KB) resident in
+//                     shared memory in fragment order.
+//   k_coef16          the same for n=16; H (512 KB) is streamed in 32 KB
+//                     K-chunks by a producer warp (cp.async.bulk) together
+//                     with the matching X chunk, 3-stage ring, 16 MMA warps.
+//   k_fused8          filter_image's per-block chain (image.hpp:214-218,
+//                     filter.hpp:71-73) for n=8 fused: u8 strip -> forward
+//                     DCT (4 DMMA/block) -> H (16 DMMA/block) -> inverse DCT
+//                     (4 DMMA/block) -> round/clamp -> u8; one HBM read and
+//                     one HBM write per pixel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "internal.h"
+
+// ---------------------------------------------------------------------------
+// bookkeeping
+namespace dctf {
+namespace {
+thread_local std::string t_err;
+thread_local int t_launches = 0;
+}  // namespace
+dctf_status set_error(dctf_status s, const std::string& msg) {
+  t_err = msg;
+  return s;
+}
+void add_launches(int k) { t_launches += k; }
+void reset_launches() { t_launches = 0; }
+}  // namespace dctf
+
+using dctf::set_error;
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return set_error(DCTF_CUDA_ERROR, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device helpers
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64. Lane l: A[l>>2][l&3],
+// B[l&3][l>>2], D[l>>2][2(l&3)+{0,1}].
+__device__ __forceinline__ void dmma(double2& d, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d.x), "+d"(d.y)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t addr = smem_u32(bar);
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// quantize_sample (spatial.hpp:71-75): round half away from zero, clamp.
+__device__ __forceinline__ uint32_t quantize(double v, int* nan_flag) {
+  if (v != v) {
+    if (nan_flag) atomicOr(nan_flag, 1);
+    return 0u;
+  }
+  const double r = fmin(fmax(round(v), 0.0), 255.0);
+  return static_cast<uint32_t>(r);
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_stream(void* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// forward_2d / inverse_2d, reference operation order.
+//
+// One CTA = 256 threads = 256/N blocks; thread (lb, r) owns row r of block lb.
+// forward: T = C X (row r of T needs row r of C and all of X), out = T C^t.
+// inverse: T = C^t Y, out = T C.
+// Each product is matmul (block_matrix.hpp:67-81): k ascending, skip a == 0,
+// separately rounded multiply and add (the reference has no FMA
+// contraction), so results are bit-identical to forward_2d / inverse_2d.
+
+template <int N, bool FROM_U8>
+__global__ void __launch_bounds__(256) k_forward(const uint8_t* __restrict__ img, int w, int h,
+                                                 size_t pitch, int bw,
+                                                 const double* __restrict__ blocks,
+                                                 double* __restrict__ out, long long nblocks,
+                                                 const double* __restrict__ cb) {
+  constexpr int NN = N * N, BPC = 256 / N, STR = NN + 1;
+  __shared__ double xs[BPC * STR];
+  __shared__ double cs[NN];
+  for (int i = threadIdx.x; i < NN; i += 256) cs[i] = cb[i];
+  const long long b0 = static_cast<long long>(blockIdx.x) * BPC;
+  for (int e = threadIdx.x; e < BPC * NN; e += 256) {
+    const int lb = e / NN, idx = e % NN;
+    const long long blk = b0 + lb;
+    double v = 0.0;
+    if (blk < nblocks) {
+      if (FROM_U8) {
+        const int by = static_cast<int>(blk / bw), bx = static_cast<int>(blk % bw);
+        const int y = min(by * N + idx / N, h - 1), x = min(bx * N + idx % N, w - 1);
+        v = static_cast<double>(img[static_cast<size_t>(y) * pitch + x]);
+      } else {
+        v = blocks[blk * NN + idx];
+      }
+    }
+    xs[lb * STR + idx] = v;
+  }
+  __syncthreads();
+  const int lb = threadIdx.x / N, r = threadIdx.x % N;
+  const long long blk = b0 + lb;
+  const double* x = xs + lb * STR;
+  double crow[N], trow[N], o[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) crow[k] = cs[r * N + k];
+#pragma unroll
+  for (int j = 0; j < N; ++j) trow[j] = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double a = crow[k];
+    if (a != 0.0) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) trow[j] = __dadd_rn(trow[j], __dmul_rn(a, x[k * N + j]));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j) o[j] = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double a = trow[k];
+    if (a != 0.0) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, cs[j * N + k]));
+    }
+  }
+  if (blk < nblocks) {
+    double* dst = out + blk * NN + r * N;
+#pragma unroll
+    for (int j = 0; j < N; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(o[j], o[j + 1]);
+  }
+}
+
+template <int N, bool TO_U8>
+__global__ void __launch_bounds__(256) k_inverse(const double* __restrict__ coeffs,
+                                                 double* __restrict__ blocks_out,
+                                                 uint8_t* __restrict__ img, int w, int h,
+                                                 size_t pitch, int bw, long long nblocks,
+                                                 const double* __restrict__ cb, int* nan_flag) {
+  constexpr int NN = N * N, BPC = 256 / N, STR = NN + 1;
+  __shared__ double ys[BPC * STR];
+  __shared__ double cs[NN];
+  for (int i = threadIdx.x; i < NN; i += 256) cs[i] = cb[i];
+  const long long b0 = static_cast<long long>(blockIdx.x) * BPC;
+  for (int e = threadIdx.x; e < BPC * NN; e += 256) {
+    const int lb = e / NN, idx = e % NN;
+    const long long blk = b0 + lb;
+    ys[lb * STR + idx] = blk < nblocks ? coeffs[blk * NN + idx] : 0.0;
+  }
+  __syncthreads();
+  const int lb = threadIdx.x / N, r = threadIdx.x % N;
+  const long long blk = b0 + lb;
+  const double* y = ys + lb * STR;
+  double ccol[N], trow[N], o[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) ccol[k] = cs[k * N + r];  // C^t[r][k]
+#pragma unroll
+  for (int j = 0; j < N; ++j) trow[j] = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double a = ccol[k];
+    if (a != 0.0) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) trow[j] = __dadd_rn(trow[j], __dmul_rn(a, y[k * N + j]));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j) o[j] = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double a = trow[k];
+    if (a != 0.0) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, cs[k * N + j]));
+    }
+  }
+  if (blk >= nblocks) return;
+  if (!TO_U8) {
+    double* dst = blocks_out + blk * NN + r * N;
+#pragma unroll
+    for (int j = 0; j < N; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(o[j], o[j + 1]);
+  } else {
+    const int by = static_cast<int>(blk / bw), bx = static_cast<int>(blk % bw);
+    const int yy = by * N + r;
+    if (yy >= h) return;
+    uint8_t* dst = img + static_cast<size_t>(yy) * pitch + bx * N;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (bx * N + j < w) dst[j] = static_cast<uint8_t>(quantize(o[j], nan_flag));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_coef8: Y^T (blocks x 64) = X^T (blocks x 64) * H^T, FP64 DMMA.
+//
+// Work unit: a tile of 16 consecutive blocks (8 KB of X). Each warp owns a
+// strided sequence of tiles and its own STAGES-deep ring of 8 KB buffers;
+// lane 0 issues four TMA box loads per tile ([16 blocks x 16 coefficients],
+// 128B swizzle: 16-byte chunk c of row r lands at chunk c ^ (r & 7)) and the
+// warp waits on that stage's mbarrier. Contraction index of k-step pair q in
+// K-chunk kc for lane t: 16kc + 8q + 2t + {0,1} (natural coefficient order),
+// so a lane's two k-steps are one swizzled 16-byte word (conflict-free
+// LDS.128). H^T fragments come from shared memory in the matching order
+// (layout_hcoef). Accumulators: 2 m-tiles x 8 n-tiles per warp (16 blocks x
+// 64 outputs), written straight from registers as 16-byte stores.
+namespace c8 {
+constexpr int WARPS = 8;
+constexpr int STAGES = 2;
+constexpr int TILE = 16;
+constexpr int STAGE_BYTES = TILE * 64 * 8;  // 8 KB
+constexpr int SMEM = 1024 + 32768 + WARPS * STAGES * STAGE_BYTES;
+}  // namespace c8
+
+__global__ void __launch_bounds__(c8::WARPS * 32, 1)
+    k_coef8(const __grid_constant__ CUtensorMap xmap, const double* __restrict__ hc,
+            double* __restrict__ out, long long nblocks) {
+  using namespace c8;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const double2* hs = reinterpret_cast<const double2*>(base);
+  uint8_t* stages = base + 32768;
+  __shared__ uint64_t bars[WARPS * STAGES];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    for (int i = 0; i < WARPS * STAGES; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  {
+    const double2* src = reinterpret_cast<const double2*>(hc);
+    double2* dst = reinterpret_cast<double2*>(base);
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+
+  const long long ntiles = (nblocks + TILE - 1) / TILE;
+  const long long total = static_cast<long long>(gridDim.x) * WARPS;
+  const long long first = static_cast<long long>(blockIdx.x) * WARPS + warp;
+  uint8_t* ring = stages + warp * STAGES * STAGE_BYTES;
+  uint64_t* wb = bars + warp * STAGES;
+
+  auto issue = [&](int s, long long tile) {
+    uint8_t* dst = ring + s * STAGE_BYTES;
+    mbar_expect_tx(&wb[s], STAGE_BYTES);
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+      tma_load_2d(dst + cc * 2048, &xmap, &wb[s], cc * 16, static_cast<int>(tile * TILE));
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      const long long tile = first + s * total;
+      if (tile < ntiles) issue(s, tile);
+    }
+  }
+  __syncwarp();
+
+  for (long long i = 0;; ++i) {
+    const long long tile = first + i * total;
+    if (tile >= ntiles) break;
+    const int s = static_cast<int>(i % STAGES);
+    mbar_wait(&wb[s], static_cast<uint32_t>((i / STAGES) & 1));
+    const uint8_t* st = ring + s * STAGE_BYTES;
+
+    double2 acc[2][8];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[m][j] = make_double2(0.0, 0.0);
+
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int sw = ((4 * q + t) ^ g) << 4;
+        const double2 a0 = *reinterpret_cast<const double2*>(st + kc * 2048 + g * 128 + sw);
+        const double2 a1 = *reinterpret_cast<const double2*>(st + kc * 2048 + (8 + g) * 128 + sw);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double2 b = hs[((kc * 8 + j) * 2 + q) * 32 + lane];
+          dmma(acc[0][j], a0.x, b.x);
+          dmma(acc[0][j], a0.y, b.y);
+          dmma(acc[1][j], a1.x, b.x);
+          dmma(acc[1][j], a1.y, b.y);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const long long nt = tile + STAGES * total;
+      if (nt < ntiles) {
+        fence_proxy_async();
+        issue(s, nt);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const long long blk = tile * TILE + 8 * m + g;
+      if (blk < nblocks) {
+        double* dst = out + blk * 64 + 2 * t;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) *reinterpret_cast<double2*>(dst + 8 * j) = acc[m][j];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_coef16: Y^T (blocks x 256) = X^T (blocks x 256) * H^T, FP64 DMMA.
+//
+// CTA tile: 64 blocks x 256 outputs; K = 256 streamed in 16 chunks of 16.
+// Warp 16 is the producer: per chunk one TMA box [64 blocks x 16 coeffs]
+// (8 KB, 128B swizzle) plus one 32 KB bulk copy of the H^T chunk (fragment
+// order, layout_hcoef), into a 3-stage ring (full/empty mbarriers).
+// Warps 0..15 consume: warp w covers blocks 16(w&3)..+16 (2 m-tiles) and
+// outputs 64(w>>2)..+64 (8 n-tiles).
+namespace c16 {
+constexpr int CWARPS = 16;
+constexpr int STAGES = 3;
+constexpr int TILE = 64;
+constexpr int XBYTES = TILE * 16 * 8;   // 8 KB
+constexpr int HBYTES = 256 * 16 * 8;    // 32 KB
+constexpr int STAGE_BYTES = XBYTES + HBYTES;
+constexpr int SMEM = 1024 + STAGES * STAGE_BYTES;
+}  // namespace c16
+
+__global__ void __launch_bounds__((c16::CWARPS + 1) * 32, 1)
+    k_coef16(const __grid_constant__ CUtensorMap xmap, const double* __restrict__ hc,
+             double* __restrict__ out, long long nblocks) {
+  using namespace c16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CWARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const long long ntiles = (nblocks + TILE - 1) / TILE;
+
+  if (warp == CWARPS) {
+    if (lane == 0) {
+      long long it = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int kc = 0; kc < 16; ++kc, ++it) {
+          const int s = static_cast<int>(it % STAGES);
+          if (it >= STAGES) mbar_wait(&empty[s], static_cast<uint32_t>(((it / STAGES) - 1) & 1));
+          uint8_t* dst = base + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(dst, &xmap, &full[s], kc * 16, static_cast<int>(tile * TILE));
+          bulk_load(dst + XBYTES, hc + static_cast<size_t>(kc) * (HBYTES / 8), HBYTES, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2, t = lane & 3, mg = warp & 3, ng = warp >> 2;
+  long long it = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    double2 acc[2][8];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[m][j] = make_double2(0.0, 0.0);
+    for (int kc = 0; kc < 16; ++kc, ++it) {
+      const int s = static_cast<int>(it % STAGES);
+      mbar_wait(&full[s], static_cast<uint32_t>((it / STAGES) & 1));
+      const uint8_t* xs = base + s * STAGE_BYTES;
+      const double2* hs = reinterpret_cast<const double2*>(xs + XBYTES);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int sw = ((4 * q + t) ^ g) << 4;
+        const double2 a0 = *reinterpret_cast<const double2*>(xs + (16 * mg + g) * 128 + sw);
+        const double2 a1 = *reinterpret_cast<const double2*>(xs + (16 * mg + 8 + g) * 128 + sw);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double2 b = hs[((8 * ng + j) * 2 + q) * 32 + lane];
+          dmma(acc[0][j], a0.x, b.x);
+          dmma(acc[0][j], a0.y, b.y);
+          dmma(acc[1][j], a1.x, b.x);
+          dmma(acc[1][j], a1.y, b.y);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const long long blk = tile * TILE + 16 * mg + 8 * m + g;
+      if (blk < nblocks) {
+        double* dst = out + blk * 256 + 64 * ng + 2 * t;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) *reinterpret_cast<double2*>(dst + 8 * j) = acc[m][j];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_fused8: u8 -> C X C^t -> H -> C^t Y C -> round/clamp -> u8, n = 8.
+//
+// Work unit ("strip"): 16 horizontally adjacent blocks = 8 pixel rows x 128
+// bytes, owned by one warp. Pixels arrive through 16-byte streaming loads
+// issued one strip ahead (prefetch into registers), are staged in a padded
+// per-warp buffer (row stride 144 B), and every stage is a DMMA chain whose
+// fragment layouts line up so no shuffles are needed:
+//   forward pass 1  T1^T = C P^T  : A = C[g][2t+s] (registers), B = pixels
+//   forward pass 2  X^T = T1^T C^t: A = pass-1 accumulators, B = C[g][2t+s]
+//     -> lane (g,t) holds X[2t][g], X[2t+1][g] of each block.
+//   filter          Y^T = X^T H^T : blocks on M (2 m-tiles), H^T from shared
+//     memory (layout_hfused8), X via a swizzled per-warp staging buffer
+//     (16-byte word (row t, chunk c) of block b at chunk c ^ (b & 7)).
+//   inverse pass 1  Z = C^t Y     : A = C[2t+s][g], B = Y via staging
+//   inverse pass 2  O = Z C       : A = pass-1 accumulators, B = C[2t+s][g]
+//     -> lane (g,t) holds O[g][2t], O[g][2t+1]: two adjacent output pixels.
+// Ragged strips (image edge, block grid tail) take a clamped per-byte path
+// with the same compute.
+namespace f8 {
+constexpr int WARPS = 8;
+constexpr int SB = 16;
+constexpr int PS = 144;
+constexpr int XY_BYTES = SB * 512;
+constexpr int PIX_BYTES = 8 * PS;
+constexpr int WARP_BYTES = XY_BYTES + PIX_BYTES;
+constexpr int SMEM = 32768 + WARPS * WARP_BYTES;
+}  // namespace f8
+
+__global__ void __launch_bounds__(f8::WARPS * 32, 2)
+    k_fused8(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
+             long long frame_stride, int nframes, int bw, int bh, int nsx,
+             const double* __restrict__ hf, const double* __restrict__ cb,
+             double* __restrict__ coef_out) {
+  using namespace f8;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const double2* hs = reinterpret_cast<const double2*>(smem);
+  {
+    const double2* src = reinterpret_cast<const double2*>(hf);
+    double2* dst = reinterpret_cast<double2*>(smem);
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  uint8_t* xy = smem + 32768 + warp * WARP_BYTES;
+  uint8_t* pix = xy + XY_BYTES;
+  const double af0 = cb[g * 8 + 2 * t], af1 = cb[g * 8 + 2 * t + 1];
+  const double ai0 = cb[(2 * t) * 8 + g], ai1 = cb[(2 * t + 1) * 8 + g];
+
+  const long long spf = static_cast<long long>(bh) * nsx;
+  const long long nstrips = spf * nframes;
+  const long long total = static_cast<long long>(gridDim.x) * WARPS;
+  const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
+  const int r0 = lane >> 3, c16 = (lane & 7) * 16;
+
+  uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
+  long long s = static_cast<long long>(blockIdx.x) * WARPS + warp;
+  auto strip_at = [&](long long si, int& f, int& by, int& bx0) {
+    f = static_cast<int>(si / spf);
+    const long long rem = si - static_cast<long long>(f) * spf;
+    by = static_cast<int>(rem / nsx);
+    bx0 = static_cast<int>(rem - static_cast<long long>(by) * nsx) * SB;
+  };
+  auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && bx0 * 8 + 128 <= w; };
+  auto prefetch = [&](long long si) {
+    int f, by, bx0;
+    strip_at(si, f, by, bx0);
+    if (is_fast(by, bx0)) {
+      const uint8_t* p = in + f * frame_stride + static_cast<size_t>(by * 8) * pitch + bx0 * 8 + c16;
+      pf0 = ldg_stream(p + r0 * pitch);
+      pf1 = ldg_stream(p + (r0 + 4) * pitch);
+    }
+  };
+  if (s < nstrips) prefetch(s);
+
+  for (; s < nstrips; s += total) {
+    int f, by, bx0;
+    strip_at(s, f, by, bx0);
+    const bool fast = is_fast(by, bx0);
+    if (fast) {
+      *reinterpret_cast<uint4*>(pix + r0 * PS + c16) = pf0;
+      *reinterpret_cast<uint4*>(pix + (r0 + 4) * PS + c16) = pf1;
+    } else {
+      const uint8_t* ib = in + f * frame_stride;
+      for (int e = lane; e < 8 * 128; e += 32) {
+        const int r = e >> 7, c = e & 127;
+        const int y = min(by * 8 + r, h - 1), x = min(bx0 * 8 + c, w - 1);
+        pix[r * PS + c] = ib[static_cast<size_t>(y) * pitch + x];
+      }
+    }
+    __syncwarp();
+    if (s + total < nstrips) prefetch(s + total);
+
+    // forward DCT, 16 blocks
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const uint32_t pp = *reinterpret_cast<const uint16_t*>(pix + g * PS + 8 * b + 2 * t);
+      double2 d = make_double2(0.0, 0.0);
+      dmma(d, af0, static_cast<double>(pp & 0xffu));
+      dmma(d, af1, static_cast<double>(pp >> 8));
+      double2 x = make_double2(0.0, 0.0);
+      dmma(x, d.x, af0);
+      dmma(x, d.y, af1);
+      *reinterpret_cast<double2*>(xy + b * 512 + t * 128 + ((g ^ (b & 7)) << 4)) = x;
+    }
+    __syncwarp();
+
+    // DCT-domain filter: 16 blocks x 64 outputs, K = 64
+    double2 acc[2][8];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[m][j] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int sw = (q ^ g) << 4;
+      const double2 a0 = *reinterpret_cast<const double2*>(xy + g * 512 + t * 128 + sw);
+      const double2 a1 = *reinterpret_cast<const double2*>(xy + (8 + g) * 512 + t * 128 + sw);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double2 b = hs[(j * 8 + q) * 32 + lane];
+        dmma(acc[0][j], a0.x, b.x);
+        dmma(acc[0][j], a0.y, b.y);
+        dmma(acc[1][j], a1.x, b.x);
+        dmma(acc[1][j], a1.y, b.y);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<double2*>(xy + (8 * m + g) * 512 + (j >> 1) * 128 +
+                                    (((4 * (j & 1) + t) ^ g) << 4)) = acc[m][j];
+    if (coef_out) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int bx = bx0 + 8 * m + g;
+        if (bx < bw) {
+          double* dst = coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 64;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int u = 2 * (j >> 1), v = 4 * (j & 1) + t;
+            dst[u * 8 + v] = acc[m][j].x;
+            dst[(u + 1) * 8 + v] = acc[m][j].y;
+          }
+        }
+      }
+    }
+    __syncwarp();
+
+    // inverse DCT + quantize, 16 blocks
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const double2 yv =
+          *reinterpret_cast<const double2*>(xy + b * 512 + t * 128 + ((g ^ (b & 7)) << 4));
+      double2 z = make_double2(0.0, 0.0);
+      dmma(z, ai0, yv.x);
+      dmma(z, ai1, yv.y);
+      double2 o = make_double2(0.0, 0.0);
+      dmma(o, z.x, ai0);
+      dmma(o, z.y, ai1);
+      const uint32_t q = quantize(o.x, nullptr) | (quantize(o.y, nullptr) << 8);
+      *reinterpret_cast<uint16_t*>(pix + g * PS + 8 * b + 2 * t) = static_cast<uint16_t>(q);
+    }
+    __syncwarp();
+
+    uint8_t* ob = out + f * frame_stride;
+    if (fast) {
+      uint8_t* p = ob + static_cast<size_t>(by * 8) * pitch + bx0 * 8 + c16;
+      stg_stream(p + r0 * pitch, *reinterpret_cast<const uint4*>(pix + r0 * PS + c16));
+      stg_stream(p + (r0 + 4) * pitch, *reinterpret_cast<const uint4*>(pix + (r0 + 4) * PS + c16));
+    } else {
+      for (int e = lane; e < 8 * 128; e += 32) {
+        const int r = e >> 7, c = e & 127;
+        const int y = by * 8 + r, x = bx0 * 8 + c;
+        if (y < h && x < w) ob[static_cast<size_t>(y) * pitch + x] = pix[r * PS + c];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  });
+  return fn;
+}
+
+// 2-D FP64 view [nblocks rows x nn cols] of block-major coefficients; box
+// [box_rows x 16 cols] (128 bytes inner), 128B swizzle, OOB rows -> 0.
+dctf_status make_xmap(CUtensorMap* map, const double* d, long long nblocks, int nn, int box_rows) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(nn), static_cast<cuuint64_t>(nblocks)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(nn) * 8};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(d), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return DCTF_OK;
+}
+
+int sm_count(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cached[device]) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cached[device] = v;
+  }
+  return cached[device];
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+bool misaligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; }
+
+dctf_status check_plan(const dctf_plan* p) {
+  if (!p) return set_error(DCTF_INVALID_ARGUMENT, "plan is NULL");
+  if (p->precision != DCTF_PREC_FP64)
+    return set_error(DCTF_UNSUPPORTED, "precision mode not available for this entry point");
+  return DCTF_OK;
+}
+
+dctf_status check_image(int w, int h, size_t pitch) {
+  if (w < 1 || h < 1) return set_error(DCTF_INVALID_ARGUMENT, "image dimensions must be >= 1");
+  if (pitch < static_cast<size_t>(w)) return set_error(DCTF_INVALID_ARGUMENT, "pitch < width");
+  return DCTF_OK;
+}
+
+dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
+                        cudaStream_t st) {
+  if (nb == 0) return DCTF_OK;
+  if (misaligned16(d_in) || misaligned16(d_out))
+    return set_error(DCTF_INVALID_ARGUMENT, "coefficient buffers must be 16-byte aligned");
+  if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in-place filter_coeffs not supported");
+  CUtensorMap map;
+  const int nn = p->n * p->n;
+  dctf_status s = make_xmap(&map, d_in, nb, nn, p->n == 8 ? c8::TILE : c16::TILE);
+  if (s != DCTF_OK) return s;
+  const int sms = sm_count(p->device);
+  if (p->n == 8) {
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(k_coef8, cudaFuncAttributeMaxDynamicSharedMemorySize, c8::SMEM));
+      attr = true;
+    }
+    const long long ntiles = (nb + c8::TILE - 1) / c8::TILE;
+    const long long ctas = std::min<long long>(sms, (ntiles + c8::WARPS - 1) / c8::WARPS);
+    k_coef8<<<static_cast<unsigned>(ctas), c8::WARPS * 32, c8::SMEM, st>>>(map, p->d_hcoef, d_out, nb);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(k_coef16, cudaFuncAttributeMaxDynamicSharedMemorySize, c16::SMEM));
+      attr = true;
+    }
+    const long long ntiles = (nb + c16::TILE - 1) / c16::TILE;
+    const long long ctas = std::min<long long>(sms, ntiles);
+    k_coef16<<<static_cast<unsigned>(ctas), (c16::CWARPS + 1) * 32, c16::SMEM, st>>>(map, p->d_hcoef,
+                                                                                   d_out, nb);
+  }
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
+dctf_status launch_forward_u8(const dctf_plan* p, const uint8_t* img, int w, int h, size_t pitch,
+                              double* coeffs, cudaStream_t st) {
+  const int n = p->n, bw = (w + n - 1) / n, bh = (h + n - 1) / n;
+  const long long nb = static_cast<long long>(bw) * bh;
+  const int bpc = 256 / n;
+  const unsigned grid = static_cast<unsigned>((nb + bpc - 1) / bpc);
+  if (n == 8)
+    k_forward<8, true><<<grid, 256, 0, st>>>(img, w, h, pitch, bw, nullptr, coeffs, nb, p->d_basis);
+  else
+    k_forward<16, true><<<grid, 256, 0, st>>>(img, w, h, pitch, bw, nullptr, coeffs, nb, p->d_basis);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
+dctf_status launch_inverse_u8(const dctf_plan* p, const double* coeffs, uint8_t* img, int w, int h,
+                              size_t pitch, cudaStream_t st) {
+  const int n = p->n, bw = (w + n - 1) / n, bh = (h + n - 1) / n;
+  const long long nb = static_cast<long long>(bw) * bh;
+  const int bpc = 256 / n;
+  const unsigned grid = static_cast<unsigned>((nb + bpc - 1) / bpc);
+  if (n == 8)
+    k_inverse<8, true><<<grid, 256, 0, st>>>(coeffs, nullptr, img, w, h, pitch, bw, nb, p->d_basis, p->d_nan);
+  else
+    k_inverse<16, true><<<grid, 256, 0, st>>>(coeffs, nullptr, img, w, h, pitch, bw, nb, p->d_basis, p->d_nan);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
+dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
+                          size_t pitch, long long frame_stride, int nframes, double* coef_out,
+                          cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_fused8, cudaFuncAttributeMaxDynamicSharedMemorySize, f8::SMEM));
+    attr = true;
+  }
+  const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8::SB - 1) / f8::SB;
+  const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
+  const long long ctas =
+      std::min<long long>(2LL * sm_count(p->device), (nstrips + f8::WARPS - 1) / f8::WARPS);
+  if (ctas <= 0) return DCTF_OK;
+  k_fused8<<<static_cast<unsigned>(ctas), f8::WARPS * 32, f8::SMEM, st>>>(
+      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
+// filter_image on device buffers, one frame or a strided frame batch.
+dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
+                                size_t pitch, long long frame_stride, int nframes, double* coef_out,
+                                cudaStream_t st) {
+  if (p->n == 8) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+  // n = 16: forward -> H -> inverse through a stream-ordered scratch buffer.
+  const int bw = (w + 15) / 16, bh = (h + 15) / 16;
+  const long long nb = static_cast<long long>(bw) * bh;
+  double* xbuf = nullptr;
+  double* ybuf = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&xbuf), nb * 256 * sizeof(double), st));
+  if (!coef_out) CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ybuf), nb * 256 * sizeof(double), st));
+  dctf_status s = DCTF_OK;
+  for (int f = 0; f < nframes && s == DCTF_OK; ++f) {
+    double* y = coef_out ? coef_out + f * nb * 256 : ybuf;
+    s = launch_forward_u8(p, in + f * frame_stride, w, h, pitch, xbuf, st);
+    if (s == DCTF_OK) s = launch_coef(p, xbuf, y, nb, st);
+    if (s == DCTF_OK) s = launch_inverse_u8(p, y, out + f * frame_stride, w, h, pitch, st);
+  }
+  cudaFreeAsync(xbuf, st);
+  if (ybuf) cudaFreeAsync(ybuf, st);
+  return s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+extern "C" {
+
+const char* dctf_last_error_message(void) { return dctf::t_err.c_str(); }
+int dctf_last_launch_count(void) { return dctf::t_launches; }
+const char* dctf_version(void) { return "dctf_b200 0.1 (sm_100a, fp64-dmma)"; }
+
+dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int padding,
+                             int precision, int device, dctf_plan** out) {
+  dctf::reset_launches();
+  if (!out || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (precision != DCTF_PREC_FP64 && precision != DCTF_PREC_TF32X3 && precision != DCTF_PREC_BF16X3)
+    return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
+  if (kr < 1 || kc < 1) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
+  auto* p = new dctf_plan();
+  p->n = n;
+  p->kr = kr;
+  p->kc = kc;
+  p->padding = padding;
+  p->precision = precision;
+  p->device = device;
+  p->weights.assign(h_weights, h_weights + static_cast<size_t>(kr) * kc);
+  dctf_status s = dctf::compile_operator(*p);
+  if (s != DCTF_OK) {
+    delete p;
+    return s;
+  }
+  if (precision != DCTF_PREC_FP64) {
+    delete p;
+    return set_error(DCTF_UNSUPPORTED, "split-precision modes are not built yet");
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    delete p;
+    return set_error(DCTF_CUDA_ERROR, "no CUDA device available");
+  }
+  if (device < 0 || device >= ndev) {
+    delete p;
+    return set_error(DCTF_INVALID_ARGUMENT, "device ordinal out of range");
+  }
+  DeviceGuard guard(device);
+  std::vector<double> hcoef, hfused;
+  dctf::layout_hcoef(n, p->op, hcoef);
+  const size_t nn = static_cast<size_t>(n) * n;
+  cudaError_t e = cudaMalloc(&p->d_basis, nn * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_hcoef, nn * nn * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_nan, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_basis, p->basis.data(), nn * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_hcoef, hcoef.data(), nn * nn * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(p->d_nan, 0, sizeof(int));
+  if (e == cudaSuccess && n == 8) {
+    dctf::layout_hfused8(p->op, hfused);
+    e = cudaMalloc(&p->d_hfused, 64 * 64 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_hfused, hfused.data(), 64 * 64 * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    const std::string msg = cudaGetErrorString(e);
+    dctf_plan_destroy(p);
+    return set_error(DCTF_CUDA_ERROR, "plan upload: " + msg);
+  }
+  *out = p;
+  return DCTF_OK;
+}
+
+dctf_status dctf_compile_operator(const double* h_weights, int kr, int kc, int n, int padding,
+                                  double* h_c, double* h_op, int* npairs, int* merged) {
+  if (!h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  if (kr < 1 || kc < 1) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
+  dctf_plan p;
+  p.n = n;
+  p.kr = kr;
+  p.kc = kc;
+  p.padding = padding;
+  p.weights.assign(h_weights, h_weights + static_cast<size_t>(kr) * kc);
+  const dctf_status s = dctf::compile_operator(p);
+  if (s != DCTF_OK) return s;
+  if (h_c) std::memcpy(h_c, p.basis.data(), p.basis.size() * sizeof(double));
+  if (h_op) std::memcpy(h_op, p.op.data(), p.op.size() * sizeof(double));
+  if (npairs) *npairs = p.npairs;
+  if (merged) *merged = p.merged;
+  return DCTF_OK;
+}
+
+dctf_status dctf_plan_destroy(dctf_plan* p) {
+  if (!p) return DCTF_OK;
+  {
+    DeviceGuard guard(p->device);
+    cudaFree(p->d_basis);
+    cudaFree(p->d_hcoef);
+    cudaFree(p->d_hfused);
+    cudaFree(p->d_nan);
+    cudaFree(p->io_in);
+    cudaFree(p->io_out);
+    for (void* s : p->streams)
+      if (s) cudaStreamDestroy(as_stream(s));
+  }
+  delete p;
+  return DCTF_OK;
+}
+
+dctf_status dctf_plan_info(const dctf_plan* p, int* n, int* npairs, int* merged) {
+  if (!p) return set_error(DCTF_INVALID_ARGUMENT, "plan is NULL");
+  if (n) *n = p->n;
+  if (npairs) *npairs = p->npairs;
+  if (merged) *merged = p->merged;
+  return DCTF_OK;
+}
+
+dctf_status dctf_plan_basis(const dctf_plan* p, double* h_c) {
+  if (!p || !h_c) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  std::memcpy(h_c, p->basis.data(), p->basis.size() * sizeof(double));
+  return DCTF_OK;
+}
+
+dctf_status dctf_plan_operator(const dctf_plan* p, double* h_op) {
+  if (!p || !h_op) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  std::memcpy(h_op, p->op.data(), p->op.size() * sizeof(double));
+  return DCTF_OK;
+}
+
+dctf_status dctf_forward(const dctf_plan* p, const uint8_t* d_img, int w, int h, size_t pitch,
+                         double* d_coeffs, void* stream) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s == DCTF_OK) s = check_image(w, h, pitch);
+  if (s != DCTF_OK) return s;
+  if (!d_img || !d_coeffs) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  return launch_forward_u8(p, d_img, w, h, pitch, d_coeffs, as_stream(stream));
+}
+
+dctf_status dctf_forward_blocks(const dctf_plan* p, const double* d_blocks, double* d_coeffs,
+                                size_t nblocks, void* stream) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s != DCTF_OK) return s;
+  if (nblocks == 0) return DCTF_OK;
+  if (!d_blocks || !d_coeffs) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  if (misaligned16(d_coeffs)) return set_error(DCTF_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
+  DeviceGuard guard(p->device);
+  const long long nb = static_cast<long long>(nblocks);
+  const int bpc = 256 / p->n;
+  const unsigned grid = static_cast<unsigned>((nb + bpc - 1) / bpc);
+  if (p->n == 8)
+    k_forward<8, false><<<grid, 256, 0, as_stream(stream)>>>(nullptr, 0, 0, 0, 1, d_blocks, d_coeffs, nb, p->d_basis);
+  else
+    k_forward<16, false><<<grid, 256, 0, as_stream(stream)>>>(nullptr, 0, 0, 0, 1, d_blocks, d_coeffs, nb, p->d_basis);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
+dctf_status dctf_inverse_blocks(const dctf_plan* p, const double* d_coeffs, double* d_blocks,
+                                size_t nblocks, void* stream) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s != DCTF_OK) return s;
+  if (nblocks == 0) return DCTF_OK;
+  if (!d_blocks || !d_coeffs) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  if (misaligned16(d_blocks)) return set_error(DCTF_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
+  DeviceGuard guard(p->device);
+  const long long nb = static_cast<long long>(nblocks);
+  const int bpc = 256 / p->n;
+  const unsigned grid = static_cast<unsigned>((nb + bpc - 1) / bpc);
+  if (p->n == 8)
+    k_inverse<8, false><<<grid, 256, 0, as_stream(stream)>>>(d_coeffs, d_blocks, nullptr, 0, 0, 0, 1, nb, p->d_basis, nullptr);
+  else
+    k_inverse<16, false><<<grid, 256, 0, as_stream(stream)>>>(d_coeffs, d_blocks, nullptr, 0, 0, 0, 1, nb, p->d_basis, nullptr);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
+dctf_status dctf_filter_coeffs(const dctf_plan* p, const double* d_in, double* d_out,
+                               size_t nblocks, void* stream) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s != DCTF_OK) return s;
+  if (nblocks == 0) return DCTF_OK;
+  if (!d_in || !d_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  return launch_coef(p, d_in, d_out, static_cast<long long>(nblocks), as_stream(stream));
+}
+
+dctf_status dctf_inverse_u8(const dctf_plan* p, const double* d_coeffs, uint8_t* d_img, int w,
+                            int h, size_t pitch, void* stream) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s == DCTF_OK) s = check_image(w, h, pitch);
+  if (s != DCTF_OK) return s;
+  if (!d_img || !d_coeffs) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  return launch_inverse_u8(p, d_coeffs, d_img, w, h, pitch, as_stream(stream));
+}
+
+dctf_status dctf_filter_image_u8(const dctf_plan* p, const uint8_t* d_in, uint8_t* d_out, int w,
+                                 int h, size_t pitch, double* d_coeffs_out, void* stream) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s == DCTF_OK) s = check_image(w, h, pitch);
+  if (s != DCTF_OK) return s;
+  if (!d_in || !d_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in/out images may not alias");
+  DeviceGuard guard(p->device);
+  return filter_image_device(p, d_in, d_out, w, h, pitch, 0, 1, d_coeffs_out, as_stream(stream));
+}
+
+dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
+                                  const int* h_plan_of_frame, const uint8_t* d_in, uint8_t* d_out,
+                                  int nframes, int w, int h, size_t pitch, size_t frame_stride,
+                                  void* stream) {
+  dctf::reset_launches();
+  if (!plans || nplans < 1 || !h_plan_of_frame || nframes < 0)
+    return set_error(DCTF_INVALID_ARGUMENT, "bad plan list");
+  dctf_status s = check_image(w, h, pitch);
+  if (s != DCTF_OK) return s;
+  if (frame_stride < pitch * static_cast<size_t>(h))
+    return set_error(DCTF_INVALID_ARGUMENT, "frame_stride smaller than one frame");
+  for (int i = 0; i < nplans; ++i) {
+    s = check_plan(plans[i]);
+    if (s != DCTF_OK) return s;
+    if (plans[i]->n != plans[0]->n || plans[i]->device != plans[0]->device)
+      return set_error(DCTF_INVALID_ARGUMENT, "plans must share n and device");
+  }
+  for (int f = 0; f < nframes; ++f)
+    if (h_plan_of_frame[f] < 0 || h_plan_of_frame[f] >= nplans)
+      return set_error(DCTF_INVALID_ARGUMENT, "plan_of_frame index out of range");
+  DeviceGuard guard(plans[0]->device);
+  const cudaStream_t st = as_stream(stream);
+  // Frames sharing a plan and evenly spaced go in one launch (round-robin
+  // assignment -> one launch per plan); anything else falls back per frame.
+  for (int pi = 0; pi < nplans && s == DCTF_OK; ++pi) {
+    int first = -1, second = -1, count = 0;
+    bool arith = true;
+    for (int f = 0; f < nframes; ++f) {
+      if (h_plan_of_frame[f] != pi) continue;
+      if (first < 0) first = f;
+      else if (second < 0) second = f;
+      else if ((f - first) != count * (second - first)) arith = false;
+      ++count;
+    }
+    if (count == 0) continue;
+    if (arith) {
+      const long long step = count > 1 ? static_cast<long long>(second - first) : 1;
+      s = filter_image_device(plans[pi], d_in + first * frame_stride, d_out + first * frame_stride,
+                              w, h, pitch, step * static_cast<long long>(frame_stride), count,
+                              nullptr, st);
+    } else {
+      for (int f = 0; f < nframes && s == DCTF_OK; ++f)
+        if (h_plan_of_frame[f] == pi)
+          s = filter_image_device(plans[pi], d_in + f * frame_stride, d_out + f * frame_stride, w,
+                                  h, pitch, 0, 1, nullptr, st);
+    }
+  }
+  return s;
+}
+
+dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w,
+                                   int h, size_t pitch) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s == DCTF_OK) s = check_image(w, h, pitch);
+  if (s != DCTF_OK) return s;
+  if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  std::lock_guard<std::mutex> lock(p->scratch_mu);
+  const size_t dpitch = (static_cast<size_t>(w) + 15) & ~size_t(15);
+  const size_t bytes = dpitch * static_cast<size_t>(h);
+  if (p->io_bytes < bytes) {
+    cudaFree(p->io_in);
+    cudaFree(p->io_out);
+    p->io_in = p->io_out = nullptr;
+    p->io_bytes = 0;
+    CUDA_TRY(cudaMalloc(&p->io_in, bytes));
+    CUDA_TRY(cudaMalloc(&p->io_out, bytes));
+    p->io_bytes = bytes;
+  }
+  for (auto& st : p->streams)
+    if (!st) {
+      cudaStream_t x;
+      CUDA_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+      st = x;
+    }
+  CUDA_TRY(cudaMemsetAsync(p->d_nan, 0, sizeof(int), as_stream(p->streams[0])));
+  CUDA_TRY(cudaStreamSynchronize(as_stream(p->streams[0])));
+  const int n = p->n, bh = (h + n - 1) / n;
+  const int nchunks = std::min(bh, 8);
+  const int brows = (bh + nchunks - 1) / nchunks;
+  auto* din = static_cast<uint8_t*>(p->io_in);
+  auto* dout = static_cast<uint8_t*>(p->io_out);
+  int launches = 0;
+  for (int c = 0; c * brows < bh && s == DCTF_OK; ++c) {
+    const int y0 = c * brows * n;
+    const int rows = std::min(brows * n, h - y0);
+    const cudaStream_t st = as_stream(p->streams[c & 1]);
+    CUDA_TRY(cudaMemcpy2DAsync(din + y0 * dpitch, dpitch, h_in + y0 * pitch, pitch, w, rows,
+                               cudaMemcpyHostToDevice, st));
+    dctf::reset_launches();
+    s = filter_image_device(p, din + y0 * dpitch, dout + y0 * dpitch, w, rows, dpitch, 0, 1,
+                            nullptr, st);
+    launches += dctf::t_launches;
+    if (s != DCTF_OK) break;
+    CUDA_TRY(cudaMemcpy2DAsync(h_out + y0 * pitch, pitch, dout + y0 * dpitch, dpitch, w, rows,
+                               cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(as_stream(p->streams[0])));
+  CUDA_TRY(cudaStreamSynchronize(as_stream(p->streams[1])));
+  dctf::t_launches = launches;
+  if (s != DCTF_OK) return s;
+  int nan_seen = 0;
+  CUDA_TRY(cudaMemcpy(&nan_seen, p->d_nan, sizeof(int), cudaMemcpyDeviceToHost));
+  if (nan_seen) return set_error(DCTF_NAN_ENCOUNTERED, "quantize: NaN sample");
+  return DCTF_OK;
+}
+
+dctf_status dctf_plan_nan_check(const dctf_plan* p, void* stream, int* nan_seen) {
+  if (!p || !nan_seen) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard guard(p->device);
+  const cudaStream_t st = as_stream(stream);
+  int v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, p->d_nan, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemsetAsync(p->d_nan, 0, sizeof(int), st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *nan_seen = v;
+  return DCTF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,228 @@
+// Host-side operator compiler: mask -> DCT basis C -> dense DCT-domain
+// operator H (n^2 x n^2), plus the fragment-order layouts the sm_100a kernels
+// stream into shared memory. One-time work per plan (filter.hpp:54-56 does
+// the same once per FilterPlan); nothing here runs per block.
+//
+// Reference-domain masks (square, odd k <= n) compile exactly like
+// FilterPlan::compile (filter.hpp:76-83):
+//   build_spatial_operator_set (operators.hpp:104-119): one pair per mask row
+//     r, (S_{h-r}, T_r) with build_shift_matrix (61-75) / build_band_matrix
+//     (80-98);
+//   merge_symmetric (146-169) when row_symmetric (mask.hpp:100-108);
+//   to_dct_domain (124-141): M -> (C M) C^t with the zero-skipping i-k-j
+//     matmul (block_matrix.hpp:67-81);
+// and the pairs are then densified: H[(u,v),(a,b)] = sum_p L_p[u][a] R_p[b][v]
+// (apply_pairs, filter.hpp:30-38, computes Y = sum_p L_p X R_p).
+//
+// Other masks (kr != kc, or wider than the block — outside the reference's
+// domain, needed for BASELINE config 5's 1x9 motion blur on 8x8 blocks) use
+// the convolve formula (spatial.hpp:36-37) for H_spatial and
+// H = (C (x) C) H_spatial (C (x) C)^t; for reference-domain masks both
+// constructions agree to ~1e-15 (tests/test_host_api.py).
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+namespace dctf {
+namespace {
+
+void matmul(int n, const double* a, const double* b, double* out) {
+  std::memset(out, 0, sizeof(double) * size_t(n) * n);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) {
+      const double aik = a[i * n + k];
+      if (aik == 0.0) continue;
+      for (int j = 0; j < n; ++j) out[i * n + j] += aik * b[k * n + j];
+    }
+}
+
+void transpose(int n, const double* a, double* out) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) out[j * n + i] = a[i * n + j];
+}
+
+int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// DctBasis::build (dct.hpp:40-52), same expression order as the reference.
+void dct_basis(int n, double* c) {
+  const double pi = 3.141592653589793238462643383279502884;
+  const double a0 = std::sqrt(1.0 / n);
+  const double au = std::sqrt(2.0 / n);
+  for (int u = 0; u < n; ++u)
+    for (int x = 0; x < n; ++x) {
+      const double angle = (2 * x + 1) * u * pi / (2.0 * n);
+      c[u * n + x] = (u == 0 ? a0 : au) * std::cos(angle);
+    }
+}
+
+void sandwich_operator(dctf_plan& p) {
+  const int n = p.n, k = p.kr, h = (k - 1) / 2;
+  const size_t nn = size_t(n) * n;
+  const int rep = p.padding == DCTF_PAD_REPLICATE;
+  std::vector<double> left(nn * k, 0.0), right(nn * k, 0.0);
+  for (int r = 0; r < k; ++r) {
+    double* s = &left[r * nn];
+    const int offset = h - r;
+    for (int i = 0; i < n; ++i) {
+      const int j = i - offset;
+      if (!rep) {
+        if (j >= 0 && j < n) s[i * n + j] = 1.0;
+      } else {
+        s[i * n + clampi(j, 0, n - 1)] = 1.0;
+      }
+    }
+    double* t = &right[r * nn];
+    const double* row = &p.weights[size_t(r) * k];
+    for (int j = 0; j < n; ++j)
+      for (int c = 0; c < k; ++c) {
+        const int src = j + c - h;
+        if (!rep) {
+          if (src >= 0 && src < n) t[src * n + j] += row[c];
+        } else {
+          t[clampi(src, 0, n - 1) * n + j] += row[c];
+        }
+      }
+  }
+  bool sym = true;
+  for (int r = 0; r < k / 2 && sym; ++r)
+    for (int c = 0; c < k; ++c)
+      if (p.weights[size_t(r) * k + c] != p.weights[size_t(k - 1 - r) * k + c]) {
+        sym = false;
+        break;
+      }
+  int np = k;
+  if (sym) {
+    np = (k + 1) / 2;
+    for (int r = 0; r < np; ++r) {
+      const int mirror = k - 1 - r;
+      if (r != mirror)
+        for (size_t i = 0; i < nn; ++i) left[r * nn + i] += left[mirror * nn + i];
+    }
+  }
+  p.npairs = np;
+  p.merged = sym ? 1 : 0;
+  std::vector<double> ct(nn), tmp(nn), L(nn * np), R(nn * np);
+  transpose(n, p.basis.data(), ct.data());
+  for (int q = 0; q < np; ++q) {
+    matmul(n, p.basis.data(), &left[q * nn], tmp.data());
+    matmul(n, tmp.data(), ct.data(), &L[q * nn]);
+    matmul(n, p.basis.data(), &right[q * nn], tmp.data());
+    matmul(n, tmp.data(), ct.data(), &R[q * nn]);
+  }
+  p.op.assign(nn * nn, 0.0);
+  for (int u = 0; u < n; ++u)
+    for (int v = 0; v < n; ++v)
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+          double acc = 0.0;
+          for (int q = 0; q < np; ++q) acc += L[q * nn + u * n + a] * R[q * nn + b * n + v];
+          p.op[(size_t(u) * n + v) * nn + size_t(a) * n + b] = acc;
+        }
+}
+
+void convolution_operator(dctf_plan& p) {
+  const int n = p.n, kr = p.kr, kc = p.kc, hr = (kr - 1) / 2, hc = (kc - 1) / 2;
+  const size_t nn = size_t(n) * n;
+  const int rep = p.padding == DCTF_PAD_REPLICATE;
+  std::vector<double> hsp(nn * nn, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int r = 0; r < kr; ++r)
+        for (int c = 0; c < kc; ++c) {
+          int si = i + r - hr, sj = j + c - hc;
+          if (!rep) {
+            if (si < 0 || si >= n || sj < 0 || sj >= n) continue;
+          } else {
+            si = clampi(si, 0, n - 1);
+            sj = clampi(sj, 0, n - 1);
+          }
+          hsp[(size_t(i) * n + j) * nn + size_t(si) * n + sj] += p.weights[size_t(r) * kc + c];
+        }
+  // K = C (x) C acting on vec(X) (index a*n+b): K[(u,v),(a,b)] = C[u][a] C[v][b].
+  // H = K H_spatial K^t.
+  const double* C = p.basis.data();
+  std::vector<double> m1(nn * nn, 0.0);  // m1 = H_spatial K^t
+  for (size_t row = 0; row < nn; ++row)
+    for (int u = 0; u < n; ++u)
+      for (int v = 0; v < n; ++v) {
+        double acc = 0.0;
+        for (int a = 0; a < n; ++a)
+          for (int b = 0; b < n; ++b) acc += hsp[row * nn + size_t(a) * n + b] * C[u * n + a] * C[v * n + b];
+        m1[row * nn + size_t(u) * n + v] = acc;
+      }
+  p.op.assign(nn * nn, 0.0);
+  for (int u = 0; u < n; ++u)
+    for (int v = 0; v < n; ++v)
+      for (size_t col = 0; col < nn; ++col) {
+        double acc = 0.0;
+        for (int a = 0; a < n; ++a)
+          for (int b = 0; b < n; ++b) acc += C[u * n + a] * C[v * n + b] * m1[(size_t(a) * n + b) * nn + col];
+        p.op[(size_t(u) * n + v) * nn + col] = acc;
+      }
+  p.npairs = kr;
+  p.merged = 0;
+}
+
+}  // namespace
+
+dctf_status compile_operator(dctf_plan& p) {
+  if (p.n != 8 && p.n != 16) return set_error(DCTF_INVALID_ARGUMENT, "block side n must be 8 or 16");
+  if (p.kr < 1 || p.kc < 1 || (p.kr % 2) == 0 || (p.kc % 2) == 0)
+    return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
+  if (p.padding != DCTF_PAD_ZERO && p.padding != DCTF_PAD_REPLICATE)
+    return set_error(DCTF_INVALID_ARGUMENT, "padding must be DCTF_PAD_ZERO or DCTF_PAD_REPLICATE");
+  for (double v : p.weights)
+    if (!std::isfinite(v)) return set_error(DCTF_INVALID_ARGUMENT, "Mask: weights must be finite");
+  p.basis.assign(size_t(p.n) * p.n, 0.0);
+  dct_basis(p.n, p.basis.data());
+  p.reference_domain = (p.kr == p.kc) && (p.kr <= p.n);
+  if (p.reference_domain)
+    sandwich_operator(p);
+  else
+    convolution_operator(p);
+  return DCTF_OK;
+}
+
+// Coefficient-kernel layout, n in {8,16}, NN = n^2:
+//   [kc < NN/16][J < NN/8][q < 2][lane < 32][e < 2]
+//   = H[8J + g][16kc + 8q + 2t + e],  g = lane>>2, t = lane&3.
+// One (kc) slice is the B operand of one 16-wide K chunk for every n-tile J;
+// each lane's two k-steps sit in one 16-byte word (one LDS.128).
+void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out) {
+  const int nn = n * n, nkc = nn / 16, nj = nn / 8;
+  out.assign(size_t(nn) * nn, 0.0);
+  size_t o = 0;
+  for (int kc = 0; kc < nkc; ++kc)
+    for (int J = 0; J < nj; ++J)
+      for (int q = 0; q < 2; ++q)
+        for (int lane = 0; lane < 32; ++lane)
+          for (int e = 0; e < 2; ++e) {
+            const int g = lane >> 2, t = lane & 3;
+            out[o++] = op[size_t(8 * J + g) * nn + 16 * kc + 8 * q + 2 * t + e];
+          }
+}
+
+// Fused n=8 kernel layout: [j < 8][q < 8][lane < 32][e < 2]
+//   = H[o(j,g)][(2t+e)*8 + q]
+// where the output coefficient of n-tile j, column c is
+//   o(j,c) = (2(j>>1) + (c&1)) * 8 + 4(j&1) + (c>>1)
+// and the contraction index of k-step s = 2q+e for lane t is coefficient
+// (u = 2t+e, v = q). Both permutations are chosen so the per-warp shared
+// staging of X and Y is written and read with conflict-free 16-byte accesses
+// (see kernels.cu, fused8).
+void layout_hfused8(const std::vector<double>& op, std::vector<double>& out) {
+  out.assign(64 * 64, 0.0);
+  size_t o = 0;
+  for (int j = 0; j < 8; ++j)
+    for (int q = 0; q < 8; ++q)
+      for (int lane = 0; lane < 32; ++lane)
+        for (int e = 0; e < 2; ++e) {
+          const int g = lane >> 2, t = lane & 3;
+          const int orow = (2 * (j >> 1) + (g & 1)) * 8 + 4 * (j & 1) + (g >> 1);
+          const int kcol = (2 * t + e) * 8 + q;
+          out[o++] = op[size_t(orow) * 64 + kcol];
+        }
+}
+
+}  // namespace dctf
