@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the DCT-domain block filter on B200 (BASELINE.json metric).
+
+Workload (BASELINE configs[1], "config 2"): one 4096x4096 uint8 image per GPU
+(seeded sinusoid+noise generator S(2+rank), see csrc/synth.cc), 8x8 blocks
+(262,144 blocks), 5x5 Gaussian mask sigma=1 normalised to sum 1, border
+replication, FP64. One step = one fused filter_image pass (u8 -> forward DCT
+-> H_dct -> inverse DCT -> round/clamp -> u8) over the device-resident image:
+exactly one launch of k_fused8. L2 (126 MB) is flushed between timed steps by
+writing a 256 MiB buffer (the 16 MiB input would otherwise stay L2-resident).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 runs under torchrun, one rank per GPU; every rank filters its own image
+(block-range sharding of an N-image batch, no data-path collective:
+"scaling": "weak"); the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DCT-domain filtered blocks/sec"
+UNIT = "blocks/s"
+W, H, N = 4096, 4096, 8
+NBLOCKS = (W // N) * (H // N)
+FLOP_PER_BLOCK_FUSED = 2 * N ** 4 + 8 * N ** 3      # 12,288: forward + H + inverse
+FLOP_PER_BLOCK_COEF = 2 * N ** 4                      # 8,192
+BYTES_PER_BLOCK_FUSED = 2 * N * N                     # u8 in + u8 out
+BYTES_PER_BLOCK_COEF = 16 * N * N                     # fp64 in + out
+WORKLOAD = ("config2: 4096x4096 u8 S(seed) sinusoid+noise image per GPU, 8x8 blocks "
+            "(262144/GPU), gaussian 5x5 sigma=1 (sum 1), replicate padding, FP64, "
+            "fused spatial-in/spatial-out filter_image")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        time.sleep(0.05)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic():
+    """dram bytes per launch of k_fused8 from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_fused8_config2.json")
+    try:
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    except Exception:
+        return None, None
+
+
+def cpu_reference_baseline(img, mask, budget_s=10.0):
+    """The reference's own CPU path (oracle/_ref = reference headers compiled
+    in place): filter_image's per-tile loop split over all host threads
+    (filter.hpp:47-51 thread-safety contract), on the full config-2 image,
+    repeated until ~budget_s of CPU time."""
+    from oracle import Reference
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    ref.filter_image(img, mask, 5, 1, N, threads=threads)  # warm
+    times, t_end = [], time.perf_counter() + budget_s
+    while time.perf_counter() < t_end and len(times) < 20:
+        t0 = time.perf_counter()
+        ref.filter_image(img, mask, 5, 1, N, threads=threads)
+        times.append(time.perf_counter() - t0)
+    return {"value": NBLOCKS / statistics.median(times), "unit": UNIT, "cores": threads,
+            "kind": "reference",
+            "sample": f"full 4096x4096 config-2 image x {len(times)} passes (median), "
+                      f"filter_image DCT path, tiles split over {threads} threads"}
+
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return 0
+    import numpy as np  # noqa: F401
+    from oracle import Reference
+    from paper_1710_07193_b200 import synth
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    img = synth.sinusoid_image(2, W, H)
+    mask = synth.gaussian_mask(5, 1.0)
+    # calibrate a band size so warmup+steps fit in ~90 s
+    band = img[:64]
+    t0 = time.perf_counter()
+    ref.filter_image(band, mask, 5, 1, N, threads=threads)
+    per_block = (time.perf_counter() - t0) / ((64 // N) * (W // N))
+    rows = int(90.0 / max(1, args.steps + args.warmup) / per_block / (W // N)) * N
+    rows = max(N, min(H, rows))
+    sample = img[:rows]
+    nb = (rows // N) * (W // N)
+    for _ in range(args.warmup):
+        ref.filter_image(sample, mask, 5, 1, N, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref.filter_image(sample, mask, 5, 1, N, threads=threads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    value = nb / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "reference_sample_rows": rows,
+                       "blocks_per_step": nb},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{rows}x4096 band of the config-2 image per step, "
+                                       f"reference filter_image tiles over {threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gb_per_s": value * BYTES_PER_BLOCK_FUSED / 1e9}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-aux", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1710_07193_b200 as P
+    from paper_1710_07193_b200 import _lib, synth
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    img = synth.sinusoid_image(2 + rank, W, H)
+    mask = synth.gaussian_mask(5, 1.0)
+    plan = P.FilterPlan(P.Mask(5, mask), N, P.PaddingMode.kReplicate)
+    d_in = torch.from_numpy(img).cuda()
+    d_out = torch.empty_like(d_in)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = int(stream.cuda_stream)
+    lib = _lib.lib
+
+    def step():
+        _lib.check(lib.dctf_filter_image_u8(plan.handle, d_in.data_ptr(), d_out.data_ptr(), W, H, W,
+                                            None, sp))
+        return _lib.last_launch_count()
+
+    # FP64 pipe peak (roofline denominator; MEASURED_PEAKS.json has no FP64 entry)
+    peak_dmma, peak_dfma = (np.zeros(1), np.zeros(1))
+    _lib.check(lib.dctf_measure_fp64_peak(local, 0, peak_dmma.ctypes.data_as(_lib._d)))
+    _lib.check(lib.dctf_measure_fp64_peak(local, 1, peak_dfma.ctypes.data_as(_lib._d)))
+    peak_dmma, peak_dfma = float(peak_dmma[0]), float(peak_dfma[0])
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    launches = 0
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # evict the image from L2 (outside the timed events)
+        starts[i].record(stream)
+        launches += step()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = statistics.mean(step_ms)
+    ms = max_over_ranks(ms_local)
+    value = world * NBLOCKS / (ms / 1e3)
+
+    # correctness spot check of the timed output against a single-threaded
+    # reference band (rank 0; outside timing)
+    parity = None
+    if rank == 0:
+        try:
+            from oracle import Reference
+            band = img[:256]
+            r = Reference().filter_image(band, mask, 5, 1, N)
+            parity = int(np.count_nonzero(d_out[:256].cpu().numpy() != r))
+        except Exception as exc:  # reference .so missing on this box
+            parity = f"unchecked: {exc}"
+
+    achieved_tf = FLOP_PER_BLOCK_FUSED * NBLOCKS / (ms_local / 1e3) / 1e12
+    traffic, traffic_src = ncu_traffic()
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    gbs = value * BYTES_PER_BLOCK_FUSED / 1e9
+
+    # end to end through the public host-buffer API (pinned host memory)
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.from_numpy(img).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        hin, hout = h_in.numpy(), h_out.numpy()
+        ke = max(3, min(args.steps, 300))
+        for _ in range(3):
+            plan.filter_image_host(hin, hout)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            plan.filter_image_host(hin, hout)
+        t_e2e = (time.perf_counter() - t0) / ke
+        t_e2e = max_over_ranks(t_e2e)
+        assert np.array_equal(hout, d_out.cpu().numpy())
+        e2e = {"value": world * NBLOCKS / t_e2e, "unit": UNIT, "h2d_bytes_per_step": W * H,
+               "d2h_bytes_per_step": W * H, "steps": ke,
+               "api": "dctf_filter_image_host (FilterPlan.filter_image_host), pinned buffers"}
+
+    # auxiliary: the coefficient path on the same config (forward once,
+    # then filter_coeffs timed), FP64 in/out through HBM
+    aux = None
+    if not args.no_aux:
+        coeffs = plan.forward_image(d_in)
+        y = torch.empty_like(coeffs)
+        ka = max(3, min(args.steps, 200))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(ka)]
+        for i in range(ka + 3):
+            flush.fill_(2)
+            if i >= 3:
+                ev[i - 3][0].record(stream)
+            _lib.check(lib.dctf_filter_coeffs(plan.handle, coeffs.data_ptr(), y.data_ptr(),
+                                              NBLOCKS, sp))
+            if i >= 3:
+                ev[i - 3][1].record(stream)
+        torch.cuda.synchronize()
+        ms_c = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        aux = {"coef_path": {
+            "kernel": "k_coef8", "blocks_per_s": NBLOCKS / (ms_c / 1e3), "ms": ms_c,
+            "gb_per_s": NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9,
+            "fp64_tflops": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_c / 1e3) / 1e12,
+            "fp64_frac": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_c / 1e3) / 1e12 / peak_dmma,
+            "hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9) / hbm_peak
+            if hbm_peak else None}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_baseline(img, mask)
+        except Exception as exc:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "blocks_per_gpu": NBLOCKS, "block": "8x8",
+                       "mask": "gaussian5x5 sigma=1", "padding": "replicate",
+                       "l2": "flushed between steps (256 MiB write, untimed)",
+                       "parallelism": f"block-range shards x{world} (one image per GPU)"},
+            "gb_per_s": gbs,
+            "hbm_frac_of_measured": gbs / hbm_peak if hbm_peak else None,
+            "roofline": {
+                "bound": "tensor", "pipe": "FP64 DMMA.8x8x4 (mma.sync.m8n8k4.f64)",
+                "kernel": "k_fused8", "achieved": achieved_tf, "peak": peak_dmma,
+                "unit": "TFLOP/s", "frac": achieved_tf / peak_dmma,
+                "peak_source": "measured in this run (dctf_measure_fp64_peak, DMMA "
+                               "throughput microbenchmark); MEASURED_PEAKS.json has no FP64 entry",
+                "peak_dfma_tflops": peak_dfma,
+                "flop_per_block": FLOP_PER_BLOCK_FUSED, "units_per_launch": NBLOCKS,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": NBLOCKS * BYTES_PER_BLOCK_FUSED,
+                "hbm_bound_frac": gbs / world / hbm_peak if hbm_peak else None},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "parity_u8_mismatches_first_256_rows": parity,
+            "aux": aux,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -138,6 +138,13 @@ dctf_status dctf_filter_image_host(const dctf_plan* plan, const uint8_t* h_in, u
  * 1 if any quantised sample was NaN since the last check. */
 dctf_status dctf_plan_nan_check(const dctf_plan* plan, void* stream, int* nan_seen);
 
+/* Diagnostics: measures this device's FP64 peak with a throughput
+ * microbenchmark (mode 0: DMMA.8x8x4 via mma.sync.m8n8k4.f64 — the pipe the
+ * filter kernels use; mode 1: DFMA). Synchronous; ~50 ms. Used as the
+ * roofline denominator because the driver's MEASURED_PEAKS.json has no FP64
+ * entry. */
+dctf_status dctf_measure_fp64_peak(int device, int mode, double* tflops);
+
 /* Number of kernels the last call on this host thread launched (bench
  * accounting of gpu_launches). */
 int dctf_last_launch_count(void);

@@ -671,6 +671,38 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
 }
 
 // ---------------------------------------------------------------------------
+// FP64 peak microbenchmarks (diagnostics; roofline denominator).
+__global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
+  double2 acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = make_double2(threadIdx.x * 1e-3 + j, 0.5 * j);
+  const double a = 1.0 + threadIdx.x * 1e-12, b = 1.0 - threadIdx.x * 1e-12;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dmma(acc[j], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += acc[j].x + acc[j].y;
+  if (s == 1.2345) out[threadIdx.x] = s;  // practically never; defeats DCE
+}
+
+__global__ void __launch_bounds__(256) k_peak_dfma(double* out, int iters) {
+  double x[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x[j] = threadIdx.x * 1e-3 + j;
+  const double a = 1.0 + threadIdx.x * 1e-12, b = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = fma(x[j], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += x[j];
+  if (s == 1.2345) out[threadIdx.x] = s;
+}
+
+// ---------------------------------------------------------------------------
 // host helpers
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1174,6 +1206,36 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   int nan_seen = 0;
   CUDA_TRY(cudaMemcpy(&nan_seen, p->d_nan, sizeof(int), cudaMemcpyDeviceToHost));
   if (nan_seen) return set_error(DCTF_NAN_ENCOUNTERED, "quantize: NaN sample");
+  return DCTF_OK;
+}
+
+dctf_status dctf_measure_fp64_peak(int device, int mode, double* tflops) {
+  if (!tflops || (mode != 0 && mode != 1)) return set_error(DCTF_INVALID_ARGUMENT, "bad argument");
+  DeviceGuard guard(device);
+  double* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, 256 * sizeof(double)));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  const int blocks = sm_count(device) * 8, iters = mode == 0 ? 2048 : 16384;
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0);
+    if (mode == 0) k_peak_dmma<<<blocks, 256>>>(d, iters);
+    else k_peak_dfma<<<blocks, 256>>>(d, iters);
+    cudaEventRecord(e1);
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0) best = std::min(best, ms);
+  }
+  CUDA_TRY(cudaGetLastError());
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const double flops = mode == 0 ? double(blocks) * 8 * iters * 8 * 512.0    // warps * iters * 8 DMMA * 512
+                                 : double(blocks) * 256 * iters * 8 * 2.0;
+  *tflops = flops / (best * 1e-3) / 1e12;
   return DCTF_OK;
 }
 

@@ -1,0 +1,204 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference.
+
+The reference runs in the same process on the box's host cores
+(oracle/_ref/libdctf_ref.so, built from the reference headers) on identical
+seeded inputs. Tolerances (north_star):
+  * FP64 coefficients: max |err| <= 1e-9 * max |coef|   (TOL_COEF)
+  * u8 pixels: bit-exact except where the reference's pre-quantization value
+    lies within 1e-6 of a .5 rounding boundary; those are counted.
+  * forward_2d / inverse_2d kernels use the reference's operation order and
+    must be bit-identical.
+"""
+import numpy as np
+import pytest
+
+from conftest import blocks_to_image, nthreads, tie_report
+
+pytestmark = pytest.mark.gpu
+TOL_COEF = 1e-9
+
+
+@pytest.fixture(scope="module")
+def P(cuda):
+    import paper_1710_07193_b200 as P
+    return P
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _host(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def _plan(P, w, k, n, pad, kc=None):
+    m = P.Mask(k, w) if kc is None else P.Mask.rect(k, kc, w)
+    return P.FilterPlan(m, n, P.PaddingMode(pad))
+
+
+MASKS8 = ["average3", "gaussian3", "magic3", "random3", "random5", "random7", "identity"]
+
+
+def _mask(ref, name, rng):
+    if name.startswith("random"):
+        k = int(name[-1])
+        return rng.uniform(-1, 1, k * k), k
+    return ref.mask_preset(name)
+
+
+@pytest.mark.parametrize("n", [8, 16])
+def test_operator_and_basis_exact(P, ref, n):
+    rng = np.random.default_rng(n)
+    for name in MASKS8:
+        w, k = _mask(ref, name, rng)
+        for pad in (0, 1):
+            plan = _plan(P, w, k, n, pad)
+            assert np.array_equal(plan.basis(), ref.dct_basis(n))
+            assert np.abs(plan.operator() - ref.plan_operator(w, k, n, pad)).max() <= 1e-15
+
+
+@pytest.mark.parametrize("n", [8, 16])
+def test_forward_inverse_blocks_bitexact(P, ref, n):
+    rng = np.random.default_rng(100 + n)
+    plan = _plan(P, [1.0], 1, n, 0)
+    for blocks in (rng.integers(0, 256, (1000, n, n)).astype(np.float64),
+                   rng.uniform(-300, 300, (333, n, n))):
+        x = _host(P.forward_2d(plan, _dev(blocks)))
+        assert x.tobytes() == ref.forward_blocks(blocks, threads=nthreads()).tobytes()
+        y = _host(P.inverse_2d(plan, _dev(x)))
+        assert y.tobytes() == ref.inverse_blocks(x, threads=nthreads()).tobytes()
+
+
+@pytest.mark.parametrize("n", [8, 16])
+@pytest.mark.parametrize("nblocks", [1, 15, 16, 17, 64, 1000, 4099])
+def test_filter_coeffs_tolerance(P, ref, n, nblocks):
+    rng = np.random.default_rng(nblocks + n)
+    x = ref.forward_blocks(rng.integers(0, 256, (nblocks, n, n)).astype(np.float64))
+    for name in ("gaussian3", "magic3", "random5"):
+        w, k = _mask(ref, name, rng)
+        for pad in (0, 1):
+            plan = _plan(P, w, k, n, pad)
+            y = _host(plan.filter_coeffs(_dev(x)))
+            yr = ref.filter_coeffs(w, k, n, pad, x, threads=nthreads())
+            err = np.abs(y - yr).max() / max(1.0, np.abs(yr).max())
+            assert err <= TOL_COEF, (name, pad, err)
+
+
+def test_filter_coeffs_random_real(P, ref):
+    rng = np.random.default_rng(9)
+    for n in (8, 16):
+        x = rng.uniform(-100, 100, (257, n, n))
+        w, k = rng.uniform(-1, 1, 9), 3
+        plan = _plan(P, w, k, n, 1)
+        y = _host(plan.filter_coeffs(_dev(x)))
+        yr = ref.filter_coeffs(w, k, n, 1, x)
+        assert np.abs(y - yr).max() <= TOL_COEF * np.abs(yr).max()
+
+
+def _image_case(P, ref, img, w, k, pad, n, kc=None, coeffs=True):
+    import torch
+    h, wd = img.shape
+    plan = _plan(P, w, k, n, pad, kc)
+    d_img = _dev(img)
+    nb = ((wd + n - 1) // n) * ((h + n - 1) // n)
+    co = torch.empty((nb, n, n), dtype=torch.float64, device="cuda") if coeffs else None
+    out = _host(plan.filter_image(d_img, co))
+    return plan, d_img, out, (_host(co) if coeffs else None)
+
+
+@pytest.mark.parametrize("shape", [(33, 40), (8, 8), (16, 16), (9, 13), (64, 136), (200, 263),
+                                   (1, 1), (7, 300)])
+@pytest.mark.parametrize("pad", [0, 1])
+def test_fused_image_ragged_shapes(P, ref, shape, pad):
+    from paper_1710_07193_b200 import synth
+    h, w = shape
+    img = synth.uniform_image(h * 1000 + w, w, h)
+    for name in ("gaussian3", "magic3", "average3"):
+        wm, k = ref.mask_preset(name)
+        r_out, r_ci, r_co, r_pq = ref.filter_image(img, wm, k, pad, 8, side_outputs=True)
+        plan, d_img, out, co = _image_case(P, ref, img, wm, k, pad, 8)
+        mism, excused, _ = tie_report(out, r_out, blocks_to_image(r_pq, w, h))
+        assert mism == excused, (name, mism)
+        assert np.abs(co - r_co).max() <= TOL_COEF * max(1.0, np.abs(r_co).max())
+        ci = _host(plan.forward_image(d_img))
+        assert ci.tobytes() == r_ci.tobytes()  # forward kernel is bit-exact
+
+
+def test_golden_fixtures_gpu(P):
+    import hashlib
+    import json
+    import os
+    from golden.make_golden import synth_input
+    gd = os.path.join(os.path.dirname(__file__), "golden")
+    meta = json.load(open(os.path.join(gd, "manifest.json")))
+    data = np.load(os.path.join(gd, "golden.npz"))
+    exact = 0
+    for case in meta["cases"]:
+        inp = case["input"]
+        img = data[inp] if isinstance(inp, str) else synth_input(inp)
+        plan, d_img, out, co = _image_case(P, None, img, np.array(case["mask"]), case["k"],
+                                           case["padding"], case["n"])
+        if hashlib.sha256(out.tobytes()).hexdigest() == case["sha256_u8"]:
+            exact += 1
+        if case["stored"]:
+            ref_u8 = data[case["name"] + "_u8"]
+            assert np.count_nonzero(out != ref_u8) == 0, case["name"]
+            rc = data[case["name"] + "_coef_out"]
+            assert np.abs(co - rc).max() <= TOL_COEF * max(1.0, np.abs(rc).max()), case["name"]
+    assert exact == len(meta["cases"])
+
+
+def test_inverse_u8_and_nan(P, ref):
+    from paper_1710_07193_b200 import synth
+    img = synth.uniform_image(77, 48, 40)
+    wm, k = ref.mask_preset("gaussian3")
+    r_out, _, r_co, r_pq = ref.filter_image(img, wm, k, 1, 8, side_outputs=True)
+    plan = _plan(P, wm, k, 8, 1)
+    out = _host(plan.inverse_image_u8(_dev(r_co), 48, 40))
+    mism, excused, _ = tie_report(out, r_out, blocks_to_image(r_pq, 48, 40))
+    assert mism == excused
+    bad = r_co.copy()
+    bad[3, 2, 2] = np.nan
+    with pytest.raises(ValueError):
+        plan.inverse_image_u8(_dev(bad), 48, 40)
+
+
+def test_host_entry_matches_device(P, ref):
+    from paper_1710_07193_b200 import synth
+    img = synth.sinusoid_image(5, 1000, 777)
+    w = synth.gaussian_mask(5, 1.0)
+    for n in (8, 16):
+        plan = _plan(P, w, 5, n, 1)
+        a = plan.filter_image_host(img)
+        b = _host(plan.filter_image(_dev(img)))
+        assert np.array_equal(a, b)
+        assert np.array_equal(a, P.filter_image(img, P.Mask(5, w), P.PaddingMode.kReplicate, n=n))
+
+
+def test_errors(P, ref):
+    import torch
+    plan = _plan(P, np.ones(9) / 9, 3, 8, 0)
+    with pytest.raises(ValueError):
+        plan.filter_coeffs(torch.zeros((4, 16, 16), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        P.filter_image(np.zeros((8, 8), np.uint8), P.Mask(5, [0.04] * 25), P.PaddingMode.kZero, n=4)
+    with pytest.raises(ValueError):
+        P.FilterPlan(P.Mask(9, [1.0] * 81), 8, P.PaddingMode.kZero)
+
+
+def test_identity_and_constant_properties(P):
+    """Size-independent properties (image_test.cc:113-125, filter_test.cc:77-85)."""
+    import torch
+    from paper_1710_07193_b200 import synth
+    img = synth.uniform_image(3, 4096, 4096)
+    d = _dev(img)
+    for n in (8, 16):
+        ident = P.FilterPlan(P.Mask.identity(), n, P.PaddingMode.kReplicate)
+        assert torch.equal(ident.filter_image(d), d)
+        const = torch.full((2048, 2048), 77, dtype=torch.uint8, device="cuda")
+        avg = P.FilterPlan(P.Mask.average3(), n, P.PaddingMode.kReplicate)
+        assert bool((avg.filter_image(const) == 77).all())
