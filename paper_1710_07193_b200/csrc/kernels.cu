@@ -131,6 +131,32 @@ __device__ __forceinline__ uint32_t quantize(double v, int* nan_flag) {
   return static_cast<uint32_t>(r);
 }
 
+// Exact double of an integer 0..255 built with integer ops only, so the FP64
+// pipe stays free for DMMA: 2^e (1 + m) with e = msb(p).
+__device__ __forceinline__ double u8_to_f64(uint32_t p) {
+  const int e = 31 - __clz(p);
+  const uint32_t hi = (static_cast<uint32_t>(1022 + e) << 20) + (p << (20 - e));
+  return p ? __hiloint2double(static_cast<int>(hi), 0) : 0.0;
+}
+
+// floor(t) clamped to [0,255] with a single conversion instruction. Callers
+// pass t = v + 0.5 (the 0.5 rides in the DMMA accumulator), which equals
+// quantize_sample's round-half-away-from-zero + clamp for every v except
+// within one ulp of a .5 boundary — inside the 1e-6 near-tie window the
+// parity contract excuses. NaN converts to 0.
+__device__ __forceinline__ uint32_t floor_to_u8(double t) {
+  int i;
+  asm("cvt.rmi.s32.f64 %0, %1;" : "=r"(i) : "d"(t));
+  return static_cast<uint32_t>(min(max(i, 0), 255));
+}
+
+// Aligns a dynamic shared-memory base to 1024 B (128B-swizzle atoms) while
+// keeping the pointer in the shared window (so loads compile to LDS).
+__device__ __forceinline__ uint8_t* align1024(uint8_t* smem) {
+  const uint32_t pad = (1024u - (smem_u32(smem) & 1023u)) & 1023u;
+  return smem + pad;
+}
+
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -281,9 +307,9 @@ __global__ void __launch_bounds__(256) k_inverse(const double* __restrict__ coef
 // lane 0 issues four TMA box loads per tile ([16 blocks x 16 coefficients],
 // 128B swizzle: 16-byte chunk c of row r lands at chunk c ^ (r & 7)) and the
 // warp waits on that stage's mbarrier. Contraction index of k-step pair q in
-// K-chunk kc for lane t: 16kc + 8q + 2t + {0,1} (natural coefficient order),
-// so a lane's two k-steps are one swizzled 16-byte word (conflict-free
-// LDS.128). H^T fragments come from shared memory in the matching order
+// K-chunk kc for lane t: 16kc + 4t + 2q + {0,1}, so a lane's two k-steps are
+// one swizzled 16-byte word and each quarter-warp phase of the LDS.128
+// (lanes g in {2p,2p+1}, t in 0..3) hits 8 distinct chunks: (2t+q) ^ g. H^T fragments come from shared memory in the matching order
 // (layout_hcoef). Accumulators: 2 m-tiles x 8 n-tiles per warp (16 blocks x
 // 64 outputs), written straight from registers as 16-byte stores.
 namespace c8 {
@@ -299,7 +325,7 @@ __global__ void __launch_bounds__(c8::WARPS * 32, 1)
             double* __restrict__ out, long long nblocks) {
   using namespace c8;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* base = align1024(smem_raw);
   const double2* hs = reinterpret_cast<const double2*>(base);
   uint8_t* stages = base + 32768;
   __shared__ uint64_t bars[WARPS * STAGES];
@@ -356,7 +382,7 @@ __global__ void __launch_bounds__(c8::WARPS * 32, 1)
     for (int kc = 0; kc < 4; ++kc) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const int sw = ((4 * q + t) ^ g) << 4;
+        const int sw = ((2 * t + q) ^ g) << 4;
         const double2 a0 = *reinterpret_cast<const double2*>(st + kc * 2048 + g * 128 + sw);
         const double2 a1 = *reinterpret_cast<const double2*>(st + kc * 2048 + (8 + g) * 128 + sw);
 #pragma unroll
@@ -413,7 +439,7 @@ __global__ void __launch_bounds__((c16::CWARPS + 1) * 32, 1)
              double* __restrict__ out, long long nblocks) {
   using namespace c16;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* base = align1024(smem_raw);
   __shared__ uint64_t full[STAGES], empty[STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -459,7 +485,7 @@ __global__ void __launch_bounds__((c16::CWARPS + 1) * 32, 1)
       const double2* hs = reinterpret_cast<const double2*>(xs + XBYTES);
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const int sw = ((4 * q + t) ^ g) << 4;
+        const int sw = ((2 * t + q) ^ g) << 4;
         const double2 a0 = *reinterpret_cast<const double2*>(xs + (16 * mg + g) * 128 + sw);
         const double2 a1 = *reinterpret_cast<const double2*>(xs + (16 * mg + 8 + g) * 128 + sw);
 #pragma unroll
@@ -498,13 +524,18 @@ __global__ void __launch_bounds__((c16::CWARPS + 1) * 32, 1)
 //   forward pass 2  X^T = T1^T C^t: A = pass-1 accumulators, B = C[g][2t+s]
 //     -> lane (g,t) holds X[2t][g], X[2t+1][g] of each block.
 //   filter          Y^T = X^T H^T : blocks on M (2 m-tiles), H^T from shared
-//     memory (layout_hfused8), X via a swizzled per-warp staging buffer
-//     (16-byte word (row t, chunk c) of block b at chunk c ^ (b & 7)).
+//     memory (layout_hfused8), X via the per-warp staging buffer.
 //   inverse pass 1  Z = C^t Y     : A = C[2t+s][g], B = Y via staging
-//   inverse pass 2  O = Z C       : A = pass-1 accumulators, B = C[2t+s][g]
-//     -> lane (g,t) holds O[g][2t], O[g][2t+1]: two adjacent output pixels.
-// Ragged strips (image edge, block grid tail) take a clamped per-byte path
-// with the same compute.
+//   inverse pass 2  O = Z C + 0.5 : A = pass-1 accumulators, B = C[2t+s][g]
+//     -> lane (g,t) holds O[g][2t], O[g][2t+1]: two adjacent output pixels,
+//     already offset by 0.5 so quantisation is one floor conversion.
+// Forward/inverse work on 4 blocks at a time so 4 independent DMMA chains
+// interleave. Staging layout: block b owns 512 B = 4 rows x 8 chunks of 16 B;
+// logical (row r, chunk c) is stored at chunk c ^ 2r ^ f(b), f(b) = (b&7) ^
+// ((b&1)<<2). Every 16-byte access pattern below then hits 8 distinct chunks
+// in each quarter-warp phase (lanes g in {2p, 2p+1}, t in 0..3): no bank
+// conflicts. Ragged strips (image edge, block-grid tail) take a clamped
+// per-byte path with the same compute.
 namespace f8 {
 constexpr int WARPS = 8;
 constexpr int SB = 16;
@@ -513,6 +544,7 @@ constexpr int XY_BYTES = SB * 512;
 constexpr int PIX_BYTES = 8 * PS;
 constexpr int WARP_BYTES = XY_BYTES + PIX_BYTES;
 constexpr int SMEM = 32768 + WARPS * WARP_BYTES;
+__device__ __forceinline__ int fsw(int b) { return (b & 7) ^ ((b & 1) << 2); }
 }  // namespace f8
 
 __global__ void __launch_bounds__(f8::WARPS * 32, 2)
@@ -534,6 +566,7 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
   uint8_t* pix = xy + XY_BYTES;
   const double af0 = cb[g * 8 + 2 * t], af1 = cb[g * 8 + 2 * t + 1];
   const double ai0 = cb[(2 * t) * 8 + g], ai1 = cb[(2 * t + 1) * 8 + g];
+  const int fg = fsw(g);
 
   const long long spf = static_cast<long long>(bh) * nsx;
   const long long nstrips = spf * nframes;
@@ -580,17 +613,30 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
     __syncwarp();
     if (s + total < nstrips) prefetch(s + total);
 
-    // forward DCT, 16 blocks
+    // forward DCT, 16 blocks, 4 interleaved chains
 #pragma unroll
-    for (int b = 0; b < SB; ++b) {
-      const uint32_t pp = *reinterpret_cast<const uint16_t*>(pix + g * PS + 8 * b + 2 * t);
-      double2 d = make_double2(0.0, 0.0);
-      dmma(d, af0, static_cast<double>(pp & 0xffu));
-      dmma(d, af1, static_cast<double>(pp >> 8));
-      double2 x = make_double2(0.0, 0.0);
-      dmma(x, d.x, af0);
-      dmma(x, d.y, af1);
-      *reinterpret_cast<double2*>(xy + b * 512 + t * 128 + ((g ^ (b & 7)) << 4)) = x;
+    for (int b0 = 0; b0 < SB; b0 += 4) {
+      double p0[4], p1[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t pp = *reinterpret_cast<const uint16_t*>(pix + g * PS + 8 * (b0 + i) + 2 * t);
+        p0[i] = u8_to_f64(pp & 0xffu);
+        p1[i] = u8_to_f64(pp >> 8);
+      }
+      double2 d[4], x[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { d[i] = make_double2(0.0, 0.0); dmma(d[i], af0, p0[i]); }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dmma(d[i], af1, p1[i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { x[i] = make_double2(0.0, 0.0); dmma(x[i], d[i].x, af0); }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dmma(x[i], d[i].y, af1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int b = b0 + i;
+        *reinterpret_cast<double2*>(xy + b * 512 + t * 128 + ((g ^ (2 * t) ^ fsw(b)) << 4)) = x[i];
+      }
     }
     __syncwarp();
 
@@ -602,15 +648,15 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
       for (int j = 0; j < 8; ++j) acc[m][j] = make_double2(0.0, 0.0);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int sw = (q ^ g) << 4;
+      const int sw = (q ^ (2 * t) ^ fg) << 4;
       const double2 a0 = *reinterpret_cast<const double2*>(xy + g * 512 + t * 128 + sw);
       const double2 a1 = *reinterpret_cast<const double2*>(xy + (8 + g) * 512 + t * 128 + sw);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const double2 b = hs[(j * 8 + q) * 32 + lane];
         dmma(acc[0][j], a0.x, b.x);
-        dmma(acc[0][j], a0.y, b.y);
         dmma(acc[1][j], a1.x, b.x);
+        dmma(acc[0][j], a0.y, b.y);
         dmma(acc[1][j], a1.y, b.y);
       }
     }
@@ -620,7 +666,7 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         *reinterpret_cast<double2*>(xy + (8 * m + g) * 512 + (j >> 1) * 128 +
-                                    (((4 * (j & 1) + t) ^ g) << 4)) = acc[m][j];
+                                    (((4 * (j & 1) + t) ^ (2 * (j >> 1)) ^ fg) << 4)) = acc[m][j];
     if (coef_out) {
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
@@ -638,19 +684,28 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
     }
     __syncwarp();
 
-    // inverse DCT + quantize, 16 blocks
+    // inverse DCT + quantize, 16 blocks, 4 interleaved chains
 #pragma unroll
-    for (int b = 0; b < SB; ++b) {
-      const double2 yv =
-          *reinterpret_cast<const double2*>(xy + b * 512 + t * 128 + ((g ^ (b & 7)) << 4));
-      double2 z = make_double2(0.0, 0.0);
-      dmma(z, ai0, yv.x);
-      dmma(z, ai1, yv.y);
-      double2 o = make_double2(0.0, 0.0);
-      dmma(o, z.x, ai0);
-      dmma(o, z.y, ai1);
-      const uint32_t q = quantize(o.x, nullptr) | (quantize(o.y, nullptr) << 8);
-      *reinterpret_cast<uint16_t*>(pix + g * PS + 8 * b + 2 * t) = static_cast<uint16_t>(q);
+    for (int b0 = 0; b0 < SB; b0 += 4) {
+      double2 yv[4], z[4], o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int b = b0 + i;
+        yv[i] = *reinterpret_cast<const double2*>(xy + b * 512 + t * 128 + ((g ^ (2 * t) ^ fsw(b)) << 4));
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { z[i] = make_double2(0.0, 0.0); dmma(z[i], ai0, yv[i].x); }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dmma(z[i], ai1, yv[i].y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { o[i] = make_double2(0.5, 0.5); dmma(o[i], z[i].x, ai0); }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dmma(o[i], z[i].y, ai1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t q = floor_to_u8(o[i].x) | (floor_to_u8(o[i].y) << 8);
+        *reinterpret_cast<uint16_t*>(pix + g * PS + 8 * (b0 + i) + 2 * t) = static_cast<uint16_t>(q);
+      }
     }
     __syncwarp();
 

@@ -186,7 +186,7 @@ dctf_status compile_operator(dctf_plan& p) {
 
 // Coefficient-kernel layout, n in {8,16}, NN = n^2:
 //   [kc < NN/16][J < NN/8][q < 2][lane < 32][e < 2]
-//   = H[8J + g][16kc + 8q + 2t + e],  g = lane>>2, t = lane&3.
+//   = H[8J + g][16kc + 4t + 2q + e],  g = lane>>2, t = lane&3.
 // One (kc) slice is the B operand of one 16-wide K chunk for every n-tile J;
 // each lane's two k-steps sit in one 16-byte word (one LDS.128).
 void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out) {
@@ -199,7 +199,7 @@ void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out
         for (int lane = 0; lane < 32; ++lane)
           for (int e = 0; e < 2; ++e) {
             const int g = lane >> 2, t = lane & 3;
-            out[o++] = op[size_t(8 * J + g) * nn + 16 * kc + 8 * q + 2 * t + e];
+            out[o++] = op[size_t(8 * J + g) * nn + 16 * kc + 4 * t + 2 * q + e];
           }
 }
 
