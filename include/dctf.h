@@ -134,6 +134,17 @@ dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
 dctf_status dctf_filter_image_host(const dctf_plan* plan, const uint8_t* h_in, uint8_t* h_out,
                                    int width, int height, size_t pitch);
 
+/* Host-buffer batch variants (synchronous): copy nblocks blocks in, run the
+ * device kernel, copy out. For callers without device memory management —
+ * the C++ drop-in layer (include/dctfilter_b200.hpp) builds the reference's
+ * per-block functions on these. */
+dctf_status dctf_forward_blocks_host(const dctf_plan* plan, const double* h_blocks,
+                                     double* h_coeffs, size_t nblocks);
+dctf_status dctf_inverse_blocks_host(const dctf_plan* plan, const double* h_coeffs,
+                                     double* h_blocks, size_t nblocks);
+dctf_status dctf_filter_coeffs_host(const dctf_plan* plan, const double* h_in, double* h_out,
+                                    size_t nblocks);
+
 /* Synchronises `stream`, reads and clears the plan's NaN flag; *nan_seen is
  * 1 if any quantised sample was NaN since the last check. */
 dctf_status dctf_plan_nan_check(const dctf_plan* plan, void* stream, int* nan_seen);

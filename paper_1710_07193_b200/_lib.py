@@ -47,6 +47,9 @@ _SIGS = {
                                     C.c_int, C.c_size_t, C.c_size_t, _vp]),
     "dctf_filter_image_host": (_st, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_size_t]),
     "dctf_plan_nan_check": (_st, [_vp, _vp, _i]),
+    "dctf_forward_blocks_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
+    "dctf_inverse_blocks_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
+    "dctf_filter_coeffs_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
     "dctf_measure_fp64_peak": (_st, [C.c_int, C.c_int, _d]),
     "dctf_last_launch_count": (C.c_int, []),
     "dctf_last_error_message": (C.c_char_p, []),

@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(c8::WARPS * 32, 1)
       }
     }
     __syncwarp();
+    __threadfence_block();  // drain in-flight LDS of this stage before TMA reuses it
     if (lane == 0) {
       const long long nt = tile + STAGES * total;
       if (nt < ntiles) {
@@ -497,7 +498,11 @@ __global__ void __launch_bounds__((c16::CWARPS + 1) * 32, 1)
           dmma(acc[1][j], a1.y, b.y);
         }
       }
+      // Release the stage only after this warp's shared loads have landed:
+      // SYNCS.ARRIVE does not wait for in-flight LDS (observed: the producer's
+      // bulk copy overwrote n-tile 7's fragment), MEMBAR.CTA drains them.
       __syncwarp();
+      __threadfence_block();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
 #pragma unroll
@@ -1262,6 +1267,52 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   CUDA_TRY(cudaMemcpy(&nan_seen, p->d_nan, sizeof(int), cudaMemcpyDeviceToHost));
   if (nan_seen) return set_error(DCTF_NAN_ENCOUNTERED, "quantize: NaN sample");
   return DCTF_OK;
+}
+
+// Host-buffer batch wrappers: stream-ordered scratch, synchronous.
+static dctf_status run_host_blocks(const dctf_plan* p, const double* h_in, double* h_out,
+                                   size_t nblocks, int op) {
+  dctf_status s = check_plan(p);
+  if (s != DCTF_OK) return s;
+  if (nblocks == 0) return DCTF_OK;
+  if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  const size_t bytes = nblocks * static_cast<size_t>(p->n) * p->n * sizeof(double);
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double *din = nullptr, *dout = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&din), bytes, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dout), bytes, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(din, h_in, bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) s = set_error(DCTF_CUDA_ERROR, cudaGetErrorString(e));
+  if (s == DCTF_OK) {
+    if (op == 0) s = dctf_forward_blocks(p, din, dout, nblocks, st);
+    else if (op == 1) s = dctf_inverse_blocks(p, din, dout, nblocks, st);
+    else s = dctf_filter_coeffs(p, din, dout, nblocks, st);
+  }
+  if (s == DCTF_OK) {
+    e = cudaMemcpyAsync(h_out, dout, bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) s = set_error(DCTF_CUDA_ERROR, cudaGetErrorString(e));
+  }
+  cudaFreeAsync(din, st);
+  cudaFreeAsync(dout, st);
+  e = cudaStreamSynchronize(st);
+  if (s == DCTF_OK && e != cudaSuccess) s = set_error(DCTF_CUDA_ERROR, cudaGetErrorString(e));
+  cudaStreamDestroy(st);
+  return s;
+}
+
+dctf_status dctf_forward_blocks_host(const dctf_plan* p, const double* h_in, double* h_out,
+                                     size_t nblocks) {
+  return run_host_blocks(p, h_in, h_out, nblocks, 0);
+}
+dctf_status dctf_inverse_blocks_host(const dctf_plan* p, const double* h_in, double* h_out,
+                                     size_t nblocks) {
+  return run_host_blocks(p, h_in, h_out, nblocks, 1);
+}
+dctf_status dctf_filter_coeffs_host(const dctf_plan* p, const double* h_in, double* h_out,
+                                    size_t nblocks) {
+  return run_host_blocks(p, h_in, h_out, nblocks, 2);
 }
 
 dctf_status dctf_measure_fp64_peak(int device, int mode, double* tflops) {

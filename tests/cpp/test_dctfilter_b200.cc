@@ -1,0 +1,107 @@
+// C++ drop-in layer (include/dctfilter_b200.hpp) exercised the way the
+// reference's own GTest suites exercise dctfilter (filter_test.cc,
+// image_test.cc, dct_test.cc), on the GPU. Built by `make cpp-test`, run by
+// tests/test_gpu_cpp.py. Prints one line per check, exits non-zero on failure.
+#include <cstdio>
+#include <random>
+
+#include "dctfilter_b200.hpp"
+
+using namespace dctfilter_b200;
+
+static int failures = 0;
+#define CHECK(cond, what)                                         \
+  do {                                                            \
+    const bool ok_ = (cond);                                      \
+    std::printf("[%s] %s\n", ok_ ? "PASS" : "FAIL", what);        \
+    if (!ok_) ++failures;                                         \
+  } while (0)
+
+static BlockMatrix random_u8_block(std::mt19937_64& rng, int n) {
+  std::uniform_int_distribution<int> d(0, 255);
+  BlockMatrix m(n);
+  for (double& v : m.data()) v = double(d(rng));
+  return m;
+}
+
+int main() {
+  std::mt19937_64 rng(3);
+  // dct_test.cc: orthonormal basis, constant block -> DC = 8
+  {
+    const DctBasis basis(8);
+    double orth = 0;
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) {
+        double s = 0;
+        for (int k = 0; k < 8; ++k) s += basis.c()(i, k) * basis.c()(j, k);
+        orth = std::max(orth, std::abs(s - (i == j)));
+      }
+    CHECK(orth < 1e-12, "DctBasis(8) orthonormal");
+    BlockMatrix ones(8);
+    for (double& v : ones.data()) v = 1.0;
+    const BlockMatrix x = forward_2d(basis, ones);
+    CHECK(std::abs(x(0, 0) - 8.0) < 1e-12, "constant block -> DC 8");
+    CHECK(max_abs_diff(inverse_2d(basis, x), ones) < 1e-12, "round trip");
+  }
+  // filter_test.cc: identity plan keeps coefficients; constant block scaling
+  {
+    const FilterPlan plan(Mask::identity(), 8, PaddingMode::kReplicate);
+    std::uniform_real_distribution<double> u(-100, 100);
+    BlockMatrix c(8);
+    for (double& v : c.data()) v = u(rng);
+    CHECK(max_abs_diff(plan.filter_coeffs(c), c) < 1e-12, "identity plan keeps coefficients");
+    const BlockMatrix b = random_u8_block(rng, 8);
+    CHECK(max_abs_diff(plan.filter_block(b), b) < 1e-10, "identity plan keeps blocks");
+  }
+  {
+    const FilterPlan g(Mask::gaussian3(), 8, PaddingMode::kZero);
+    const FilterPlan m(Mask::magic3(), 8, PaddingMode::kZero);
+    CHECK(g.symmetric_merged() && g.npairs() == 2, "gaussian3 compiles merged to 2 pairs");
+    CHECK(!m.symmetric_merged() && m.npairs() == 3, "magic3 compiles to 3 pairs");
+  }
+  {
+    std::uniform_real_distribution<double> u(-1, 1);
+    std::vector<double> w(9);
+    double sum = 0;
+    for (double& v : w) sum += (v = u(rng));
+    const FilterPlan plan(Mask(3, w), 8, PaddingMode::kReplicate);
+    BlockMatrix blk(8);
+    for (double& v : blk.data()) v = 100.0;
+    const BlockMatrix f = plan.filter_coeffs(forward_2d(plan.basis(), blk));
+    bool ac = true;
+    for (int i = 0; i < 64; ++i) ac = ac && (i == 0 || std::abs(f.data()[i]) < 1e-9);
+    CHECK(std::abs(f(0, 0) - 8.0 * sum * 100.0) < 1e-9 && ac, "constant block scales DC by weight sum");
+  }
+  // batched filter_block over many blocks == per-block
+  {
+    const FilterPlan plan(Mask::magic3(), 16, PaddingMode::kReplicate);
+    std::vector<BlockMatrix> blocks;
+    for (int i = 0; i < 300; ++i) blocks.push_back(random_u8_block(rng, 16));
+    const auto out = plan.filter_block(blocks);
+    CHECK(max_abs_diff(out[17], plan.filter_block(blocks[17])) == 0.0, "batched == single (n=16)");
+  }
+  // errors
+  {
+    bool t1 = false, t2 = false, t3 = false;
+    try { Mask(2, {1, 2, 3, 4}); } catch (const std::invalid_argument&) { t1 = true; }
+    try { FilterPlan(Mask(9, std::vector<double>(81, 1.0)), 8, PaddingMode::kZero); } catch (const std::invalid_argument&) { t2 = true; }
+    const FilterPlan plan(Mask::average3(), 8, PaddingMode::kZero);
+    try { plan.filter_coeffs(BlockMatrix(4)); } catch (const std::invalid_argument&) { t3 = true; }
+    CHECK(t1 && t2 && t3, "invalid_argument on bad mask / oversized mask / block side mismatch");
+  }
+  // image_test.cc: identity mask, constant image under averaging
+  {
+    GrayImage img{24, 17, std::vector<std::uint8_t>(24 * 17)};
+    for (auto& s : img.samples) s = std::uint8_t(rng() & 255);
+    CHECK(filter_image(img, Mask::identity(), PaddingMode::kReplicate).samples == img.samples,
+          "identity mask reproduces the image");
+    GrayImage c{20, 12, std::vector<std::uint8_t>(240, 77)};
+    const GrayImage o = filter_image(c, Mask::average3(), PaddingMode::kReplicate, Domain::kDct, 16);
+    bool all = true;
+    for (auto s : o.samples) all = all && s == 77;
+    CHECK(all, "constant image stays constant under averaging (n=16)");
+  }
+  CHECK(quantize_sample(127.5) == 128 && quantize_sample(0.5) == 1 && quantize_sample(-3) == 0, "quantize KATs");
+  std::printf("%s\n", failures ? "FAILED" : "ALL PASSED");
+  return failures ? 1 : 0;
+}

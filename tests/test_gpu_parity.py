@@ -74,7 +74,7 @@ def test_forward_inverse_blocks_bitexact(P, ref, n):
 
 
 @pytest.mark.parametrize("n", [8, 16])
-@pytest.mark.parametrize("nblocks", [1, 15, 16, 17, 64, 1000, 4099])
+@pytest.mark.parametrize("nblocks", [1, 15, 16, 17, 64, 1000, 4099, 28423, 262144])
 def test_filter_coeffs_tolerance(P, ref, n, nblocks):
     rng = np.random.default_rng(nblocks + n)
     x = ref.forward_blocks(rng.integers(0, 256, (nblocks, n, n)).astype(np.float64))
