@@ -31,7 +31,8 @@ struct dctf_plan {
   mutable void* io_in = nullptr;
   mutable void* io_out = nullptr;
   mutable size_t io_bytes = 0;
-  mutable void* streams[2] = {nullptr, nullptr};
+  mutable void* streams[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
+  mutable void* events[64] = {};                              // per-chunk ordering
 };
 
 namespace dctf {
