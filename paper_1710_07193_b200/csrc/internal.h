@@ -50,5 +50,6 @@ dctf_status compile_operator(dctf_plan& p);
 // Fragment-order permutations of H for the kernels (plan.cc).
 void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out);
 void layout_hfused8(const std::vector<double>& op, std::vector<double>& out);
+void layout_hfused16(const std::vector<double>& op, std::vector<double>& out);
 
 }  // namespace dctf

@@ -421,11 +421,11 @@ __global__ void __launch_bounds__(c8::WARPS * 32, 1)
 // k_coef16: Y^T (blocks x 256) = X^T (blocks x 256) * H^T, FP64 DMMA.
 //
 // CTA tile: 64 blocks x 256 outputs; K = 256 streamed in 16 chunks of 16.
-// Warp 16 is the producer: per chunk one TMA box [64 blocks x 16 coeffs]
-// (8 KB, 128B swizzle) plus one 32 KB bulk copy of the H^T chunk (fragment
-// order, layout_hcoef), into a 3-stage ring (full/empty mbarriers).
-// Warps 0..15 consume: warp w covers blocks 16(w&3)..+16 (2 m-tiles) and
-// outputs 64(w>>2)..+64 (8 n-tiles).
+// Per chunk one TMA box [64 blocks x 16 coeffs] (8 KB, 128B swizzle) plus one
+// 32 KB bulk copy of the H^T chunk (fragment order, layout_hcoef) land in a
+// 3-stage ring (full/empty mbarriers); lane 0 of warp 0 refills a stage as
+// soon as all 16 warps released it. Warp w covers blocks 16(w&3)..+16
+// (2 m-tiles) and outputs 64(w>>2)..+64 (8 n-tiles).
 namespace c16 {
 constexpr int CWARPS = 16;
 constexpr int STAGES = 3;
@@ -436,7 +436,7 @@ constexpr int STAGE_BYTES = XBYTES + HBYTES;
 constexpr int SMEM = 1024 + STAGES * STAGE_BYTES;
 }  // namespace c16
 
-__global__ void __launch_bounds__((c16::CWARPS + 1) * 32, 1)
+__global__ void __launch_bounds__(c16::CWARPS * 32, 1)
     k_coef16(const __grid_constant__ CUtensorMap xmap, const double* __restrict__ hc,
              double* __restrict__ out, long long nblocks) {
   using namespace c16;
@@ -454,23 +454,19 @@ __global__ void __launch_bounds__((c16::CWARPS + 1) * 32, 1)
   }
   __syncthreads();
   const long long ntiles = (nblocks + TILE - 1) / TILE;
-
-  if (warp == CWARPS) {
-    if (lane == 0) {
-      long long it = 0;
-      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int kc = 0; kc < 16; ++kc, ++it) {
-          const int s = static_cast<int>(it % STAGES);
-          if (it >= STAGES) mbar_wait(&empty[s], static_cast<uint32_t>(((it / STAGES) - 1) & 1));
-          uint8_t* dst = base + s * STAGE_BYTES;
-          mbar_expect_tx(&full[s], STAGE_BYTES);
-          tma_load_2d(dst, &xmap, &full[s], kc * 16, static_cast<int>(tile * TILE));
-          bulk_load(dst + XBYTES, hc + static_cast<size_t>(kc) * (HBYTES / 8), HBYTES, &full[s]);
-        }
-      }
-    }
-    return;
-  }
+  // chunk c of this CTA: tile blockIdx.x + (c / 16) * gridDim.x, K-chunk c % 16
+  const long long nchunks = ntiles > blockIdx.x ? ((ntiles - 1 - blockIdx.x) / gridDim.x + 1) * 16 : 0;
+  auto refill = [&](long long c) {
+    const int s = static_cast<int>(c % STAGES);
+    const int kc = static_cast<int>(c % 16);
+    const long long tile = blockIdx.x + (c / 16) * gridDim.x;
+    uint8_t* dst = base + s * STAGE_BYTES;
+    mbar_expect_tx(&full[s], STAGE_BYTES);
+    tma_load_2d(dst, &xmap, &full[s], kc * 16, static_cast<int>(tile * TILE));
+    bulk_load(dst + XBYTES, hc + static_cast<size_t>(kc) * (HBYTES / 8), HBYTES, &full[s]);
+  };
+  if (warp == 0 && lane == 0)
+    for (long long c = 0; c < STAGES && c < nchunks; ++c) refill(c);
 
   const int g = lane >> 2, t = lane & 3, mg = warp & 3, ng = warp >> 2;
   long long it = 0;
@@ -494,17 +490,22 @@ __global__ void __launch_bounds__((c16::CWARPS + 1) * 32, 1)
         for (int j = 0; j < 8; ++j) {
           const double2 b = hs[((8 * ng + j) * 2 + q) * 32 + lane];
           dmma(acc[0][j], a0.x, b.x);
-          dmma(acc[0][j], a0.y, b.y);
           dmma(acc[1][j], a1.x, b.x);
+          dmma(acc[0][j], a0.y, b.y);
           dmma(acc[1][j], a1.y, b.y);
         }
       }
       // Release the stage only after this warp's shared loads have landed:
-      // SYNCS.ARRIVE does not wait for in-flight LDS (observed: the producer's
-      // bulk copy overwrote n-tile 7's fragment), MEMBAR.CTA drains them.
+      // SYNCS.ARRIVE does not wait for in-flight LDS (observed: the refill
+      // overwrote n-tile 7's fragment), MEMBAR.CTA drains them.
       __syncwarp();
       __threadfence_block();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (warp == 0 && lane == 0 && it + STAGES < nchunks) {
+        mbar_wait(&empty[s], static_cast<uint32_t>((it / STAGES) & 1));
+        refill(it + STAGES);
+      }
+      __syncwarp();
     }
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
@@ -732,6 +733,308 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
 }
 
 // ---------------------------------------------------------------------------
+// k_fused16: the n = 16 chain fused, one HBM pass per pixel.
+//
+// CTA tile = a strip of 64 horizontally adjacent 16x16 blocks (16 rows x 1024
+// px). 16 warps; lane 0 of warp 0 also streams the operator. Phases per tile
+// (CTA barrier between them):
+//   pixels -> shared (16-byte loads, prefetched one tile ahead into registers)
+//   forward DCT, 4 blocks per warp, 32 DMMA/block:
+//     T1^T = C P^T (A = C rows in registers, B = pixel pairs), X^T = T1^T C^t
+//   filter Y^T = X^T H^T: warp (mg = w&3, ng = w>>2) owns 16 blocks x 64
+//     outputs; K = 256 streamed as 16 chunks of H^T fragments (32 KB each,
+//     cp.async.bulk into a 2-stage ring, refilled as soon as a stage is
+//     released by all warps); X stays in
+//     shared memory (128 KB)
+//   Y -> shared (over X), inverse DCT (O = C^t Y C + 0.5) -> u8 -> strip store.
+// Block staging layout: 2 KB per block = 128 words of 16 B; word w holds the
+// coefficient pair (u = 2a + {0,1}, v) with v = w >> 3, a = (w & 7) ^ 4(v & 1),
+// stored at chunk (w & 7) ^ f(b) of its 128-byte row. The k-mapping of every
+// DMMA stage (k(s,t) = 8(s>>1) + 2t + (s&1)) makes each lane's pair one word
+// and each quarter-warp phase of every 16-byte access conflict-free.
+namespace f16 {
+constexpr int CWARPS = 16;  // all warps run MMA; warp 0 lane 0 also streams H
+constexpr int TILE = 64;
+constexpr int STAGES = 2;
+constexpr int HBYTES = 32768;
+constexpr int XY_BYTES = TILE * 2048;
+constexpr int PS = 1040;
+constexpr int PIX_BYTES = 16 * PS;
+constexpr int SMEM = 1024 + XY_BYTES + STAGES * HBYTES + PIX_BYTES;
+__device__ __forceinline__ int fsw(int b) { return (b & 7) ^ ((b & 1) << 2); }
+__device__ __forceinline__ int xw(int b, int w) {
+  return b * 2048 + ((w & ~7) << 4) + (((w & 7) ^ fsw(b)) << 4);
+}
+__device__ __forceinline__ void bar_mma() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
+}  // namespace f16
+
+__global__ void __launch_bounds__(f16::CWARPS * 32, 1)
+    k_fused16(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
+              long long frame_stride, int nframes, int bw, int bh, int nsx,
+              const double* __restrict__ hf, const double* __restrict__ cb,
+              double* __restrict__ coef_out) {
+  using namespace f16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = align1024(smem_raw);
+  uint8_t* xy = base;
+  uint8_t* hst = base + XY_BYTES;
+  uint8_t* pix = hst + STAGES * HBYTES;
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CWARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const long long spf = static_cast<long long>(bh) * nsx;
+  const long long ntiles = spf * nframes;
+
+  // H^T chunk stream: the same 16 K-chunks for every tile. Lane 0 of warp 0
+  // refills a stage as soon as all 16 warps have released it (no producer
+  // warp: 16 warps keep 4 per SM sub-partition and 128 registers each).
+  const long long nchunks = ntiles > blockIdx.x ? ((ntiles - 1 - blockIdx.x) / gridDim.x + 1) * 16 : 0;
+  auto refill = [&](long long chunk) {
+    const int s = static_cast<int>(chunk % STAGES);
+    mbar_expect_tx(&full[s], HBYTES);
+    bulk_load(hst + s * HBYTES, hf + static_cast<size_t>(chunk % 16) * (HBYTES / 8), HBYTES, &full[s]);
+  };
+  if (warp == 0 && lane == 0)
+    for (long long c = 0; c < STAGES && c < nchunks; ++c) refill(c);
+
+  const int g = lane >> 2, t = lane & 3, mg = warp & 3, ng = warp >> 2;
+  const int tid = threadIdx.x;  // 0..511
+  const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
+  auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {
+    f = static_cast<int>(ti / spf);
+    const long long rem = ti - static_cast<long long>(f) * spf;
+    by = static_cast<int>(rem / nsx);
+    bx0 = static_cast<int>(rem - static_cast<long long>(by) * nsx) * TILE;
+  };
+  auto is_fast = [&](int by, int bx0) { return aligned && by * 16 + 16 <= h && bx0 * 16 + 1024 <= w; };
+  // thread tid moves 16-byte chunks (row tid>>6, col 16*(tid&63)) and (row+8)
+  const int prow = tid >> 6, pcol = (tid & 63) * 16;
+  uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
+  auto prefetch = [&](long long ti) {
+    int f, by, bx0;
+    tile_at(ti, f, by, bx0);
+    if (is_fast(by, bx0)) {
+      const uint8_t* p = in + f * frame_stride + static_cast<size_t>(by * 16) * pitch + bx0 * 16 + pcol;
+      pf0 = ldg_stream(p + prow * pitch);
+      pf1 = ldg_stream(p + (prow + 8) * pitch);
+    }
+  };
+  long long tile = blockIdx.x;
+  if (tile < ntiles) prefetch(tile);
+  long long it = 0;
+  for (; tile < ntiles; tile += gridDim.x) {
+    int f, by, bx0;
+    tile_at(tile, f, by, bx0);
+    const bool fast = is_fast(by, bx0);
+    if (fast) {
+      *reinterpret_cast<uint4*>(pix + prow * PS + pcol) = pf0;
+      *reinterpret_cast<uint4*>(pix + (prow + 8) * PS + pcol) = pf1;
+    } else {
+      const uint8_t* ib = in + f * frame_stride;
+      for (int e = tid; e < 16 * 1024; e += 512) {
+        const int r = e >> 10, c = e & 1023;
+        const int y = min(by * 16 + r, h - 1), x = min(bx0 * 16 + c, w - 1);
+        pix[r * PS + c] = ib[static_cast<size_t>(y) * pitch + x];
+      }
+    }
+    if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
+    bar_mma();
+
+    // ---- forward DCT: blocks 4*warp .. +3
+    {
+      double cf[2][4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) cf[x][s] = cb[(8 * x + g) * 16 + 8 * (s >> 1) + 2 * t + (s & 1)];
+#pragma unroll 1
+      for (int bb = 0; bb < 4; ++bb) {
+        const int b = 4 * warp + bb;
+        double p[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const uint32_t pp = *reinterpret_cast<const uint16_t*>(pix + (8 * nt + g) * PS + b * 16 + 8 * a + 2 * t);
+            p[nt][2 * a] = u8_to_f64(pp & 0xffu);
+            p[nt][2 * a + 1] = u8_to_f64(pp >> 8);
+          }
+        double2 d[2][2], x[2][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) d[mt][nt] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) dmma(d[mt][nt], cf[mt][s], p[nt][s]);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) x[mt][nt] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const double a = (s & 1) ? d[mt][s >> 1].y : d[mt][s >> 1].x;
+              dmma(x[mt][nt], a, cf[nt][s]);
+            }
+        // x[mt][nt] = X[u = 8nt + 2t + {0,1}][v = 8mt + g] -> word 8v + (a ^ 4(v&1)), a = 4nt + t
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int v = 8 * mt + g;
+            *reinterpret_cast<double2*>(xy + xw(b, 8 * v + ((4 * nt + t) ^ (4 * (v & 1))))) = x[mt][nt];
+          }
+      }
+    }
+    bar_mma();
+
+    // ---- filter: 16 blocks x 64 outputs per warp, K streamed from the ring
+    double2 acc[2][8];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[m][j] = make_double2(0.0, 0.0);
+    const int b0 = 16 * mg + g, b1 = 16 * mg + 8 + g;
+    for (int kc = 0; kc < 16; ++kc, ++it) {
+      const int s = static_cast<int>(it % STAGES);
+      mbar_wait(&full[s], static_cast<uint32_t>((it / STAGES) & 1));
+      const double2* hs = reinterpret_cast<const double2*>(hst + s * HBYTES);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int wd = 8 * kc + 4 * q + t;
+        const double2 a0 = *reinterpret_cast<const double2*>(xy + xw(b0, wd));
+        const double2 a1 = *reinterpret_cast<const double2*>(xy + xw(b1, wd));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double2 bf = hs[((8 * ng + j) * 2 + q) * 32 + lane];
+          dmma(acc[0][j], a0.x, bf.x);
+          dmma(acc[1][j], a1.x, bf.x);
+          dmma(acc[0][j], a0.y, bf.y);
+          dmma(acc[1][j], a1.y, bf.y);
+        }
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (warp == 0 && lane == 0 && it + STAGES < nchunks) {
+        mbar_wait(&empty[s], static_cast<uint32_t>((it / STAGES) & 1));
+        refill(it + STAGES);
+      }
+      __syncwarp();
+    }
+    bar_mma();  // every warp is done reading X
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int b = m ? b1 : b0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<double2*>(xy + xw(b, 4 * (8 * ng + j) + t)) = acc[m][j];
+    }
+    if (coef_out) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int bx = bx0 + (m ? b1 : b0);
+        if (bx < bw) {
+          double* dst = coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 256;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int wd = 4 * (8 * ng + j) + t, v = wd >> 3, a = (wd & 7) ^ (4 * (v & 1));
+            dst[(2 * a) * 16 + v] = acc[m][j].x;
+            dst[(2 * a + 1) * 16 + v] = acc[m][j].y;
+          }
+        }
+      }
+    }
+    bar_mma();
+
+    // ---- inverse DCT + quantize: blocks 4*warp .. +3
+    {
+      double ci[2][4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) ci[x][s] = cb[(8 * (s >> 1) + 2 * t + (s & 1)) * 16 + 8 * x + g];
+#pragma unroll 1
+      for (int bb = 0; bb < 4; ++bb) {
+        const int b = 4 * warp + bb;
+        double2 yv[2][2];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const int v = 8 * nt + g;
+            yv[nt][a] = *reinterpret_cast<const double2*>(xy + xw(b, 8 * v + ((4 * a + t) ^ (4 * (v & 1)))));
+          }
+        double2 z[2][2], o[2][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) z[mt][nt] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const double bv = (s & 1) ? yv[nt][s >> 1].y : yv[nt][s >> 1].x;
+              dmma(z[mt][nt], ci[mt][s], bv);
+            }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) o[mt][nt] = make_double2(0.5, 0.5);
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const double a = (s & 1) ? z[mt][s >> 1].y : z[mt][s >> 1].x;
+              dmma(o[mt][nt], a, ci[nt][s]);
+            }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const uint32_t q = floor_to_u8(o[mt][nt].x) | (floor_to_u8(o[mt][nt].y) << 8);
+            *reinterpret_cast<uint16_t*>(pix + (8 * mt + g) * PS + b * 16 + 8 * nt + 2 * t) =
+                static_cast<uint16_t>(q);
+          }
+      }
+    }
+    bar_mma();
+    uint8_t* ob = out + f * frame_stride;
+    if (fast) {
+      uint8_t* p = ob + static_cast<size_t>(by * 16) * pitch + bx0 * 16 + pcol;
+      stg_stream(p + prow * pitch, *reinterpret_cast<const uint4*>(pix + prow * PS + pcol));
+      stg_stream(p + (prow + 8) * pitch, *reinterpret_cast<const uint4*>(pix + (prow + 8) * PS + pcol));
+    } else {
+      for (int e = tid; e < 16 * 1024; e += 512) {
+        const int r = e >> 10, c = e & 1023;
+        const int y = by * 16 + r, x = bx0 * 16 + c;
+        if (y < h && x < w) ob[static_cast<size_t>(y) * pitch + x] = pix[r * PS + c];
+      }
+    }
+    bar_mma();  // pixel buffer is rewritten by the next tile
+  }
+}
+
+// ---------------------------------------------------------------------------
 // FP64 peak microbenchmarks (diagnostics; roofline denominator).
 __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
   double2 acc[8];
@@ -868,7 +1171,7 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
     }
     const long long ntiles = (nb + c16::TILE - 1) / c16::TILE;
     const long long ctas = std::min<long long>(sms, ntiles);
-    k_coef16<<<static_cast<unsigned>(ctas), (c16::CWARPS + 1) * 32, c16::SMEM, st>>>(map, p->d_hcoef,
+    k_coef16<<<static_cast<unsigned>(ctas), c16::CWARPS * 32, c16::SMEM, st>>>(map, p->d_hcoef,
                                                                                    d_out, nb);
   }
   dctf::add_launches(1);
@@ -926,12 +1229,33 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
   return DCTF_OK;
 }
 
+dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
+                           size_t pitch, long long frame_stride, int nframes, double* coef_out,
+                           cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_fused16, cudaFuncAttributeMaxDynamicSharedMemorySize, f16::SMEM));
+    attr = true;
+  }
+  const int bw = (w + 15) / 16, bh = (h + 15) / 16, nsx = (bw + f16::TILE - 1) / f16::TILE;
+  const long long ntiles = static_cast<long long>(bh) * nsx * nframes;
+  const long long ctas = std::min<long long>(sm_count(p->device), ntiles);
+  if (ctas <= 0) return DCTF_OK;
+  k_fused16<<<static_cast<unsigned>(ctas), f16::CWARPS * 32, f16::SMEM, st>>>(
+      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
 // filter_image on device buffers, one frame or a strided frame batch.
 dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
                                 cudaStream_t st) {
   if (p->n == 8) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
-  // n = 16: forward -> H -> inverse through a stream-ordered scratch buffer.
+  if (!std::getenv("DCTF_N16_UNFUSED"))
+    return launch_fused16(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+  // n = 16 unfused (diagnostics): forward -> H -> inverse through scratch.
   const int bw = (w + 15) / 16, bh = (h + 15) / 16;
   const long long nb = static_cast<long long>(bw) * bh;
   double* xbuf = nullptr;
@@ -1005,10 +1329,12 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
   if (e == cudaSuccess) e = cudaMemcpy(p->d_basis, p->basis.data(), nn * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(p->d_hcoef, hcoef.data(), nn * nn * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(p->d_nan, 0, sizeof(int));
-  if (e == cudaSuccess && n == 8) {
-    dctf::layout_hfused8(p->op, hfused);
-    e = cudaMalloc(&p->d_hfused, 64 * 64 * sizeof(double));
-    if (e == cudaSuccess) e = cudaMemcpy(p->d_hfused, hfused.data(), 64 * 64 * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    if (n == 8) dctf::layout_hfused8(p->op, hfused);
+    else dctf::layout_hfused16(p->op, hfused);
+    e = cudaMalloc(&p->d_hfused, hfused.size() * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_hfused, hfused.data(), hfused.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) {
     const std::string msg = cudaGetErrorString(e);

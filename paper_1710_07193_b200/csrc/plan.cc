@@ -225,4 +225,29 @@ void layout_hfused8(const std::vector<double>& op, std::vector<double>& out) {
         }
 }
 
+// Fused n=16 kernel layout: [kc < 16][J < 32][q < 2][lane < 32][e < 2]
+//   = H[out(J, g)][in(kc, q, t, e)].
+// Staging word w of a block holds coefficients (u = 2a + e, v) with
+// v = w >> 3, a = (w & 7) ^ 4(v & 1) (see kernels.cu, k_fused16). K-step pair
+// q of chunk kc for lane t reads word 8kc + 4q + t; column c of n-tile J is
+// word 4J + (c >> 1), element c & 1.
+void layout_hfused16(const std::vector<double>& op, std::vector<double>& out) {
+  auto coef = [](int word, int e) {
+    const int v = word >> 3, a = (word & 7) ^ (4 * (v & 1));
+    return (2 * a + e) * 16 + v;
+  };
+  out.assign(256 * 256, 0.0);
+  size_t o = 0;
+  for (int kc = 0; kc < 16; ++kc)
+    for (int J = 0; J < 32; ++J)
+      for (int q = 0; q < 2; ++q)
+        for (int lane = 0; lane < 32; ++lane)
+          for (int e = 0; e < 2; ++e) {
+            const int g = lane >> 2, t = lane & 3;
+            const int orow = coef(4 * J + (g >> 1), g & 1);
+            const int kcol = coef(8 * kc + 4 * q + t, e);
+            out[o++] = op[size_t(orow) * 256 + kcol];
+          }
+}
+
 }  // namespace dctf

@@ -113,14 +113,17 @@ def _image_case(P, ref, img, w, k, pad, n, kc=None, coeffs=True):
 @pytest.mark.parametrize("shape", [(33, 40), (8, 8), (16, 16), (9, 13), (64, 136), (200, 263),
                                    (1, 1), (7, 300)])
 @pytest.mark.parametrize("pad", [0, 1])
-def test_fused_image_ragged_shapes(P, ref, shape, pad):
+@pytest.mark.parametrize("n", [8, 16])
+def test_fused_image_ragged_shapes(P, ref, shape, pad, n):
     from paper_1710_07193_b200 import synth
     h, w = shape
+    if n == 16:
+        h, w = 2 * h + 1, 4 * w + 3   # partial 64-block strips and ragged edges
     img = synth.uniform_image(h * 1000 + w, w, h)
     for name in ("gaussian3", "magic3", "average3"):
         wm, k = ref.mask_preset(name)
-        r_out, r_ci, r_co, r_pq = ref.filter_image(img, wm, k, pad, 8, side_outputs=True)
-        plan, d_img, out, co = _image_case(P, ref, img, wm, k, pad, 8)
+        r_out, r_ci, r_co, r_pq = ref.filter_image(img, wm, k, pad, n, side_outputs=True)
+        plan, d_img, out, co = _image_case(P, ref, img, wm, k, pad, n)
         mism, excused, _ = tie_report(out, r_out, blocks_to_image(r_pq, w, h))
         assert mism == excused, (name, mism)
         assert np.abs(co - r_co).max() <= TOL_COEF * max(1.0, np.abs(r_co).max())
