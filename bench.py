@@ -342,7 +342,49 @@ def main():
         ms16 = statistics.mean(a.elapsed_time(b) for a, b in ev16)
         nb16, flop16 = 262144, 2 * 16 ** 4 + 8 * 16 ** 3
         del img16, out16
-        aux = {"n16_fused": {
+        # coefficient path at n = 16 (config 4 shapes): FP64 DMMA vs 3xTF32 tcgen05
+        x16 = plan16.forward_image(torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda())
+        y16 = torch.empty_like(x16)
+        plan16t = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate,
+                               precision=P.Precision.kTf32x3)
+
+        def time_coef(pl, xx, yy, nbk, reps=10):
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(reps)]
+            for i in range(reps + 3):
+                flush.fill_(4)
+                if i >= 3:
+                    evs[i - 3][0].record(stream)
+                _lib.check(lib.dctf_filter_coeffs(pl.handle, xx.data_ptr(), yy.data_ptr(), nbk, sp))
+                if i >= 3:
+                    evs[i - 3][1].record(stream)
+            torch.cuda.synchronize()
+            return statistics.mean(a.elapsed_time(b) for a, b in evs)
+        ms_c16 = time_coef(plan16, x16, y16, 262144)
+        ref16 = y16.clone()
+        ms_t16 = time_coef(plan16t, x16, y16, 262144)
+        err_t16 = float((y16 - ref16).abs().max() / ref16.abs().max())
+        y8t = torch.empty((NBLOCKS, 8, 8), dtype=torch.float64, device="cuda")
+        plan8t = P.FilterPlan(P.Mask(5, mask), N, P.PaddingMode.kReplicate, precision=P.Precision.kTf32x3)
+        coeffs8 = plan.forward_image(d_in)
+        ms_t8 = time_coef(plan8t, coeffs8, y8t, NBLOCKS, reps=50)
+        y8r = plan.filter_coeffs(coeffs8)
+        err_t8 = float((y8t - y8r).abs().max() / y8r.abs().max())
+        del x16, y16, ref16
+        hbm = hbm_peak or 1.0
+
+        def coefline(kernel, ms, nbk, nn, prec, err=None):
+            gbs_c = nbk * 16 * nn / (ms / 1e3) / 1e9
+            d = {"kernel": kernel, "precision": prec, "blocks_per_s": nbk / (ms / 1e3), "ms": ms,
+                 "gb_per_s": gbs_c, "hbm_frac": gbs_c / hbm,
+                 "fp64_equiv_tflops": 2 * nn * nn * nbk / (ms / 1e3) / 1e12}
+            if err is not None:
+                d["max_rel_err_vs_fp64"] = err
+            return d
+        aux = {"n16_coef_fp64": coefline("k_coef16", ms_c16, 262144, 256, "fp64"),
+               "n16_coef_tf32x3": coefline("k_coef_tf32x3<256>", ms_t16, 262144, 256, "3xtf32", err_t16),
+               "n8_coef_tf32x3": coefline("k_coef_tf32x3<64>", ms_t8, NBLOCKS, 64, "3xtf32", err_t8),
+               "n16_fused": {
             "kernel": "k_fused16", "workload": "config4: 8192x8192 U(4), 16x16 blocks, gaussian "
             "7x7 sigma=2, replicate, FP64", "blocks_per_s": nb16 / (ms16 / 1e3), "ms": ms16,
             "fp64_tflops": flop16 * nb16 / (ms16 / 1e3) / 1e12,

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "../../include/dctf.h"
 
 struct dctf_plan {
@@ -21,7 +23,8 @@ struct dctf_plan {
   // Device-resident copies (owned). Layouts: see kernels.cu.
   double* d_basis = nullptr;     // C, n*n
   double* d_hcoef = nullptr;     // H in coefficient-kernel fragment order
-  double* d_hfused = nullptr;    // H in fused-kernel fragment order (n = 8)
+  double* d_hfused = nullptr;    // H in fused-kernel fragment order
+  void* d_hsplit = nullptr;      // TF32 hi/lo split of H, swizzled (precision TF32X3)
   int* d_nan = nullptr;          // NaN flag
 
   // Scratch for multi-kernel paths and the host-buffer entry (guarded).
@@ -51,5 +54,10 @@ dctf_status compile_operator(dctf_plan& p);
 void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out);
 void layout_hfused8(const std::vector<double>& op, std::vector<double>& out);
 void layout_hfused16(const std::vector<double>& op, std::vector<double>& out);
+void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>& out);
+
+// 3xTF32 tcgen05 coefficient filter (tc.cu).
+dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
+                               cudaStream_t st, int sms);
 
 }  // namespace dctf

@@ -1132,8 +1132,6 @@ bool misaligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) 
 
 dctf_status check_plan(const dctf_plan* p) {
   if (!p) return set_error(DCTF_INVALID_ARGUMENT, "plan is NULL");
-  if (p->precision != DCTF_PREC_FP64)
-    return set_error(DCTF_UNSUPPORTED, "precision mode not available for this entry point");
   return DCTF_OK;
 }
 
@@ -1149,6 +1147,7 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
   if (misaligned16(d_in) || misaligned16(d_out))
     return set_error(DCTF_INVALID_ARGUMENT, "coefficient buffers must be 16-byte aligned");
   if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in-place filter_coeffs not supported");
+  if (p->precision == DCTF_PREC_TF32X3) return dctf::launch_coef_tf32x3(p, d_in, d_out, nb, st, sm_count(p->device));
   CUtensorMap map;
   const int nn = p->n * p->n;
   dctf_status s = make_xmap(&map, d_in, nb, nn, p->n == 8 ? c8::TILE : c16::TILE);
@@ -1252,19 +1251,22 @@ dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, 
 dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
                                 cudaStream_t st) {
-  if (p->n == 8) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
-  if (!std::getenv("DCTF_N16_UNFUSED"))
+  const bool split = p->precision != DCTF_PREC_FP64;
+  if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+  if (!split && !std::getenv("DCTF_N16_UNFUSED"))
     return launch_fused16(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
-  // n = 16 unfused (diagnostics): forward -> H -> inverse through scratch.
-  const int bw = (w + 15) / 16, bh = (h + 15) / 16;
+  // Unfused: forward (exact) -> H (split-precision tensor cores, or FP64 when
+  // DCTF_N16_UNFUSED is set for diagnostics) -> inverse (exact) + quantize.
+  const int n = p->n, nn = n * n;
+  const int bw = (w + n - 1) / n, bh = (h + n - 1) / n;
   const long long nb = static_cast<long long>(bw) * bh;
   double* xbuf = nullptr;
   double* ybuf = nullptr;
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&xbuf), nb * 256 * sizeof(double), st));
-  if (!coef_out) CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ybuf), nb * 256 * sizeof(double), st));
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&xbuf), nb * nn * sizeof(double), st));
+  if (!coef_out) CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ybuf), nb * nn * sizeof(double), st));
   dctf_status s = DCTF_OK;
   for (int f = 0; f < nframes && s == DCTF_OK; ++f) {
-    double* y = coef_out ? coef_out + f * nb * 256 : ybuf;
+    double* y = coef_out ? coef_out + f * nb * nn : ybuf;
     s = launch_forward_u8(p, in + f * frame_stride, w, h, pitch, xbuf, st);
     if (s == DCTF_OK) s = launch_coef(p, xbuf, y, nb, st);
     if (s == DCTF_OK) s = launch_inverse_u8(p, y, out + f * frame_stride, w, h, pitch, st);
@@ -1305,9 +1307,9 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
     delete p;
     return s;
   }
-  if (precision != DCTF_PREC_FP64) {
+  if (precision == DCTF_PREC_BF16X3) {
     delete p;
-    return set_error(DCTF_UNSUPPORTED, "split-precision modes are not built yet");
+    return set_error(DCTF_UNSUPPORTED, "BF16x3 is not built; use DCTF_PREC_TF32X3 or DCTF_PREC_FP64");
   }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -1335,6 +1337,12 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
     e = cudaMalloc(&p->d_hfused, hfused.size() * sizeof(double));
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_hfused, hfused.data(), hfused.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess && precision == DCTF_PREC_TF32X3) {
+    std::vector<float> hs;
+    dctf::layout_hsplit_tf32(n, p->op, hs);
+    e = cudaMalloc(&p->d_hsplit, hs.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_hsplit, hs.data(), hs.size() * sizeof(float), cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) {
     const std::string msg = cudaGetErrorString(e);
@@ -1371,6 +1379,7 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_basis);
     cudaFree(p->d_hcoef);
     cudaFree(p->d_hfused);
+    cudaFree(p->d_hsplit);
     cudaFree(p->d_nan);
     cudaFree(p->io_in);
     cudaFree(p->io_out);
