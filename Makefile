@@ -6,7 +6,7 @@ CSRC := $(PKG)/csrc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-O3 -Xptxas -v --expt-relaxed-constexpr
 
-all: $(PKG)/libdctf_b200.so $(PKG)/libdctf_synth.so oracle cpp-test
+all: $(PKG)/libdctf_b200.so $(PKG)/libdctf_synth.so oracle cpp-test cli
 
 $(PKG)/libdctf_b200.so: $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/plan.cc $(CSRC)/internal.h include/dctf.h
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/plan.cc 2> build_ptxas.log || (cat build_ptxas.log; false)
@@ -14,15 +14,23 @@ $(PKG)/libdctf_b200.so: $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/plan.cc $(CSRC)
 $(PKG)/libdctf_synth.so: $(CSRC)/synth.cc
 	g++ -O3 -std=c++17 -fPIC -shared -pthread -o $@ $<
 
-cpp-test: tests/cpp/test_dctfilter_b200
+cpp-test: tests/cpp/test_dctfilter_b200 tests/cpp/test_pgm
+
+tests/cpp/test_pgm: tests/cpp/test_pgm.cc include/dctfilter_b200.hpp include/dctf.h $(PKG)/libdctf_b200.so
+	g++ -O2 -std=c++17 -Iinclude -o $@ $< -L$(PKG) -ldctf_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 tests/cpp/test_dctfilter_b200: tests/cpp/test_dctfilter_b200.cc include/dctfilter_b200.hpp include/dctf.h $(PKG)/libdctf_b200.so
 	g++ -O2 -std=c++17 -Iinclude -o $@ $< -L$(PKG) -ldctf_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+cli: tools/dctfilter_b200
+
+tools/dctfilter_b200: tools/dctfilter_b200_cli.cc include/dctfilter_b200.hpp include/dctf.h $(PKG)/libdctf_b200.so
+	g++ -O2 -std=c++17 -Iinclude -o $@ $< -L$(PKG) -ldctf_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(PKG)/*.so oracle/*.so oracle/_ref/*.so tests/cpp/test_dctfilter_b200
+	rm -f $(PKG)/*.so oracle/*.so oracle/_ref/*.so tests/cpp/test_dctfilter_b200 tests/cpp/test_pgm tools/dctfilter_b200
 
-.PHONY: all oracle clean cpp-test
+.PHONY: all oracle clean cpp-test cli

@@ -70,6 +70,34 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
                              int precision, int device, dctf_plan** out);
 dctf_status dctf_plan_destroy(dctf_plan* plan);
 
+/* Operator dump format of the reference (write_operator_sets /
+ * read_operator_sets, operator_io.hpp:105-217; what `build-operators` writes,
+ * dctfilter_main.cc:163-183): the plan's spatial and DCT-domain sandwich
+ * sets, every double printed with %.17g, so the text is byte-identical to the
+ * reference's and round-trips bit for bit.
+ *   dctf_plan_dump: writes up to *len bytes into buf (if buf && *len is
+ *     large enough) and sets *len to the full size. Square masks only.
+ *   dctf_plan_create_from_dump: builds a plan from a dump's DCT-domain set
+ *     (a spatial-only dump is conjugated), checking the header, version, mask
+ *     fingerprint and counts as read_operator_sets does (errors ->
+ *     DCTF_INVALID_ARGUMENT with the reference's message text). */
+dctf_status dctf_plan_dump(const dctf_plan* plan, char* buf, size_t* len);
+dctf_status dctf_plan_create_from_dump(const char* text, size_t len, int precision, int device,
+                                       dctf_plan** out);
+
+/* Host-only variants (no device): the dump of the sets FilterPlan would
+ * compile for a square k x k mask, and the dense operator H (n^4) a dump
+ * describes (plus its n, k, padding). */
+dctf_status dctf_format_operator_dump(const double* h_weights, int k, int n, int padding, char* buf,
+                                      size_t* len);
+dctf_status dctf_operator_from_dump(const char* text, size_t len, double* h_op, int* n, int* k,
+                                    int* padding);
+
+/* The plan's sandwich pairs (OperatorSet::pairs, operators.hpp:43-53):
+ * domain 0 = spatial (after merge_symmetric), 1 = DCT. npairs * n*n doubles
+ * each (see dctf_plan_info). Square masks only. */
+dctf_status dctf_plan_pairs(const dctf_plan* plan, int domain, double* h_lefts, double* h_rights);
+
 /* Plan metadata: block side, sandwich pair count and whether mirrored rows
  * were merged (OperatorSet::pairs.size(), ::symmetric_merged). */
 dctf_status dctf_plan_info(const dctf_plan* plan, int* n, int* npairs, int* symmetric_merged);
@@ -117,6 +145,22 @@ dctf_status dctf_filter_image_u8(const dctf_plan* plan, const uint8_t* d_in, uin
                                  int width, int height, size_t pitch, double* d_coeffs_out,
                                  void* stream);
 
+/* The spatial path of filter_image (Domain::kSpatial, image.hpp:219-222):
+ * convolve (spatial.hpp:41-68) per block with the plan's mask and padding, in
+ * the reference's operation order (bit-identical samples), then quantize +
+ * crop. A second on-device oracle for the DCT path, and the competing
+ * algorithm (k^2 MACs per pixel). */
+dctf_status dctf_filter_image_spatial_u8(const dctf_plan* plan, const uint8_t* d_in, uint8_t* d_out,
+                                         int width, int height, size_t pitch, void* stream);
+
+/* Host-buffer variant of the spatial path (synchronous). */
+dctf_status dctf_filter_image_spatial_host(const dctf_plan* plan, const uint8_t* h_in, uint8_t* h_out,
+                                           int width, int height, size_t pitch);
+
+/* convolve (spatial.hpp:41-68) over FP64 blocks (nblocks x n x n). */
+dctf_status dctf_convolve_blocks(const dctf_plan* plan, const double* d_blocks, double* d_out,
+                                 size_t nblocks, void* stream);
+
 /* Frame batch (video): frame f (0..nframes-1) of the d_in batch is filtered
  * with plans[plan_of_frame[f]]; frames are frame_stride bytes apart, all
  * width x height with the same pitch. All plans must share n and device. */
@@ -144,6 +188,8 @@ dctf_status dctf_inverse_blocks_host(const dctf_plan* plan, const double* h_coef
                                      double* h_blocks, size_t nblocks);
 dctf_status dctf_filter_coeffs_host(const dctf_plan* plan, const double* h_in, double* h_out,
                                     size_t nblocks);
+dctf_status dctf_convolve_blocks_host(const dctf_plan* plan, const double* h_blocks, double* h_out,
+                                      size_t nblocks);
 
 /* Synchronises `stream`, reads and clears the plan's NaN flag; *nan_seen is
  * 1 if any quantised sample was NaN since the last check. */

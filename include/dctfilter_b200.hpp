@@ -19,10 +19,15 @@
 #pragma once
 
 #include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <istream>
 #include <memory>
+#include <ostream>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -279,6 +284,27 @@ class FilterPlan {
     return filter_block(std::vector<BlockMatrix>{block})[0];
   }
 
+  // Operator dump (write_operator_sets of {spatial, dct}, operator_io.hpp).
+  std::string dump() const {
+    size_t len = 0;
+    check(dctf_plan_dump(plan_.get(), nullptr, &len));
+    std::string text(len, '\0');
+    check(dctf_plan_dump(plan_.get(), text.data(), &len));
+    return text;
+  }
+  // Plan whose operator is the dump's DCT-domain set (read_operator_sets).
+  static FilterPlan from_dump(const std::string& text, Precision precision = Precision::kFp64,
+                              int device = 0) {
+    dctf_plan* p = nullptr;
+    check(dctf_plan_create_from_dump(text.data(), text.size(), int(precision), device, &p));
+    return FilterPlan(detail::PlanPtr(p, detail::PlanDeleter()), device);
+  }
+
+  // convolve (spatial.hpp:41-68) with this plan's mask/padding, on the device.
+  std::vector<BlockMatrix> convolve(const std::vector<BlockMatrix>& blocks) const {
+    return detail::run(plan_, n_, blocks, dctf_convolve_blocks_host);
+  }
+
   // Device-pointer batch entry points (asynchronous on `stream`).
   void filter_coeffs_device(const double* d_in, double* d_out, size_t nblocks, void* stream = nullptr) const {
     check(dctf_filter_coeffs(plan_.get(), d_in, d_out, nblocks, stream));
@@ -289,6 +315,16 @@ class FilterPlan {
   }
 
  private:
+  FilterPlan(detail::PlanPtr plan, int device)
+      : mask_(Mask::identity()), padding_(PaddingMode::kZero), basis_(plan_n(plan.get()), device),
+        plan_(std::move(plan)) {
+    check(dctf_plan_info(plan_.get(), &n_, &npairs_, &merged_));
+  }
+  static int plan_n(const dctf_plan* p) {
+    int n = 0;
+    check(dctf_plan_info(p, &n, nullptr, nullptr));
+    return n;
+  }
   Mask mask_;
   PaddingMode padding_;
   DctBasis basis_;
@@ -309,14 +345,105 @@ inline GrayImage filter_image(const GrayImage& img, const Mask& mask, PaddingMod
                               Domain path = Domain::kDct, int n = 8) {
   if (mask.rows() == mask.cols() && mask.rows() > n)
     throw std::invalid_argument("filter_image: mask larger than block");
-  if (path != Domain::kDct) throw std::runtime_error("filter_image: only the DCT path runs on the device");
   if (img.samples.size() != size_t(img.width) * img.height)
     throw std::invalid_argument("GrayImage: sample count must be width*height");
   const FilterPlan plan(mask, n, padding);
   GrayImage out{img.width, img.height, std::vector<std::uint8_t>(img.samples.size())};
-  check(dctf_filter_image_host(plan.handle(), img.samples.data(), out.samples.data(), img.width,
-                               img.height, size_t(img.width)));
+  if (path == Domain::kDct)
+    check(dctf_filter_image_host(plan.handle(), img.samples.data(), out.samples.data(), img.width,
+                                 img.height, size_t(img.width)));
+  else
+    check(dctf_filter_image_spatial_host(plan.handle(), img.samples.data(), out.samples.data(),
+                                         img.width, img.height, size_t(img.width)));
   return out;
+}
+
+// ---------------------------------------------------------------------------
+// PGM I/O (image.hpp:45-152): binary P5 and ASCII P2 with maxval 255 in,
+// binary P5 out; malformed input throws PgmError.
+struct PgmError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline std::string pgm_token(std::istream& in) {
+  std::string tok;
+  int ch;
+  while ((ch = in.get()) != EOF) {
+    if (ch == '#') {
+      while ((ch = in.get()) != EOF && ch != '\n') {
+      }
+      continue;
+    }
+    if (!std::isspace(ch)) break;
+  }
+  if (ch == EOF) throw PgmError("malformed PGM header: unexpected end of data");
+  do {
+    tok.push_back(char(ch));
+  } while ((ch = in.get()) != EOF && !std::isspace(ch) && ch != '#');
+  if (ch != EOF) in.unget();
+  return tok;
+}
+inline int pgm_int(std::istream& in) {
+  const std::string tok = pgm_token(in);
+  size_t pos = 0;
+  int value = 0;
+  try {
+    value = std::stoi(tok, &pos);
+  } catch (const std::exception&) {
+    throw PgmError("malformed PGM header: expected integer, got '" + tok + "'");
+  }
+  if (pos != tok.size() || value < 0) throw PgmError("malformed PGM header: expected integer, got '" + tok + "'");
+  return value;
+}
+}  // namespace detail
+
+inline GrayImage load_pgm(std::istream& in) {
+  const std::string magic = detail::pgm_token(in);
+  if (magic != "P5" && magic != "P2") throw PgmError("unsupported format: expected P5 or P2, got '" + magic + "'");
+  const int width = detail::pgm_int(in);
+  const int height = detail::pgm_int(in);
+  if (width < 1 || height < 1) throw PgmError("malformed PGM header: bad dimensions");
+  const int maxval = detail::pgm_int(in);
+  if (maxval != 255) throw PgmError("unsupported maxval: expected 255, got " + std::to_string(maxval));
+  GrayImage img{width, height, std::vector<std::uint8_t>(size_t(width) * height)};
+  if (magic == "P5") {
+    in.get();  // the single whitespace byte after the header
+    in.read(reinterpret_cast<char*>(img.samples.data()), std::streamsize(img.samples.size()));
+    if (size_t(in.gcount()) != img.samples.size()) throw PgmError("truncated PGM data");
+  } else {
+    for (auto& v : img.samples) {
+      int x;
+      if (!(in >> x)) throw PgmError("truncated PGM data");
+      if (x < 0 || x > 255) throw PgmError("malformed PGM sample out of range");
+      v = std::uint8_t(x);
+    }
+  }
+  return img;
+}
+inline GrayImage load_pgm(const std::string& bytes) {
+  std::istringstream in(bytes);
+  return load_pgm(in);
+}
+inline void save_pgm(std::ostream& out, const GrayImage& img) {
+  out << "P5\n" << img.width << " " << img.height << "\n255\n";
+  out.write(reinterpret_cast<const char*>(img.samples.data()), std::streamsize(img.samples.size()));
+}
+inline std::string save_pgm(const GrayImage& img) {
+  std::ostringstream out;
+  save_pgm(out, img);
+  return out.str();
+}
+inline GrayImage load_pgm_file(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw PgmError("cannot open '" + path + "'");
+  return load_pgm(in);
+}
+inline void save_pgm_file(const std::string& path, const GrayImage& img) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw PgmError("cannot open '" + path + "' for writing");
+  save_pgm(out, img);
+  if (!out) throw PgmError("write failed for '" + path + "'");
 }
 
 }  // namespace dctfilter_b200

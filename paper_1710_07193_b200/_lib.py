@@ -33,6 +33,11 @@ _st = C.c_int
 _SIGS = {
     "dctf_plan_create": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
     "dctf_plan_destroy": (_st, [_vp]),
+    "dctf_plan_dump": (_st, [_vp, C.c_char_p, C.POINTER(C.c_size_t)]),
+    "dctf_plan_create_from_dump": (_st, [C.c_char_p, C.c_size_t, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "dctf_plan_pairs": (_st, [_vp, C.c_int, _d, _d]),
+    "dctf_format_operator_dump": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_size_t)]),
+    "dctf_operator_from_dump": (_st, [C.c_char_p, C.c_size_t, _d, _i, _i, _i]),
     "dctf_plan_info": (_st, [_vp, _i, _i, _i]),
     "dctf_compile_operator": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_int, _d, _d, _i, _i]),
     "dctf_plan_basis": (_st, [_vp, _d]),
@@ -46,10 +51,14 @@ _SIGS = {
     "dctf_filter_frames_u8": (_st, [C.POINTER(_vp), C.c_int, _i, _vp, _vp, C.c_int, C.c_int,
                                     C.c_int, C.c_size_t, C.c_size_t, _vp]),
     "dctf_filter_image_host": (_st, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_size_t]),
+    "dctf_filter_image_spatial_u8": (_st, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_size_t, _vp]),
+    "dctf_convolve_blocks": (_st, [_vp, _vp, _vp, C.c_size_t, _vp]),
     "dctf_plan_nan_check": (_st, [_vp, _vp, _i]),
     "dctf_forward_blocks_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
     "dctf_inverse_blocks_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
     "dctf_filter_coeffs_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
+    "dctf_convolve_blocks_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
+    "dctf_filter_image_spatial_host": (_st, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_size_t]),
     "dctf_measure_fp64_peak": (_st, [C.c_int, C.c_int, _d]),
     "dctf_last_launch_count": (C.c_int, []),
     "dctf_last_error_message": (C.c_char_p, []),

@@ -19,6 +19,9 @@ struct dctf_plan {
   std::vector<double> weights;   // kr*kc row-major
   std::vector<double> basis;     // C, n*n row-major (DctBasis::c())
   std::vector<double> op;        // H, n^4 row-major (natural coefficient order)
+  // Sandwich pairs of the compile (reference domain only): spatial (after
+  // merge_symmetric) and DCT-domain, npairs x n*n each (OperatorSet::pairs).
+  std::vector<double> sp_left, sp_right, dct_left, dct_right;
 
   // Device-resident copies (owned). Layouts: see kernels.cu.
   double* d_basis = nullptr;     // C, n*n
@@ -26,6 +29,7 @@ struct dctf_plan {
   double* d_hfused = nullptr;    // H in fused-kernel fragment order
   void* d_hsplit = nullptr;      // TF32 hi/lo split of H, swizzled (precision TF32X3)
   int* d_nan = nullptr;          // NaN flag
+  double* d_weights = nullptr;   // mask, kr*kc (spatial path)
 
   // Scratch for multi-kernel paths and the host-buffer entry (guarded).
   mutable std::mutex scratch_mu;
@@ -49,6 +53,14 @@ void reset_launches();
 // Builds C and the dense DCT-domain operator H for the mask.
 // Returns DCTF_INVALID_ARGUMENT with a message on bad input.
 dctf_status compile_operator(dctf_plan& p);
+
+// Operator dump format (operator_io.hpp:105-217), plan.cc.
+std::string format_operator_dump(const dctf_plan& p);
+// Parses a dump; fills weights/n/padding/merged and the pairs of the DCT set
+// (or the conjugated spatial set) and densifies H. Returns INVALID_ARGUMENT
+// with the reference's OperatorDumpError messages on malformed input.
+dctf_status parse_operator_dump(const std::string& text, dctf_plan& p);
+std::uint64_t mask_fingerprint(int k, const std::vector<double>& w);
 
 // Fragment-order permutations of H for the kernels (plan.cc).
 void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out);

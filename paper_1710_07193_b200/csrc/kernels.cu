@@ -1035,6 +1035,55 @@ __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// k_spatial: convolve (spatial.hpp:41-68) per block, one thread per sample,
+// correlation orientation, zero-drop or clamp padding at the block edge; the
+// accumulation order (r, c ascending) and separately rounded multiply/add
+// match the reference, so samples are bit-identical. Input samples come from
+// the u8 image through tile()'s edge replication, or from FP64 blocks.
+template <bool U8>
+__global__ void __launch_bounds__(256) k_spatial(const uint8_t* __restrict__ img, int w, int h,
+                                                 size_t pitch, int bw, const double* __restrict__ blocks,
+                                                 uint8_t* __restrict__ out_img, double* __restrict__ out_blocks,
+                                                 long long nblocks, int n, const double* __restrict__ wts,
+                                                 int kr, int kc, int replicate) {
+  __shared__ double ws[1024];
+  for (int i = threadIdx.x; i < kr * kc && i < 1024; i += blockDim.x) ws[i] = wts[i];
+  __syncthreads();
+  const int nn = n * n;
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long blk = idx / nn;
+  if (blk >= nblocks) return;
+  const int i = static_cast<int>(idx % nn) / n, j = static_cast<int>(idx % nn) % n;
+  const int hr = (kr - 1) / 2, hc = (kc - 1) / 2;
+  const int by = U8 ? static_cast<int>(blk / bw) : 0, bx = U8 ? static_cast<int>(blk % bw) : 0;
+  double acc = 0.0;
+  for (int r = 0; r < kr; ++r) {
+    int si = i + r - hr;
+    if (!replicate && (si < 0 || si >= n)) continue;
+    si = min(max(si, 0), n - 1);
+    for (int c = 0; c < kc; ++c) {
+      int sj = j + c - hc;
+      if (!replicate && (sj < 0 || sj >= n)) continue;
+      sj = min(max(sj, 0), n - 1);
+      double v;
+      if (U8) {
+        const int y = min(by * n + si, h - 1), x = min(bx * n + sj, w - 1);
+        v = static_cast<double>(img[static_cast<size_t>(y) * pitch + x]);
+      } else {
+        v = blocks[blk * nn + si * n + sj];
+      }
+      acc = __dadd_rn(acc, __dmul_rn(ws[r * kc + c], v));
+    }
+  }
+  if (U8) {
+    const int y = by * n + i, x = bx * n + j;
+    if (y < h && x < w) out_img[static_cast<size_t>(y) * pitch + x] = static_cast<uint8_t>(quantize(acc, nullptr));
+  } else {
+    out_blocks[blk * nn + i * n + j] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // FP64 peak microbenchmarks (diagnostics; roofline denominator).
 __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
   double2 acc[8];
@@ -1286,27 +1335,13 @@ const char* dctf_last_error_message(void) { return dctf::t_err.c_str(); }
 int dctf_last_launch_count(void) { return dctf::t_launches; }
 const char* dctf_version(void) { return "dctf_b200 0.1 (sm_100a, fp64-dmma)"; }
 
-dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int padding,
-                             int precision, int device, dctf_plan** out) {
-  dctf::reset_launches();
-  if (!out || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
-  *out = nullptr;
-  if (precision != DCTF_PREC_FP64 && precision != DCTF_PREC_TF32X3 && precision != DCTF_PREC_BF16X3)
-    return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
-  if (kr < 1 || kc < 1) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
-  auto* p = new dctf_plan();
-  p->n = n;
-  p->kr = kr;
-  p->kc = kc;
-  p->padding = padding;
-  p->precision = precision;
-  p->device = device;
-  p->weights.assign(h_weights, h_weights + static_cast<size_t>(kr) * kc);
-  dctf_status s = dctf::compile_operator(*p);
-  if (s != DCTF_OK) {
-    delete p;
-    return s;
-  }
+}  // extern "C"
+
+namespace {
+// Device-side half of plan construction: validates the device and uploads the
+// operator in every layout the kernels use. Takes ownership of p.
+dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
+  const int n = p->n, device = p->device, precision = p->precision;
   if (precision == DCTF_PREC_BF16X3) {
     delete p;
     return set_error(DCTF_UNSUPPORTED, "BF16x3 is not built; use DCTF_PREC_TF32X3 or DCTF_PREC_FP64");
@@ -1328,6 +1363,9 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
   cudaError_t e = cudaMalloc(&p->d_basis, nn * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&p->d_hcoef, nn * nn * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&p->d_nan, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_weights, p->weights.size() * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->d_weights, p->weights.data(), p->weights.size() * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(p->d_basis, p->basis.data(), nn * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(p->d_hcoef, hcoef.data(), nn * nn * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(p->d_nan, 0, sizeof(int));
@@ -1350,6 +1388,99 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
     return set_error(DCTF_CUDA_ERROR, "plan upload: " + msg);
   }
   *out = p;
+  return DCTF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int padding,
+                             int precision, int device, dctf_plan** out) {
+  dctf::reset_launches();
+  if (!out || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (precision != DCTF_PREC_FP64 && precision != DCTF_PREC_TF32X3 && precision != DCTF_PREC_BF16X3)
+    return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
+  if (kr < 1 || kc < 1) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
+  auto* p = new dctf_plan();
+  p->n = n;
+  p->kr = kr;
+  p->kc = kc;
+  p->padding = padding;
+  p->precision = precision;
+  p->device = device;
+  p->weights.assign(h_weights, h_weights + static_cast<size_t>(kr) * kc);
+  dctf_status s = dctf::compile_operator(*p);
+  if (s != DCTF_OK) {
+    delete p;
+    return s;
+  }
+  return finish_plan(p, out);
+}
+
+dctf_status dctf_plan_create_from_dump(const char* text, size_t len, int precision, int device,
+                                       dctf_plan** out) {
+  dctf::reset_launches();
+  if (!out || !text) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (precision != DCTF_PREC_FP64 && precision != DCTF_PREC_TF32X3 && precision != DCTF_PREC_BF16X3)
+    return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
+  auto* p = new dctf_plan();
+  p->precision = precision;
+  p->device = device;
+  dctf_status s = dctf::parse_operator_dump(std::string(text, len), *p);
+  if (s != DCTF_OK) {
+    delete p;
+    return s;
+  }
+  return finish_plan(p, out);
+}
+
+dctf_status dctf_plan_dump(const dctf_plan* p, char* buf, size_t* len) {
+  if (!p || !len) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  if (p->dct_left.empty() || p->sp_left.empty())
+    return set_error(DCTF_UNSUPPORTED, "operator dump needs a square mask compiled as sandwich pairs");
+  const std::string text = dctf::format_operator_dump(*p);
+  if (buf && *len >= text.size()) std::memcpy(buf, text.data(), text.size());
+  *len = text.size();
+  return DCTF_OK;
+}
+
+dctf_status dctf_format_operator_dump(const double* h_weights, int k, int n, int padding, char* buf,
+                                      size_t* len) {
+  if (!h_weights || !len) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  if (k < 1) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
+  if (k > n) return set_error(DCTF_INVALID_ARGUMENT, "build_spatial_operator_set: mask larger than block");
+  dctf_plan p;
+  p.n = n;
+  p.kr = p.kc = k;
+  p.padding = padding;
+  p.weights.assign(h_weights, h_weights + static_cast<size_t>(k) * k);
+  const dctf_status s = dctf::compile_operator(p);
+  if (s != DCTF_OK) return s;
+  return dctf_plan_dump(&p, buf, len);
+}
+
+dctf_status dctf_operator_from_dump(const char* text, size_t len, double* h_op, int* n, int* k,
+                                    int* padding) {
+  if (!text) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  dctf_plan p;
+  const dctf_status s = dctf::parse_operator_dump(std::string(text, len), p);
+  if (s != DCTF_OK) return s;
+  if (h_op) std::memcpy(h_op, p.op.data(), p.op.size() * sizeof(double));
+  if (n) *n = p.n;
+  if (k) *k = p.kr;
+  if (padding) *padding = p.padding;
+  return DCTF_OK;
+}
+
+dctf_status dctf_plan_pairs(const dctf_plan* p, int domain, double* h_lefts, double* h_rights) {
+  if (!p) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  const std::vector<double>& L = domain ? p->dct_left : p->sp_left;
+  const std::vector<double>& R = domain ? p->dct_right : p->sp_right;
+  if (L.empty()) return set_error(DCTF_UNSUPPORTED, "plan has no sandwich pairs in that domain");
+  if (h_lefts) std::memcpy(h_lefts, L.data(), L.size() * sizeof(double));
+  if (h_rights) std::memcpy(h_rights, R.data(), R.size() * sizeof(double));
   return DCTF_OK;
 }
 
@@ -1381,6 +1512,7 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_hfused);
     cudaFree(p->d_hsplit);
     cudaFree(p->d_nan);
+    cudaFree(p->d_weights);
     cudaFree(p->io_in);
     cudaFree(p->io_out);
     for (void* s : p->streams)
@@ -1497,6 +1629,44 @@ dctf_status dctf_filter_image_u8(const dctf_plan* p, const uint8_t* d_in, uint8_
   if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in/out images may not alias");
   DeviceGuard guard(p->device);
   return filter_image_device(p, d_in, d_out, w, h, pitch, 0, 1, d_coeffs_out, as_stream(stream));
+}
+
+dctf_status dctf_filter_image_spatial_u8(const dctf_plan* p, const uint8_t* d_in, uint8_t* d_out,
+                                         int w, int h, size_t pitch, void* stream) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s == DCTF_OK) s = check_image(w, h, pitch);
+  if (s != DCTF_OK) return s;
+  if (!d_in || !d_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  if (p->kr * p->kc > 1024) return set_error(DCTF_UNSUPPORTED, "spatial path supports masks up to 1024 taps");
+  DeviceGuard guard(p->device);
+  const int n = p->n, bw = (w + n - 1) / n, bh = (h + n - 1) / n;
+  const long long nb = static_cast<long long>(bw) * bh;
+  const unsigned grid = static_cast<unsigned>((nb * n * n + 255) / 256);
+  k_spatial<true><<<grid, 256, 0, as_stream(stream)>>>(d_in, w, h, pitch, bw, nullptr, d_out, nullptr, nb, n,
+                                                       p->d_weights, p->kr, p->kc, p->padding);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
+dctf_status dctf_convolve_blocks(const dctf_plan* p, const double* d_blocks, double* d_out, size_t nblocks,
+                                 void* stream) {
+  dctf::reset_launches();
+  dctf_status s = check_plan(p);
+  if (s != DCTF_OK) return s;
+  if (nblocks == 0) return DCTF_OK;
+  if (!d_blocks || !d_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  if (p->kr * p->kc > 1024) return set_error(DCTF_UNSUPPORTED, "spatial path supports masks up to 1024 taps");
+  DeviceGuard guard(p->device);
+  const int n = p->n;
+  const long long nb = static_cast<long long>(nblocks);
+  const unsigned grid = static_cast<unsigned>((nb * n * n + 255) / 256);
+  k_spatial<false><<<grid, 256, 0, as_stream(stream)>>>(nullptr, 0, 0, 0, 1, d_blocks, nullptr, d_out, nb, n,
+                                                        p->d_weights, p->kr, p->kc, p->padding);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
 }
 
 dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
@@ -1682,7 +1852,8 @@ static dctf_status run_host_blocks(const dctf_plan* p, const double* h_in, doubl
   if (s == DCTF_OK) {
     if (op == 0) s = dctf_forward_blocks(p, din, dout, nblocks, st);
     else if (op == 1) s = dctf_inverse_blocks(p, din, dout, nblocks, st);
-    else s = dctf_filter_coeffs(p, din, dout, nblocks, st);
+    else if (op == 2) s = dctf_filter_coeffs(p, din, dout, nblocks, st);
+    else s = dctf_convolve_blocks(p, din, dout, nblocks, st);
   }
   if (s == DCTF_OK) {
     e = cudaMemcpyAsync(h_out, dout, bytes, cudaMemcpyDeviceToHost, st);
@@ -1707,6 +1878,33 @@ dctf_status dctf_inverse_blocks_host(const dctf_plan* p, const double* h_in, dou
 dctf_status dctf_filter_coeffs_host(const dctf_plan* p, const double* h_in, double* h_out,
                                     size_t nblocks) {
   return run_host_blocks(p, h_in, h_out, nblocks, 2);
+}
+
+dctf_status dctf_convolve_blocks_host(const dctf_plan* p, const double* h_in, double* h_out,
+                                      size_t nblocks) {
+  return run_host_blocks(p, h_in, h_out, nblocks, 3);
+}
+
+dctf_status dctf_filter_image_spatial_host(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w,
+                                           int h, size_t pitch) {
+  dctf_status s = check_plan(p);
+  if (s == DCTF_OK) s = check_image(w, h, pitch);
+  if (s != DCTF_OK) return s;
+  if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  const size_t bytes = pitch * static_cast<size_t>(h);
+  uint8_t *din = nullptr, *dout = nullptr;
+  CUDA_TRY(cudaMalloc(&din, bytes));
+  cudaError_t e = cudaMalloc(&dout, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(din, h_in, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    s = dctf_filter_image_spatial_u8(p, din, dout, w, h, pitch, nullptr);
+    if (s == DCTF_OK) e = cudaMemcpy(h_out, dout, bytes, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(din);
+  cudaFree(dout);
+  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, cudaGetErrorString(e));
+  return s;
 }
 
 dctf_status dctf_measure_fp64_peak(int device, int mode, double* tflops) {

@@ -19,8 +19,11 @@
 // the convolve formula (spatial.hpp:36-37) for H_spatial and
 // H = (C (x) C) H_spatial (C (x) C)^t; for reference-domain masks both
 // constructions agree to ~1e-15 (tests/test_host_api.py).
+#include <cinttypes>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <sstream>
 
 #include "internal.h"
 
@@ -54,6 +57,24 @@ void dct_basis(int n, double* c) {
       const double angle = (2 * x + 1) * u * pi / (2.0 * n);
       c[u * n + x] = (u == 0 ? a0 : au) * std::cos(angle);
     }
+}
+
+// H[(u,v),(a,b)] = sum_p L_p[u][a] R_p[b][v]  (apply_pairs, filter.hpp:30-38).
+void densify(dctf_plan& p) {
+  const int n = p.n;
+  const size_t nn = size_t(n) * n;
+  const int np = static_cast<int>(p.dct_left.size() / nn);
+  const double* L = p.dct_left.data();
+  const double* R = p.dct_right.data();
+  p.op.assign(nn * nn, 0.0);
+  for (int u = 0; u < n; ++u)
+    for (int v = 0; v < n; ++v)
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+          double acc = 0.0;
+          for (int q = 0; q < np; ++q) acc += L[q * nn + u * n + a] * R[q * nn + b * n + v];
+          p.op[(size_t(u) * n + v) * nn + size_t(a) * n + b] = acc;
+        }
 }
 
 void sandwich_operator(dctf_plan& p) {
@@ -110,15 +131,11 @@ void sandwich_operator(dctf_plan& p) {
     matmul(n, p.basis.data(), &right[q * nn], tmp.data());
     matmul(n, tmp.data(), ct.data(), &R[q * nn]);
   }
-  p.op.assign(nn * nn, 0.0);
-  for (int u = 0; u < n; ++u)
-    for (int v = 0; v < n; ++v)
-      for (int a = 0; a < n; ++a)
-        for (int b = 0; b < n; ++b) {
-          double acc = 0.0;
-          for (int q = 0; q < np; ++q) acc += L[q * nn + u * n + a] * R[q * nn + b * n + v];
-          p.op[(size_t(u) * n + v) * nn + size_t(a) * n + b] = acc;
-        }
+  p.sp_left.assign(left.begin(), left.begin() + nn * np);
+  p.sp_right.assign(right.begin(), right.begin() + nn * np);
+  p.dct_left = L;
+  p.dct_right = R;
+  densify(p);
 }
 
 void convolution_operator(dctf_plan& p) {
@@ -164,7 +181,180 @@ void convolution_operator(dctf_plan& p) {
   p.merged = 0;
 }
 
+std::string fmt17(double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+
+void write_matrix(std::ostringstream& out, const double* m, int n) {
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < n; ++j) out << (j ? " " : "") << fmt17(m[i * n + j]);
+    out << "\n";
+  }
+}
+
+void write_set(std::ostringstream& out, const dctf_plan& p, bool dct) {
+  const int n = p.n, k = p.kr;
+  const size_t nn = size_t(n) * n;
+  const std::vector<double>& L = dct ? p.dct_left : p.sp_left;
+  const std::vector<double>& R = dct ? p.dct_right : p.sp_right;
+  const size_t np = L.size() / nn;
+  out << "set\n";
+  out << "n " << n << "\n";
+  out << "k " << k << "\n";
+  out << "padding " << (p.padding == DCTF_PAD_ZERO ? "zero" : "replicate") << "\n";
+  out << "domain " << (dct ? "dct" : "spatial") << "\n";
+  out << "symmetric_merged " << (p.merged ? 1 : 0) << "\n";
+  char fp[24];
+  std::snprintf(fp, sizeof fp, "%016llx", static_cast<unsigned long long>(mask_fingerprint(k, p.weights)));
+  out << "mask_fingerprint " << fp << "\n";
+  out << "mask\n";
+  write_matrix(out, p.weights.data(), k);
+  out << "pairs " << np << "\n";
+  for (size_t q = 0; q < np; ++q) {
+    out << "pair\n";
+    out << "left\n";
+    write_matrix(out, &L[q * nn], n);
+    out << "right\n";
+    write_matrix(out, &R[q * nn], n);
+  }
+}
+
+struct DumpReader {
+  std::istringstream in;
+  explicit DumpReader(const std::string& t) : in(t) {}
+  bool token(std::string& tok) { return static_cast<bool>(in >> tok); }
+};
+
 }  // namespace
+
+// FNV-1a over the side length and the IEEE bits of the weights (mask.hpp:49-65).
+std::uint64_t mask_fingerprint(int k, const std::vector<double>& w) {
+  std::uint64_t h = 14695981039346656037ull;
+  auto mix = [&h](std::uint64_t v) {
+    for (int byte = 0; byte < 8; ++byte) {
+      h ^= (v >> (8 * byte)) & 0xff;
+      h *= 1099511628211ull;
+    }
+  };
+  mix(std::uint64_t(k));
+  for (double v : w) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &v, sizeof bits);
+    mix(bits);
+  }
+  return h;
+}
+
+// write_operator_sets (operator_io.hpp:105-137) of {spatial, dct}: the dump
+// the reference CLI's build-operators writes (dctfilter_main.cc:163-183).
+std::string format_operator_dump(const dctf_plan& p) {
+  std::ostringstream out;
+  out << "dctfilter-operators 1\n";
+  out << "sets 2\n";
+  write_set(out, p, false);
+  write_set(out, p, true);
+  return out.str();
+}
+
+// read_operator_sets (operator_io.hpp:145-217). The plan takes its operator
+// from the last DCT-domain set in the dump (a spatial-only dump is
+// conjugated with the basis, to_dct_domain operators.hpp:124-141).
+dctf_status parse_operator_dump(const std::string& text, dctf_plan& p) {
+  DumpReader r(text);
+  std::string tok;
+  auto err = [](const std::string& m) { return set_error(DCTF_INVALID_ARGUMENT, "operator dump: " + m); };
+  auto expect = [&](const char* kw) -> bool {
+    if (!r.token(tok)) return false;
+    return tok == kw;
+  };
+  auto read_long = [&](long& v) -> bool { return static_cast<bool>(r.in >> v); };
+  if (!r.token(tok)) return err("truncated, expected dctfilter-operators");
+  if (tok != "dctfilter-operators") return err("expected 'dctfilter-operators', got '" + tok + "'");
+  long version = 0, count = 0;
+  if (!read_long(version)) return err("bad value for format version");
+  if (version != 1) return err("unsupported version " + std::to_string(version));
+  if (!expect("sets")) return err("expected 'sets'");
+  if (!read_long(count) || count < 0) return err("bad set count");
+  bool have = false;
+  for (long sidx = 0; sidx < count; ++sidx) {
+    long n = 0, k = 0, merged = 0, npairs = 0;
+    if (!expect("set")) return err("expected 'set'");
+    if (!expect("n") || !read_long(n)) return err("bad value for n");
+    if (!expect("k") || !read_long(k)) return err("bad value for k");
+    if (!expect("padding") || !r.token(tok)) return err("truncated, expected padding mode");
+    int padding;
+    if (tok == "zero") padding = DCTF_PAD_ZERO;
+    else if (tok == "replicate") padding = DCTF_PAD_REPLICATE;
+    else return err("unknown padding '" + tok + "'");
+    if (!expect("domain") || !r.token(tok)) return err("truncated, expected domain");
+    bool dct;
+    if (tok == "spatial") dct = false;
+    else if (tok == "dct") dct = true;
+    else return err("unknown domain '" + tok + "'");
+    if (!expect("symmetric_merged") || !read_long(merged)) return err("bad value for symmetric_merged");
+    std::string fp;
+    if (!expect("mask_fingerprint") || !r.token(fp)) return err("truncated, expected mask fingerprint");
+    if (!expect("mask")) return err("expected 'mask'");
+    if (k < 1) return err("bad mask side");
+    if (n < 2 || n > 16) return err("bad block side");
+    std::vector<double> w(size_t(k) * k);
+    for (double& v : w)
+      if (!(r.in >> v)) return err("bad numeric entry");
+    for (double v : w)
+      if (!std::isfinite(v)) return set_error(DCTF_INVALID_ARGUMENT, "Mask: weights must be finite");
+    if (k % 2 == 0) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
+    char expect_fp[24];
+    std::snprintf(expect_fp, sizeof expect_fp, "%016llx", static_cast<unsigned long long>(mask_fingerprint(int(k), w)));
+    if (fp != expect_fp) return err("mask fingerprint mismatch");
+    if (!expect("pairs") || !read_long(npairs) || npairs < 0) return err("bad pair count");
+    const size_t nn = size_t(n) * n;
+    std::vector<double> L(nn * npairs), R(nn * npairs);
+    for (long q = 0; q < npairs; ++q) {
+      if (!expect("pair")) return err("expected 'pair'");
+      if (!expect("left")) return err("expected 'left'");
+      for (size_t i = 0; i < nn; ++i)
+        if (!(r.in >> L[q * nn + i])) return err("bad numeric entry");
+      if (!expect("right")) return err("expected 'right'");
+      for (size_t i = 0; i < nn; ++i)
+        if (!(r.in >> R[q * nn + i])) return err("bad numeric entry");
+    }
+    if (!have || dct) {
+      p.n = int(n);
+      p.kr = p.kc = int(k);
+      p.padding = padding;
+      p.merged = merged != 0;
+      p.weights = w;
+      p.npairs = int(npairs);
+      p.basis.assign(nn, 0.0);
+      dct_basis(p.n, p.basis.data());
+      if (dct) {
+        p.dct_left = L;
+        p.dct_right = R;
+      } else {
+        p.sp_left = L;
+        p.sp_right = R;
+        std::vector<double> ct(nn), tmp(nn);
+        transpose(p.n, p.basis.data(), ct.data());
+        p.dct_left.assign(nn * npairs, 0.0);
+        p.dct_right.assign(nn * npairs, 0.0);
+        for (long q = 0; q < npairs; ++q) {
+          matmul(p.n, p.basis.data(), &L[q * nn], tmp.data());
+          matmul(p.n, tmp.data(), ct.data(), &p.dct_left[q * nn]);
+          matmul(p.n, p.basis.data(), &R[q * nn], tmp.data());
+          matmul(p.n, tmp.data(), ct.data(), &p.dct_right[q * nn]);
+        }
+      }
+      have = true;
+    }
+  }
+  if (!have) return err("no operator set in dump");
+  if (p.n != 8 && p.n != 16) return set_error(DCTF_INVALID_ARGUMENT, "block side n must be 8 or 16");
+  p.reference_domain = true;
+  densify(p);
+  return DCTF_OK;
+}
 
 dctf_status compile_operator(dctf_plan& p) {
   if (p.n != 8 && p.n != 16) return set_error(DCTF_INVALID_ARGUMENT, "block side n must be 8 or 16");

@@ -32,6 +32,7 @@ from ._lib import InvalidArgument, Unsupported, check
 __all__ = [
     "PaddingMode", "Domain", "Precision", "Mask", "row_symmetric", "DctBasis", "FilterPlan",
     "forward_2d", "inverse_2d", "filter_image", "filter_frames", "InvalidArgument", "Unsupported",
+    "format_operator_dump", "operator_from_dump",
 ]
 
 
@@ -189,6 +190,36 @@ class FilterPlan:
         check(_lib.lib.dctf_plan_info(h, C.byref(nn), C.byref(np_), C.byref(mg)))
         self._n, self.npairs, self.symmetric_merged = nn.value, np_.value, bool(mg.value)
 
+    @classmethod
+    def from_dump(cls, text: str, precision: "Precision" = None, device: int | None = None):
+        """Plan from an operator dump (read_operator_sets, operator_io.hpp:145-217):
+        the operator is the dump's DCT-domain set, not a recompile of the mask."""
+        if device is None:
+            import torch
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        raw = text.encode()
+        h = C.c_void_p()
+        check(_lib.lib.dctf_plan_create_from_dump(raw, len(raw), int(precision or Precision.kFp64),
+                                                  int(device), C.byref(h)))
+        self = cls.__new__(cls)
+        self._h, self._device = h, int(device)
+        nn, np_, mg = C.c_int(), C.c_int(), C.c_int()
+        check(_lib.lib.dctf_plan_info(h, C.byref(nn), C.byref(np_), C.byref(mg)))
+        self._n, self.npairs, self.symmetric_merged = nn.value, np_.value, bool(mg.value)
+        _, k, pad = operator_from_dump(text)
+        self._padding = PaddingMode(pad)
+        self._mask = None
+        return self
+
+    def dump(self) -> str:
+        """write_operator_sets of the plan's {spatial, dct} sets (byte-identical
+        to the reference's build-operators output)."""
+        ln = C.c_size_t(0)
+        check(_lib.lib.dctf_plan_dump(self._h, None, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value)
+        check(_lib.lib.dctf_plan_dump(self._h, buf, C.byref(ln)))
+        return buf.raw[: ln.value].decode()
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and _lib is not None and getattr(_lib, "lib", None) is not None:
@@ -290,6 +321,26 @@ class FilterPlan:
                                             cp or None, _stream(img.device)))
         return out
 
+    def filter_image_spatial(self, img):
+        """Spatial path (Domain::kSpatial): convolve per block, bit-identical to
+        the reference's samples, then quantize (image.hpp:219-222)."""
+        import torch
+        img = _check_image(img)
+        h, w = img.shape
+        out = torch.empty_like(img)
+        check(_lib.lib.dctf_filter_image_spatial_u8(self._h, _dptr(img), _dptr(out), w, h,
+                                                    img.stride(0), _stream(img.device)))
+        return out
+
+    def convolve(self, blocks):
+        """convolve (spatial.hpp:41-68) on a (B, n, n) fp64 CUDA tensor."""
+        import torch
+        x = self._check_blocks(blocks)
+        y = torch.empty_like(x)
+        check(_lib.lib.dctf_convolve_blocks(self._h, _dptr(x), _dptr(y), x.shape[0],
+                                            _stream(x.device)))
+        return y
+
     def filter_image_host(self, img: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
         """End-to-end host-buffer filter (H2D, fused kernel, D2H)."""
         img = np.ascontiguousarray(img, dtype=np.uint8)
@@ -301,6 +352,30 @@ class FilterPlan:
         check(_lib.lib.dctf_filter_image_host(self._h, img.ctypes.data, out.ctypes.data, w, h,
                                               img.strides[0]))
         return out
+
+
+def format_operator_dump(mask: Mask, n: int, padding: PaddingMode) -> str:
+    """Host-only: the dump FilterPlan(mask, n, padding) would write."""
+    w = mask._w
+    ln = C.c_size_t(0)
+    check(_lib.lib.dctf_format_operator_dump(w.ctypes.data_as(_lib._d), mask.k(), int(n),
+                                             int(padding), None, C.byref(ln)))
+    buf = C.create_string_buffer(ln.value)
+    check(_lib.lib.dctf_format_operator_dump(w.ctypes.data_as(_lib._d), mask.k(), int(n),
+                                             int(padding), buf, C.byref(ln)))
+    return buf.raw[: ln.value].decode()
+
+
+def operator_from_dump(text: str):
+    """Host-only: (H, k, padding) described by an operator dump."""
+    raw = text.encode()
+    n, k, pad = C.c_int(), C.c_int(), C.c_int()
+    check(_lib.lib.dctf_operator_from_dump(raw, len(raw), None, C.byref(n), C.byref(k),
+                                           C.byref(pad)))
+    h = np.zeros((n.value ** 2, n.value ** 2))
+    check(_lib.lib.dctf_operator_from_dump(raw, len(raw), h.ctypes.data_as(_lib._d), C.byref(n),
+                                           C.byref(k), C.byref(pad)))
+    return h, k.value, pad.value
 
 
 def _check_image(img):
@@ -346,9 +421,13 @@ def filter_image(img, mask: Mask, padding: PaddingMode, path: Domain = Domain.kD
     entry, or a CUDA uint8 tensor -> CUDA tensor."""
     if mask.kr == mask.kc and mask.kr > n:
         raise InvalidArgument("filter_image: mask larger than block")
-    if path != Domain.kDct:
-        raise Unsupported("the spatial path runs only in the reference / oracle")
     plan = FilterPlan(mask, n, padding)
+    if path == Domain.kSpatial:
+        if isinstance(img, np.ndarray):
+            import torch
+            d = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+            return plan.filter_image_spatial(d).cpu().numpy()
+        return plan.filter_image_spatial(img)
     if isinstance(img, np.ndarray):
         return plan.filter_image_host(img)
     return plan.filter_image(img)
