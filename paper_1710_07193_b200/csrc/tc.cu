@@ -10,12 +10,14 @@
 // 128B-swizzled shared-memory image the UMMA descriptors expect, so it is
 // streamed with plain bulk copies.
 //
-// CTA = 8 warps, one CTA per SM, persistent over tiles of 128 blocks (MMA M):
-//   warps 0-3 : load their block row of X (FP64) for the next K-chunk, split
-//               it into TF32 hi/lo, write the swizzled A tiles; thread 0 also
-//               bulk-copies the H chunk and issues the MMAs (single thread).
-//   warps 4-7 : epilogue — tcgen05.ld the FP32 accumulator (lanes = blocks,
-//               columns = outputs), widen to FP64, store Y.
+// CTA = 12 warps, one CTA per SM, persistent over tiles of 128 blocks (MMA M):
+//   warps 0-7 : two threads per tile row load X (FP64) two K-chunks ahead
+//               into registers, split it into TF32 hi/lo and write the
+//               swizzled A tiles; thread 0 also bulk-copies the H chunk and
+//               issues the MMAs (single thread).
+//   warps 8-11: epilogue — tcgen05.ld the FP32 accumulator (lanes = blocks,
+//               columns = outputs), widen to FP64, stage rows in shared
+//               memory and store them as coalesced 128-byte row segments.
 // TMEM holds two accumulators (tile parity) so the epilogue of tile i
 // overlaps the MMAs of tile i+1; shared memory holds two K-chunk stages.
 #include <cuda.h>
@@ -120,16 +122,22 @@ struct TcCfg {
   static constexpr int STAGE = 2 * ABYTES + 2 * BBYTES;
   static constexpr int STAGES = 2;
   static constexpr int TMEM_COLS = 2 * NN <= 128 ? 128 : (2 * NN <= 256 ? 256 : 512);
-  static constexpr int SMEM = 1024 + STAGES * STAGE;
+  static constexpr int CONV_WARPS = 8;      // converter warps (2 threads per tile row)
+  static constexpr int EPI_WARPS = 4;       // epilogue warps (one TMEM lane quarter each)
+  static constexpr int THREADS = 32 * (CONV_WARPS + EPI_WARPS);
+  static constexpr int EPI_STRIDE = 144;    // 16 doubles + 16 B pad per staged row
+  static constexpr int EPI_BYTES = 32 * EPI_STRIDE;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI_WARPS * EPI_BYTES;
 };
 
 template <int NN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
     k_coef_tf32x3(const double* __restrict__ x, const float* __restrict__ hsplit,
                   double* __restrict__ y, long long nblocks) {
   using Cfg = TcCfg<NN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
+  uint8_t* epi = base + Cfg::STAGES * Cfg::STAGE;
   __shared__ uint64_t a_full[2], b_full[2], empty[2], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -142,11 +150,11 @@ __global__ void __launch_bounds__(256, 1)
   }
   if (threadIdx.x == 32) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&a_full[i], 128);
+      mbar_init(&a_full[i], 32 * Cfg::CONV_WARPS);
       mbar_init(&b_full[i], 1);
       mbar_init(&empty[i], 1);
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], 32 * Cfg::EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -155,119 +163,123 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
   const long long ntiles = (nblocks + Cfg::TILE - 1) / Cfg::TILE;
+  const long long my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long nchunks = my_tiles * Cfg::KCH;
 
-  if (warp < 4) {
-    // ---------------- A-side producer (+ thread 0: B loads and MMA issue)
-    const int r = threadIdx.x;  // row of the tile = block
+  if (warp < Cfg::CONV_WARPS) {
+    // ---------------- converters (+ thread 0: B loads and MMA issue)
+    const int r = threadIdx.x >> 1, hh = threadIdx.x & 1;  // tile row, half of the 32-wide chunk
     constexpr uint32_t idesc = idesc_tf32(128, NN);
-    long long it = 0;
-    int ti = 0;
-    double2 pre[16];
-    auto load_chunk = [&](long long tile, int kc) {
+    auto load = [&](long long c, double2 (&pre)[8]) {
+      const long long tile = blockIdx.x + (c / Cfg::KCH) * gridDim.x;
+      const int kc = static_cast<int>(c % Cfg::KCH);
       const long long blk = tile * Cfg::TILE + r;
-      if (blk < nblocks) {
-        const double2* src = reinterpret_cast<const double2*>(x + blk * NN + 32 * kc);
+      if (c < nchunks && blk < nblocks) {
+        const double2* src = reinterpret_cast<const double2*>(x + blk * NN + 32 * kc + 16 * hh);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) pre[j] = __ldg(src + j);
+        for (int j = 0; j < 8; ++j) pre[j] = __ldg(src + j);
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) pre[j] = make_double2(0.0, 0.0);
+        for (int j = 0; j < 8; ++j) pre[j] = make_double2(0.0, 0.0);
       }
     };
-    if (blockIdx.x < ntiles) load_chunk(blockIdx.x, 0);
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
-      const int ab = ti & 1;
-      for (int kc = 0; kc < Cfg::KCH; ++kc, ++it) {
-        const int s = static_cast<int>(it & 1);
-        const uint32_t ph = static_cast<uint32_t>((it >> 1) & 1);
-        uint8_t* st = base + s * Cfg::STAGE;
-        if (it >= 2) mbar_wait(&empty[s], ph ^ 1u);  // MMAs of chunk it-2 retired
-        if (threadIdx.x == 0) {
-          mbar_expect_tx(&b_full[s], 2 * Cfg::BBYTES);
-          const float* hs = hsplit + static_cast<size_t>(kc) * 2 * (Cfg::BBYTES / 4);
-          bulk_load(st + 2 * Cfg::ABYTES, hs, Cfg::BBYTES, &b_full[s]);
-          bulk_load(st + 2 * Cfg::ABYTES + Cfg::BBYTES, hs + Cfg::BBYTES / 4, Cfg::BBYTES, &b_full[s]);
-        }
-        // split this chunk's row into TF32 hi/lo, swizzled 16-byte chunks
-        uint8_t* ah = st + r * 128;
-        uint8_t* al = st + Cfg::ABYTES + r * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float4 h4, l4;
-          split_tf32(pre[2 * c].x, h4.x, l4.x);
-          split_tf32(pre[2 * c].y, h4.y, l4.y);
-          split_tf32(pre[2 * c + 1].x, h4.z, l4.z);
-          split_tf32(pre[2 * c + 1].y, h4.w, l4.w);
-          const int off = (c ^ (r & 7)) << 4;
-          *reinterpret_cast<float4*>(ah + off) = h4;
-          *reinterpret_cast<float4*>(al + off) = l4;
-        }
-        // prefetch the next chunk (possibly of the next tile) into registers
-        {
-          long long nt = tile;
-          int nk = kc + 1;
-          if (nk == Cfg::KCH) {
-            nk = 0;
-            nt = tile + gridDim.x;
-          }
-          if (nt < ntiles) load_chunk(nt, nk);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&a_full[s]);
-        if (threadIdx.x == 0) {
-          mbar_wait(&a_full[s], ph);
-          mbar_wait(&b_full[s], ph);
-          if (kc == 0 && ti >= 2) mbar_wait(&acc_empty[ab], static_cast<uint32_t>(((ti >> 1) & 1) ^ 1));
-          tc_fence_after();
-          const uint32_t sa = smem_u32(st);
-          const uint32_t d = tmem_base + static_cast<uint32_t>(ab * NN);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t ah_d = umma_desc_sw128(sa + 32 * k);
-            const uint64_t al_d = umma_desc_sw128(sa + Cfg::ABYTES + 32 * k);
-            const uint64_t bh_d = umma_desc_sw128(sa + 2 * Cfg::ABYTES + 32 * k);
-            const uint64_t bl_d = umma_desc_sw128(sa + 2 * Cfg::ABYTES + Cfg::BBYTES + 32 * k);
-            mma_tf32(d, ah_d, bh_d, idesc, (kc | k) != 0);
-            mma_tf32(d, ah_d, bl_d, idesc, 1);
-            mma_tf32(d, al_d, bh_d, idesc, 1);
-          }
-          mma_commit(&empty[s]);
-          if (kc == Cfg::KCH - 1) mma_commit(&acc_full[ab]);
-        }
-        __syncwarp();
+    auto step = [&](long long c, double2 (&pre)[8]) {
+      const int s = static_cast<int>(c & 1);
+      const uint32_t ph = static_cast<uint32_t>((c >> 1) & 1);
+      const long long ti = c / Cfg::KCH;
+      const int kc = static_cast<int>(c % Cfg::KCH);
+      const int ab = static_cast<int>(ti & 1);
+      uint8_t* st = base + s * Cfg::STAGE;
+      if (c >= 2) mbar_wait(&empty[s], ph ^ 1u);  // MMAs of chunk c-2 retired
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&b_full[s], 2 * Cfg::BBYTES);
+        const float* hs = hsplit + static_cast<size_t>(kc) * 2 * (Cfg::BBYTES / 4);
+        bulk_load(st + 2 * Cfg::ABYTES, hs, Cfg::BBYTES, &b_full[s]);
+        bulk_load(st + 2 * Cfg::ABYTES + Cfg::BBYTES, hs + Cfg::BBYTES / 4, Cfg::BBYTES, &b_full[s]);
       }
+      uint8_t* ah = st + r * 128;
+      uint8_t* al = st + Cfg::ABYTES + r * 128;
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        float4 h4, l4;
+        split_tf32(pre[2 * c4].x, h4.x, l4.x);
+        split_tf32(pre[2 * c4].y, h4.y, l4.y);
+        split_tf32(pre[2 * c4 + 1].x, h4.z, l4.z);
+        split_tf32(pre[2 * c4 + 1].y, h4.w, l4.w);
+        const int off = ((4 * hh + c4) ^ (r & 7)) << 4;
+        *reinterpret_cast<float4*>(ah + off) = h4;
+        *reinterpret_cast<float4*>(al + off) = l4;
+      }
+      load(c + 2, pre);  // two chunks in flight per thread
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a_full[s]);
+      if (threadIdx.x == 0) {
+        mbar_wait(&a_full[s], ph);
+        mbar_wait(&b_full[s], ph);
+        if (kc == 0 && ti >= 2) mbar_wait(&acc_empty[ab], static_cast<uint32_t>(((ti >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t sa = smem_u32(st);
+        const uint32_t d = tmem_base + static_cast<uint32_t>(ab * NN);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t ah_d = umma_desc_sw128(sa + 32 * k);
+          const uint64_t al_d = umma_desc_sw128(sa + Cfg::ABYTES + 32 * k);
+          const uint64_t bh_d = umma_desc_sw128(sa + 2 * Cfg::ABYTES + 32 * k);
+          const uint64_t bl_d = umma_desc_sw128(sa + 2 * Cfg::ABYTES + Cfg::BBYTES + 32 * k);
+          mma_tf32(d, ah_d, bh_d, idesc, (kc | k) != 0);
+          mma_tf32(d, ah_d, bl_d, idesc, 1);
+          mma_tf32(d, al_d, bh_d, idesc, 1);
+        }
+        mma_commit(&empty[s]);
+        if (kc == Cfg::KCH - 1) mma_commit(&acc_full[ab]);
+      }
+      __syncwarp();
+    };
+    double2 pre0[8], pre1[8];
+    load(0, pre0);
+    load(1, pre1);
+    for (long long c = 0; c < nchunks; c += 2) {
+      step(c, pre0);
+      if (c + 1 < nchunks) step(c + 1, pre1);
     }
   } else {
-    // ---------------- epilogue: TMEM -> FP64 Y
-    const int q = warp - 4;
+    // ---------------- epilogue: TMEM -> FP64 -> staged rows -> coalesced stores
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* stg = epi + (warp - Cfg::CONV_WARPS) * Cfg::EPI_BYTES;
     int ti = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
       const int ab = ti & 1;
       mbar_wait(&acc_full[ab], static_cast<uint32_t>((ti >> 1) & 1));
       tc_fence_after();
-      const long long blk = tile * Cfg::TILE + 32 * q + lane;
+      const long long row0 = tile * Cfg::TILE + 32 * q;  // first block of this warp's 32 rows
 #pragma unroll 1
-      for (int c = 0; c < NN / 32; ++c) {
-        uint32_t v[32];
+      for (int c = 0; c < NN / 16; ++c) {
+        uint32_t v[16];
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) +
-                               static_cast<uint32_t>(ab * NN + 32 * c);
+                               static_cast<uint32_t>(ab * NN + 16 * c);
         asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-            "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
               "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              "=r"(v[14]), "=r"(v[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (blk < nblocks) {
-          double2* dst = reinterpret_cast<double2*>(y + blk * NN + 32 * c);
+        double2* myrow = reinterpret_cast<double2*>(stg + lane * Cfg::EPI_STRIDE);
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            dst[j] = make_double2(static_cast<double>(__uint_as_float(v[2 * j])),
+        for (int j = 0; j < 8; ++j)
+          myrow[j] = make_double2(static_cast<double>(__uint_as_float(v[2 * j])),
                                   static_cast<double>(__uint_as_float(v[2 * j + 1])));
+        __syncwarp();
+        // 32 rows x 128 B: 8 lanes per row, 4 rows per pass
+#pragma unroll
+        for (int ps = 0; ps < 8; ++ps) {
+          const int rr = 4 * ps + (lane >> 3), ch = lane & 7;
+          const long long blk = row0 + rr;
+          if (blk < nblocks)
+            *reinterpret_cast<double2*>(y + blk * NN + 16 * c + 2 * ch) =
+                *reinterpret_cast<const double2*>(stg + rr * Cfg::EPI_STRIDE + ch * 16);
         }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[ab]);
@@ -324,7 +336,7 @@ dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d
       attr = true;
     }
     const long long ntiles = (nb + Cfg::TILE - 1) / Cfg::TILE;
-    k_coef_tf32x3<64><<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), 256, Cfg::SMEM, st>>>(
+    k_coef_tf32x3<64><<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), Cfg::THREADS, Cfg::SMEM, st>>>(
         d_in, static_cast<const float*>(p->d_hsplit), d_out, nb);
   } else {
     using Cfg = TcCfg<256>;
@@ -335,7 +347,7 @@ dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d
       attr = true;
     }
     const long long ntiles = (nb + Cfg::TILE - 1) / Cfg::TILE;
-    k_coef_tf32x3<256><<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), 256, Cfg::SMEM, st>>>(
+    k_coef_tf32x3<256><<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), Cfg::THREADS, Cfg::SMEM, st>>>(
         d_in, static_cast<const float*>(p->d_hsplit), d_out, nb);
   }
   add_launches(1);
