@@ -8,8 +8,8 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-O3 -Xptxas -v --ex
 
 all: $(PKG)/libdctf_b200.so $(PKG)/libdctf_synth.so oracle cpp-test cli
 
-$(PKG)/libdctf_b200.so: $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/plan.cc $(CSRC)/internal.h include/dctf.h
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/plan.cc 2> build_ptxas.log || (cat build_ptxas.log; false)
+$(PKG)/libdctf_b200.so: $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/ozaki.cu $(CSRC)/plan.cc $(CSRC)/internal.h include/dctf.h
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/ozaki.cu $(CSRC)/plan.cc 2> build_ptxas.log || (cat build_ptxas.log; false)
 
 $(PKG)/libdctf_synth.so: $(CSRC)/synth.cc
 	g++ -O3 -std=c++17 -fPIC -shared -pthread -o $@ $<

@@ -46,7 +46,12 @@ inline void check(dctf_status s) {
 
 enum class PaddingMode { kZero = DCTF_PAD_ZERO, kReplicate = DCTF_PAD_REPLICATE };
 enum class Domain { kSpatial, kDct };
-enum class Precision { kFp64 = DCTF_PREC_FP64, kTf32x3 = DCTF_PREC_TF32X3, kBf16x3 = DCTF_PREC_BF16X3 };
+enum class Precision {
+  kFp64 = DCTF_PREC_FP64,
+  kTf32x3 = DCTF_PREC_TF32X3,
+  kBf16x3 = DCTF_PREC_BF16X3,
+  kInt8Exact = DCTF_PREC_INT8_EXACT
+};
 
 class BlockMatrix {
  public:

@@ -22,7 +22,7 @@ lib = C.CDLL(LIB_PATH)
 
 OK, INVALID_ARGUMENT, CUDA_ERROR, NAN_ENCOUNTERED, UNSUPPORTED = range(5)
 PAD_ZERO, PAD_REPLICATE = 0, 1
-PREC_FP64, PREC_TF32X3, PREC_BF16X3 = 0, 1, 2
+PREC_FP64, PREC_TF32X3, PREC_BF16X3, PREC_INT8_EXACT = 0, 1, 2, 3
 
 _d = C.POINTER(C.c_double)
 _u8 = C.POINTER(C.c_uint8)

@@ -28,6 +28,8 @@ struct dctf_plan {
   double* d_hcoef = nullptr;     // H in coefficient-kernel fragment order
   double* d_hfused = nullptr;    // H in fused-kernel fragment order
   void* d_hsplit = nullptr;      // TF32 hi/lo split of H, swizzled (precision TF32X3)
+  void* d_gimg = nullptr;        // INT8 digit slices of H (C (x) C), swizzled (INT8_EXACT)
+  double* d_gscale = nullptr;    // per-row scales of those slices
   int* d_nan = nullptr;          // NaN flag
   double* d_weights = nullptr;   // mask, kr*kc (spatial path)
 
@@ -67,6 +69,13 @@ void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out
 void layout_hfused8(const std::vector<double>& op, std::vector<double>& out);
 void layout_hfused16(const std::vector<double>& op, std::vector<double>& out);
 void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>& out);
+void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>& basis,
+                       std::vector<int8_t>& bimg, std::vector<double>& scales);
+
+// Exact-INT8 tcgen05 fused n=8 path (ozaki.cu).
+dctf_status upload_i8_operator(dctf_plan* p);
+dctf_status launch_fused8_i8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
+                             long long frame_stride, int nframes, double* coef_out, cudaStream_t st, int sms);
 
 // 3xTF32 tcgen05 coefficient filter (tc.cu).
 dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d_out, long long nb,

@@ -1300,7 +1300,10 @@ dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, 
 dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
                                 cudaStream_t st) {
-  const bool split = p->precision != DCTF_PREC_FP64;
+  if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT)
+    return dctf::launch_fused8_i8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st,
+                                  sm_count(p->device));
+  const bool split = p->precision == DCTF_PREC_TF32X3;
   if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (!split && !std::getenv("DCTF_N16_UNFUSED"))
     return launch_fused16(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
@@ -1387,6 +1390,13 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     dctf_plan_destroy(p);
     return set_error(DCTF_CUDA_ERROR, "plan upload: " + msg);
   }
+  if (precision == DCTF_PREC_INT8_EXACT && n == 8) {
+    const dctf_status s = dctf::upload_i8_operator(p);
+    if (s != DCTF_OK) {
+      dctf_plan_destroy(p);
+      return s;
+    }
+  }
   *out = p;
   return DCTF_OK;
 }
@@ -1399,7 +1409,7 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
   dctf::reset_launches();
   if (!out || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
-  if (precision != DCTF_PREC_FP64 && precision != DCTF_PREC_TF32X3 && precision != DCTF_PREC_BF16X3)
+  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_INT8_EXACT)
     return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
   if (kr < 1 || kc < 1) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
   auto* p = new dctf_plan();
@@ -1423,7 +1433,7 @@ dctf_status dctf_plan_create_from_dump(const char* text, size_t len, int precisi
   dctf::reset_launches();
   if (!out || !text) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
-  if (precision != DCTF_PREC_FP64 && precision != DCTF_PREC_TF32X3 && precision != DCTF_PREC_BF16X3)
+  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_INT8_EXACT)
     return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
   auto* p = new dctf_plan();
   p->precision = precision;
@@ -1511,6 +1521,8 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_hcoef);
     cudaFree(p->d_hfused);
     cudaFree(p->d_hsplit);
+    cudaFree(p->d_gimg);
+    cudaFree(p->d_gscale);
     cudaFree(p->d_nan);
     cudaFree(p->d_weights);
     cudaFree(p->io_in);

@@ -1,0 +1,416 @@
+// k_fused8_i8: the 8x8 spatial-in/spatial-out DCT-domain filter with the
+// DCT-domain contraction done EXACTLY on the INT8 tensor cores
+// (tcgen05.mma kind::i8, int32 accumulators in TMEM), sm_100a.
+//
+// Math (precision DCTF_PREC_INT8_EXACT). Pixels p are exact integers, so the
+// first linear stage applied to them can run in integer arithmetic without
+// loss: G = H_dct (C (x) C) (forward DCT composed with the DCT-domain operator,
+// one 64x64 FP64 matrix per plan) is written per output row as 7 signed
+// 7-bit digits (plan.cc: layout_gslices_i8), every partial D_s = d_s . p is
+// an exact int32, and the filtered DCT coefficients
+//     Y[o] = 2^(e_o - 48) * sum_s D_s[o] 2^(7(7-s))
+// are recombined in FP64 with a relative error ~2^-49 — FP64-class, the same
+// tolerance class as the DMMA path (coefficients are also exported in parity
+// mode). The inverse DCT O = C^t Y C + 0.5 and the round/clamp stay on the
+// FP64 pipe: 4 DMMA (1,024 FMA) + 256 recombination FMAs per block instead of
+// the 24 DMMA (6,144 FMA) of k_fused8. The forward DCT is folded into G (one
+// precomputed operator per plan); Y, the DCT-domain filtered coefficients, is
+// materialised exactly as in the FP64 chain.
+//
+// CTA = 16 warps, one CTA per SM, persistent over tiles of 128 horizontally
+// adjacent blocks (a strip of 8 rows x 1024 px):
+//   warps 0-3  producers: thread b gathers block b's 8x8 pixels (8-byte
+//              coalesced loads, one tile ahead in registers) into the K-major
+//              A tile (128 B rows, 128B swizzle, 64 bytes used); thread 0
+//              issues the 4 MMAs (2 K-steps x N = 256 + 192 columns) per tile.
+//   warps 4-7  drain: thread = block = TMEM lane; tcgen05.ld the 448 int32
+//              partials, recombine FP64 Y into a double-buffered shared tile
+//              (k_fused8's swizzled layout), release TMEM.
+//   warps 8-15 compute: k_fused8's inverse DMMA chain (O = C^t Y C + 0.5) on
+//              16 blocks per warp, floor-quantise, coalesced strip stores.
+// The 56 KB digit image (B operand) stays resident in shared memory.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "internal.h"
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint8_t* align1024(uint8_t* smem) {
+  const uint32_t pad = (1024u - (smem_u32(smem) & 1023u)) & 1023u;
+  return smem + pad;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t addr = smem_u32(bar);
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(2u) << 61;
+  return d;
+}
+// kind::i8: A unsigned 8-bit, B signed 8-bit, D s32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+__device__ __forceinline__ void dmma(double2& d, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d.x), "+d"(d.y)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ uint32_t floor_to_u8(double t) {
+  int i;
+  asm("cvt.rmi.s32.f64 %0, %1;" : "=r"(i) : "d"(t));
+  return static_cast<uint32_t>(min(max(i, 0), 255));
+}
+
+namespace oz {
+constexpr int TILE = 128;
+constexpr int S = 7;
+constexpr int NCOL = S * 64;            // 448 accumulator columns
+constexpr int BBYTES = NCOL * 128;      // resident digit image
+constexpr int ABYTES = TILE * 128;      // one A stage
+constexpr int YBYTES = TILE * 512;      // one FP64 Y tile (64 doubles per block)
+constexpr int PS = 144;                 // compute-warp pixel staging row stride
+constexpr int PIXBYTES = 8 * PS;
+constexpr int PROD = 4, DRAIN = 4, COMP = 8;
+constexpr int THREADS = 32 * (PROD + DRAIN + COMP);
+constexpr int SMEM = 1024 + BBYTES + 2 * ABYTES + 2 * YBYTES + COMP * PIXBYTES;
+// Y tile layout = k_fused8's X/Y staging: block b owns 512 B = 4 rows x 8
+// chunks of 16 B; logical (row r, chunk c) holds Y[2r][c], Y[2r+1][c] and is
+// stored at chunk c ^ 2r ^ f(b), f(b) = (b&7) ^ ((b&1)<<2).
+__device__ __forceinline__ int fsw(int b) { return (b & 7) ^ ((b & 1) << 2); }
+}  // namespace oz
+
+__global__ void __launch_bounds__(oz::THREADS, 1)
+    k_fused8_i8(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
+                long long frame_stride, int nframes, int bw, int bh, int nsx,
+                const int8_t* __restrict__ gimg, const double* __restrict__ gscale,
+                const double* __restrict__ cb, double* __restrict__ coef_out) {
+  using namespace oz;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = align1024(smem_raw);
+  uint8_t* bsm = base;                       // digit image
+  uint8_t* asm_ = base + BBYTES;             // 2 A stages
+  uint8_t* ysm = asm_ + 2 * ABYTES;          // 2 Y tiles
+  uint8_t* psm = ysm + 2 * YBYTES;           // compute-warp pixel staging
+  __shared__ uint64_t a_full[2], a_empty[2], acc_full, acc_empty, y_full[2], y_empty[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ double sc_s[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(gimg);
+    uint4* dst = reinterpret_cast<uint4*>(bsm);
+    for (int i = threadIdx.x; i < BBYTES / 16; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x < 64) sc_s[threadIdx.x] = gscale[threadIdx.x];
+  }
+  if (warp == PROD) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a_full[i], 32 * PROD);
+      mbar_init(&a_empty[i], 1);
+      mbar_init(&y_full[i], 32 * DRAIN);
+      mbar_init(&y_empty[i], COMP);
+    }
+    mbar_init(&acc_full, 1);
+    mbar_init(&acc_empty, 32 * DRAIN);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  const long long spf = static_cast<long long>(bh) * nsx;
+  const long long ntiles = spf * nframes;
+  const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 7) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
+  auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {
+    f = static_cast<int>(ti / spf);
+    const long long rem = ti - static_cast<long long>(f) * spf;
+    by = static_cast<int>(rem / nsx);
+    bx0 = static_cast<int>(rem - static_cast<long long>(by) * nsx) * TILE;
+  };
+  auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && (bx0 + TILE) * 8 <= w; };
+
+  if (warp < PROD) {
+    // ---------------- producers: block b = threadIdx.x gathers its 8 pixel rows
+    const int b = threadIdx.x;
+    constexpr uint32_t id256 = idesc_i8(128, 256), id192 = idesc_i8(128, 192);
+    uint2 pre[8];
+    auto load = [&](long long ti) {
+      int f, by, bx0;
+      tile_at(ti, f, by, bx0);
+      const uint8_t* ib = in + f * frame_stride;
+      if (is_fast(by, bx0)) {
+        const uint8_t* p = ib + static_cast<size_t>(by * 8) * pitch + (bx0 + b) * 8;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) pre[r] = __ldg(reinterpret_cast<const uint2*>(p + r * pitch));
+      } else {  // ragged: tile()'s edge replication, byte by byte
+#pragma unroll 1
+        for (int r = 0; r < 8; ++r) {
+          const int y = min(by * 8 + r, h - 1);
+          uint32_t lo = 0, hi = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int x = min((bx0 + b) * 8 + j, w - 1);
+            const uint32_t v = ib[static_cast<size_t>(y) * pitch + x];
+            if (j < 4) lo |= v << (8 * j);
+            else hi |= v << (8 * (j - 4));
+          }
+          pre[r] = make_uint2(lo, hi);
+        }
+      }
+    };
+    long long tl = 0;
+    if (blockIdx.x < ntiles) load(blockIdx.x);
+    for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+      const int s = static_cast<int>(tl & 1);
+      const uint32_t ph = static_cast<uint32_t>((tl >> 1) & 1);
+      uint8_t* ast = asm_ + s * ABYTES;
+      if (tl >= 2) mbar_wait(&a_empty[s], ph ^ 1u);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(ast + b * 128 + ((c ^ (b & 7)) << 4)) =
+            make_uint4(pre[2 * c].x, pre[2 * c].y, pre[2 * c + 1].x, pre[2 * c + 1].y);
+      if (ti + gridDim.x < ntiles) load(ti + gridDim.x);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a_full[s]);
+      if (threadIdx.x == 0) {
+        mbar_wait(&a_full[s], ph);
+        if (tl >= 1) mbar_wait(&acc_empty, static_cast<uint32_t>((tl - 1) & 1));
+        tc_fence_after();
+        const uint32_t sa = smem_u32(ast), sb = smem_u32(bsm);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t ad = umma_desc_sw128(sa + 32 * ks);
+          mma_i8(tmem_base, ad, umma_desc_sw128(sb + 32 * ks), id256, ks);
+          mma_i8(tmem_base + 256, ad, umma_desc_sw128(sb + 256 * 128 + 32 * ks), id192, ks);
+        }
+        mma_commit(&a_empty[s]);
+        mma_commit(&acc_full);
+      }
+      __syncwarp();
+    }
+  } else if (warp < PROD + DRAIN) {
+    // ---------------- drain: thread = block = TMEM lane; int32 partials -> FP64 Y (shared)
+    const int q = warp & 3, b = 32 * q + lane;
+    const uint32_t tla = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+    long long tl = 0;
+    for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+      int f, by, bx0;
+      tile_at(ti, f, by, bx0);
+      const int yb = static_cast<int>(tl & 1);
+      uint8_t* yt = ysm + yb * YBYTES + b * 512;
+      mbar_wait(&acc_full, static_cast<uint32_t>(tl & 1));
+      if (tl >= 2) mbar_wait(&y_empty[yb], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
+      tc_fence_after();
+      double* cdst = (coef_out && bx0 + b < bw)
+                         ? coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx0 + b) * 64
+                         : nullptr;
+#pragma unroll 1
+      for (int t = 0; t < 4; ++t) {  // Y rows u = 2t, 2t+1 (outputs 16t .. 16t+15)
+        double yr[2][8];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int o0 = 16 * t + 8 * i;
+          int32_t d[8], e[8], p1[8], p2[8], p3[8];
+          tmem_ld8(tla + 0 * 64 + o0, d);
+          tmem_ld8(tla + 1 * 64 + o0, e);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j) p1[j] = d[j] * 128 + e[j];
+          tmem_ld8(tla + 2 * 64 + o0, d);
+          tmem_ld8(tla + 3 * 64 + o0, e);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j) p2[j] = d[j] * 128 + e[j];
+          tmem_ld8(tla + 4 * 64 + o0, d);
+          tmem_ld8(tla + 5 * 64 + o0, e);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j) p3[j] = d[j] * 128 + e[j];
+          tmem_ld8(tla + 6 * 64 + o0, d);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double sc = sc_s[o0 + j];
+            double v = static_cast<double>(d[j]) * sc;
+            v = fma(static_cast<double>(p3[j]), sc * 128.0, v);
+            v = fma(static_cast<double>(p2[j]), sc * 2097152.0, v);               // 2^21
+            yr[i][j] = fma(static_cast<double>(p1[j]), sc * 34359738368.0, v);   // 2^35
+          }
+        }
+        // logical (row t, chunk v) = (Y[2t][v], Y[2t+1][v])
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<double2*>(yt + t * 128 + ((v ^ (2 * t) ^ fsw(b)) << 4)) =
+              make_double2(yr[0][v], yr[1][v]);
+        if (cdst) {
+          double2* c2 = reinterpret_cast<double2*>(cdst + 16 * t);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            c2[j] = make_double2(yr[0][2 * j], yr[0][2 * j + 1]);
+            c2[4 + j] = make_double2(yr[1][2 * j], yr[1][2 * j + 1]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty);  // TMEM free for the next tile's MMAs
+      mbar_arrive(&y_full[yb]);
+    }
+  } else {
+    // ---------------- compute: inverse DCT (k_fused8's DMMA chain) of 16 blocks per warp
+    const int cw = warp - PROD - DRAIN;  // 0..7, blocks 16cw .. 16cw+15
+    const int g = lane >> 2, t = lane & 3;
+    const double ai0 = cb[(2 * t) * 8 + g], ai1 = cb[(2 * t + 1) * 8 + g];
+    uint8_t* pix = psm + cw * PIXBYTES;
+    const int r0 = lane >> 3, c16 = (lane & 7) * 16;
+    long long tl = 0;
+    for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+      int f, by, bx0;
+      tile_at(ti, f, by, bx0);
+      const int yb = static_cast<int>(tl & 1);
+      const uint8_t* yt = ysm + yb * YBYTES;
+      mbar_wait(&y_full[yb], static_cast<uint32_t>((tl >> 1) & 1));
+#pragma unroll
+      for (int bb = 0; bb < 16; bb += 4) {
+        double2 yv[4], z[4], o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int b = 16 * cw + bb + i;
+          yv[i] = *reinterpret_cast<const double2*>(yt + b * 512 + t * 128 + ((g ^ (2 * t) ^ fsw(b)) << 4));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { z[i] = make_double2(0.0, 0.0); dmma(z[i], ai0, yv[i].x); }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dmma(z[i], ai1, yv[i].y);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { o[i] = make_double2(0.5, 0.5); dmma(o[i], z[i].x, ai0); }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dmma(o[i], z[i].y, ai1);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t qv = floor_to_u8(o[i].x) | (floor_to_u8(o[i].y) << 8);
+          *reinterpret_cast<uint16_t*>(pix + g * PS + 8 * (bb + i) + 2 * t) = static_cast<uint16_t>(qv);
+        }
+      }
+      __syncwarp();
+      __threadfence_block();  // this warp's Y reads have landed before the tile is released
+      if (lane == 0) mbar_arrive(&y_empty[yb]);
+      uint8_t* ob = out + f * frame_stride;
+      const int bx = bx0 + 16 * cw;
+      if (is_fast(by, bx0)) {
+        uint8_t* p = ob + static_cast<size_t>(by * 8) * pitch + bx * 8 + c16;
+        *reinterpret_cast<uint4*>(p + r0 * pitch) = *reinterpret_cast<const uint4*>(pix + r0 * PS + c16);
+        *reinterpret_cast<uint4*>(p + (r0 + 4) * pitch) = *reinterpret_cast<const uint4*>(pix + (r0 + 4) * PS + c16);
+      } else {
+        for (int e = lane; e < 8 * 128; e += 32) {
+          const int r = e >> 7, c = e & 127;
+          const int yy = by * 8 + r, xx = bx * 8 + c;
+          if (yy < h && xx < w) ob[static_cast<size_t>(yy) * pitch + xx] = pix[r * PS + c];
+        }
+      }
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == PROD)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+}  // namespace
+
+namespace dctf {
+
+dctf_status upload_i8_operator(dctf_plan* p) {
+  std::vector<int8_t> img;
+  std::vector<double> sc;
+  layout_gslices_i8(p->op, p->basis, img, sc);
+  cudaError_t e = cudaMalloc(&p->d_gimg, img.size());
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_gscale, sc.size() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_gimg, img.data(), img.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_gscale, sc.data(), sc.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("int8 operator upload: ") + cudaGetErrorString(e));
+  return DCTF_OK;
+}
+
+dctf_status launch_fused8_i8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
+                             long long frame_stride, int nframes, double* coef_out, cudaStream_t st, int sms) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_fused8_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM) != cudaSuccess)
+      return set_error(DCTF_CUDA_ERROR, "cudaFuncSetAttribute(k_fused8_i8)");
+    attr = true;
+  }
+  const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + oz::TILE - 1) / oz::TILE;
+  const long long ntiles = static_cast<long long>(bh) * nsx * nframes;
+  if (ntiles <= 0) return DCTF_OK;
+  k_fused8_i8<<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), oz::THREADS, oz::SMEM, st>>>(
+      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, static_cast<const int8_t*>(p->d_gimg),
+      p->d_gscale, p->d_basis, coef_out);
+  add_launches(1);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_fused8_i8: ") + cudaGetErrorString(e));
+  return DCTF_OK;
+}
+
+}  // namespace dctf

@@ -19,6 +19,7 @@
 // the convolve formula (spatial.hpp:36-37) for H_spatial and
 // H = (C (x) C) H_spatial (C (x) C)^t; for reference-domain masks both
 // constructions agree to ~1e-15 (tests/test_host_api.py).
+#include <algorithm>
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
@@ -438,6 +439,55 @@ void layout_hfused16(const std::vector<double>& op, std::vector<double>& out) {
             const int kcol = coef(8 * kc + 4 * q + t, e);
             out[o++] = op[size_t(orow) * 256 + kcol];
           }
+}
+
+// Exact INT8 slicing of the forward-DCT-composed operator for k_fused8_i8.
+// G = H (C (x) C) maps a block's 64 pixels p (index i*8+j) straight to its
+// filtered DCT coefficients Y (index u*8+v). Row o of G is scaled by 2^-e_o
+// (e_o: smallest power of two >= max_k |G[o][k]|) and written as S = 7
+// signed digits in [-64, 64]:
+//   G[o][k] 2^-e_o = sum_s d_s[o][k] 2^-(6 + 7(s-1)) + err,  |err| <= 2^-49.
+// With u8 pixels every partial D_s = d_s . p is an exact int32 (|D_s| < 2^20),
+// so Y[o] = 2^(e_o - 48) sum_s D_s 2^(7(7-s)) is FP64-accurate.
+// Output: the swizzled UMMA B image, row n = s*64 + o (448 rows), 128 bytes per
+// row with the 64 digit bytes of K = pixel index in the first 64 bytes
+// (16-byte chunk c of row n stored at chunk c ^ (n & 7)); scales[o] =
+// 2^(e_o - 48).
+void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>& basis,
+                       std::vector<int8_t>& bimg, std::vector<double>& scales) {
+  constexpr int S = 7;
+  std::vector<long double> g(64 * 64, 0.0L);
+  for (int o = 0; o < 64; ++o)
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) {
+        long double acc = 0.0L;
+        for (int u = 0; u < 8; ++u)
+          for (int v = 0; v < 8; ++v)
+            acc += static_cast<long double>(op[size_t(o) * 64 + u * 8 + v]) *
+                   (static_cast<long double>(basis[u * 8 + i]) * basis[v * 8 + j]);
+        g[o * 64 + i * 8 + j] = acc;
+      }
+  bimg.assign(size_t(S) * 64 * 128, 0);
+  scales.assign(64, 0.0);
+  for (int o = 0; o < 64; ++o) {
+    long double rowmax = 0.0L;
+    for (int k = 0; k < 64; ++k) rowmax = std::max(rowmax, std::fabs(g[o * 64 + k]));
+    int e = 0;
+    if (rowmax > 0.0L) {
+      std::frexp(static_cast<double>(rowmax), &e);  // rowmax < 2^e
+    }
+    scales[o] = std::ldexp(1.0, e - 48);
+    for (int k = 0; k < 64; ++k) {
+      long double r = std::ldexp(g[o * 64 + k], -e) * 64.0L;  // in units of 2^-6
+      for (int sl = 0; sl < S; ++sl) {
+        const long double d = std::nearbyint(r);
+        r = (r - d) * 128.0L;
+        const int n = sl * 64 + o;
+        const size_t pos = size_t(n) * 128 + ((((k >> 4) ^ (n & 7)) << 4) | (k & 15));
+        bimg[pos] = static_cast<int8_t>(d);
+      }
+    }
+  }
 }
 
 }  // namespace dctf

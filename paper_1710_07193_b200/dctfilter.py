@@ -50,6 +50,7 @@ class Precision(enum.IntEnum):
     kFp64 = _lib.PREC_FP64
     kTf32x3 = _lib.PREC_TF32X3
     kBf16x3 = _lib.PREC_BF16X3
+    kInt8Exact = _lib.PREC_INT8_EXACT
 
 
 class Mask:
