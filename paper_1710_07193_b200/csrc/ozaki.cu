@@ -23,10 +23,12 @@
 //              coalesced loads, one tile ahead in registers) into the K-major
 //              A tile (128 B rows, 128B swizzle, 64 bytes used); thread 0
 //              issues the 4 MMAs (2 K-steps x N = 256 + 192 columns) per tile.
-//   warps 4-7  drain: thread = block = TMEM lane; tcgen05.ld the 448 int32
-//              partials, recombine FP64 Y into a double-buffered shared tile
-//              (k_fused8's swizzled layout), release TMEM.
-//   warps 8-15 compute: k_fused8's inverse DMMA chain (O = C^t Y C + 0.5) on
+//   warps 4-11 drain: thread = block = TMEM lane (two warps per lane quarter,
+//              each half of the outputs); tcgen05.ld the int32 partials,
+//              recombine exactly in int64, scale to FP64 Y in a
+//              double-buffered shared tile (k_fused8's swizzled layout),
+//              release TMEM so the next tile's MMAs start.
+//   warps 12-19 compute: k_fused8's inverse DMMA chain (O = C^t Y C + 0.5) on
 //              16 blocks per warp, floor-quantise, coalesced strip stores.
 // The 56 KB digit image (B operand) stays resident in shared memory.
 #include <cuda.h>
@@ -120,9 +122,10 @@ constexpr int NCOL = S * 64;            // 448 accumulator columns
 constexpr int BBYTES = NCOL * 128;      // resident digit image
 constexpr int ABYTES = TILE * 128;      // one A stage
 constexpr int YBYTES = TILE * 512;      // one FP64 Y tile (64 doubles per block)
-constexpr int PS = 144;                 // compute-warp pixel staging row stride
+constexpr int PS = 144;                 // compute-warp pixel staging row stride (16 blocks)
 constexpr int PIXBYTES = 8 * PS;
-constexpr int PROD = 4, DRAIN = 4, COMP = 8;
+constexpr int PROD = 4, DRAIN = 8, COMP = 8;
+constexpr int CB = TILE / COMP;          // blocks per compute warp
 constexpr int THREADS = 32 * (PROD + DRAIN + COMP);
 constexpr int SMEM = 1024 + BBYTES + 2 * ABYTES + 2 * YBYTES + COMP * PIXBYTES;
 // Y tile layout = k_fused8's X/Y staging: block b owns 512 B = 4 rows x 8
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r) pre[r] = __ldg(reinterpret_cast<const uint2*>(p + r * pitch));
       } else {  // ragged: tile()'s edge replication, byte by byte
-#pragma unroll 1
+#pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int y = min(by * 8 + r, h - 1);
           uint32_t lo = 0, hi = 0;
@@ -249,8 +252,10 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       __syncwarp();
     }
   } else if (warp < PROD + DRAIN) {
-    // ---------------- drain: thread = block = TMEM lane; int32 partials -> FP64 Y (shared)
-    const int q = warp & 3, b = 32 * q + lane;
+    // ---------------- drain: thread = block = TMEM lane; int32 partials -> FP64 Y (shared).
+    // Two warps share each TMEM lane quarter and split the outputs: Y rows
+    // u = 0..3 (half 0) and u = 4..7 (half 1).
+    const int q = warp & 3, b = 32 * q + lane, dh = (warp - PROD) >> 2;
     const uint32_t tla = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
     long long tl = 0;
     for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
@@ -265,37 +270,33 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                          ? coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx0 + b) * 64
                          : nullptr;
 #pragma unroll 1
-      for (int t = 0; t < 4; ++t) {  // Y rows u = 2t, 2t+1 (outputs 16t .. 16t+15)
+      for (int t = 2 * dh; t < 2 * dh + 2; ++t) {  // Y rows u = 2t, 2t+1 (outputs 16t .. 16t+15)
         double yr[2][8];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int o0 = 16 * t + 8 * i;
-          int32_t d[8], e[8], p1[8], p2[8], p3[8];
+          // exact int64 recombination: sum_s D_s 2^(7(6-s)) < 2^63, then one
+          // conversion and one power-of-two scale per output
+          int32_t d[8], e[8];
+          long long acc[8];
           tmem_ld8(tla + 0 * 64 + o0, d);
           tmem_ld8(tla + 1 * 64 + o0, e);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 8; ++j) p1[j] = d[j] * 128 + e[j];
-          tmem_ld8(tla + 2 * 64 + o0, d);
-          tmem_ld8(tla + 3 * 64 + o0, e);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int j = 0; j < 8; ++j) acc[j] = static_cast<long long>(d[j]) * 128 + e[j];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) p2[j] = d[j] * 128 + e[j];
-          tmem_ld8(tla + 4 * 64 + o0, d);
-          tmem_ld8(tla + 5 * 64 + o0, e);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int sl = 2; sl < 6; sl += 2) {
+            tmem_ld8(tla + sl * 64 + o0, d);
+            tmem_ld8(tla + (sl + 1) * 64 + o0, e);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 8; ++j) p3[j] = d[j] * 128 + e[j];
+            for (int j = 0; j < 8; ++j) acc[j] = (acc[j] << 14) + static_cast<long long>(d[j] * 128 + e[j]);
+          }
           tmem_ld8(tla + 6 * 64 + o0, d);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const double sc = sc_s[o0 + j];
-            double v = static_cast<double>(d[j]) * sc;
-            v = fma(static_cast<double>(p3[j]), sc * 128.0, v);
-            v = fma(static_cast<double>(p2[j]), sc * 2097152.0, v);               // 2^21
-            yr[i][j] = fma(static_cast<double>(p1[j]), sc * 34359738368.0, v);   // 2^35
-          }
+          for (int j = 0; j < 8; ++j)
+            yr[i][j] = static_cast<double>((acc[j] << 7) + d[j]) * sc_s[o0 + j];
         }
         // logical (row t, chunk v) = (Y[2t][v], Y[2t+1][v])
 #pragma unroll
@@ -316,12 +317,11 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       mbar_arrive(&y_full[yb]);
     }
   } else {
-    // ---------------- compute: inverse DCT (k_fused8's DMMA chain) of 16 blocks per warp
-    const int cw = warp - PROD - DRAIN;  // 0..7, blocks 16cw .. 16cw+15
+    // ---------------- compute: inverse DCT (k_fused8's DMMA chain) of CB blocks per warp
+    const int cw = warp - PROD - DRAIN;  // blocks CB*cw .. CB*cw + CB-1
     const int g = lane >> 2, t = lane & 3;
     const double ai0 = cb[(2 * t) * 8 + g], ai1 = cb[(2 * t + 1) * 8 + g];
     uint8_t* pix = psm + cw * PIXBYTES;
-    const int r0 = lane >> 3, c16 = (lane & 7) * 16;
     long long tl = 0;
     for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
       int f, by, bx0;
@@ -329,12 +329,12 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       const int yb = static_cast<int>(tl & 1);
       const uint8_t* yt = ysm + yb * YBYTES;
       mbar_wait(&y_full[yb], static_cast<uint32_t>((tl >> 1) & 1));
-#pragma unroll
-      for (int bb = 0; bb < 16; bb += 4) {
+#pragma unroll 2
+      for (int bb = 0; bb < CB; bb += 4) {
         double2 yv[4], z[4], o[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int b = 16 * cw + bb + i;
+          const int b = CB * cw + bb + i;
           yv[i] = *reinterpret_cast<const double2*>(yt + b * 512 + t * 128 + ((g ^ (2 * t) ^ fsw(b)) << 4));
         }
 #pragma unroll
@@ -355,14 +355,19 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       __threadfence_block();  // this warp's Y reads have landed before the tile is released
       if (lane == 0) mbar_arrive(&y_empty[yb]);
       uint8_t* ob = out + f * frame_stride;
-      const int bx = bx0 + 16 * cw;
+      const int bx = bx0 + CB * cw;
       if (is_fast(by, bx0)) {
-        uint8_t* p = ob + static_cast<size_t>(by * 8) * pitch + bx * 8 + c16;
-        *reinterpret_cast<uint4*>(p + r0 * pitch) = *reinterpret_cast<const uint4*>(pix + r0 * PS + c16);
-        *reinterpret_cast<uint4*>(p + (r0 + 4) * pitch) = *reinterpret_cast<const uint4*>(pix + (r0 + 4) * PS + c16);
+        // 8 rows x 8*CB bytes, 16-byte chunks
+#pragma unroll
+        for (int ps = 0; ps < CB / 8; ++ps) {
+          const int chunks = CB / 2;  // per row
+          const int e = ps * 32 + lane, r = e / chunks, c = (e % chunks) * 16;
+          *reinterpret_cast<uint4*>(ob + static_cast<size_t>(by * 8 + r) * pitch + bx * 8 + c) =
+              *reinterpret_cast<const uint4*>(pix + r * PS + c);
+        }
       } else {
-        for (int e = lane; e < 8 * 128; e += 32) {
-          const int r = e >> 7, c = e & 127;
+        for (int e = lane; e < 8 * 8 * CB; e += 32) {
+          const int r = e / (8 * CB), c = e % (8 * CB);
           const int yy = by * 8 + r, xx = bx * 8 + c;
           if (yy < h && xx < w) ob[static_cast<size_t>(yy) * pitch + xx] = pix[r * PS + c];
         }
