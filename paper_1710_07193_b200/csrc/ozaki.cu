@@ -22,7 +22,10 @@
 //   warps 0-3  producers: thread b gathers block b's 8x8 pixels (8-byte
 //              coalesced loads, one tile ahead in registers) into the K-major
 //              A tile (128 B rows, 128B swizzle, 64 bytes used); thread 0
-//              issues the 4 MMAs (2 K-steps x N = 256 + 192 columns) per tile.
+//              issues the 4 MMAs (2 K-steps x 2 output halves, N = 224
+//              columns each) per tile; each half has its own accumulator, so
+//              the next tile's MMA into one half overlaps the drain of the
+//              other.
 //   warps 4-11 drain: thread = block = TMEM lane (two warps per lane quarter,
 //              each half of the outputs); tcgen05.ld the int32 partials,
 //              recombine exactly in int64, scale to FP64 Y in a
@@ -35,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <string>
 
 #include "internal.h"
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   uint8_t* asm_ = base + BBYTES;             // 2 A stages
   uint8_t* ysm = asm_ + 2 * ABYTES;          // 2 Y tiles
   uint8_t* psm = ysm + 2 * YBYTES;           // compute-warp pixel staging
-  __shared__ uint64_t a_full[2], a_empty[2], acc_full, acc_empty, y_full[2], y_empty[2];
+  __shared__ uint64_t a_full[2], a_empty[2], acc_full[2], acc_empty[2], y_full[2], y_empty[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ double sc_s[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,8 +174,10 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       mbar_init(&y_full[i], 32 * DRAIN);
       mbar_init(&y_empty[i], COMP);
     }
-    mbar_init(&acc_full, 1);
-    mbar_init(&acc_empty, 32 * DRAIN);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 32 * DRAIN / 2);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   if (warp < PROD) {
     // ---------------- producers: block b = threadIdx.x gathers its 8 pixel rows
     const int b = threadIdx.x;
-    constexpr uint32_t id256 = idesc_i8(128, 256), id192 = idesc_i8(128, 192);
+    constexpr uint32_t id224 = idesc_i8(128, 224);
     uint2 pre[8];
     auto load = [&](long long ti) {
       int f, by, bx0;
@@ -237,17 +243,20 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       mbar_arrive(&a_full[s]);
       if (threadIdx.x == 0) {
         mbar_wait(&a_full[s], ph);
-        if (tl >= 1) mbar_wait(&acc_empty, static_cast<uint32_t>((tl - 1) & 1));
-        tc_fence_after();
         const uint32_t sa = smem_u32(ast), sb = smem_u32(bsm);
+        // one 224-column accumulator per output half: the half of tile i+1
+        // only waits for the drain of the same half of tile i
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          const uint64_t ad = umma_desc_sw128(sa + 32 * ks);
-          mma_i8(tmem_base, ad, umma_desc_sw128(sb + 32 * ks), id256, ks);
-          mma_i8(tmem_base + 256, ad, umma_desc_sw128(sb + 256 * 128 + 32 * ks), id192, ks);
+        for (int hf = 0; hf < 2; ++hf) {
+          if (tl >= 1) mbar_wait(&acc_empty[hf], static_cast<uint32_t>((tl - 1) & 1));
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+            mma_i8(tmem_base + 224 * hf, umma_desc_sw128(sa + 32 * ks),
+                   umma_desc_sw128(sb + hf * 224 * 128 + 32 * ks), id224, ks);
+          mma_commit(&acc_full[hf]);
         }
         mma_commit(&a_empty[s]);
-        mma_commit(&acc_full);
       }
       __syncwarp();
     }
@@ -263,7 +272,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       tile_at(ti, f, by, bx0);
       const int yb = static_cast<int>(tl & 1);
       uint8_t* yt = ysm + yb * YBYTES + b * 512;
-      mbar_wait(&acc_full, static_cast<uint32_t>(tl & 1));
+      mbar_wait(&acc_full[dh], static_cast<uint32_t>(tl & 1));
       if (tl >= 2) mbar_wait(&y_empty[yb], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
       tc_fence_after();
       double* cdst = (coef_out && bx0 + b < bw)
@@ -275,28 +284,30 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int o0 = 16 * t + 8 * i;
+          // this half's accumulator: column 224*dh + 32*slice + (o & 31)
+          const uint32_t col = 224 * dh + (o0 & 31);
           // exact int64 recombination: sum_s D_s 2^(7(6-s)) < 2^63, then one
           // conversion and one power-of-two scale per output
           int32_t d[8], e[8];
           long long acc[8];
-          tmem_ld8(tla + 0 * 64 + o0, d);
-          tmem_ld8(tla + 1 * 64 + o0, e);
+          tmem_ld8(tla + col + 0 * 32, d);
+          tmem_ld8(tla + col + 1 * 32, e);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] = static_cast<long long>(d[j]) * 128 + e[j];
 #pragma unroll
           for (int sl = 2; sl < 6; sl += 2) {
-            tmem_ld8(tla + sl * 64 + o0, d);
-            tmem_ld8(tla + (sl + 1) * 64 + o0, e);
+            tmem_ld8(tla + col + sl * 32, d);
+            tmem_ld8(tla + col + (sl + 1) * 32, e);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = (acc[j] << 14) + static_cast<long long>(d[j] * 128 + e[j]);
           }
-          tmem_ld8(tla + 6 * 64 + o0, d);
+          tmem_ld8(tla + col + 6 * 32, d);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            yr[i][j] = static_cast<double>((acc[j] << 7) + d[j]) * sc_s[o0 + j];
+          for (int j = 0; j < 8; ++j)  // unscaled; 2^(e-48) is folded into the inverse constants
+            yr[i][j] = static_cast<double>((acc[j] << 7) + d[j]);
         }
         // logical (row t, chunk v) = (Y[2t][v], Y[2t+1][v])
 #pragma unroll
@@ -304,23 +315,31 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
           *reinterpret_cast<double2*>(yt + t * 128 + ((v ^ (2 * t) ^ fsw(b)) << 4)) =
               make_double2(yr[0][v], yr[1][v]);
         if (cdst) {
+          const double sc = sc_s[0];
           double2* c2 = reinterpret_cast<double2*>(cdst + 16 * t);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            c2[j] = make_double2(yr[0][2 * j], yr[0][2 * j + 1]);
-            c2[4 + j] = make_double2(yr[1][2 * j], yr[1][2 * j + 1]);
+            c2[j] = make_double2(yr[0][2 * j] * sc, yr[0][2 * j + 1] * sc);
+            c2[4 + j] = make_double2(yr[1][2 * j] * sc, yr[1][2 * j + 1] * sc);
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(&acc_empty);  // TMEM free for the next tile's MMAs
+      mbar_arrive(&acc_empty[dh]);  // this half's TMEM free for the next tile's MMA
       mbar_arrive(&y_full[yb]);
     }
   } else {
     // ---------------- compute: inverse DCT (k_fused8's DMMA chain) of CB blocks per warp
     const int cw = warp - PROD - DRAIN;  // blocks CB*cw .. CB*cw + CB-1
     const int g = lane >> 2, t = lane & 3;
-    const double ai0 = cb[(2 * t) * 8 + g], ai1 = cb[(2 * t + 1) * 8 + g];
+    // O = C^t (2^(e-48) Yint) C: the power of two is split between the two
+    // passes' constants (exact)
+    int esc;
+    std::frexp(sc_s[0], &esc);  // sc = 2^(esc-1)
+    const int ea = (esc - 1) / 2, eb = (esc - 1) - ea;
+    const double pa = ldexp(1.0, ea), pb = ldexp(1.0, eb);
+    const double ai0 = cb[(2 * t) * 8 + g] * pa, ai1 = cb[(2 * t + 1) * 8 + g] * pa;
+    const double bi0 = cb[(2 * t) * 8 + g] * pb, bi1 = cb[(2 * t + 1) * 8 + g] * pb;
     uint8_t* pix = psm + cw * PIXBYTES;
     long long tl = 0;
     for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
@@ -342,9 +361,9 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) dmma(z[i], ai1, yv[i].y);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { o[i] = make_double2(0.5, 0.5); dmma(o[i], z[i].x, ai0); }
+        for (int i = 0; i < 4; ++i) { o[i] = make_double2(0.5, 0.5); dmma(o[i], z[i].x, bi0); }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dmma(o[i], z[i].y, ai1);
+        for (int i = 0; i < 4; ++i) dmma(o[i], z[i].y, bi1);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t qv = floor_to_u8(o[i].x) | (floor_to_u8(o[i].y) << 8);

@@ -443,13 +443,13 @@ void layout_hfused16(const std::vector<double>& op, std::vector<double>& out) {
 
 // Exact INT8 slicing of the forward-DCT-composed operator for k_fused8_i8.
 // G = H (C (x) C) maps a block's 64 pixels p (index i*8+j) straight to its
-// filtered DCT coefficients Y (index u*8+v). Row o of G is scaled by 2^-e_o
-// (e_o: smallest power of two >= max_k |G[o][k]|) and written as S = 7
-// signed digits in [-64, 64]:
-//   G[o][k] 2^-e_o = sum_s d_s[o][k] 2^-(6 + 7(s-1)) + err,  |err| <= 2^-49.
+// filtered DCT coefficients Y (index u*8+v). G is scaled by 2^-e (e: smallest
+// power of two > max |G|) and written as S = 7 signed digits in [-64, 64]:
+//   G[o][k] 2^-e = sum_s d_s[o][k] 2^-(6 + 7(s-1)) + err,  |err| <= 2^-49.
 // With u8 pixels every partial D_s = d_s . p is an exact int32 (|D_s| < 2^20),
-// so Y[o] = 2^(e_o - 48) sum_s D_s 2^(7(7-s)) is FP64-accurate.
-// Output: the swizzled UMMA B image, row n = s*64 + o (448 rows), 128 bytes per
+// so Y[o] = 2^(e - 48) sum_s D_s 2^(7(7-s)) is FP64-accurate.
+// Output: the swizzled UMMA B image, row n = half*224 + s*32 + (o & 31) with
+// half = o >> 5 (448 rows: two 224-row halves, one MMA each), 128 bytes per
 // row with the 64 digit bytes of K = pixel index in the first 64 bytes
 // (16-byte chunk c of row n stored at chunk c ^ (n & 7)); scales[o] =
 // 2^(e_o - 48).
@@ -469,20 +469,21 @@ void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>&
       }
   bimg.assign(size_t(S) * 64 * 128, 0);
   scales.assign(64, 0.0);
+  // One exponent for the whole operator (|G| < 2^e): the error bound
+  // |dY| <= 2^e * 64 * 255 * 2^-49 is what the pixels see either way, and a
+  // common power-of-two scale folds into the inverse-DCT constants.
+  long double gmax = 0.0L;
+  for (long double v : g) gmax = std::max(gmax, std::fabs(v));
+  int e = 0;
+  if (gmax > 0.0L) std::frexp(static_cast<double>(gmax), &e);
   for (int o = 0; o < 64; ++o) {
-    long double rowmax = 0.0L;
-    for (int k = 0; k < 64; ++k) rowmax = std::max(rowmax, std::fabs(g[o * 64 + k]));
-    int e = 0;
-    if (rowmax > 0.0L) {
-      std::frexp(static_cast<double>(rowmax), &e);  // rowmax < 2^e
-    }
     scales[o] = std::ldexp(1.0, e - 48);
     for (int k = 0; k < 64; ++k) {
       long double r = std::ldexp(g[o * 64 + k], -e) * 64.0L;  // in units of 2^-6
       for (int sl = 0; sl < S; ++sl) {
         const long double d = std::nearbyint(r);
         r = (r - d) * 128.0L;
-        const int n = sl * 64 + o;
+        const int n = (o >> 5) * 224 + sl * 32 + (o & 31);
         const size_t pos = size_t(n) * 128 + ((((k >> 4) ^ (n & 7)) << 4) | (k & 15));
         bimg[pos] = static_cast<int8_t>(d);
       }
