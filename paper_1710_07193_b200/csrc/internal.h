@@ -33,10 +33,8 @@ struct dctf_plan {
   int* d_nan = nullptr;          // NaN flag
   double* d_weights = nullptr;   // mask, kr*kc (spatial path)
 
-  // Scratch for multi-kernel paths and the host-buffer entry (guarded).
-  mutable std::mutex scratch_mu;
-  mutable void* scratch = nullptr;
-  mutable size_t scratch_bytes = 0;
+  // Device staging of the host-buffer entry (copy mode), guarded by io_mu.
+  mutable std::mutex io_mu;
   mutable void* io_in = nullptr;
   mutable void* io_out = nullptr;
   mutable size_t io_bytes = 0;

@@ -1739,7 +1739,7 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   if (s != DCTF_OK) return s;
   if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
-  std::lock_guard<std::mutex> lock(p->scratch_mu);
+  std::lock_guard<std::mutex> lock(p->io_mu);
   const size_t dpitch = (static_cast<size_t>(w) + 15) & ~size_t(15);
   const size_t bytes = dpitch * static_cast<size_t>(h);
   if (p->io_bytes < bytes) {
