@@ -48,7 +48,7 @@ for rep in sys.argv[3:]:
                          text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     hh, units, vals = rr[0], rr[1], rr[2]
-    name = vals[hh.index("Kernel Name")].split("(")[0].split("::")[-1]
+    name = vals[hh.index("Kernel Name")].split("(")[0].split("::")[-1].replace("<", "_").replace(">", "")
     m = {k: {"value": vals[hh.index(k)], "unit": units[hh.index(k)]} for k in KEYS if k in hh}
     json.dump({"report": os.path.basename(rep), "kernel": name, "metrics": m},
               open(os.path.join(out, f"ncu_{name}.json"), "w"), indent=1)
