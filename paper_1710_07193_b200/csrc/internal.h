@@ -70,6 +70,10 @@ void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>
 void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>& basis,
                        std::vector<int8_t>& bimg, std::vector<double>& scales);
 
+// TMA tensor map over block-major FP64 coefficients (kernels.cu): 2-D
+// [nblocks rows x nn cols], box [box_rows x 16 cols], 128B swizzle.
+dctf_status make_xmap(void* map, const double* d, long long nblocks, int nn, int box_rows);
+
 // Exact-INT8 tcgen05 fused n=8 path (ozaki.cu).
 dctf_status upload_i8_operator(dctf_plan* p);
 dctf_status launch_fused8_i8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,

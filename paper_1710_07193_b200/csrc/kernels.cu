@@ -1135,9 +1135,13 @@ PFN_encodeTiled_t encode_fn() {
   return fn;
 }
 
+}  // namespace
+
+namespace dctf {
 // 2-D FP64 view [nblocks rows x nn cols] of block-major coefficients; box
 // [box_rows x 16 cols] (128 bytes inner), 128B swizzle, OOB rows -> 0.
-dctf_status make_xmap(CUtensorMap* map, const double* d, long long nblocks, int nn, int box_rows) {
+dctf_status make_xmap(void* vmap, const double* d, long long nblocks, int nn, int box_rows) {
+  CUtensorMap* map = static_cast<CUtensorMap*>(vmap);
   PFN_encodeTiled_t fn = encode_fn();
   if (!fn) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(nn), static_cast<cuuint64_t>(nblocks)};
@@ -1150,6 +1154,9 @@ dctf_status make_xmap(CUtensorMap* map, const double* d, long long nblocks, int 
   if (r != CUDA_SUCCESS) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   return DCTF_OK;
 }
+}  // namespace dctf
+
+namespace {
 
 int sm_count(int device) {
   static int cached[64] = {0};
@@ -1199,7 +1206,7 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
   if (p->precision == DCTF_PREC_TF32X3) return dctf::launch_coef_tf32x3(p, d_in, d_out, nb, st, sm_count(p->device));
   CUtensorMap map;
   const int nn = p->n * p->n;
-  dctf_status s = make_xmap(&map, d_in, nb, nn, p->n == 8 ? c8::TILE : c16::TILE);
+  dctf_status s = dctf::make_xmap(&map, d_in, nb, nn, p->n == 8 ? c8::TILE : c16::TILE);
   if (s != DCTF_OK) return s;
   const int sms = sm_count(p->device);
   if (p->n == 8) {
@@ -1779,10 +1786,13 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   const bool out_pinned = cudaPointerGetAttributes(&ao, h_out) == cudaSuccess &&
                           ao.type == cudaMemoryTypeHost && ao.devicePointer != nullptr;
   cudaGetLastError();
-  int mode = (in_pinned && out_pinned && p->n == 8) ? 2 : (out_pinned && p->n == 8 ? 1 : 0);
+  // zero-copy needs a single fused kernel (every precision except the
+  // split-precision path, which runs forward/filter/inverse as three kernels)
+  const bool fused = p->precision != DCTF_PREC_TF32X3;
+  int mode = (in_pinned && out_pinned && fused) ? 2 : (out_pinned && fused ? 1 : 0);
   if (const char* env = std::getenv("DCTF_E2E_MODE")) {
     const int m = std::atoi(env);
-    if (m == 0 || (m == 1 && out_pinned && p->n == 8) || (m == 2 && in_pinned && out_pinned && p->n == 8)) mode = m;
+    if (m == 0 || (m == 1 && out_pinned && fused) || (m == 2 && in_pinned && out_pinned && fused)) mode = m;
   }
   if (p->n != 8) CUDA_TRY(cudaMemsetAsync(p->d_nan, 0, sizeof(int), s_run));
   const int n = p->n, bh = (h + n - 1) / n;

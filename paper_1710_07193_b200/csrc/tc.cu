@@ -10,14 +10,17 @@
 // 128B-swizzled shared-memory image the UMMA descriptors expect, so it is
 // streamed with plain bulk copies.
 //
-// CTA = 12 warps, one CTA per SM, persistent over tiles of 128 blocks (MMA M):
-//   warps 0-7 : two threads per tile row load X (FP64) two K-chunks ahead
-//               into registers, split it into TF32 hi/lo and write the
-//               swizzled A tiles; thread 0 also bulk-copies the H chunk and
-//               issues the MMAs (single thread).
-//   warps 8-11: epilogue — tcgen05.ld the FP32 accumulator (lanes = blocks,
-//               columns = outputs), widen to FP64, stage rows in shared
-//               memory and store them as coalesced 128-byte row segments.
+// CTA = 14 warps, one CTA per SM, persistent over tiles of 128 blocks (MMA
+// M), K streamed in chunks of 16:
+//   warp 8     producer: TMA loads of the raw FP64 X chunk (128 blocks x 16
+//              coefficients, 128B swizzle) into a 3-stage staging ring, and
+//              bulk copies of the H hi/lo chunk into the operand ring.
+//   warps 0-7  converters: FP64 staging -> TF32 hi/lo operand cores
+//              (canonical no-swizzle K-major layout, 8-row x 16-byte cores).
+//   warp 9     single-thread tcgen05.mma issue (3 passes x 2 K-steps per chunk).
+//   warps 10-13 epilogue: tcgen05.ld the FP32 accumulator (lanes = blocks,
+//              columns = outputs), widen to FP64, stage rows in shared
+//              memory, store them as coalesced 128-byte row segments.
 // TMEM holds two accumulators (tile parity) so the epilogue of tile i
 // overlaps the MMAs of tile i+1; shared memory holds two K-chunk stages.
 #include <cuda.h>
@@ -113,32 +116,57 @@ __device__ __forceinline__ void split_tf32(double x, float& hi, float& lo) {
   lo = __uint_as_float(l);
 }
 
+// UMMA shared-memory descriptor, K-major, no swizzle: 8-row x 16-byte core
+// matrices, LBO = 128 B between K-adjacent cores, SBO = 512 B between 8-row
+// groups (a 16-wide TF32 K chunk per 64-byte row), version 1, layout type 0.
+__device__ __forceinline__ uint64_t umma_desc_k16(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(128u >> 4) << 16;   // LBO
+  d |= static_cast<uint64_t>(512u >> 4) << 32;   // SBO
+  d |= static_cast<uint64_t>(1u) << 46;          // version
+  return d;
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 template <int NN>
 struct TcCfg {
   static constexpr int TILE = 128;          // MMA M (blocks per tile)
-  static constexpr int KCH = NN / 32;       // K chunks of 32 TF32 (128 B rows)
-  static constexpr int ABYTES = TILE * 128;
-  static constexpr int BBYTES = NN * 128;
-  static constexpr int STAGE = 2 * ABYTES + 2 * BBYTES;
-  static constexpr int STAGES = 2;
+  static constexpr int KCH = NN / 16;       // K chunks of 16 (64-byte TF32 rows)
+  static constexpr int XBYTES = TILE * 128; // FP64 chunk staging (TMA box 128 rows x 16 doubles, SW128)
+  static constexpr int ABYTES = TILE * 64;  // one TF32 part of A
+  static constexpr int BBYTES = NN * 64;    // one TF32 part of B
+  static constexpr int XS = 3;              // FP64 staging stages
+  static constexpr int AS = 3;              // operand stages
+  static constexpr int OPBYTES = 2 * ABYTES + 2 * BBYTES;
+  static constexpr int CONV_WARPS = 8;
+  static constexpr int PROD_WARP = CONV_WARPS, MMA_WARP = CONV_WARPS + 1, EPI0 = CONV_WARPS + 2;
+  static constexpr int EPI_WARPS = 4;
+  static constexpr int THREADS = 32 * (EPI0 + EPI_WARPS);
   static constexpr int TMEM_COLS = 2 * NN <= 128 ? 128 : (2 * NN <= 256 ? 256 : 512);
-  static constexpr int CONV_WARPS = 8;      // converter warps (2 threads per tile row)
-  static constexpr int EPI_WARPS = 4;       // epilogue warps (one TMEM lane quarter each)
-  static constexpr int THREADS = 32 * (CONV_WARPS + EPI_WARPS);
   static constexpr int EPI_STRIDE = 144;    // 16 doubles + 16 B pad per staged row
   static constexpr int EPI_BYTES = 32 * EPI_STRIDE;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI_WARPS * EPI_BYTES;
+  static constexpr int SMEM = 1024 + XS * XBYTES + AS * OPBYTES + EPI_WARPS * EPI_BYTES;
 };
 
 template <int NN>
 __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
-    k_coef_tf32x3(const double* __restrict__ x, const float* __restrict__ hsplit,
+    k_coef_tf32x3(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ hsplit,
                   double* __restrict__ y, long long nblocks) {
   using Cfg = TcCfg<NN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
-  uint8_t* epi = base + Cfg::STAGES * Cfg::STAGE;
-  __shared__ uint64_t a_full[2], b_full[2], empty[2], acc_full[2], acc_empty[2];
+  uint8_t* xst = base;                               // FP64 staging ring
+  uint8_t* ops = xst + Cfg::XS * Cfg::XBYTES;        // operand ring: [Ah | Al | Bh | Bl]
+  uint8_t* epi = ops + Cfg::AS * Cfg::OPBYTES;
+  __shared__ uint64_t x_full[Cfg::XS], x_empty[Cfg::XS], a_full[Cfg::AS], b_full[Cfg::AS], a_empty[Cfg::AS];
+  __shared__ uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -149,10 +177,16 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 32) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < Cfg::XS; ++i) {
+      mbar_init(&x_full[i], 1);
+      mbar_init(&x_empty[i], Cfg::CONV_WARPS);
+    }
+    for (int i = 0; i < Cfg::AS; ++i) {
       mbar_init(&a_full[i], 32 * Cfg::CONV_WARPS);
       mbar_init(&b_full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 32 * Cfg::EPI_WARPS);
     }
@@ -166,92 +200,93 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
   const long long my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const long long nchunks = my_tiles * Cfg::KCH;
 
-  if (warp < Cfg::CONV_WARPS) {
-    // ---------------- converters (+ thread 0: B loads and MMA issue)
-    const int r = threadIdx.x >> 1, hh = threadIdx.x & 1;  // tile row, half of the 32-wide chunk
-    constexpr uint32_t idesc = idesc_tf32(128, NN);
-    auto load = [&](long long c, double2 (&pre)[8]) {
-      const long long tile = blockIdx.x + (c / Cfg::KCH) * gridDim.x;
-      const int kc = static_cast<int>(c % Cfg::KCH);
-      const long long blk = tile * Cfg::TILE + r;
-      if (c < nchunks && blk < nblocks) {
-        const double2* src = reinterpret_cast<const double2*>(x + blk * NN + 32 * kc + 16 * hh);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) pre[j] = __ldg(src + j);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) pre[j] = make_double2(0.0, 0.0);
-      }
-    };
-    auto step = [&](long long c, double2 (&pre)[8]) {
-      const int s = static_cast<int>(c & 1);
-      const uint32_t ph = static_cast<uint32_t>((c >> 1) & 1);
-      const long long ti = c / Cfg::KCH;
-      const int kc = static_cast<int>(c % Cfg::KCH);
-      const int ab = static_cast<int>(ti & 1);
-      uint8_t* st = base + s * Cfg::STAGE;
-      if (c >= 2) mbar_wait(&empty[s], ph ^ 1u);  // MMAs of chunk c-2 retired
-      if (threadIdx.x == 0) {
-        mbar_expect_tx(&b_full[s], 2 * Cfg::BBYTES);
+  if (warp == Cfg::PROD_WARP) {
+    // ---------------- producer: X chunks by TMA (raw FP64), H chunks by bulk copy
+    if (lane == 0) {
+      for (long long c = 0; c < nchunks; ++c) {
+        const long long tile = blockIdx.x + (c / Cfg::KCH) * gridDim.x;
+        const int kc = static_cast<int>(c % Cfg::KCH);
+        const int xs = static_cast<int>(c % Cfg::XS), as = static_cast<int>(c % Cfg::AS);
+        if (c >= Cfg::XS) mbar_wait(&x_empty[xs], static_cast<uint32_t>(((c / Cfg::XS) - 1) & 1));
+        mbar_expect_tx(&x_full[xs], Cfg::XBYTES);
+        tma_load_2d(xst + xs * Cfg::XBYTES, &xmap, &x_full[xs], 16 * kc, static_cast<int>(tile * Cfg::TILE));
+        if (c >= Cfg::AS) mbar_wait(&a_empty[as], static_cast<uint32_t>(((c / Cfg::AS) - 1) & 1));
+        uint8_t* op = ops + as * Cfg::OPBYTES;
         const float* hs = hsplit + static_cast<size_t>(kc) * 2 * (Cfg::BBYTES / 4);
-        bulk_load(st + 2 * Cfg::ABYTES, hs, Cfg::BBYTES, &b_full[s]);
-        bulk_load(st + 2 * Cfg::ABYTES + Cfg::BBYTES, hs + Cfg::BBYTES / 4, Cfg::BBYTES, &b_full[s]);
+        mbar_expect_tx(&b_full[as], 2 * Cfg::BBYTES);
+        bulk_load(op + 2 * Cfg::ABYTES, hs, 2 * Cfg::BBYTES, &b_full[as]);
       }
-      uint8_t* ah = st + r * 128;
-      uint8_t* al = st + Cfg::ABYTES + r * 128;
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        float4 h4, l4;
-        split_tf32(pre[2 * c4].x, h4.x, l4.x);
-        split_tf32(pre[2 * c4].y, h4.y, l4.y);
-        split_tf32(pre[2 * c4 + 1].x, h4.z, l4.z);
-        split_tf32(pre[2 * c4 + 1].y, h4.w, l4.w);
-        const int off = ((4 * hh + c4) ^ (r & 7)) << 4;
-        *reinterpret_cast<float4*>(ah + off) = h4;
-        *reinterpret_cast<float4*>(al + off) = l4;
-      }
-      load(c + 2, pre);  // two chunks in flight per thread
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&a_full[s]);
-      if (threadIdx.x == 0) {
-        mbar_wait(&a_full[s], ph);
-        mbar_wait(&b_full[s], ph);
+    }
+  } else if (warp == Cfg::MMA_WARP) {
+    // ---------------- single-thread MMA issue
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(128, NN);
+      for (long long c = 0; c < nchunks; ++c) {
+        const long long ti = c / Cfg::KCH;
+        const int kc = static_cast<int>(c % Cfg::KCH), as = static_cast<int>(c % Cfg::AS);
+        const int ab = static_cast<int>(ti & 1);
+        const uint32_t ph = static_cast<uint32_t>((c / Cfg::AS) & 1);
+        mbar_wait(&a_full[as], ph);
+        mbar_wait(&b_full[as], ph);
         if (kc == 0 && ti >= 2) mbar_wait(&acc_empty[ab], static_cast<uint32_t>(((ti >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t sa = smem_u32(st);
+        const uint32_t so = smem_u32(ops + as * Cfg::OPBYTES);
         const uint32_t d = tmem_base + static_cast<uint32_t>(ab * NN);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t ah_d = umma_desc_sw128(sa + 32 * k);
-          const uint64_t al_d = umma_desc_sw128(sa + Cfg::ABYTES + 32 * k);
-          const uint64_t bh_d = umma_desc_sw128(sa + 2 * Cfg::ABYTES + 32 * k);
-          const uint64_t bl_d = umma_desc_sw128(sa + 2 * Cfg::ABYTES + Cfg::BBYTES + 32 * k);
-          mma_tf32(d, ah_d, bh_d, idesc, (kc | k) != 0);
-          mma_tf32(d, ah_d, bl_d, idesc, 1);
-          mma_tf32(d, al_d, bh_d, idesc, 1);
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint32_t koff = 256u * ks;  // two 16-byte cores per K step
+          const uint64_t ah = umma_desc_k16(so + koff);
+          const uint64_t al = umma_desc_k16(so + Cfg::ABYTES + koff);
+          const uint64_t bh = umma_desc_k16(so + 2 * Cfg::ABYTES + koff);
+          const uint64_t bl = umma_desc_k16(so + 2 * Cfg::ABYTES + Cfg::BBYTES + koff);
+          mma_tf32(d, ah, bh, idesc, (kc | ks) != 0);
+          mma_tf32(d, ah, bl, idesc, 1);
+          mma_tf32(d, al, bh, idesc, 1);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&a_empty[as]);
         if (kc == Cfg::KCH - 1) mma_commit(&acc_full[ab]);
       }
+    }
+  } else if (warp < Cfg::CONV_WARPS) {
+    // ---------------- converters: FP64 staging -> TF32 hi/lo operand cores
+    const int r = threadIdx.x & (Cfg::TILE - 1), kp = threadIdx.x >> 7;  // row, K-core pair
+    for (long long c = 0; c < nchunks; ++c) {
+      const int xs = static_cast<int>(c % Cfg::XS), as = static_cast<int>(c % Cfg::AS);
+      mbar_wait(&x_full[xs], static_cast<uint32_t>((c / Cfg::XS) & 1));
+      if (c >= Cfg::AS) mbar_wait(&a_empty[as], static_cast<uint32_t>(((c / Cfg::AS) - 1) & 1));
+      const uint8_t* xrow = xst + xs * Cfg::XBYTES + r * 128;
+      uint8_t* op = ops + as * Cfg::OPBYTES;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int kk = 2 * kp + i;  // 16-byte TF32 core column = K 4kk..4kk+3
+        const double2 v0 = *reinterpret_cast<const double2*>(xrow + (((2 * kk) ^ (r & 7)) << 4));
+        const double2 v1 = *reinterpret_cast<const double2*>(xrow + (((2 * kk + 1) ^ (r & 7)) << 4));
+        float4 h4, l4;
+        split_tf32(v0.x, h4.x, l4.x);
+        split_tf32(v0.y, h4.y, l4.y);
+        split_tf32(v1.x, h4.z, l4.z);
+        split_tf32(v1.y, h4.w, l4.w);
+        const int off = (r >> 3) * 512 + kk * 128 + (r & 7) * 16;
+        *reinterpret_cast<float4*>(op + off) = h4;
+        *reinterpret_cast<float4*>(op + Cfg::ABYTES + off) = l4;
+      }
+      // release the FP64 stage once this warp's reads have landed
       __syncwarp();
-    };
-    double2 pre0[8], pre1[8];
-    load(0, pre0);
-    load(1, pre1);
-    for (long long c = 0; c < nchunks; c += 2) {
-      step(c, pre0);
-      if (c + 1 < nchunks) step(c + 1, pre1);
+      __threadfence_block();
+      if (lane == 0) mbar_arrive(&x_empty[xs]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a_full[as]);
     }
   } else {
     // ---------------- epilogue: TMEM -> FP64 -> staged rows -> coalesced stores
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    uint8_t* stg = epi + (warp - Cfg::CONV_WARPS) * Cfg::EPI_BYTES;
+    const int q = warp & 3;
+    uint8_t* stg = epi + (warp - Cfg::EPI0) * Cfg::EPI_BYTES;
     int ti = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
       const int ab = ti & 1;
       mbar_wait(&acc_full[ab], static_cast<uint32_t>((ti >> 1) & 1));
       tc_fence_after();
-      const long long row0 = tile * Cfg::TILE + 32 * q;  // first block of this warp's 32 rows
+      const long long row0 = tile * Cfg::TILE + 32 * q;
 #pragma unroll 1
       for (int c = 0; c < NN / 16; ++c) {
         uint32_t v[16];
@@ -270,7 +305,6 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
           myrow[j] = make_double2(static_cast<double>(__uint_as_float(v[2 * j])),
                                   static_cast<double>(__uint_as_float(v[2 * j + 1])));
         __syncwarp();
-        // 32 rows x 128 B: 8 lanes per row, 4 rows per pass
 #pragma unroll
         for (int ps = 0; ps < 8; ++ps) {
           const int rr = 4 * ps + (lane >> 3), ch = lane & 7;
@@ -297,13 +331,15 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
 
 namespace dctf {
 
-// H split image for k_coef_tf32x3: [kc][part h/l][row n < NN][32 TF32 of
-// columns 32kc..] with the 128B swizzle applied (16-byte chunk c of row n at
-// chunk c ^ (n & 7)), i.e. exactly the shared-memory tile the UMMA B
-// descriptor reads.
+// H split image for k_coef_tf32x3: [kc < NN/16][part h/l][row n < NN] in the
+// canonical no-swizzle K-major UMMA layout of a 16-wide K chunk: 8-row x
+// 16-byte core matrices, core (n/8, kk) at byte (n/8)*512 + kk*128, row n%8
+// at +16*(n%8) (LBO = 128 B between K-adjacent cores, SBO = 512 B between
+// 8-row groups), i.e. exactly the shared-memory tile the UMMA B descriptor
+// reads, so each chunk is one plain bulk copy.
 void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>& out) {
-  const int nn = n * n, kch = nn / 32;
-  out.assign(static_cast<size_t>(kch) * 2 * nn * 32, 0.0f);
+  const int nn = n * n, kch = nn / 16;
+  out.assign(static_cast<size_t>(kch) * 2 * nn * 16, 0.0f);
   auto rna_tf32 = [](float f) {
     uint32_t u;
     std::memcpy(&u, &f, 4);
@@ -314,42 +350,35 @@ void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>
   };
   for (int kc = 0; kc < kch; ++kc)
     for (int row = 0; row < nn; ++row)
-      for (int k = 0; k < 32; ++k) {
-        const double v = op[static_cast<size_t>(row) * nn + 32 * kc + k];
+      for (int k = 0; k < 16; ++k) {
+        const double v = op[static_cast<size_t>(row) * nn + 16 * kc + k];
         const float hi = rna_tf32(static_cast<float>(v));
         const float lo = rna_tf32(static_cast<float>(v - static_cast<double>(hi)));
-        const size_t pos = static_cast<size_t>(row) * 32 + (((k >> 2) ^ (row & 7)) << 2) + (k & 3);
-        out[(static_cast<size_t>(kc) * 2 + 0) * nn * 32 + pos] = hi;
-        out[(static_cast<size_t>(kc) * 2 + 1) * nn * 32 + pos] = lo;
+        const size_t pos = static_cast<size_t>(row >> 3) * 128 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
+        out[(static_cast<size_t>(kc) * 2 + 0) * nn * 16 + pos] = hi;
+        out[(static_cast<size_t>(kc) * 2 + 1) * nn * 16 + pos] = lo;
       }
 }
 
 dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
                                cudaStream_t st, int sms) {
   if (nb == 0) return DCTF_OK;
-  if (p->n == 8) {
-    using Cfg = TcCfg<64>;
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(k_coef_tf32x3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
-        return set_error(DCTF_CUDA_ERROR, "cudaFuncSetAttribute(k_coef_tf32x3<64>)");
-      attr = true;
-    }
-    const long long ntiles = (nb + Cfg::TILE - 1) / Cfg::TILE;
-    k_coef_tf32x3<64><<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), Cfg::THREADS, Cfg::SMEM, st>>>(
-        d_in, static_cast<const float*>(p->d_hsplit), d_out, nb);
-  } else {
-    using Cfg = TcCfg<256>;
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(k_coef_tf32x3<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
-        return set_error(DCTF_CUDA_ERROR, "cudaFuncSetAttribute(k_coef_tf32x3<256>)");
-      attr = true;
-    }
-    const long long ntiles = (nb + Cfg::TILE - 1) / Cfg::TILE;
-    k_coef_tf32x3<256><<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), Cfg::THREADS, Cfg::SMEM, st>>>(
-        d_in, static_cast<const float*>(p->d_hsplit), d_out, nb);
-  }
+  CUtensorMap map;
+  const int nn = p->n * p->n;
+  const dctf_status s = make_xmap(&map, d_in, nb, nn, 128);
+  if (s != DCTF_OK) return s;
+  auto run = [&](auto kernel, int smem, int threads) -> dctf_status {
+    static_cast<void>(0);
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return set_error(DCTF_CUDA_ERROR, "cudaFuncSetAttribute(k_coef_tf32x3)");
+    const long long ntiles = (nb + 127) / 128;
+    kernel<<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), threads, smem, st>>>(
+        map, static_cast<const float*>(p->d_hsplit), d_out, nb);
+    return DCTF_OK;
+  };
+  const dctf_status r = p->n == 8 ? run(k_coef_tf32x3<64>, TcCfg<64>::SMEM, TcCfg<64>::THREADS)
+                                  : run(k_coef_tf32x3<256>, TcCfg<256>::SMEM, TcCfg<256>::THREADS);
+  if (r != DCTF_OK) return r;
   add_launches(1);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_coef_tf32x3: ") + cudaGetErrorString(e));
