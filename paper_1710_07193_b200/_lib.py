@@ -10,7 +10,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdctf_b200.so")
+LIB_PATH = os.environ.get("DCTF_LIB_PATH") or os.path.join(_HERE, "libdctf_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "dctf.h")
 
 if not os.path.exists(LIB_PATH):

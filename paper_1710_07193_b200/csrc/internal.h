@@ -72,7 +72,7 @@ void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>&
 
 // TMA tensor map over block-major FP64 coefficients (kernels.cu): 2-D
 // [nblocks rows x nn cols], box [box_rows x 16 cols], 128B swizzle.
-dctf_status make_xmap(void* map, const double* d, long long nblocks, int nn, int box_rows);
+dctf_status make_xmap(void* map, const double* d, long long nblocks, int nn, int box_rows, int l2promo = 3);
 
 // Exact-INT8 tcgen05 fused n=8 path (ozaki.cu).
 dctf_status upload_i8_operator(dctf_plan* p);

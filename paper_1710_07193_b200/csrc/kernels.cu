@@ -1140,7 +1140,7 @@ PFN_encodeTiled_t encode_fn() {
 namespace dctf {
 // 2-D FP64 view [nblocks rows x nn cols] of block-major coefficients; box
 // [box_rows x 16 cols] (128 bytes inner), 128B swizzle, OOB rows -> 0.
-dctf_status make_xmap(void* vmap, const double* d, long long nblocks, int nn, int box_rows) {
+dctf_status make_xmap(void* vmap, const double* d, long long nblocks, int nn, int box_rows, int l2promo) {
   CUtensorMap* map = static_cast<CUtensorMap*>(vmap);
   PFN_encodeTiled_t fn = encode_fn();
   if (!fn) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
@@ -1150,7 +1150,7 @@ dctf_status make_xmap(void* vmap, const double* d, long long nblocks, int nn, in
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(d), dims, strides,
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        static_cast<CUtensorMapL2promotion>(l2promo), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   return DCTF_OK;
 }

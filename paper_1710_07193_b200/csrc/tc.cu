@@ -10,15 +10,16 @@
 // 128B-swizzled shared-memory image the UMMA descriptors expect, so it is
 // streamed with plain bulk copies.
 //
-// CTA = 14 warps, one CTA per SM, persistent over tiles of 128 blocks (MMA
+// CTA = 15 warps, one CTA per SM, persistent over tiles of 128 blocks (MMA
 // M), K streamed in chunks of 16:
-//   warp 8     producer: TMA loads of the raw FP64 X chunk (128 blocks x 16
-//              coefficients, 128B swizzle) into a 3-stage staging ring, and
-//              bulk copies of the H hi/lo chunk into the operand ring.
+//   warp 8     X producer: TMA loads of the raw FP64 X chunk (128 blocks x 16
+//              coefficients, 128B swizzle) into the staging ring (XS deep, so
+//              HBM latency is covered independently of the operand ring).
+//   warp 9     H producer: bulk copies of the H hi/lo chunk into the operand ring.
 //   warps 0-7  converters: FP64 staging -> TF32 hi/lo operand cores
 //              (canonical no-swizzle K-major layout, 8-row x 16-byte cores).
-//   warp 9     single-thread tcgen05.mma issue (3 passes x 2 K-steps per chunk).
-//   warps 10-13 epilogue: tcgen05.ld the FP32 accumulator (lanes = blocks,
+//   warp 10    single-thread tcgen05.mma issue (3 passes x 2 K-steps per chunk).
+//   warps 11-14 epilogue: tcgen05.ld the FP32 accumulator (lanes = blocks,
 //              columns = outputs), widen to FP64, stage rows in shared
 //              memory, store them as coalesced 128-byte row segments.
 // TMEM holds two accumulators (tile parity) so the epilogue of tile i
@@ -57,7 +58,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!done) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
         : "r"(addr), "r"(parity)
@@ -74,17 +75,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// UMMA shared-memory descriptor, K-major, 128B swizzle: rows of 128 bytes,
-// 8-row atoms 1024 B apart (SBO), version 1 (sm_100), layout type 2.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>(1u) << 16;             // LBO (unused for swizzled K-major)
-  d |= static_cast<uint64_t>(1024u >> 4) << 32;     // SBO
-  d |= static_cast<uint64_t>(1u) << 46;             // version
-  d |= static_cast<uint64_t>(2u) << 61;             // SWIZZLE_128B
-  return d;
-}
 
 // Instruction descriptor: kind::tf32, A/B TF32 K-major, D FP32, M x N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
@@ -108,11 +98,16 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 }
 
 // tf32 hi/lo split of a double: hi = rna_tf32(float(x)), lo = rna_tf32(float(x - hi)).
+// x ~= hi + lo with hi, lo TF32. The split runs in FP32 after one rounding
+// of x to float (relative 2^-24, far below the 3xTF32 truncation of the
+// dropped lo*lo term), so each element costs one FP64-pipe conversion
+// instead of three plus a DADD.
 __device__ __forceinline__ void split_tf32(double x, float& hi, float& lo) {
+  const float xf = __double2float_rn(x);
   uint32_t h, l;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(__double2float_rn(x)));
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(xf));
   hi = __uint_as_float(h);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(__double2float_rn(x - static_cast<double>(hi))));
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(xf - hi));
   lo = __uint_as_float(l);
 }
 
@@ -142,11 +137,12 @@ struct TcCfg {
   static constexpr int XBYTES = TILE * 128; // FP64 chunk staging (TMA box 128 rows x 16 doubles, SW128)
   static constexpr int ABYTES = TILE * 64;  // one TF32 part of A
   static constexpr int BBYTES = NN * 64;    // one TF32 part of B
-  static constexpr int XS = 3;              // FP64 staging stages
-  static constexpr int AS = 3;              // operand stages
+  static constexpr int XS = NN == 64 ? 8 : 5;  // FP64 staging stages (HBM latency cover)
+  static constexpr int AS = NN == 64 ? 3 : 2;  // operand stages
   static constexpr int OPBYTES = 2 * ABYTES + 2 * BBYTES;
   static constexpr int CONV_WARPS = 8;
-  static constexpr int PROD_WARP = CONV_WARPS, MMA_WARP = CONV_WARPS + 1, EPI0 = CONV_WARPS + 2;
+  static constexpr int XPROD_WARP = CONV_WARPS, BPROD_WARP = CONV_WARPS + 1, MMA_WARP = CONV_WARPS + 2,
+                       EPI0 = CONV_WARPS + 3;
   static constexpr int EPI_WARPS = 4;
   static constexpr int THREADS = 32 * (EPI0 + EPI_WARPS);
   static constexpr int TMEM_COLS = 2 * NN <= 128 ? 128 : (2 * NN <= 256 ? 256 : 512);
@@ -200,21 +196,27 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
   const long long my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const long long nchunks = my_tiles * Cfg::KCH;
 
-  if (warp == Cfg::PROD_WARP) {
-    // ---------------- producer: X chunks by TMA (raw FP64), H chunks by bulk copy
+  if (warp == Cfg::XPROD_WARP) {
+    // ---------------- X producer: TMA loads of raw FP64 chunks, XS ahead
     if (lane == 0) {
       for (long long c = 0; c < nchunks; ++c) {
         const long long tile = blockIdx.x + (c / Cfg::KCH) * gridDim.x;
-        const int kc = static_cast<int>(c % Cfg::KCH);
-        const int xs = static_cast<int>(c % Cfg::XS), as = static_cast<int>(c % Cfg::AS);
+        const int kc = static_cast<int>((c + tile) % Cfg::KCH), xs = static_cast<int>(c % Cfg::XS);
         if (c >= Cfg::XS) mbar_wait(&x_empty[xs], static_cast<uint32_t>(((c / Cfg::XS) - 1) & 1));
         mbar_expect_tx(&x_full[xs], Cfg::XBYTES);
         tma_load_2d(xst + xs * Cfg::XBYTES, &xmap, &x_full[xs], 16 * kc, static_cast<int>(tile * Cfg::TILE));
+      }
+    }
+  } else if (warp == Cfg::BPROD_WARP) {
+    // ---------------- H producer: bulk copies of the hi/lo chunk, AS ahead
+    if (lane == 0) {
+      for (long long c = 0; c < nchunks; ++c) {
+        const long long tile = blockIdx.x + (c / Cfg::KCH) * gridDim.x;
+        const int kc = static_cast<int>((c + tile) % Cfg::KCH), as = static_cast<int>(c % Cfg::AS);
         if (c >= Cfg::AS) mbar_wait(&a_empty[as], static_cast<uint32_t>(((c / Cfg::AS) - 1) & 1));
-        uint8_t* op = ops + as * Cfg::OPBYTES;
         const float* hs = hsplit + static_cast<size_t>(kc) * 2 * (Cfg::BBYTES / 4);
         mbar_expect_tx(&b_full[as], 2 * Cfg::BBYTES);
-        bulk_load(op + 2 * Cfg::ABYTES, hs, 2 * Cfg::BBYTES, &b_full[as]);
+        bulk_load(ops + as * Cfg::OPBYTES + 2 * Cfg::ABYTES, hs, 2 * Cfg::BBYTES, &b_full[as]);
       }
     }
   } else if (warp == Cfg::MMA_WARP) {
@@ -223,12 +225,12 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
       constexpr uint32_t idesc = idesc_tf32(128, NN);
       for (long long c = 0; c < nchunks; ++c) {
         const long long ti = c / Cfg::KCH;
-        const int kc = static_cast<int>(c % Cfg::KCH), as = static_cast<int>(c % Cfg::AS);
+        const int j = static_cast<int>(c % Cfg::KCH), as = static_cast<int>(c % Cfg::AS);
         const int ab = static_cast<int>(ti & 1);
         const uint32_t ph = static_cast<uint32_t>((c / Cfg::AS) & 1);
         mbar_wait(&a_full[as], ph);
         mbar_wait(&b_full[as], ph);
-        if (kc == 0 && ti >= 2) mbar_wait(&acc_empty[ab], static_cast<uint32_t>(((ti >> 1) & 1) ^ 1));
+        if (j == 0 && ti >= 2) mbar_wait(&acc_empty[ab], static_cast<uint32_t>(((ti >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t so = smem_u32(ops + as * Cfg::OPBYTES);
         const uint32_t d = tmem_base + static_cast<uint32_t>(ab * NN);
@@ -239,12 +241,12 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
           const uint64_t al = umma_desc_k16(so + Cfg::ABYTES + koff);
           const uint64_t bh = umma_desc_k16(so + 2 * Cfg::ABYTES + koff);
           const uint64_t bl = umma_desc_k16(so + 2 * Cfg::ABYTES + Cfg::BBYTES + koff);
-          mma_tf32(d, ah, bh, idesc, (kc | ks) != 0);
+          mma_tf32(d, ah, bh, idesc, (j | ks) != 0);
           mma_tf32(d, ah, bl, idesc, 1);
           mma_tf32(d, al, bh, idesc, 1);
         }
         mma_commit(&a_empty[as]);
-        if (kc == Cfg::KCH - 1) mma_commit(&acc_full[ab]);
+        if (j == Cfg::KCH - 1) mma_commit(&acc_full[ab]);
       }
     }
   } else if (warp < Cfg::CONV_WARPS) {
@@ -288,7 +290,10 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
       tc_fence_after();
       const long long row0 = tile * Cfg::TILE + 32 * q;
 #pragma unroll 1
-      for (int c = 0; c < NN / 16; ++c) {
+      for (int c0 = 0; c0 < NN / 16; ++c0) {
+        // rotate the column order per quarter and tile: spreads the strided
+        // row segments of concurrent stores over more DRAM channels
+        const int c = (c0 + q + static_cast<int>(tile)) % (NN / 16);
         uint32_t v[16];
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) +
                                static_cast<uint32_t>(ab * NN + 16 * c);
