@@ -65,6 +65,10 @@ std::uint64_t mask_fingerprint(int k, const std::vector<double>& w);
 // Fragment-order permutations of H for the kernels (plan.cc).
 void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out);
 void layout_hfused8(const std::vector<double>& op, std::vector<double>& out);
+// G = H (C (x) C): the operator with the forward DCT composed in (pixels ->
+// filtered coefficients), accumulated in long double and rounded once.
+std::vector<long double> compose_forward_ld(const std::vector<double>& op, const std::vector<double>& basis, int n);
+std::vector<double> compose_forward(const std::vector<double>& op, const std::vector<double>& basis, int n);
 void layout_hfused16(const std::vector<double>& op, std::vector<double>& out);
 void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>& out);
 void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>& basis,

@@ -520,23 +520,26 @@ __global__ void __launch_bounds__(c16::CWARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
-// k_fused8: u8 -> C X C^t -> H -> C^t Y C -> round/clamp -> u8, n = 8.
+// k_fused8: u8 -> G p -> C^t Y C -> round/clamp -> u8, n = 8, where
+// G = H (C (x) C) is the DCT-domain operator with the forward DCT composed in
+// on the host (compose_forward, long-double accumulation), so Y = G vec(P) are
+// the filtered DCT coefficients of filter_block (filter.hpp:71-73) and the
+// FP64 pipe does 2N^4 + 4N^3 flop per block instead of 2N^4 + 8N^3.
 //
 // Work unit ("strip"): 16 horizontally adjacent blocks = 8 pixel rows x 128
 // bytes, owned by one warp. Pixels arrive through 16-byte streaming loads
 // issued one strip ahead (prefetch into registers), are staged in a padded
 // per-warp buffer (row stride 144 B), and every stage is a DMMA chain whose
 // fragment layouts line up so no shuffles are needed:
-//   forward pass 1  T1^T = C P^T  : A = C[g][2t+s] (registers), B = pixels
-//   forward pass 2  X^T = T1^T C^t: A = pass-1 accumulators, B = C[g][2t+s]
-//     -> lane (g,t) holds X[2t][g], X[2t+1][g] of each block.
-//   filter          Y^T = X^T H^T : blocks on M (2 m-tiles), H^T from shared
-//     memory (layout_hfused8), X via the per-warp staging buffer.
+//   pixels -> FP64 staging: lane (g,t) writes pixels (2t,g), (2t+1,g) of each
+//     block (the slots the forward DCT's X[2t][g], X[2t+1][g] would take).
+//   filter          Y^T = P^T G^T : blocks on M (2 m-tiles), G^T from shared
+//     memory (layout_hfused8 of G), P via the per-warp staging buffer.
 //   inverse pass 1  Z = C^t Y     : A = C[2t+s][g], B = Y via staging
 //   inverse pass 2  O = Z C + 0.5 : A = pass-1 accumulators, B = C[2t+s][g]
 //     -> lane (g,t) holds O[g][2t], O[g][2t+1]: two adjacent output pixels,
 //     already offset by 0.5 so quantisation is one floor conversion.
-// Forward/inverse work on 4 blocks at a time so 4 independent DMMA chains
+// The inverse works on 4 blocks at a time so 4 independent DMMA chains
 // interleave. Staging layout: block b owns 512 B = 4 rows x 8 chunks of 16 B;
 // logical (row r, chunk c) is stored at chunk c ^ 2r ^ f(b), f(b) = (b&7) ^
 // ((b&1)<<2). Every 16-byte access pattern below then hits 8 distinct chunks
@@ -620,30 +623,16 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
     __syncwarp();
     if (s + total < nstrips) prefetch(s + total);
 
-    // forward DCT, 16 blocks, 4 interleaved chains
+    // The forward DCT is folded into the operator (G = H (C (x) C), see
+    // compose_forward): stage each block's pixels as FP64 in X's layout, lane
+    // (g, t) writing pixels (2t, g) and (2t+1, g) where X[2t][g], X[2t+1][g]
+    // would go.
 #pragma unroll
-    for (int b0 = 0; b0 < SB; b0 += 4) {
-      double p0[4], p1[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t pp = *reinterpret_cast<const uint16_t*>(pix + g * PS + 8 * (b0 + i) + 2 * t);
-        p0[i] = u8_to_f64(pp & 0xffu);
-        p1[i] = u8_to_f64(pp >> 8);
-      }
-      double2 d[4], x[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { d[i] = make_double2(0.0, 0.0); dmma(d[i], af0, p0[i]); }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dmma(d[i], af1, p1[i]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { x[i] = make_double2(0.0, 0.0); dmma(x[i], d[i].x, af0); }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dmma(x[i], d[i].y, af1);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int b = b0 + i;
-        *reinterpret_cast<double2*>(xy + b * 512 + t * 128 + ((g ^ (2 * t) ^ fsw(b)) << 4)) = x[i];
-      }
+    for (int b = 0; b < SB; ++b) {
+      const uint32_t q0 = pix[(2 * t) * PS + 8 * b + g];
+      const uint32_t q1 = pix[(2 * t + 1) * PS + 8 * b + g];
+      *reinterpret_cast<double2*>(xy + b * 512 + t * 128 + ((g ^ (2 * t) ^ fsw(b)) << 4)) =
+          make_double2(u8_to_f64(q0), u8_to_f64(q1));
     }
     __syncwarp();
 
@@ -739,9 +728,9 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
 // px). 16 warps; lane 0 of warp 0 also streams the operator. Phases per tile
 // (CTA barrier between them):
 //   pixels -> shared (16-byte loads, prefetched one tile ahead into registers)
-//   forward DCT, 4 blocks per warp, 32 DMMA/block:
-//     T1^T = C P^T (A = C rows in registers, B = pixel pairs), X^T = T1^T C^t
-//   filter Y^T = X^T H^T: warp (mg = w&3, ng = w>>2) owns 16 blocks x 64
+//   pixels -> FP64 block staging (the forward DCT is composed into the
+//     operator on the host, G = H (C (x) C), as in k_fused8)
+//   filter Y^T = P^T G^T: warp (mg = w&3, ng = w>>2) owns 16 blocks x 64
 //     outputs; K = 256 streamed as 16 chunks of H^T fragments (32 KB each,
 //     cp.async.bulk into a 2-stage ring, refilled as soon as a stage is
 //     released by all warps); X stays in
@@ -848,57 +837,18 @@ __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
     if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
     bar_mma();
 
-    // ---- forward DCT: blocks 4*warp .. +3
-    {
-      double cf[2][4];
+    // ---- pixels -> FP64 staging, blocks 4*warp .. +3. The forward DCT is
+    // composed into the operator (G = H (C (x) C)), so word w of a block takes
+    // the pixel pair (2a, v), (2a+1, v) in the slot of coefficients (u = 2a+e, v).
 #pragma unroll
-      for (int x = 0; x < 2; ++x)
+    for (int bb = 0; bb < 4; ++bb) {
+      const int b = 4 * warp + bb;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) cf[x][s] = cb[(8 * x + g) * 16 + 8 * (s >> 1) + 2 * t + (s & 1)];
-#pragma unroll 1
-      for (int bb = 0; bb < 4; ++bb) {
-        const int b = 4 * warp + bb;
-        double p[2][4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int a = 0; a < 2; ++a) {
-            const uint32_t pp = *reinterpret_cast<const uint16_t*>(pix + (8 * nt + g) * PS + b * 16 + 8 * a + 2 * t);
-            p[nt][2 * a] = u8_to_f64(pp & 0xffu);
-            p[nt][2 * a + 1] = u8_to_f64(pp >> 8);
-          }
-        double2 d[2][2], x[2][2];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) d[mt][nt] = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) dmma(d[mt][nt], cf[mt][s], p[nt][s]);
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) x[mt][nt] = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              const double a = (s & 1) ? d[mt][s >> 1].y : d[mt][s >> 1].x;
-              dmma(x[mt][nt], a, cf[nt][s]);
-            }
-        // x[mt][nt] = X[u = 8nt + 2t + {0,1}][v = 8mt + g] -> word 8v + (a ^ 4(v&1)), a = 4nt + t
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const int v = 8 * mt + g;
-            *reinterpret_cast<double2*>(xy + xw(b, 8 * v + ((4 * nt + t) ^ (4 * (v & 1))))) = x[mt][nt];
-          }
+      for (int i = 0; i < 4; ++i) {
+        const int wd = lane + 32 * i, v = wd >> 3, a = (wd & 7) ^ (4 * (v & 1));
+        const uint32_t q0 = pix[(2 * a) * PS + b * 16 + v];
+        const uint32_t q1 = pix[(2 * a + 1) * PS + b * 16 + v];
+        *reinterpret_cast<double2*>(xy + xw(b, wd)) = make_double2(u8_to_f64(q0), u8_to_f64(q1));
       }
     }
     bar_mma();
@@ -1380,8 +1330,8 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
   if (e == cudaSuccess) e = cudaMemcpy(p->d_hcoef, hcoef.data(), nn * nn * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(p->d_nan, 0, sizeof(int));
   if (e == cudaSuccess) {
-    if (n == 8) dctf::layout_hfused8(p->op, hfused);
-    else dctf::layout_hfused16(p->op, hfused);
+    if (n == 8) dctf::layout_hfused8(dctf::compose_forward(p->op, p->basis, 8), hfused);
+    else dctf::layout_hfused16(dctf::compose_forward(p->op, p->basis, 16), hfused);
     e = cudaMalloc(&p->d_hfused, hfused.size() * sizeof(double));
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_hfused, hfused.data(), hfused.size() * sizeof(double), cudaMemcpyHostToDevice);

@@ -441,6 +441,35 @@ void layout_hfused16(const std::vector<double>& op, std::vector<double>& out) {
           }
 }
 
+// G[o][i*n+j] = sum_{u,v} H[o][u*n+v] C[u][i] C[v][j]: vec(C P C^t) =
+// (C (x) C) vec(P), so G vec(P) = H vec(forward_2d(P)) up to rounding.
+// Separable: first T[o][u*n+j] = sum_v H[o][u*n+v] C[v][j], then contract u.
+std::vector<long double> compose_forward_ld(const std::vector<double>& op, const std::vector<double>& basis, int n) {
+  const int nn = n * n;
+  std::vector<long double> t(size_t(nn) * nn, 0.0L), g(size_t(nn) * nn, 0.0L);
+  for (int o = 0; o < nn; ++o)
+    for (int u = 0; u < n; ++u)
+      for (int j = 0; j < n; ++j) {
+        long double acc = 0.0L;
+        for (int v = 0; v < n; ++v)
+          acc += static_cast<long double>(op[size_t(o) * nn + u * n + v]) * basis[v * n + j];
+        t[size_t(o) * nn + u * n + j] = acc;
+      }
+  for (int o = 0; o < nn; ++o)
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        long double acc = 0.0L;
+        for (int u = 0; u < n; ++u) acc += t[size_t(o) * nn + u * n + j] * basis[u * n + i];
+        g[size_t(o) * nn + i * n + j] = acc;
+      }
+  return g;
+}
+
+std::vector<double> compose_forward(const std::vector<double>& op, const std::vector<double>& basis, int n) {
+  const std::vector<long double> g = compose_forward_ld(op, basis, n);
+  return std::vector<double>(g.begin(), g.end());
+}
+
 // Exact INT8 slicing of the forward-DCT-composed operator for k_fused8_i8.
 // G = H (C (x) C) maps a block's 64 pixels p (index i*8+j) straight to its
 // filtered DCT coefficients Y (index u*8+v). G is scaled by 2^-e (e: smallest
@@ -456,17 +485,7 @@ void layout_hfused16(const std::vector<double>& op, std::vector<double>& out) {
 void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>& basis,
                        std::vector<int8_t>& bimg, std::vector<double>& scales) {
   constexpr int S = 7;
-  std::vector<long double> g(64 * 64, 0.0L);
-  for (int o = 0; o < 64; ++o)
-    for (int i = 0; i < 8; ++i)
-      for (int j = 0; j < 8; ++j) {
-        long double acc = 0.0L;
-        for (int u = 0; u < 8; ++u)
-          for (int v = 0; v < 8; ++v)
-            acc += static_cast<long double>(op[size_t(o) * 64 + u * 8 + v]) *
-                   (static_cast<long double>(basis[u * 8 + i]) * basis[v * 8 + j]);
-        g[o * 64 + i * 8 + j] = acc;
-      }
+  const std::vector<long double> g = compose_forward_ld(op, basis, 8);
   bimg.assign(size_t(S) * 64 * 128, 0);
   scales.assign(64, 0.0);
   // One exponent for the whole operator (|G| < 2^e): the error bound
