@@ -54,9 +54,14 @@ typedef enum {
   DCTF_PREC_FP64 = 0,    /* FP64 DMMA tensor pipe; coefficients within 1e-9 rel. */
   DCTF_PREC_TF32X3 = 1,  /* split-precision tcgen05 kind::tf32, 3 passes          */
   DCTF_PREC_BF16X3 = 2,  /* split-precision tcgen05 kind::f16 (bf16), 3 passes     */
-  DCTF_PREC_INT8_EXACT = 3 /* n = 8 image path: DCT-domain contraction as exact INT8
+  DCTF_PREC_INT8_EXACT = 3, /* n = 8 image path: DCT-domain contraction as exact INT8
                               tcgen05 slices (FP64-class accuracy); other entry
                               points of such a plan run the FP64 kernels        */
+  DCTF_PREC_FP64_DENSE = 4  /* as FP64, but never exploit operator structure: the
+                              n = 8 image path of a DCTF_PREC_FP64 plan whose H is
+                              block-diagonal in the (u mod 2, v mod 2) classes
+                              (masks symmetric in both axes) runs the parity-
+                              class kernel; this mode keeps the dense one     */
 } dctf_precision;
 
 typedef struct dctf_plan dctf_plan;
@@ -104,6 +109,11 @@ dctf_status dctf_plan_pairs(const dctf_plan* plan, int domain, double* h_lefts, 
 /* Plan metadata: block side, sandwich pair count and whether mirrored rows
  * were merged (OperatorSet::pairs.size(), ::symmetric_merged). */
 dctf_status dctf_plan_info(const dctf_plan* plan, int* n, int* npairs, int* symmetric_merged);
+
+/* Name of the kernel dctf_filter_image_u8 runs for this plan: "k_fused8",
+ * "k_fused8_sym" (parity-class structure), "k_fused8_i8", "k_fused16" or
+ * "unfused" (forward -> filter_coeffs -> inverse). NULL for a NULL plan. */
+const char* dctf_plan_image_kernel(const dctf_plan* plan);
 
 /* Host-only operator compile (no device needed): the same compile
  * dctf_plan_create performs, returning C (n*n) and H (n^4) into host buffers

@@ -50,7 +50,8 @@ enum class Precision {
   kFp64 = DCTF_PREC_FP64,
   kTf32x3 = DCTF_PREC_TF32X3,
   kBf16x3 = DCTF_PREC_BF16X3,
-  kInt8Exact = DCTF_PREC_INT8_EXACT
+  kInt8Exact = DCTF_PREC_INT8_EXACT,
+  kFp64Dense = DCTF_PREC_FP64_DENSE
 };
 
 class BlockMatrix {

@@ -22,7 +22,7 @@ lib = C.CDLL(LIB_PATH)
 
 OK, INVALID_ARGUMENT, CUDA_ERROR, NAN_ENCOUNTERED, UNSUPPORTED = range(5)
 PAD_ZERO, PAD_REPLICATE = 0, 1
-PREC_FP64, PREC_TF32X3, PREC_BF16X3, PREC_INT8_EXACT = 0, 1, 2, 3
+PREC_FP64, PREC_TF32X3, PREC_BF16X3, PREC_INT8_EXACT, PREC_FP64_DENSE = 0, 1, 2, 3, 4
 
 _d = C.POINTER(C.c_double)
 _u8 = C.POINTER(C.c_uint8)
@@ -39,6 +39,7 @@ _SIGS = {
     "dctf_format_operator_dump": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_size_t)]),
     "dctf_operator_from_dump": (_st, [C.c_char_p, C.c_size_t, _d, _i, _i, _i]),
     "dctf_plan_info": (_st, [_vp, _i, _i, _i]),
+    "dctf_plan_image_kernel": (C.c_char_p, [_vp]),
     "dctf_compile_operator": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_int, _d, _d, _i, _i]),
     "dctf_plan_basis": (_st, [_vp, _d]),
     "dctf_plan_operator": (_st, [_vp, _d]),

@@ -722,6 +722,208 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
 }
 
 // ---------------------------------------------------------------------------
+// k_fused8_sym: k_fused8 for operators that are block-diagonal in the four
+// (u mod 2, v mod 2) parity classes (masks symmetric in both axes; see
+// layout_sym8 in plan.cc). Since C[u][7-i] = (-1)^u C[u][i], a block's pixels
+// enter the DCT only through the quad butterflies
+//   q_c(i,j) = p(i,j) +/- p(7-i,j) +/- p(i,7-j) +/- p(7-i,7-j),  i, j < 4,
+// exact integers formed on the integer ALUs; per class c the filtered
+// coefficients are Y_c = G_c q_c (16 x 16, G_c = H_c (C_c (x) C_c)) and the
+// inverse is Z_c = W_c Y_c (16 x 16); output pixels are +/- sums of the Z_c
+// (8 DADD per quad), +0.5 folded into Z_ee's accumulator, floor -> u8.
+// DMMA per block: 8 (vs 20 dense) — 1,024 + 1,024 FMA.
+// Work unit as in k_fused8: a warp owns a 16-block strip (two m-tiles of 8
+// blocks on the DMMA M axis); lane (g, t) owns block g of the m-tile, k-step
+// s <-> quad position (s, t) in the filter and Y chains straight into the
+// inverse's A operand (k-step (nt, e) <-> output o = 8nt + 2t + e).
+namespace f8s {
+#ifndef F8S_MINB
+#define F8S_MINB 2
+#endif
+constexpr int WARPS = 8;
+constexpr int SB = 16;
+constexpr int PS = 192;  // adjacent rows 16 banks apart: conflict-free u16 output stores
+constexpr int PIX_BYTES = 8 * PS;
+constexpr int SMEM = 16384 + WARPS * PIX_BYTES;
+}  // namespace f8s
+
+// small signed integer (|v| < 2^20) -> double, exactly, on the integer pipes
+__device__ __forceinline__ double i32_to_f64(int v) {
+  const uint32_t m = static_cast<uint32_t>(v < 0 ? -v : v);
+  const int e = 31 - __clz(m);
+  const uint32_t hi = ((static_cast<uint32_t>(1022 + e) << 20) + (m << (20 - e))) |
+                      (static_cast<uint32_t>(v) & 0x80000000u);
+  return m ? __hiloint2double(static_cast<int>(hi), 0) : 0.0;
+}
+
+__global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
+    k_fused8_sym(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
+                 long long frame_stride, int nframes, int bw, int bh, int nsx,
+                 const double* __restrict__ hsym, double* __restrict__ coef_out) {
+  using namespace f8s;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const double2* gs = reinterpret_cast<const double2*>(smem);          // [c][nt][sp][lane]
+  const double2* ws = reinterpret_cast<const double2*>(smem + 8192);   // [c][nt2][nt][lane]
+  {
+    const double2* src = reinterpret_cast<const double2*>(hsym);
+    double2* dst = reinterpret_cast<double2*>(smem);
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  uint8_t* pix = smem + 16384 + warp * PIX_BYTES;
+
+  const long long spf = static_cast<long long>(bh) * nsx;
+  const long long nstrips = spf * nframes;
+  const long long total = static_cast<long long>(gridDim.x) * WARPS;
+  const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
+  const int r0 = lane >> 3, c16 = (lane & 7) * 16;
+
+  uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
+  long long s = static_cast<long long>(blockIdx.x) * WARPS + warp;
+  auto strip_at = [&](long long si, int& f, int& by, int& bx0) {
+    f = static_cast<int>(si / spf);
+    const long long rem = si - static_cast<long long>(f) * spf;
+    by = static_cast<int>(rem / nsx);
+    bx0 = static_cast<int>(rem - static_cast<long long>(by) * nsx) * SB;
+  };
+  auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && bx0 * 8 + 128 <= w; };
+  auto prefetch = [&](long long si) {
+    int f, by, bx0;
+    strip_at(si, f, by, bx0);
+    if (is_fast(by, bx0)) {
+      const uint8_t* p = in + f * frame_stride + static_cast<size_t>(by * 8) * pitch + bx0 * 8 + c16;
+      pf0 = ldg_stream(p + r0 * pitch);
+      pf1 = ldg_stream(p + (r0 + 4) * pitch);
+    }
+  };
+  if (s < nstrips) prefetch(s);
+
+  for (; s < nstrips; s += total) {
+    int f, by, bx0;
+    strip_at(s, f, by, bx0);
+    const bool fast = is_fast(by, bx0);
+    if (fast) {
+      *reinterpret_cast<uint4*>(pix + r0 * PS + c16) = pf0;
+      *reinterpret_cast<uint4*>(pix + (r0 + 4) * PS + c16) = pf1;
+    } else {
+      const uint8_t* ib = in + f * frame_stride;
+      for (int e = lane; e < 8 * 128; e += 32) {
+        const int r = e >> 7, c = e & 127;
+        const int y = min(by * 8 + r, h - 1), x = min(bx0 * 8 + c, w - 1);
+        pix[r * PS + c] = ib[static_cast<size_t>(y) * pitch + x];
+      }
+    }
+    __syncwarp();
+    if (s + total < nstrips) prefetch(s + total);
+
+#pragma unroll 1
+    for (int mt = 0; mt < 2; ++mt) {
+      const int b = 8 * mt + g;
+      uint8_t* pb = pix + 8 * b;
+      // quad butterflies at positions (sq, t), sq = 0..3, all four classes
+      double q[4][4];
+#pragma unroll
+      for (int sq = 0; sq < 4; ++sq) {
+        const uint2 top = *reinterpret_cast<const uint2*>(pb + sq * PS);
+        const uint2 bot = *reinterpret_cast<const uint2*>(pb + (7 - sq) * PS);
+        const int p00 = (top.x >> (8 * t)) & 0xff, p01 = (top.y >> (24 - 8 * t)) & 0xff;
+        const int p10 = (bot.x >> (8 * t)) & 0xff, p11 = (bot.y >> (24 - 8 * t)) & 0xff;
+        const int rs0 = p00 + p10, ra0 = p00 - p10, rs1 = p01 + p11, ra1 = p01 - p11;
+        q[0][sq] = i32_to_f64(rs0 + rs1);
+        q[1][sq] = i32_to_f64(rs0 - rs1);
+        q[2][sq] = i32_to_f64(ra0 + ra1);
+        q[3][sq] = i32_to_f64(ra0 - ra1);
+      }
+      // filter: Y_c^T = q_c^T G_c^T, 8 independent chains of 4
+      double2 y[4][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) y[c][nt] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int sp = 0; sp < 2; ++sp)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const double2 bb = gs[((c * 2 + nt) * 2 + sp) * 32 + lane];
+            dmma(y[c][nt], q[c][2 * sp], bb.x);
+            dmma(y[c][nt], q[c][2 * sp + 1], bb.y);
+          }
+      if (coef_out) {
+        const int bx = bx0 + b;
+        if (bx < bw) {
+          double* dst = coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 64;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int o = 8 * nt + 2 * t + e;
+                dst[(2 * (o >> 2) + (c >> 1)) * 8 + 2 * (o & 3) + (c & 1)] = e ? y[c][nt].y : y[c][nt].x;
+              }
+        }
+      }
+      // inverse: Z_c^T = Y_c^T W_c^T (+0.5 in the ee class)
+      double2 z[4][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int nt2 = 0; nt2 < 2; ++nt2) z[c][nt2] = c == 0 ? make_double2(0.5, 0.5) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int nt2 = 0; nt2 < 2; ++nt2) {
+            const double2 bb = ws[((c * 2 + nt2) * 2 + nt) * 32 + lane];
+            dmma(z[c][nt2], y[c][nt].x, bb.x);
+            dmma(z[c][nt2], y[c][nt].y, bb.y);
+          }
+      __syncwarp();
+      // un-butterfly, quantise, write the four reflections of each position
+#pragma unroll
+      for (int nt2 = 0; nt2 < 2; ++nt2) {
+        const int i = 2 * nt2 + (t >> 1), j = 2 * (t & 1);
+        uint32_t o_ij[2], o_rj[2], o_ir[2], o_rr[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double zee = e ? z[0][nt2].y : z[0][nt2].x, zeo = e ? z[1][nt2].y : z[1][nt2].x;
+          const double zoe = e ? z[2][nt2].y : z[2][nt2].x, zoo = e ? z[3][nt2].y : z[3][nt2].x;
+          const double a = zee + zeo, bq = zee - zeo, cq = zoe + zoo, d = zoe - zoo;
+          o_ij[e] = floor_to_u8(a + cq);   // (i, j+e)
+          o_rj[e] = floor_to_u8(a - cq);   // (7-i, j+e)
+          o_ir[e] = floor_to_u8(bq + d);   // (i, 7-j-e)
+          o_rr[e] = floor_to_u8(bq - d);   // (7-i, 7-j-e)
+        }
+        *reinterpret_cast<uint16_t*>(pb + i * PS + j) = static_cast<uint16_t>(o_ij[0] | (o_ij[1] << 8));
+        *reinterpret_cast<uint16_t*>(pb + (7 - i) * PS + j) = static_cast<uint16_t>(o_rj[0] | (o_rj[1] << 8));
+        *reinterpret_cast<uint16_t*>(pb + i * PS + 6 - j) = static_cast<uint16_t>(o_ir[1] | (o_ir[0] << 8));
+        *reinterpret_cast<uint16_t*>(pb + (7 - i) * PS + 6 - j) = static_cast<uint16_t>(o_rr[1] | (o_rr[0] << 8));
+      }
+    }
+    __syncwarp();
+
+    uint8_t* ob = out + f * frame_stride;
+    if (fast) {
+      uint8_t* p = ob + static_cast<size_t>(by * 8) * pitch + bx0 * 8 + c16;
+      stg_stream(p + r0 * pitch, *reinterpret_cast<const uint4*>(pix + r0 * PS + c16));
+      stg_stream(p + (r0 + 4) * pitch, *reinterpret_cast<const uint4*>(pix + (r0 + 4) * PS + c16));
+    } else {
+      for (int e = lane; e < 8 * 128; e += 32) {
+        const int r = e >> 7, c = e & 127;
+        const int y = by * 8 + r, x = bx0 * 8 + c;
+        if (y < h && x < w) ob[static_cast<size_t>(y) * pitch + x] = pix[r * PS + c];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_fused16: the n = 16 chain fused, one HBM pass per pixel.
 //
 // CTA tile = a strip of 64 horizontally adjacent 16x16 blocks (16 rows x 1024
@@ -1234,6 +1436,26 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
   return DCTF_OK;
 }
 
+dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
+                              size_t pitch, long long frame_stride, int nframes, double* coef_out,
+                              cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_fused8_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, f8s::SMEM));
+    attr = true;
+  }
+  const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8s::SB - 1) / f8s::SB;
+  const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
+  const long long ctas = std::min<long long>(static_cast<long long>(F8S_MINB) * sm_count(p->device),
+                                             (nstrips + f8s::WARPS - 1) / f8s::WARPS);
+  if (ctas <= 0) return DCTF_OK;
+  k_fused8_sym<<<static_cast<unsigned>(ctas), f8s::WARPS * 32, f8s::SMEM, st>>>(
+      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hsym, coef_out);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
 dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                            size_t pitch, long long frame_stride, int nframes, double* coef_out,
                            cudaStream_t st) {
@@ -1261,6 +1483,7 @@ dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* 
     return dctf::launch_fused8_i8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st,
                                   sm_count(p->device));
   const bool split = p->precision == DCTF_PREC_TF32X3;
+  if (p->n == 8 && p->sym) return launch_fused8_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (!split && !std::getenv("DCTF_N16_UNFUSED"))
     return launch_fused16(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
@@ -1336,6 +1559,14 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_hfused, hfused.data(), hfused.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
+  p->sym = n == 8 && precision == DCTF_PREC_FP64 && dctf::parity_block_diagonal(p->op, n);
+  if (e == cudaSuccess && p->sym) {
+    std::vector<double> hsym;
+    dctf::layout_sym8(p->op, p->basis, hsym);
+    e = cudaMalloc(&p->d_hsym, hsym.size() * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_hsym, hsym.data(), hsym.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess && precision == DCTF_PREC_TF32X3) {
     std::vector<float> hs;
     dctf::layout_hsplit_tf32(n, p->op, hs);
@@ -1366,7 +1597,7 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
   dctf::reset_launches();
   if (!out || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
-  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_INT8_EXACT)
+  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DENSE)
     return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
   if (kr < 1 || kc < 1) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
   auto* p = new dctf_plan();
@@ -1390,7 +1621,7 @@ dctf_status dctf_plan_create_from_dump(const char* text, size_t len, int precisi
   dctf::reset_launches();
   if (!out || !text) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
-  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_INT8_EXACT)
+  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DENSE)
     return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
   auto* p = new dctf_plan();
   p->precision = precision;
@@ -1477,6 +1708,7 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_basis);
     cudaFree(p->d_hcoef);
     cudaFree(p->d_hfused);
+    cudaFree(p->d_hsym);
     cudaFree(p->d_hsplit);
     cudaFree(p->d_gimg);
     cudaFree(p->d_gscale);
@@ -1499,6 +1731,14 @@ dctf_status dctf_plan_info(const dctf_plan* p, int* n, int* npairs, int* merged)
   if (npairs) *npairs = p->npairs;
   if (merged) *merged = p->merged;
   return DCTF_OK;
+}
+
+const char* dctf_plan_image_kernel(const dctf_plan* p) {
+  if (!p) return nullptr;
+  if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT) return "k_fused8_i8";
+  if (p->precision == DCTF_PREC_TF32X3) return "unfused";
+  if (p->n == 8) return p->sym ? "k_fused8_sym" : "k_fused8";
+  return std::getenv("DCTF_N16_UNFUSED") ? "unfused" : "k_fused16";
 }
 
 dctf_status dctf_plan_basis(const dctf_plan* p, double* h_c) {

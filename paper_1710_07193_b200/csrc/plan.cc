@@ -470,6 +470,69 @@ std::vector<double> compose_forward(const std::vector<double>& op, const std::ve
   return std::vector<double>(g.begin(), g.end());
 }
 
+// Parity structure ("Structure"): for a mask symmetric in both
+// axes under either padding, the spatial operator commutes with the row and
+// column reflections, and since C[u][n-1-i] = (-1)^u C[u][i] the DCT-domain
+// operator is block-diagonal in the four (u mod 2, v mod 2) classes. The
+// reference's H carries only rounding residue (<= 1e-15 relative) off those
+// blocks. True when every off-class entry is <= 1e-13 x max|H|.
+bool parity_block_diagonal(const std::vector<double>& op, int n) {
+  const int nn = n * n;
+  double hmax = 0.0, off = 0.0;
+  for (int o = 0; o < nn; ++o)
+    for (int k = 0; k < nn; ++k) {
+      const double a = std::fabs(op[size_t(o) * nn + k]);
+      hmax = std::max(hmax, a);
+      const int uo = o / n, vo = o % n, uk = k / n, vk = k % n;
+      if (((uo ^ uk) & 1) || ((vo ^ vk) & 1)) off = std::max(off, a);
+    }
+  return hmax > 0.0 && off <= 1e-13 * hmax;
+}
+
+// Operator image of k_fused8_sym (2 x 8 KB of FP64). Class c = 2 pu + pv
+// (pu: row/u parity, pv: column/v parity); inside a class, output o = 4u' + v'
+// is coefficient (u, v) = (2u' + pu, 2v' + pv) and quad position (i, j),
+// i, j < 4, is pixel (i, j) together with its reflections (7-i, j), (i, 7-j),
+// (7-i, 7-j). The butterflied pixels q_c(i, j) (exact integers) give
+//   Y_c = G_c q_c,   G_c[o][(i,j)] = sum_{(u2,v2) in c} H[(u,v)][(u2,v2)] C[u2][i] C[v2][j]
+//   Z_c = W_c Y_c,   W_c[(i,j)][o] = C[u][i] C[v][j]
+// and the output pixels are +/- sums of the four Z_c at (i, j).
+// Filter part, DMMA B fragments: [c][nt][sp][lane][e] = G_c[o = 8nt + g][k = (i = 2sp+e, j = t)].
+// Inverse part: [c][nt2][nt][lane][e] = W_c[pos = (2nt2 + (g>>2), g&3)][o = 8nt + 2t + e].
+void layout_sym8(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out) {
+  out.assign(2 * 1024, 0.0);
+  auto coef = [](int c, int o) {  // natural coefficient index of class output o
+    const int u = 2 * (o >> 2) + (c >> 1), v = 2 * (o & 3) + (c & 1);
+    return u * 8 + v;
+  };
+  auto C = [&](int u, int i) { return static_cast<long double>(basis[u * 8 + i]); };
+  size_t w = 0;
+  for (int c = 0; c < 4; ++c)
+    for (int nt = 0; nt < 2; ++nt)
+      for (int sp = 0; sp < 2; ++sp)
+        for (int lane = 0; lane < 32; ++lane)
+          for (int e = 0; e < 2; ++e) {
+            const int g = lane >> 2, t = lane & 3, o = 8 * nt + g, i = 2 * sp + e, j = t;
+            const int row = coef(c, o);
+            long double acc = 0.0L;
+            for (int o2 = 0; o2 < 16; ++o2) {
+              const int k = coef(c, o2), u2 = k / 8, v2 = k % 8;
+              acc += static_cast<long double>(op[size_t(row) * 64 + k]) * C(u2, i) * C(v2, j);
+            }
+            out[w++] = static_cast<double>(acc);
+          }
+  for (int c = 0; c < 4; ++c)
+    for (int nt2 = 0; nt2 < 2; ++nt2)
+      for (int nt = 0; nt < 2; ++nt)
+        for (int lane = 0; lane < 32; ++lane)
+          for (int e = 0; e < 2; ++e) {
+            const int g = lane >> 2, t = lane & 3;
+            const int i = 2 * nt2 + (g >> 2), j = g & 3, o = 8 * nt + 2 * t + e;
+            const int k = coef(c, o), u = k / 8, v = k % 8;
+            out[w++] = static_cast<double>(C(u, i) * C(v, j));
+          }
+}
+
 // Exact INT8 slicing of the forward-DCT-composed operator for k_fused8_i8.
 // G = H (C (x) C) maps a block's 64 pixels p (index i*8+j) straight to its
 // filtered DCT coefficients Y (index u*8+v). G is scaled by 2^-e (e: smallest

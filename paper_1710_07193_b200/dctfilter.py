@@ -51,6 +51,7 @@ class Precision(enum.IntEnum):
     kTf32x3 = _lib.PREC_TF32X3
     kBf16x3 = _lib.PREC_BF16X3
     kInt8Exact = _lib.PREC_INT8_EXACT
+    kFp64Dense = _lib.PREC_FP64_DENSE
 
 
 class Mask:
@@ -304,12 +305,17 @@ class FilterPlan:
             raise _lib.NanEncountered("quantize: NaN sample")
         return out
 
+    @property
+    def image_kernel(self) -> str:
+        """Kernel filter_image runs for this plan (dctf_plan_image_kernel)."""
+        return _lib.lib.dctf_plan_image_kernel(self._h).decode()
+
     def filter_image(self, img, coeffs_out=None):
         """Fused whole-image DCT path on a (h, w) uint8 CUDA tensor."""
         import torch
         img = _check_image(img)
         h, w = img.shape
-        out = torch.empty_like(img)
+        out = _empty_pitched(img)
         cp = 0
         if coeffs_out is not None:
             n = self._n
@@ -328,7 +334,7 @@ class FilterPlan:
         import torch
         img = _check_image(img)
         h, w = img.shape
-        out = torch.empty_like(img)
+        out = _empty_pitched(img)
         check(_lib.lib.dctf_filter_image_spatial_u8(self._h, _dptr(img), _dptr(out), w, h,
                                                     img.stride(0), _stream(img.device)))
         return out
@@ -377,6 +383,17 @@ def operator_from_dump(text: str):
     check(_lib.lib.dctf_operator_from_dump(raw, len(raw), h.ctypes.data_as(_lib._d), C.byref(n),
                                            C.byref(k), C.byref(pad)))
     return h, k.value, pad.value
+
+
+def _empty_pitched(img):
+    """Output buffer with the input's row pitch: the C entry points take one
+    pitch for both images (dctf_filter_image_u8)."""
+    import torch
+    h, w = img.shape
+    pitch = img.stride(0)
+    if pitch == w:
+        return torch.empty_like(img)
+    return torch.empty((h, pitch), dtype=img.dtype, device=img.device)[:, :w]
 
 
 def _check_image(img):

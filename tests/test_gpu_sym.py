@@ -1,0 +1,113 @@
+"""Parity-class kernel k_fused8_sym ("Structure": for masks
+symmetric in both axes H_dct is block-diagonal in the four (u mod 2, v mod 2)
+classes; structure exploitation is optional and reported against the dense
+count). FP64 plans pick it automatically when H is block-diagonal to 1e-13;
+DCTF_PREC_FP64_DENSE keeps the dense k_fused8.
+
+CPU: the structural premise on the reference's own operator (symmetric masks
+-> off-class residue at rounding level; asymmetric -> dense).
+GPU: same reference-parity bar as every other path (coefficients 1e-9 rel,
+u8 bit-exact except reference near-ties), against the dense kernel and the
+reference itself, on ragged sizes, frame batches and both paddings."""
+import numpy as np
+import pytest
+
+import paper_1710_07193_b200 as P
+from paper_1710_07193_b200 import synth
+from conftest import blocks_to_image, nthreads, tie_report
+
+SYMMETRIC = {
+    "average3": (np.full(9, 1.0 / 9.0), 3),
+    "gaussian3": None,                       # filled from the reference preset
+    "gaussian5": (synth.gaussian_mask(5, 1.0), 5),
+    "laplacian3": (np.array([0, -1, 0, -1, 5, -1, 0, -1, 0], dtype=np.float64), 3),
+    "gaussian7": (synth.gaussian_mask(7, 2.0), 7),
+}
+
+
+def _off_class(h, n):
+    u = np.arange(n * n) // n
+    v = np.arange(n * n) % n
+    mask = ((u[:, None] ^ u[None, :]) & 1) | ((v[:, None] ^ v[None, :]) & 1)
+    return np.abs(h[mask.astype(bool)]).max() / np.abs(h).max()
+
+
+def test_symmetric_masks_give_parity_block_diagonal_operator(ref):
+    for name, spec in SYMMETRIC.items():
+        w, k = ref.mask_preset(name) if spec is None else spec
+        for pad in (0, 1):
+            h = ref.plan_operator(w, k, 8, pad)
+            assert _off_class(h, 8) <= 1e-13, (name, pad)
+    w, _ = synth.random_mask(3, 3)
+    assert _off_class(ref.plan_operator(w, 3, 8, 0), 8) > 1e-3
+
+
+def _masks(ref):
+    for name, spec in SYMMETRIC.items():
+        w, k = ref.mask_preset(name) if spec is None else spec
+        yield name, w, k
+
+
+@pytest.mark.gpu
+def test_kernel_selection(cuda, ref):
+    for name, w, k in _masks(ref):
+        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8_sym", name
+        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero,
+                            precision=P.Precision.kFp64Dense).image_kernel == "k_fused8", name
+    w, _ = synth.random_mask(3, 3)
+    assert P.FilterPlan(P.Mask(3, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8"
+    assert P.FilterPlan(P.Mask(3, w), 16, P.PaddingMode.kZero).image_kernel == "k_fused16"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wh", [(512, 512), (333, 200), (1000, 77)])
+def test_sym_matches_reference_and_dense(cuda, ref, wh):
+    torch = cuda
+    wd, h = wh
+    img = synth.uniform_image(31, wd, h)
+    d = torch.from_numpy(img).cuda()
+    nb = ((wd + 7) // 8) * ((h + 7) // 8)
+    for name, w, k in _masks(ref):
+        for pad in (0, 1):
+            sym = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad))
+            dense = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad), precision=P.Precision.kFp64Dense)
+            cs = torch.empty((nb, 8, 8), dtype=torch.float64, device="cuda")
+            cd = torch.empty_like(cs)
+            os_, od = sym.filter_image(d, cs), dense.filter_image(d, cd)
+            r_out, _, r_co, r_pq = ref.filter_image(img, w, k, pad, 8, threads=nthreads(),
+                                                    side_outputs=True)
+            ours = os_.cpu().numpy()
+            mism, excused, _ = tie_report(ours, r_out, blocks_to_image(r_pq, wd, h))
+            assert mism == excused, (name, pad, mism)
+            scale = np.abs(r_co).max()
+            assert np.abs(cs.cpu().numpy() - r_co).max() <= 1e-9 * scale, (name, pad)
+            assert (cs - cd).abs().max().item() <= 1e-12 * scale, (name, pad)
+            m2, e2, _ = tie_report(ours, od.cpu().numpy(), blocks_to_image(r_pq, wd, h))
+            assert m2 == e2, (name, pad)
+
+
+@pytest.mark.gpu
+def test_sym_frames_and_pitch(cuda, ref):
+    """Strided frame batch (dctf_filter_frames_u8, symmetric and asymmetric
+    plans mixed) and a padded pitch."""
+    torch = cuda
+    w, k = synth.gaussian_mask(5, 1.0), 5
+    wr, _ = synth.random_mask(5, 5)
+    plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kReplicate)
+    plan_r = P.FilterPlan(P.Mask(5, wr), 8, P.PaddingMode.kReplicate)
+    assert plan.image_kernel == "k_fused8_sym" and plan_r.image_kernel == "k_fused8"
+    frames = np.stack([synth.sinusoid_image(40 + f, 264, 136) for f in range(4)])
+    d = torch.from_numpy(frames).cuda()
+    outs = P.filter_frames(d, [plan, plan_r], [0, 1, 0, 1])
+    for f in range(4):
+        wm = w if f % 2 == 0 else wr
+        r_out, _, _, r_pq = ref.filter_image(frames[f], wm, 5, 1, 8, threads=nthreads(),
+                                             side_outputs=True)
+        got = outs[f].cpu().numpy()
+        mism, excused, _ = tie_report(got, r_out, blocks_to_image(r_pq, 264, 136))
+        assert mism == excused, f
+        single = (plan if f % 2 == 0 else plan_r).filter_image(d[f].contiguous())
+        assert np.array_equal(single.cpu().numpy(), got)
+    big = torch.zeros((136, 512), dtype=torch.uint8, device="cuda")
+    big[:, :264] = d[0]
+    assert torch.equal(plan.filter_image(big[:, :264]), plan.filter_image(d[0].contiguous()))
