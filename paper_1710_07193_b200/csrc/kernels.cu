@@ -733,9 +733,10 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
 // (8 DADD per quad), +0.5 folded into Z_ee's accumulator, floor -> u8.
 // DMMA per block: 8 (vs 20 dense) — 1,024 + 1,024 FMA.
 // Work unit as in k_fused8: a warp owns a 16-block strip (two m-tiles of 8
-// blocks on the DMMA M axis); lane (g, t) owns block g of the m-tile, k-step
-// s <-> quad position (s, t) in the filter and Y chains straight into the
-// inverse's A operand (k-step (nt, e) <-> output o = 8nt + 2t + e).
+// blocks on the DMMA M axis, processed together so each operator fragment
+// from shared memory feeds 4 DMMAs); lane (g, t) owns blocks g and 8 + g,
+// k-step s <-> quad position (s, t) in the filter, and Y chains straight into
+// the inverse's A operand (k-step (nt, e) <-> output o = 8nt + 2t + e).
 namespace f8s {
 #ifndef F8S_MINB
 #define F8S_MINB 2
@@ -818,12 +819,12 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
     __syncwarp();
     if (s + total < nstrips) prefetch(s + total);
 
-#pragma unroll 1
+    // quad butterflies of both m-tiles (blocks g and 8 + g) at positions
+    // (sq, t), sq = 0..3, all four classes
+    double q[2][4][4];
+#pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      const int b = 8 * mt + g;
-      uint8_t* pb = pix + 8 * b;
-      // quad butterflies at positions (sq, t), sq = 0..3, all four classes
-      double q[4][4];
+      const uint8_t* pb = pix + 8 * (8 * mt + g);
 #pragma unroll
       for (int sq = 0; sq < 4; ++sq) {
         const uint2 top = *reinterpret_cast<const uint2*>(pb + sq * PS);
@@ -831,68 +832,77 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
         const int p00 = (top.x >> (8 * t)) & 0xff, p01 = (top.y >> (24 - 8 * t)) & 0xff;
         const int p10 = (bot.x >> (8 * t)) & 0xff, p11 = (bot.y >> (24 - 8 * t)) & 0xff;
         const int rs0 = p00 + p10, ra0 = p00 - p10, rs1 = p01 + p11, ra1 = p01 - p11;
-        q[0][sq] = i32_to_f64(rs0 + rs1);
-        q[1][sq] = i32_to_f64(rs0 - rs1);
-        q[2][sq] = i32_to_f64(ra0 + ra1);
-        q[3][sq] = i32_to_f64(ra0 - ra1);
+        q[mt][0][sq] = i32_to_f64(rs0 + rs1);
+        q[mt][1][sq] = i32_to_f64(rs0 - rs1);
+        q[mt][2][sq] = i32_to_f64(ra0 + ra1);
+        q[mt][3][sq] = i32_to_f64(ra0 - ra1);
       }
-      // filter: Y_c^T = q_c^T G_c^T, 8 independent chains of 4
-      double2 y[4][2];
+    }
+    // per class: filter Y_c^T = q_c^T G_c^T and inverse Z_c^T = Y_c^T W_c^T
+    // for both m-tiles, so every operator fragment loaded from shared memory
+    // feeds 4 DMMAs (+0.5 rides in the ee class's accumulator)
+    double2 z[2][4][2];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+    for (int c = 0; c < 4; ++c) {
+      double2 y[2][2];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) y[c][nt] = make_double2(0.0, 0.0);
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) y[mt][nt] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int sp = 0; sp < 2; ++sp)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const double2 bb = gs[((c * 2 + nt) * 2 + sp) * 32 + lane];
-            dmma(y[c][nt], q[c][2 * sp], bb.x);
-            dmma(y[c][nt], q[c][2 * sp + 1], bb.y);
-          }
+        for (int nt = 0; nt < 2; ++nt) {
+          const double2 bb = gs[((c * 2 + nt) * 2 + sp) * 32 + lane];
+          dmma(y[0][nt], q[0][c][2 * sp], bb.x);
+          dmma(y[1][nt], q[1][c][2 * sp], bb.x);
+          dmma(y[0][nt], q[0][c][2 * sp + 1], bb.y);
+          dmma(y[1][nt], q[1][c][2 * sp + 1], bb.y);
+        }
       if (coef_out) {
-        const int bx = bx0 + b;
-        if (bx < bw) {
-          double* dst = coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 64;
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+        for (int mt = 0; mt < 2; ++mt) {
+          const int bx = bx0 + 8 * mt + g;
+          if (bx < bw) {
+            double* dst = coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 64;
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int o = 8 * nt + 2 * t + e;
-                dst[(2 * (o >> 2) + (c >> 1)) * 8 + 2 * (o & 3) + (c & 1)] = e ? y[c][nt].y : y[c][nt].x;
+                dst[(2 * (o >> 2) + (c >> 1)) * 8 + 2 * (o & 3) + (c & 1)] = e ? y[mt][nt].y : y[mt][nt].x;
               }
+          }
         }
       }
-      // inverse: Z_c^T = Y_c^T W_c^T (+0.5 in the ee class)
-      double2 z[4][2];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt2 = 0; nt2 < 2; ++nt2) z[c][nt2] = c == 0 ? make_double2(0.5, 0.5) : make_double2(0.0, 0.0);
+        for (int nt2 = 0; nt2 < 2; ++nt2) z[mt][c][nt2] = c == 0 ? make_double2(0.5, 0.5) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int nt2 = 0; nt2 < 2; ++nt2) {
+          const double2 bb = ws[((c * 2 + nt2) * 2 + nt) * 32 + lane];
+          dmma(z[0][c][nt2], y[0][nt].x, bb.x);
+          dmma(z[1][c][nt2], y[1][nt].x, bb.x);
+          dmma(z[0][c][nt2], y[0][nt].y, bb.y);
+          dmma(z[1][c][nt2], y[1][nt].y, bb.y);
+        }
+    }
+    __syncwarp();
+    // un-butterfly, quantise, write the four reflections of each position
 #pragma unroll
-          for (int nt2 = 0; nt2 < 2; ++nt2) {
-            const double2 bb = ws[((c * 2 + nt2) * 2 + nt) * 32 + lane];
-            dmma(z[c][nt2], y[c][nt].x, bb.x);
-            dmma(z[c][nt2], y[c][nt].y, bb.y);
-          }
-      __syncwarp();
-      // un-butterfly, quantise, write the four reflections of each position
+    for (int mt = 0; mt < 2; ++mt) {
+      uint8_t* pb = pix + 8 * (8 * mt + g);
 #pragma unroll
       for (int nt2 = 0; nt2 < 2; ++nt2) {
         const int i = 2 * nt2 + (t >> 1), j = 2 * (t & 1);
         uint32_t o_ij[2], o_rj[2], o_ir[2], o_rr[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const double zee = e ? z[0][nt2].y : z[0][nt2].x, zeo = e ? z[1][nt2].y : z[1][nt2].x;
-          const double zoe = e ? z[2][nt2].y : z[2][nt2].x, zoo = e ? z[3][nt2].y : z[3][nt2].x;
+          const double zee = e ? z[mt][0][nt2].y : z[mt][0][nt2].x, zeo = e ? z[mt][1][nt2].y : z[mt][1][nt2].x;
+          const double zoe = e ? z[mt][2][nt2].y : z[mt][2][nt2].x, zoo = e ? z[mt][3][nt2].y : z[mt][3][nt2].x;
           const double a = zee + zeo, bq = zee - zeo, cq = zoe + zoo, d = zoe - zoo;
           o_ij[e] = floor_to_u8(a + cq);   // (i, j+e)
           o_rj[e] = floor_to_u8(a - cq);   // (7-i, j+e)
