@@ -111,11 +111,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic():
-    """dram bytes per launch of k_fused8 from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_fused8_config2.json")
+def ncu_traffic(kernel):
+    """dram bytes per launch of the headline kernel from the committed ncu
+    --set full capture (profiles/ncu_headline_config2.json), if it is of
+    that kernel."""
+    p = os.path.join(ROOT, "profiles", "ncu_headline_config2.json")
     try:
         d = json.load(open(p))
+        if d.get("kernel") != kernel:
+            return None, None
         return d.get("dram_bytes_per_launch"), d.get("source")
     except Exception:
         return None, None
@@ -284,7 +288,7 @@ def main():
             parity = f"unchecked: {exc}"
 
     achieved_tf = FLOP_PER_BLOCK_FUSED * NBLOCKS / (ms_local / 1e3) / 1e12
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src = ncu_traffic(plan.image_kernel)
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs")
     gbs = value * BYTES_PER_BLOCK_FUSED / 1e9
