@@ -49,6 +49,8 @@ namespace dctf {
 // Thread-local error / launch bookkeeping (kernels.cu).
 dctf_status set_error(dctf_status s, const std::string& msg);
 void add_launches(int k);
+// Dynamic shared-memory opt-in, once per (kernel, device), thread-safe (kernels.cu).
+dctf_status ensure_dyn_smem(const void* func, int bytes, const char* name);
 void reset_launches();
 
 // Host operator compiler (plan.cc).

@@ -1320,6 +1320,31 @@ dctf_status make_xmap(void* vmap, const double* d, long long nblocks, int nn, in
 
 namespace {
 
+}  // namespace
+
+namespace dctf {
+// Opts `func` into `bytes` of dynamic shared memory on the current device,
+// once per (kernel, device); safe under concurrent first calls and across
+// several devices in one process.
+dctf_status ensure_dyn_smem(const void* func, int bytes, const char* name) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return set_error(DCTF_CUDA_ERROR, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == func && d.second == dev) return DCTF_OK;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(DCTF_CUDA_ERROR, std::string("cudaFuncSetAttribute(") + name + ")");
+  }
+  done.emplace_back(func, dev);
+  return DCTF_OK;
+}
+}  // namespace dctf
+
+namespace {
+
 int sm_count(int device) {
   static int cached[64] = {0};
   if (device < 0 || device >= 64) return 148;
@@ -1372,19 +1397,17 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
   if (s != DCTF_OK) return s;
   const int sms = sm_count(p->device);
   if (p->n == 8) {
-    static bool attr = false;
-    if (!attr) {
-      CUDA_TRY(cudaFuncSetAttribute(k_coef8, cudaFuncAttributeMaxDynamicSharedMemorySize, c8::SMEM));
-      attr = true;
+    {
+      const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_coef8), c8::SMEM, "k_coef8");
+      if (sa != DCTF_OK) return sa;
     }
     const long long ntiles = (nb + c8::TILE - 1) / c8::TILE;
     const long long ctas = std::min<long long>(sms, (ntiles + c8::WARPS - 1) / c8::WARPS);
     k_coef8<<<static_cast<unsigned>(ctas), c8::WARPS * 32, c8::SMEM, st>>>(map, p->d_hcoef, d_out, nb);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      CUDA_TRY(cudaFuncSetAttribute(k_coef16, cudaFuncAttributeMaxDynamicSharedMemorySize, c16::SMEM));
-      attr = true;
+    {
+      const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_coef16), c16::SMEM, "k_coef16");
+      if (sa != DCTF_OK) return sa;
     }
     const long long ntiles = (nb + c16::TILE - 1) / c16::TILE;
     const long long ctas = std::min<long long>(sms, ntiles);
@@ -1429,10 +1452,9 @@ dctf_status launch_inverse_u8(const dctf_plan* p, const double* coeffs, uint8_t*
 dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                           size_t pitch, long long frame_stride, int nframes, double* coef_out,
                           cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_fused8, cudaFuncAttributeMaxDynamicSharedMemorySize, f8::SMEM));
-    attr = true;
+  {
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_fused8), f8::SMEM, "k_fused8");
+    if (sa != DCTF_OK) return sa;
   }
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8::SB - 1) / f8::SB;
   const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
@@ -1449,10 +1471,9 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
 dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                               size_t pitch, long long frame_stride, int nframes, double* coef_out,
                               cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_fused8_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, f8s::SMEM));
-    attr = true;
+  {
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_fused8_sym), f8s::SMEM, "k_fused8_sym");
+    if (sa != DCTF_OK) return sa;
   }
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8s::SB - 1) / f8s::SB;
   const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
@@ -1469,10 +1490,9 @@ dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* ou
 dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                            size_t pitch, long long frame_stride, int nframes, double* coef_out,
                            cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_fused16, cudaFuncAttributeMaxDynamicSharedMemorySize, f16::SMEM));
-    attr = true;
+  {
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_fused16), f16::SMEM, "k_fused16");
+    if (sa != DCTF_OK) return sa;
   }
   const int bw = (w + 15) / 16, bh = (h + 15) / 16, nsx = (bw + f16::TILE - 1) / f16::TILE;
   const long long ntiles = static_cast<long long>(bh) * nsx * nframes;

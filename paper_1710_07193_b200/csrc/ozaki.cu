@@ -419,11 +419,9 @@ dctf_status upload_i8_operator(dctf_plan* p) {
 
 dctf_status launch_fused8_i8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
                              long long frame_stride, int nframes, double* coef_out, cudaStream_t st, int sms) {
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_fused8_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM) != cudaSuccess)
-      return set_error(DCTF_CUDA_ERROR, "cudaFuncSetAttribute(k_fused8_i8)");
-    attr = true;
+  {
+    const dctf_status sa = ensure_dyn_smem(reinterpret_cast<const void*>(k_fused8_i8), oz::SMEM, "k_fused8_i8");
+    if (sa != DCTF_OK) return sa;
   }
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + oz::TILE - 1) / oz::TILE;
   const long long ntiles = static_cast<long long>(bh) * nsx * nframes;

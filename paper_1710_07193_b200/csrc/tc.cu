@@ -374,8 +374,8 @@ dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d
   if (s != DCTF_OK) return s;
   auto run = [&](auto kernel, int smem, int threads) -> dctf_status {
     static_cast<void>(0);
-    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return set_error(DCTF_CUDA_ERROR, "cudaFuncSetAttribute(k_coef_tf32x3)");
+    const dctf_status sa = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), smem, "k_coef_tf32x3");
+    if (sa != DCTF_OK) return sa;
     const long long ntiles = (nb + 127) / 128;
     kernel<<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), threads, smem, st>>>(
         map, static_cast<const float*>(p->d_hsplit), d_out, nb);
