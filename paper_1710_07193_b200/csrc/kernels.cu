@@ -557,6 +557,7 @@ constexpr int SMEM = 32768 + WARPS * WARP_BYTES;
 __device__ __forceinline__ int fsw(int b) { return (b & 7) ^ ((b & 1) << 2); }
 }  // namespace f8
 
+template <bool COEF>
 __global__ void __launch_bounds__(f8::WARPS * 32, 2)
     k_fused8(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
              long long frame_stride, int nframes, int bw, int bh, int nsx,
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
       for (int j = 0; j < 8; ++j)
         *reinterpret_cast<double2*>(xy + (8 * m + g) * 512 + (j >> 1) * 128 +
                                     (((4 * (j & 1) + t) ^ (2 * (j >> 1)) ^ fg) << 4)) = acc[m][j];
-    if (coef_out) {
+    if (COEF) {
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const int bx = bx0 + 8 * m + g;
@@ -757,6 +758,7 @@ __device__ __forceinline__ double i32_to_f64(int v) {
   return m ? __hiloint2double(static_cast<int>(hi), 0) : 0.0;
 }
 
+template <bool COEF>
 __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
     k_fused8_sym(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
                  long long frame_stride, int nframes, int bw, int bh, int nsx,
@@ -859,7 +861,7 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
           dmma(y[0][nt], q[0][c][2 * sp + 1], bb.y);
           dmma(y[1][nt], q[1][c][2 * sp + 1], bb.y);
         }
-      if (coef_out) {
+      if (COEF) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
           const int bx = bx0 + 8 * mt + g;
@@ -969,6 +971,7 @@ __device__ __forceinline__ int xw(int b, int w) {
 __device__ __forceinline__ void bar_mma() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 }  // namespace f16
 
+template <bool COEF>
 __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
     k_fused16(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
               long long frame_stride, int nframes, int bw, int bh, int nsx,
@@ -1107,7 +1110,7 @@ __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
       for (int j = 0; j < 8; ++j)
         *reinterpret_cast<double2*>(xy + xw(b, 4 * (8 * ng + j) + t)) = acc[m][j];
     }
-    if (coef_out) {
+    if (COEF) {
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const int bx = bx0 + (m ? b1 : b0);
@@ -1452,8 +1455,9 @@ dctf_status launch_inverse_u8(const dctf_plan* p, const double* coeffs, uint8_t*
 dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                           size_t pitch, long long frame_stride, int nframes, double* coef_out,
                           cudaStream_t st) {
+  auto kernel = coef_out ? k_fused8<true> : k_fused8<false>;
   {
-    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_fused8), f8::SMEM, "k_fused8");
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(kernel), f8::SMEM, "k_fused8");
     if (sa != DCTF_OK) return sa;
   }
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8::SB - 1) / f8::SB;
@@ -1461,7 +1465,7 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
   const long long ctas =
       std::min<long long>(2LL * sm_count(p->device), (nstrips + f8::WARPS - 1) / f8::WARPS);
   if (ctas <= 0) return DCTF_OK;
-  k_fused8<<<static_cast<unsigned>(ctas), f8::WARPS * 32, f8::SMEM, st>>>(
+  kernel<<<static_cast<unsigned>(ctas), f8::WARPS * 32, f8::SMEM, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
@@ -1471,8 +1475,9 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
 dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                               size_t pitch, long long frame_stride, int nframes, double* coef_out,
                               cudaStream_t st) {
+  auto kernel = coef_out ? k_fused8_sym<true> : k_fused8_sym<false>;
   {
-    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_fused8_sym), f8s::SMEM, "k_fused8_sym");
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(kernel), f8s::SMEM, "k_fused8_sym");
     if (sa != DCTF_OK) return sa;
   }
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8s::SB - 1) / f8s::SB;
@@ -1480,7 +1485,7 @@ dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* ou
   const long long ctas = std::min<long long>(static_cast<long long>(F8S_MINB) * sm_count(p->device),
                                              (nstrips + f8s::WARPS - 1) / f8s::WARPS);
   if (ctas <= 0) return DCTF_OK;
-  k_fused8_sym<<<static_cast<unsigned>(ctas), f8s::WARPS * 32, f8s::SMEM, st>>>(
+  kernel<<<static_cast<unsigned>(ctas), f8s::WARPS * 32, f8s::SMEM, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hsym, coef_out);
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
@@ -1490,15 +1495,16 @@ dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* ou
 dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                            size_t pitch, long long frame_stride, int nframes, double* coef_out,
                            cudaStream_t st) {
+  auto kernel = coef_out ? k_fused16<true> : k_fused16<false>;
   {
-    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_fused16), f16::SMEM, "k_fused16");
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(kernel), f16::SMEM, "k_fused16");
     if (sa != DCTF_OK) return sa;
   }
   const int bw = (w + 15) / 16, bh = (h + 15) / 16, nsx = (bw + f16::TILE - 1) / f16::TILE;
   const long long ntiles = static_cast<long long>(bh) * nsx * nframes;
   const long long ctas = std::min<long long>(sm_count(p->device), ntiles);
   if (ctas <= 0) return DCTF_OK;
-  k_fused16<<<static_cast<unsigned>(ctas), f16::CWARPS * 32, f16::SMEM, st>>>(
+  kernel<<<static_cast<unsigned>(ctas), f16::CWARPS * 32, f16::SMEM, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
