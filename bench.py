@@ -322,18 +322,24 @@ def main():
         coeffs = plan.forward_image(d_in)
         y = torch.empty_like(coeffs)
         ka = max(3, min(args.steps, 200))
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(ka)]
-        for i in range(ka + 3):
-            flush.fill_(2)
-            if i >= 3:
-                ev[i - 3][0].record(stream)
-            _lib.check(lib.dctf_filter_coeffs(plan.handle, coeffs.data_ptr(), y.data_ptr(),
-                                              NBLOCKS, sp))
-            if i >= 3:
-                ev[i - 3][1].record(stream)
-        torch.cuda.synchronize()
-        ms_c = statistics.mean(a.elapsed_time(b) for a, b in ev)
+
+        def time_coeffs(pl):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(ka)]
+            for i in range(ka + 3):
+                flush.fill_(2)
+                if i >= 3:
+                    ev[i - 3][0].record(stream)
+                _lib.check(lib.dctf_filter_coeffs(pl.handle, coeffs.data_ptr(), y.data_ptr(),
+                                                  NBLOCKS, sp))
+                if i >= 3:
+                    ev[i - 3][1].record(stream)
+            torch.cuda.synchronize()
+            return statistics.mean(a.elapsed_time(b) for a, b in ev)
+        ms_c = time_coeffs(plan)
+        plan_cd = P.FilterPlan(P.Mask(5, mask), N, P.PaddingMode.kReplicate,
+                               precision=P.Precision.kFp64Dense)
+        ms_cd = time_coeffs(plan_cd)
         # n = 16 fused path on BASELINE config 4 (8192^2 U(4), gaussian 7x7 s=2)
         img16 = torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda()
         out16 = torch.empty_like(img16)
@@ -484,11 +490,14 @@ def main():
             "pipe_flop_per_block": pipe16,
             "pipe_frac": pipe16 * nb16 / (ms16 / 1e3) / 1e12 / peak_dmma},
             "coef_path": {
-            "kernel": "k_coef8", "blocks_per_s": NBLOCKS / (ms_c / 1e3), "ms": ms_c,
+            "kernel": plan.coef_kernel, "blocks_per_s": NBLOCKS / (ms_c / 1e3), "ms": ms_c,
             "gb_per_s": NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9,
-            "fp64_tflops": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_c / 1e3) / 1e12,
-            "fp64_frac": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_c / 1e3) / 1e12 / peak_dmma,
             "hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9) / hbm_peak
+            if hbm_peak else None,
+            "fp64_tflops_dense_count": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_c / 1e3) / 1e12,
+            "dense_kernel": plan_cd.coef_kernel, "dense_blocks_per_s": NBLOCKS / (ms_cd / 1e3),
+            "dense_fp64_frac": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_cd / 1e3) / 1e12 / peak_dmma,
+            "dense_hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_cd / 1e3) / 1e9) / hbm_peak
             if hbm_peak else None}}
 
     cpu = None

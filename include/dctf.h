@@ -115,6 +115,11 @@ dctf_status dctf_plan_info(const dctf_plan* plan, int* n, int* npairs, int* symm
  * "unfused" (forward -> filter_coeffs -> inverse). NULL for a NULL plan. */
 const char* dctf_plan_image_kernel(const dctf_plan* plan);
 
+/* Name of the kernel dctf_filter_coeffs runs for this plan: "k_coef8",
+ * "k_coef8_sym" (parity-class structure), "k_coef16" or "k_coef_tf32x3".
+ * NULL for a NULL plan. */
+const char* dctf_plan_coef_kernel(const dctf_plan* plan);
+
 /* Host-only operator compile (no device needed): the same compile
  * dctf_plan_create performs, returning C (n*n) and H (n^4) into host buffers
  * (either may be NULL) plus the pair count / merge flag. */

@@ -40,6 +40,7 @@ _SIGS = {
     "dctf_operator_from_dump": (_st, [C.c_char_p, C.c_size_t, _d, _i, _i, _i]),
     "dctf_plan_info": (_st, [_vp, _i, _i, _i]),
     "dctf_plan_image_kernel": (C.c_char_p, [_vp]),
+    "dctf_plan_coef_kernel": (C.c_char_p, [_vp]),
     "dctf_compile_operator": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_int, _d, _d, _i, _i]),
     "dctf_plan_basis": (_st, [_vp, _d]),
     "dctf_plan_operator": (_st, [_vp, _d]),

@@ -123,6 +123,18 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 }
 
 // quantize_sample (spatial.hpp:71-75): round half away from zero, clamp.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ uint32_t quantize(double v, int* nan_flag) {
   if (v != v) {
     if (nan_flag) atomicOr(nan_flag, 1);
@@ -415,6 +427,148 @@ __global__ void __launch_bounds__(c8::WARPS * 32, 1)
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// k_coef8_sym: filter_coeffs for operators block-diagonal in the (u mod 2,
+// v mod 2) parity classes (see layout_sym8): per class Y_c = H_c X_c, 16 x 16,
+// 4 DMMA per block instead of 16 — the coefficient path becomes HBM-bound.
+// Per-warp pipeline over 16-block tiles (8 KB): TMA load (4 boxes [16 blocks
+// x 16 coefficients], 128B swizzle) -> class contraction from the staged
+// tile -> results written back into the same stage in the same swizzled
+// layout -> TMA store (same box geometry), so HBM sees one streaming read
+// and one streaming write. 3 stages: tile i computes while tile i+1 lands
+// and tile i-1's store drains; a stage is reloaded once the bulk store that
+// last used it has finished reading it (cp.async.bulk.wait_group.read).
+// Lane (g, t), m-tile mt: block row 8mt + g; class k-step s <-> (u' = s,
+// v' = t), i.e. box s, 16-byte chunk 4 pu + t holding classes (pu, 0) and
+// (pu, 1); lanes of odd g fetch the pu = 1 chunk first so every
+// quarter-warp phase hits 8 distinct chunks.
+namespace c8s {
+constexpr int WARPS = 8;
+constexpr int STAGES = 3;
+constexpr int TILE = 16;
+constexpr int STAGE_BYTES = TILE * 64 * 8;  // 8 KB
+constexpr int SMEM = 1024 + 8192 + WARPS * STAGES * STAGE_BYTES;
+}  // namespace c8s
+
+__global__ void __launch_bounds__(c8s::WARPS * 32, 1)
+    k_coef8_sym(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                const double* __restrict__ hc, long long nblocks) {
+  using namespace c8s;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = align1024(smem_raw);
+  const double2* hs = reinterpret_cast<const double2*>(base);
+  uint8_t* stages = base + 8192;
+  __shared__ uint64_t bars[WARPS * STAGES];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    prefetch_tmap(&ymap);
+    for (int i = 0; i < WARPS * STAGES; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  {
+    const double2* src = reinterpret_cast<const double2*>(hc);
+    double2* dst = reinterpret_cast<double2*>(base);
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+
+  const long long ntiles = (nblocks + TILE - 1) / TILE;
+  const long long total = static_cast<long long>(gridDim.x) * WARPS;
+  const long long first = static_cast<long long>(blockIdx.x) * WARPS + warp;
+  uint8_t* ring = stages + warp * STAGES * STAGE_BYTES;
+  uint64_t* wb = bars + warp * STAGES;
+  auto issue = [&](int s, long long tile) {
+    uint8_t* dst = ring + s * STAGE_BYTES;
+    mbar_expect_tx(&wb[s], STAGE_BYTES);
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+      tma_load_2d(dst + cc * 2048, &xmap, &wb[s], cc * 16, static_cast<int>(tile * TILE));
+  };
+  if (lane == 0) {
+    if (first < ntiles) issue(0, first);
+    if (first + total < ntiles) issue(1, first + total);
+  }
+  __syncwarp();
+  const int pa = g & 1;
+
+  for (long long i = 0;; ++i) {
+    const long long tile = first + i * total;
+    if (tile >= ntiles) break;
+    const int s = static_cast<int>(i % STAGES);
+    mbar_wait(&wb[s], static_cast<uint32_t>((i / STAGES) & 1));
+    uint8_t* st = ring + s * STAGE_BYTES;
+
+    double q[2][4][4];  // [m-tile][class][k-step]
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const uint8_t* rb = st + (8 * mt + g) * 128;
+#pragma unroll
+      for (int sq = 0; sq < 4; ++sq) {
+        const double2 va = *reinterpret_cast<const double2*>(rb + sq * 2048 + (((4 * pa + t) ^ g) << 4));
+        const double2 vb = *reinterpret_cast<const double2*>(rb + sq * 2048 + (((4 * (pa ^ 1) + t) ^ g) << 4));
+        const double2 v0 = pa ? vb : va, v1 = pa ? va : vb;
+        q[mt][0][sq] = v0.x;
+        q[mt][1][sq] = v0.y;
+        q[mt][2][sq] = v1.x;
+        q[mt][3][sq] = v1.y;
+      }
+    }
+    double2 y[2][4][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) y[mt][c][nt] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int sp = 0; sp < 2; ++sp)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const double2 bb = hs[((c * 2 + nt) * 2 + sp) * 32 + lane];
+          dmma(y[0][c][nt], q[0][c][2 * sp], bb.x);
+          dmma(y[1][c][nt], q[1][c][2 * sp], bb.x);
+          dmma(y[0][c][nt], q[0][c][2 * sp + 1], bb.y);
+          dmma(y[1][c][nt], q[1][c][2 * sp + 1], bb.y);
+        }
+    __syncwarp();  // every lane's reads of this stage are done
+    // Y back into the stage: coefficient (2u'+pu, 2v'+pv), u' = 2nt + (t>>1),
+    // v' = 2(t&1) + e -> box u', chunk 4pu + v', element pv
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      uint8_t* rb = st + (8 * mt + g) * 128;
+#pragma unroll
+      for (int pu = 0; pu < 2; ++pu)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int box = 2 * nt + (t >> 1), chunk = 4 * pu + 2 * (t & 1) + e;
+            const double a = e ? y[mt][2 * pu][nt].y : y[mt][2 * pu][nt].x;
+            const double b = e ? y[mt][2 * pu + 1][nt].y : y[mt][2 * pu + 1][nt].x;
+            *reinterpret_cast<double2*>(rb + box * 2048 + ((chunk ^ g) << 4)) = make_double2(a, b);
+          }
+    }
+    fence_proxy_async();  // generic-proxy writes -> visible to the bulk store
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) tma_store_2d(&ymap, st + cc * 2048, cc * 16, static_cast<int>(tile * TILE));
+      bulk_commit();
+      const long long nt2 = tile + 2 * total;
+      if (nt2 < ntiles) {
+        bulk_wait_read<1>();  // tile i-1's store has left stage (i+2) % 3
+        issue(static_cast<int>((i + 2) % STAGES), nt2);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -1387,6 +1541,22 @@ dctf_status check_image(int w, int h, size_t pitch) {
   return DCTF_OK;
 }
 
+dctf_status launch_coef8_sym(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
+                             cudaStream_t st) {
+  CUtensorMap xmap, ymap;
+  dctf_status s = dctf::make_xmap(&xmap, d_in, nb, 64, c8s::TILE);
+  if (s == DCTF_OK) s = dctf::make_xmap(&ymap, d_out, nb, 64, c8s::TILE);
+  if (s != DCTF_OK) return s;
+  s = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_coef8_sym), c8s::SMEM, "k_coef8_sym");
+  if (s != DCTF_OK) return s;
+  const long long ntiles = (nb + c8s::TILE - 1) / c8s::TILE;
+  const long long ctas = std::min<long long>(sm_count(p->device), (ntiles + c8s::WARPS - 1) / c8s::WARPS);
+  k_coef8_sym<<<static_cast<unsigned>(ctas), c8s::WARPS * 32, c8s::SMEM, st>>>(xmap, ymap, p->d_hcsym, nb);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
 dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
                         cudaStream_t st) {
   if (nb == 0) return DCTF_OK;
@@ -1394,6 +1564,7 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
     return set_error(DCTF_INVALID_ARGUMENT, "coefficient buffers must be 16-byte aligned");
   if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in-place filter_coeffs not supported");
   if (p->precision == DCTF_PREC_TF32X3) return dctf::launch_coef_tf32x3(p, d_in, d_out, nb, st, sm_count(p->device));
+  if (p->n == 8 && p->sym) return launch_coef8_sym(p, d_in, d_out, nb, st);
   CUtensorMap map;
   const int nn = p->n * p->n;
   dctf_status s = dctf::make_xmap(&map, d_in, nb, nn, p->n == 8 ? c8::TILE : c16::TILE);
@@ -1602,6 +1773,11 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     e = cudaMalloc(&p->d_hsym, hsym.size() * sizeof(double));
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_hsym, hsym.data(), hsym.size() * sizeof(double), cudaMemcpyHostToDevice);
+    std::vector<double> hcsym;
+    dctf::layout_coefsym8(p->op, hcsym);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_hcsym, hcsym.size() * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_hcsym, hcsym.data(), hcsym.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess && precision == DCTF_PREC_TF32X3) {
     std::vector<float> hs;
@@ -1745,6 +1921,7 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_hcoef);
     cudaFree(p->d_hfused);
     cudaFree(p->d_hsym);
+    cudaFree(p->d_hcsym);
     cudaFree(p->d_hsplit);
     cudaFree(p->d_gimg);
     cudaFree(p->d_gscale);
@@ -1767,6 +1944,13 @@ dctf_status dctf_plan_info(const dctf_plan* p, int* n, int* npairs, int* merged)
   if (npairs) *npairs = p->npairs;
   if (merged) *merged = p->merged;
   return DCTF_OK;
+}
+
+const char* dctf_plan_coef_kernel(const dctf_plan* p) {
+  if (!p) return nullptr;
+  if (p->precision == DCTF_PREC_TF32X3) return "k_coef_tf32x3";
+  if (p->n == 8) return p->sym ? "k_coef8_sym" : "k_coef8";
+  return "k_coef16";
 }
 
 const char* dctf_plan_image_kernel(const dctf_plan* p) {

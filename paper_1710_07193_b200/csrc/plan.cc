@@ -533,6 +533,24 @@ void layout_sym8(const std::vector<double>& op, const std::vector<double>& basis
           }
 }
 
+// Coefficient-path image of the parity classes (k_coef8_sym, 8 KB): the
+// class blocks H_c of H itself, DMMA B fragments [c][nt][sp][lane][e] =
+// H_c[o = 8nt + g][k = (u' = 2sp + e, v' = t)], class-local index (u', v')
+// <-> coefficient (2u' + pu, 2v' + pv), c = 2 pu + pv.
+void layout_coefsym8(const std::vector<double>& op, std::vector<double>& out) {
+  out.assign(1024, 0.0);
+  auto coef = [](int c, int o) { return (2 * (o >> 2) + (c >> 1)) * 8 + 2 * (o & 3) + (c & 1); };
+  size_t w = 0;
+  for (int c = 0; c < 4; ++c)
+    for (int nt = 0; nt < 2; ++nt)
+      for (int sp = 0; sp < 2; ++sp)
+        for (int lane = 0; lane < 32; ++lane)
+          for (int e = 0; e < 2; ++e) {
+            const int g = lane >> 2, t = lane & 3;
+            out[w++] = op[size_t(coef(c, 8 * nt + g)) * 64 + coef(c, 4 * (2 * sp + e) + t)];
+          }
+}
+
 // Exact INT8 slicing of the forward-DCT-composed operator for k_fused8_i8.
 // G = H (C (x) C) maps a block's 64 pixels p (index i*8+j) straight to its
 // filtered DCT coefficients Y (index u*8+v). G is scaled by 2^-e (e: smallest

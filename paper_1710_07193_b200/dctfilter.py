@@ -310,6 +310,11 @@ class FilterPlan:
         """Kernel filter_image runs for this plan (dctf_plan_image_kernel)."""
         return _lib.lib.dctf_plan_image_kernel(self._h).decode()
 
+    @property
+    def coef_kernel(self) -> str:
+        """Kernel filter_coeffs runs for this plan (dctf_plan_coef_kernel)."""
+        return _lib.lib.dctf_plan_coef_kernel(self._h).decode()
+
     def filter_image(self, img, coeffs_out=None):
         """Fused whole-image DCT path on a (h, w) uint8 CUDA tensor."""
         import torch
