@@ -30,6 +30,7 @@
 #include <mutex>
 #include <string>
 
+#include "fastdiv.cuh"
 #include "internal.h"
 
 // ---------------------------------------------------------------------------
@@ -742,11 +743,14 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
 
   uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
   long long s = static_cast<long long>(blockIdx.x) * WARPS + warp;
-  auto strip_at = [&](long long si, int& f, int& by, int& bx0) {
-    f = static_cast<int>(si / spf);
-    const long long rem = si - static_cast<long long>(f) * spf;
-    by = static_cast<int>(rem / nsx);
-    bx0 = static_cast<int>(rem - static_cast<long long>(by) * nsx) * SB;
+  const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
+                      fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
+  auto strip_at = [&](long long si, int& f, int& by, int& bx0) {  // si < 2^31 (launcher)
+    const uint32_t u = static_cast<uint32_t>(si);
+    f = static_cast<int>(dctf::fdiv(fd_spf, u));
+    const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(spf);
+    by = static_cast<int>(dctf::fdiv(fd_nsx, rem));
+    bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * SB;
   };
   auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && bx0 * 8 + 128 <= w; };
   auto prefetch = [&](long long si) {
@@ -939,11 +943,14 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
 
   uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
   long long s = static_cast<long long>(blockIdx.x) * WARPS + warp;
-  auto strip_at = [&](long long si, int& f, int& by, int& bx0) {
-    f = static_cast<int>(si / spf);
-    const long long rem = si - static_cast<long long>(f) * spf;
-    by = static_cast<int>(rem / nsx);
-    bx0 = static_cast<int>(rem - static_cast<long long>(by) * nsx) * SB;
+  const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
+                      fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
+  auto strip_at = [&](long long si, int& f, int& by, int& bx0) {  // si < 2^31 (launcher)
+    const uint32_t u = static_cast<uint32_t>(si);
+    f = static_cast<int>(dctf::fdiv(fd_spf, u));
+    const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(spf);
+    by = static_cast<int>(dctf::fdiv(fd_nsx, rem));
+    bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * SB;
   };
   auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && bx0 * 8 + 128 <= w; };
   auto prefetch = [&](long long si) {
@@ -1166,11 +1173,14 @@ __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
   const int tid = threadIdx.x;  // 0..511
   const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
-  auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {
-    f = static_cast<int>(ti / spf);
-    const long long rem = ti - static_cast<long long>(f) * spf;
-    by = static_cast<int>(rem / nsx);
-    bx0 = static_cast<int>(rem - static_cast<long long>(by) * nsx) * TILE;
+  const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
+                      fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
+  auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {  // ti < 2^31 (launcher)
+    const uint32_t u = static_cast<uint32_t>(ti);
+    f = static_cast<int>(dctf::fdiv(fd_spf, u));
+    const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(spf);
+    by = static_cast<int>(dctf::fdiv(fd_nsx, rem));
+    bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * TILE;
   };
   auto is_fast = [&](int by, int bx0) { return aligned && by * 16 + 16 <= h && bx0 * 16 + 1024 <= w; };
   // thread tid moves 16-byte chunks (row tid>>6, col 16*(tid&63)) and (row+8)
@@ -1636,6 +1646,8 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
   const long long ctas =
       std::min<long long>(2LL * sm_count(p->device), (nstrips + f8::WARPS - 1) / f8::WARPS);
   if (ctas <= 0) return DCTF_OK;
+  if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
+    return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
   kernel<<<static_cast<unsigned>(ctas), f8::WARPS * 32, f8::SMEM, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
   dctf::add_launches(1);
@@ -1656,6 +1668,8 @@ dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* ou
   const long long ctas = std::min<long long>(static_cast<long long>(F8S_MINB) * sm_count(p->device),
                                              (nstrips + f8s::WARPS - 1) / f8s::WARPS);
   if (ctas <= 0) return DCTF_OK;
+  if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
+    return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
   kernel<<<static_cast<unsigned>(ctas), f8s::WARPS * 32, f8s::SMEM, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hsym, coef_out);
   dctf::add_launches(1);
@@ -1675,6 +1689,8 @@ dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, 
   const long long ntiles = static_cast<long long>(bh) * nsx * nframes;
   const long long ctas = std::min<long long>(sm_count(p->device), ntiles);
   if (ctas <= 0) return DCTF_OK;
+  if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
+    return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
   kernel<<<static_cast<unsigned>(ctas), f16::CWARPS * 32, f16::SMEM, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
   dctf::add_launches(1);

@@ -41,6 +41,7 @@
 #include <cmath>
 #include <string>
 
+#include "fastdiv.cuh"
 #include "internal.h"
 
 namespace {
@@ -190,11 +191,14 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   const long long ntiles = spf * nframes;
   const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 7) == 0) &&
                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
-  auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {
-    f = static_cast<int>(ti / spf);
-    const long long rem = ti - static_cast<long long>(f) * spf;
-    by = static_cast<int>(rem / nsx);
-    bx0 = static_cast<int>(rem - static_cast<long long>(by) * nsx) * TILE;
+  const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
+                      fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
+  auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {  // ti < 2^31 (launcher)
+    const uint32_t u = static_cast<uint32_t>(ti);
+    f = static_cast<int>(dctf::fdiv(fd_spf, u));
+    const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(spf);
+    by = static_cast<int>(dctf::fdiv(fd_nsx, rem));
+    bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * TILE;
   };
   auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && (bx0 + TILE) * 8 <= w; };
 
@@ -426,6 +430,7 @@ dctf_status launch_fused8_i8(const dctf_plan* p, const uint8_t* in, uint8_t* out
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + oz::TILE - 1) / oz::TILE;
   const long long ntiles = static_cast<long long>(bh) * nsx * nframes;
   if (ntiles <= 0) return DCTF_OK;
+  if (ntiles >= (1LL << 31)) return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
   k_fused8_i8<<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), oz::THREADS, oz::SMEM, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, static_cast<const int8_t*>(p->d_gimg),
       p->d_gscale, p->d_basis, coef_out);
