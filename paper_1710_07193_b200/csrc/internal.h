@@ -32,9 +32,9 @@ struct dctf_plan {
   double* d_gscale = nullptr;    // per-row scales of those slices
   int* d_nan = nullptr;          // NaN flag
   double* d_weights = nullptr;   // mask, kr*kc (spatial path)
-  bool sym = false;              // H parity-block-diagonal and precision FP64 (k_fused8_sym)
+  bool sym = false;              // H parity-block-diagonal and precision FP64 (k_fused8_sym, k_coef*_sym)
   double* d_hsym = nullptr;      // layout_sym8 image (n = 8, sym)
-  double* d_hcsym = nullptr;     // layout_coefsym8 image (n = 8, sym)
+  double* d_hcsym = nullptr;     // layout_coefsym8 / layout_coefsym16 image (sym)
 
   // Device staging of the host-buffer entry (copy mode), guarded by io_mu.
   mutable std::mutex io_mu;
@@ -74,6 +74,7 @@ void layout_hfused8(const std::vector<double>& op, std::vector<double>& out);
 bool parity_block_diagonal(const std::vector<double>& op, int n);
 void layout_sym8(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out);
 void layout_coefsym8(const std::vector<double>& op, std::vector<double>& out);
+void layout_coefsym16(const std::vector<double>& op, std::vector<double>& out);
 // G = H (C (x) C): the operator with the forward DCT composed in (pixels ->
 // filtered coefficients), accumulated in long double and rounded once.
 std::vector<long double> compose_forward_ld(const std::vector<double>& op, const std::vector<double>& basis, int n);

@@ -573,6 +573,129 @@ __global__ void __launch_bounds__(c8s::WARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// k_coef16_sym: filter_coeffs at N = 16 for parity-block-diagonal operators:
+// per class Y_c = H_c X_c (64 x 64), 64 DMMA per block instead of 256.
+// CTA = C16S_WARPS warps, warp w owns class w & 3 (pu, pv) and a slice of
+// NPW output n-tiles; the four 64 x 64 H_c (128 KB of DMMA B fragments) stay
+// resident in shared memory.
+// Work unit: a tile of 16 blocks (32 KB), TMA-loaded as 16 boxes [16 blocks
+// x 16 coefficients] (box u = row u of every block, 128B swizzle) into a
+// 3-stage ring; each warp contracts its class for both 8-block m-tiles
+// (each B fragment feeds 4 DMMAs), the CTA syncs, the warps write Y back
+// into the same stage in the same layout, and one thread TMA-stores it.
+// Class k-step s <-> (u' = s >> 1, v' = 2t + (s & 1)): box 2u' + pu, chunk
+// v', element pv.
+namespace c16s {
+#ifndef C16S_WARPS
+#define C16S_WARPS 8
+#endif
+constexpr int WARPS = C16S_WARPS;
+constexpr int NPW = 32 / WARPS;  // n-tiles per warp
+constexpr int STAGES = 3;
+constexpr int TILE = 16;
+constexpr int STAGE_BYTES = TILE * 256 * 8;  // 32 KB
+constexpr int HBYTES = 4 * 8 * 8 * 32 * 16;   // 128 KB
+constexpr int SMEM = 1024 + HBYTES + STAGES * STAGE_BYTES;
+}  // namespace c16s
+
+__global__ void __launch_bounds__(c16s::WARPS * 32, 1)
+    k_coef16_sym(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                 const double* __restrict__ hc, long long nblocks) {
+  using namespace c16s;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = align1024(smem_raw);
+  const double2* hs = reinterpret_cast<const double2*>(base);
+  uint8_t* stages = base + HBYTES;
+  __shared__ uint64_t full[STAGES];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int cls = warp & 3, pu = cls >> 1, pv = cls & 1, nh = warp >> 2;  // n-tile slice
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    prefetch_tmap(&ymap);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  {
+    const double2* src = reinterpret_cast<const double2*>(hc);
+    double2* dst = reinterpret_cast<double2*>(base);
+    for (int i = threadIdx.x; i < HBYTES / 16; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+
+  const long long ntiles = (nblocks + TILE - 1) / TILE;
+  auto issue = [&](int s, long long tile) {
+    uint8_t* dst = stages + s * STAGE_BYTES;
+    mbar_expect_tx(&full[s], STAGE_BYTES);
+#pragma unroll 1
+    for (int cc = 0; cc < 16; ++cc)
+      tma_load_2d(dst + cc * 2048, &xmap, &full[s], cc * 16, static_cast<int>(tile * TILE));
+  };
+  if (threadIdx.x == 0) {
+    if (blockIdx.x < ntiles) issue(0, blockIdx.x);
+    if (blockIdx.x + gridDim.x < ntiles) issue(1, blockIdx.x + gridDim.x);
+  }
+  const double2* hw = hs + cls * (8 * 8 * 32) + nh * (NPW * 8 * 32);
+
+  long long i = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+    const int s = static_cast<int>(i % STAGES);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / STAGES) & 1));
+    uint8_t* st = stages + s * STAGE_BYTES;
+
+    double2 acc[2][NPW];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NPW; ++nt) acc[mt][nt] = make_double2(0.0, 0.0);
+#pragma unroll 2
+    for (int sp = 0; sp < 8; ++sp) {
+      // A: block rows g and 8 + g, k-steps 2sp, 2sp+1 -> (u' = sp, v' = 2t + e)
+      const uint8_t* bx = st + (2 * sp + pu) * 2048 + 8 * pv;
+      double a[2][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          a[mt][e] = *reinterpret_cast<const double*>(bx + (8 * mt + g) * 128 + (((2 * t + e) ^ g) << 4));
+#pragma unroll
+      for (int nt = 0; nt < NPW; ++nt) {
+        const double2 bb = hw[(nt * 8 + sp) * 32 + lane];
+        dmma(acc[0][nt], a[0][0], bb.x);
+        dmma(acc[1][nt], a[1][0], bb.x);
+        dmma(acc[0][nt], a[0][1], bb.y);
+        dmma(acc[1][nt], a[1][1], bb.y);
+      }
+    }
+    __syncthreads();  // all four classes have read the stage
+    // Y_c[o = 8nt + 2t + e] = coefficient (2nt + pu, 2(2t + e) + pv): box 2nt + pu, chunk 2t + e
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      uint8_t* rb = st + (8 * mt + g) * 128 + 8 * pv;
+#pragma unroll
+      for (int nt = 0; nt < NPW; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          *reinterpret_cast<double*>(rb + (2 * (NPW * nh + nt) + pu) * 2048 + (((2 * t + e) ^ g) << 4)) =
+              e ? acc[mt][nt].y : acc[mt][nt].x;
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll 1
+      for (int cc = 0; cc < 16; ++cc) tma_store_2d(&ymap, st + cc * 2048, cc * 16, static_cast<int>(tile * TILE));
+      bulk_commit();
+      const long long nt2 = tile + 2 * static_cast<long long>(gridDim.x);
+      if (nt2 < ntiles) {
+        bulk_wait_read<1>();  // the store that last used stage (i+2) % 3 has read it
+        issue(static_cast<int>((i + 2) % STAGES), nt2);
+      }
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
 // k_coef16: Y^T (blocks x 256) = X^T (blocks x 256) * H^T, FP64 DMMA.
 //
 // CTA tile: 64 blocks x 256 outputs; K = 256 streamed in 16 chunks of 16.
@@ -730,7 +853,6 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   uint8_t* xy = smem + 32768 + warp * WARP_BYTES;
   uint8_t* pix = xy + XY_BYTES;
-  const double af0 = cb[g * 8 + 2 * t], af1 = cb[g * 8 + 2 * t + 1];
   const double ai0 = cb[(2 * t) * 8 + g], ai1 = cb[(2 * t + 1) * 8 + g];
   const int fg = fsw(g);
 
@@ -1567,6 +1689,22 @@ dctf_status launch_coef8_sym(const dctf_plan* p, const double* d_in, double* d_o
   return DCTF_OK;
 }
 
+dctf_status launch_coef16_sym(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
+                              cudaStream_t st) {
+  CUtensorMap xmap, ymap;
+  dctf_status s = dctf::make_xmap(&xmap, d_in, nb, 256, c16s::TILE);
+  if (s == DCTF_OK) s = dctf::make_xmap(&ymap, d_out, nb, 256, c16s::TILE);
+  if (s != DCTF_OK) return s;
+  s = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_coef16_sym), c16s::SMEM, "k_coef16_sym");
+  if (s != DCTF_OK) return s;
+  const long long ntiles = (nb + c16s::TILE - 1) / c16s::TILE;
+  const long long ctas = std::min<long long>(sm_count(p->device), ntiles);
+  k_coef16_sym<<<static_cast<unsigned>(ctas), c16s::WARPS * 32, c16s::SMEM, st>>>(xmap, ymap, p->d_hcsym, nb);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
 dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
                         cudaStream_t st) {
   if (nb == 0) return DCTF_OK;
@@ -1574,7 +1712,7 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
     return set_error(DCTF_INVALID_ARGUMENT, "coefficient buffers must be 16-byte aligned");
   if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in-place filter_coeffs not supported");
   if (p->precision == DCTF_PREC_TF32X3) return dctf::launch_coef_tf32x3(p, d_in, d_out, nb, st, sm_count(p->device));
-  if (p->n == 8 && p->sym) return launch_coef8_sym(p, d_in, d_out, nb, st);
+  if (p->sym) return p->n == 8 ? launch_coef8_sym(p, d_in, d_out, nb, st) : launch_coef16_sym(p, d_in, d_out, nb, st);
   CUtensorMap map;
   const int nn = p->n * p->n;
   dctf_status s = dctf::make_xmap(&map, d_in, nb, nn, p->n == 8 ? c8::TILE : c16::TILE);
@@ -1782,8 +1920,15 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_hfused, hfused.data(), hfused.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
-  p->sym = n == 8 && precision == DCTF_PREC_FP64 && dctf::parity_block_diagonal(p->op, n);
-  if (e == cudaSuccess && p->sym) {
+  p->sym = precision == DCTF_PREC_FP64 && dctf::parity_block_diagonal(p->op, n);
+  if (e == cudaSuccess && p->sym && n == 16) {
+    std::vector<double> hcsym;
+    dctf::layout_coefsym16(p->op, hcsym);
+    e = cudaMalloc(&p->d_hcsym, hcsym.size() * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_hcsym, hcsym.data(), hcsym.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess && p->sym && n == 8) {
     std::vector<double> hsym;
     dctf::layout_sym8(p->op, p->basis, hsym);
     e = cudaMalloc(&p->d_hsym, hsym.size() * sizeof(double));
@@ -1966,7 +2111,7 @@ const char* dctf_plan_coef_kernel(const dctf_plan* p) {
   if (!p) return nullptr;
   if (p->precision == DCTF_PREC_TF32X3) return "k_coef_tf32x3";
   if (p->n == 8) return p->sym ? "k_coef8_sym" : "k_coef8";
-  return "k_coef16";
+  return p->sym ? "k_coef16_sym" : "k_coef16";
 }
 
 const char* dctf_plan_image_kernel(const dctf_plan* p) {

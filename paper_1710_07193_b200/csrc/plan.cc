@@ -551,6 +551,25 @@ void layout_coefsym8(const std::vector<double>& op, std::vector<double>& out) {
           }
 }
 
+// N = 16 coefficient-path image of the parity classes (k_coef16_sym,
+// 128 KB): DMMA B fragments [c][nt < 8][sp < 8][lane][e] = H_c[o = 8nt + g]
+// [k(2sp + e, t)], class-local index o = 8u' + v' <-> coefficient
+// (2u' + pu, 2v' + pv), and k-step s = 2sp + e <-> (u' = sp, v' = 2t + e).
+void layout_coefsym16(const std::vector<double>& op, std::vector<double>& out) {
+  out.assign(4 * 8 * 8 * 64, 0.0);
+  auto coef = [](int c, int u1, int v1) { return (2 * u1 + (c >> 1)) * 16 + 2 * v1 + (c & 1); };
+  size_t w = 0;
+  for (int c = 0; c < 4; ++c)
+    for (int nt = 0; nt < 8; ++nt)
+      for (int sp = 0; sp < 8; ++sp)
+        for (int lane = 0; lane < 32; ++lane)
+          for (int e = 0; e < 2; ++e) {
+            const int g = lane >> 2, t = lane & 3;
+            const int row = coef(c, nt, g), col = coef(c, sp, 2 * t + e);
+            out[w++] = op[size_t(row) * 256 + col];
+          }
+}
+
 // Exact INT8 slicing of the forward-DCT-composed operator for k_fused8_i8.
 // G = H (C (x) C) maps a block's 64 pixels p (index i*8+j) straight to its
 // filtered DCT coefficients Y (index u*8+v). G is scaled by 2^-e (e: smallest
