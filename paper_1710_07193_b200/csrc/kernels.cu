@@ -844,12 +844,6 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
   using namespace f8;
   extern __shared__ __align__(16) uint8_t smem[];
   const double2* hs = reinterpret_cast<const double2*>(smem);
-  {
-    const double2* src = reinterpret_cast<const double2*>(hf);
-    double2* dst = reinterpret_cast<double2*>(smem);
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   uint8_t* xy = smem + 32768 + warp * WARP_BYTES;
   uint8_t* pix = xy + XY_BYTES;
@@ -884,7 +878,13 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
       pf1 = ldg_stream(p + (r0 + 4) * pitch);
     }
   };
-  if (s < nstrips) prefetch(s);
+  if (s < nstrips) prefetch(s);  // first strip's pixels in flight during the operator copy
+  {
+    const double2* src = reinterpret_cast<const double2*>(hf);
+    double2* dst = reinterpret_cast<double2*>(smem);
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
 
   for (; s < nstrips; s += total) {
     int f, by, bx0;
@@ -1047,12 +1047,6 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
   extern __shared__ __align__(16) uint8_t smem[];
   const double2* gs = reinterpret_cast<const double2*>(smem);          // [c][nt][sp][lane]
   const double2* ws = reinterpret_cast<const double2*>(smem + 8192);   // [c][nt2][nt][lane]
-  {
-    const double2* src = reinterpret_cast<const double2*>(hsym);
-    double2* dst = reinterpret_cast<double2*>(smem);
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   uint8_t* pix = smem + 16384 + warp * PIX_BYTES;
 
@@ -1084,7 +1078,13 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
       pf1 = ldg_stream(p + (r0 + 4) * pitch);
     }
   };
-  if (s < nstrips) prefetch(s);
+  if (s < nstrips) prefetch(s);  // first strip's pixels in flight during the operator copy
+  {
+    const double2* src = reinterpret_cast<const double2*>(hsym);
+    double2* dst = reinterpret_cast<double2*>(smem);
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
 
   for (; s < nstrips; s += total) {
     int f, by, bx0;
