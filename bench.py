@@ -344,19 +344,32 @@ def main():
         img16 = torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda()
         out16 = torch.empty_like(img16)
         plan16 = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate)
-        ev16 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                for _ in range(10)]
-        for i in range(13):
-            flush.fill_(3)
-            if i >= 3:
-                ev16[i - 3][0].record(stream)
-            _lib.check(lib.dctf_filter_image_u8(plan16.handle, img16.data_ptr(), out16.data_ptr(),
-                                                8192, 8192, 8192, None, sp))
-            if i >= 3:
-                ev16[i - 3][1].record(stream)
-        torch.cuda.synchronize()
-        ms16 = statistics.mean(a.elapsed_time(b) for a, b in ev16)
-        nb16, flop16, pipe16 = 262144, 2 * 16 ** 4 + 8 * 16 ** 3, 2 * 16 ** 4 + 4 * 16 ** 3
+        plan16fd = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate,
+                                precision=P.Precision.kFp64Dense)
+
+        def time_image16(pl):
+            ev16 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(10)]
+            for i in range(13):
+                flush.fill_(3)
+                if i >= 3:
+                    ev16[i - 3][0].record(stream)
+                _lib.check(lib.dctf_filter_image_u8(pl.handle, img16.data_ptr(), out16.data_ptr(),
+                                                    8192, 8192, 8192, None, sp))
+                if i >= 3:
+                    ev16[i - 3][1].record(stream)
+            torch.cuda.synchronize()
+            return statistics.mean(a.elapsed_time(b) for a, b in ev16)
+        ms16 = time_image16(plan16)
+        out16s = out16.clone()
+        ms16d = time_image16(plan16fd)
+        same16 = bool(torch.equal(out16s, out16))
+        del out16s
+        nb16, flop16 = 262144, 2 * 16 ** 4 + 8 * 16 ** 3
+        # executed FP64 flop per block: k_fused16 = G p + inverse; k_fused16_sym =
+        # 4 classes x (64x64 filter + 8x8 first inverse pass) DMMA + 4 x 512 DFMA
+        pipe_of = {"k_fused16": 2 * 16 ** 4 + 4 * 16 ** 3, "k_fused16_sym": 72 * 512 + 4 * 512 * 2}
+        pipe16 = pipe_of[plan16.image_kernel]
         del img16, out16
         # coefficient path at n = 16 (config 4 shapes): FP64 DMMA vs 3xTF32 tcgen05
         x16 = plan16.forward_image(torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda())
@@ -487,12 +500,15 @@ def main():
                "n16_coef_tf32x3": coefline("k_coef_tf32x3<256>", ms_t16, 262144, 256, "3xtf32", err_t16),
                "n8_coef_tf32x3": coefline("k_coef_tf32x3<64>", ms_t8, NBLOCKS, 64, "3xtf32", err_t8),
                "n16_fused": {
-            "kernel": "k_fused16", "workload": "config4: 8192x8192 U(4), 16x16 blocks, gaussian "
-            "7x7 sigma=2, replicate, FP64", "blocks_per_s": nb16 / (ms16 / 1e3), "ms": ms16,
-            "fp64_tflops": flop16 * nb16 / (ms16 / 1e3) / 1e12,
-            "fp64_frac": flop16 * nb16 / (ms16 / 1e3) / 1e12 / peak_dmma,
+            "kernel": plan16.image_kernel, "workload": "config4: 8192x8192 U(4), 16x16 blocks, "
+            "gaussian 7x7 sigma=2, replicate, FP64", "blocks_per_s": nb16 / (ms16 / 1e3), "ms": ms16,
+            "fp64_tflops_dense_count": flop16 * nb16 / (ms16 / 1e3) / 1e12,
+            "frac_dense_count": flop16 * nb16 / (ms16 / 1e3) / 1e12 / peak_dmma,
             "pipe_flop_per_block": pipe16,
-            "pipe_frac": pipe16 * nb16 / (ms16 / 1e3) / 1e12 / peak_dmma},
+            "pipe_frac": pipe16 * nb16 / (ms16 / 1e3) / 1e12 / peak_dmma,
+            "dense_kernel": plan16fd.image_kernel, "dense_blocks_per_s": nb16 / (ms16d / 1e3),
+            "dense_pipe_frac": pipe_of["k_fused16"] * nb16 / (ms16d / 1e3) / 1e12 / peak_dmma,
+            "u8_identical_to_dense": same16},
             "coef_path": {
             "kernel": plan.coef_kernel, "blocks_per_s": NBLOCKS / (ms_c / 1e3), "ms": ms_c,
             "gb_per_s": NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9,

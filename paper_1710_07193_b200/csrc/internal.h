@@ -33,7 +33,7 @@ struct dctf_plan {
   int* d_nan = nullptr;          // NaN flag
   double* d_weights = nullptr;   // mask, kr*kc (spatial path)
   bool sym = false;              // H parity-block-diagonal and precision FP64 (k_fused8_sym, k_coef*_sym)
-  double* d_hsym = nullptr;      // layout_sym8 image (n = 8, sym)
+  double* d_hsym = nullptr;      // layout_sym8 (n = 8) / layout_gsym16 (n = 16) image (sym)
   double* d_hcsym = nullptr;     // layout_coefsym8 / layout_coefsym16 image (sym)
 
   // Device staging of the host-buffer entry (copy mode), guarded by io_mu.
@@ -75,6 +75,7 @@ bool parity_block_diagonal(const std::vector<double>& op, int n);
 void layout_sym8(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out);
 void layout_coefsym8(const std::vector<double>& op, std::vector<double>& out);
 void layout_coefsym16(const std::vector<double>& op, std::vector<double>& out);
+void layout_gsym16(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out);
 // G = H (C (x) C): the operator with the forward DCT composed in (pixels ->
 // filtered coefficients), accumulated in long double and rounded once.
 std::vector<long double> compose_forward_ld(const std::vector<double>& op, const std::vector<double>& basis, int n);

@@ -1486,6 +1486,243 @@ __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// k_fused16_sym: the N = 16 image path for parity-block-diagonal operators
+// (symmetric masks; see k_fused8_sym). Per block and class c = (pu, pv):
+//   q_c(i, j) = r(j) +/- r(15-j),  r(x) = p(i, x) +/- p(15-i, x),  i, j < 8
+//     (exact integers), Y_c = G_c q_c (64 x 64, DMMA, G_c resident in shared
+//     memory), then the inverse separably: T = Y_c C_pv along v' (DMMA,
+//     constant B fragments) and Z_c = C_pu^T T along u' (lane-local DFMA: each
+//     lane already holds all u' of its two columns), and the output pixels
+//     are +/- sums of the four Z_c (+0.5 in Z_ee, floor -> u8).
+// Dense k_fused16: 288 DMMA per block; here 4 x (128 + 16) DMMA + 4 x 512 DFMA
+// per 8 blocks = 72 DMMA + 256 DFMA per block.
+// CTA = 4 pairs of warps; a pair owns an m-tile = a strip of 8 blocks (16 rows
+// x 128 px): warp 2p handles classes (0, 0), (0, 1), warp 2p+1 classes (1, 0),
+// (1, 1); Z_c goes through the pair's shared buffer (swizzled 16-byte chunks)
+// for the butterfly, which the two warps split by row. Pixels are prefetched
+// one m-tile ahead into registers and double-buffered in shared memory.
+namespace f16s {
+constexpr int PAIRS = 4, WARPS = 2 * PAIRS;
+constexpr int TB = 8;                          // blocks per m-tile
+constexpr int PS = 144;                        // pixel row stride
+constexpr int PIX_BYTES = 16 * PS;
+constexpr int ZBYTES = 4 * TB * 512;           // [class][block][i][t] double2, 16 KB
+constexpr int GBYTES = 4 * 8 * 8 * 32 * 16;    // 128 KB
+constexpr int CBYTES = 256 * 8;
+constexpr int PAIR_BYTES = ZBYTES + 2 * PIX_BYTES;
+constexpr int SMEM = GBYTES + CBYTES + PAIRS * PAIR_BYTES;
+__device__ __forceinline__ void bar_pair(int pair) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+}
+// byte offset of Z_c[block b][row i][lane column t] (double2: j = 2t, 2t+1)
+__device__ __forceinline__ int zoff(int c, int b, int i, int t) {
+  return ((c * TB + b) * 4 + (i >> 1)) * 128 + ((((i & 1) * 4 + t) ^ ((b & 1) << 2)) << 4);
+}
+}  // namespace f16s
+
+template <bool COEF>
+__global__ void __launch_bounds__(f16s::WARPS * 32, 1)
+    k_fused16_sym(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
+                  long long frame_stride, int nframes, int bw, int bh, int nsx,
+                  const double* __restrict__ gsym, const double* __restrict__ basis,
+                  double* __restrict__ coef_out) {
+  using namespace f16s;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const double2* gs = reinterpret_cast<const double2*>(smem);
+  const double* cs = reinterpret_cast<const double*>(smem + GBYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int pair = warp >> 1, pu = warp & 1, pt = threadIdx.x & 63;  // thread within pair
+  uint8_t* zb = smem + GBYTES + CBYTES + pair * PAIR_BYTES;
+  uint8_t* pixbuf = zb + ZBYTES;
+
+  const long long spf = static_cast<long long>(bh) * nsx;
+  const long long ntiles = spf * nframes;
+  const long long stride = static_cast<long long>(gridDim.x) * PAIRS;
+  const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
+  const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
+                      fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
+  auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {  // ti < 2^31 (launcher)
+    const uint32_t u = static_cast<uint32_t>(ti);
+    f = static_cast<int>(dctf::fdiv(fd_spf, u));
+    const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(spf);
+    by = static_cast<int>(dctf::fdiv(fd_nsx, rem));
+    bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * TB;
+  };
+  auto is_fast = [&](int by, int bx0) { return aligned && by * 16 + 16 <= h && bx0 * 16 + 128 <= w; };
+  // thread pt of the pair moves 16-byte chunks (row pr, col pc) and (row pr + 8, col pc)
+  const int pr = pt >> 3, pc = (pt & 7) * 16;
+  uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
+  auto prefetch = [&](long long ti) {
+    int f, by, bx0;
+    tile_at(ti, f, by, bx0);
+    if (is_fast(by, bx0)) {
+      const uint8_t* p = in + f * frame_stride + static_cast<size_t>(by * 16) * pitch + bx0 * 16 + pc;
+      pf0 = ldg_stream(p + pr * pitch);
+      pf1 = ldg_stream(p + (pr + 8) * pitch);
+    }
+  };
+  long long tile = static_cast<long long>(blockIdx.x) * PAIRS + pair;
+  if (tile < ntiles) prefetch(tile);
+  {
+    const double2* src = reinterpret_cast<const double2*>(gsym);
+    double2* dst = reinterpret_cast<double2*>(smem);
+    for (int i = threadIdx.x; i < GBYTES / 16; i += blockDim.x) dst[i] = src[i];
+    double* cdst = reinterpret_cast<double*>(smem + GBYTES);
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) cdst[i] = basis[i];
+  }
+  __syncthreads();
+  // first inverse pass B fragments: C[2(2t + e) + pv][g], per class parity pv
+  double cb[2][2];
+#pragma unroll
+  for (int pv = 0; pv < 2; ++pv)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) cb[pv][e] = cs[(2 * (2 * t + e) + pv) * 16 + g];
+
+  int it = 0;
+  for (; tile < ntiles; tile += stride, ++it) {
+    int f, by, bx0;
+    tile_at(tile, f, by, bx0);
+    const bool fast = is_fast(by, bx0);
+    uint8_t* pix = pixbuf + (it & 1) * PIX_BYTES;
+    if (fast) {
+      *reinterpret_cast<uint4*>(pix + pr * PS + pc) = pf0;
+      *reinterpret_cast<uint4*>(pix + (pr + 8) * PS + pc) = pf1;
+    } else {
+      const uint8_t* ib = in + f * frame_stride;
+      for (int e = pt; e < 16 * 128; e += 64) {
+        const int r = e >> 7, c = e & 127;
+        const int y = min(by * 16 + r, h - 1), x = min(bx0 * 16 + c, w - 1);
+        pix[r * PS + c] = ib[static_cast<size_t>(y) * pitch + x];
+      }
+    }
+    bar_pair(pair);
+    if (tile + stride < ntiles) prefetch(tile + stride);
+
+    // quad butterflies for this warp's two classes (pu, 0), (pu, 1); lane
+    // (g, t): block g, positions (i, j = 2t + e)
+    double q[2][8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint8_t* top = pix + i * PS + 16 * g;
+      const uint8_t* bot = pix + (15 - i) * PS + 16 * g;
+      const uint32_t ta = *reinterpret_cast<const uint16_t*>(top + 2 * t);
+      const uint32_t tb = *reinterpret_cast<const uint16_t*>(top + 14 - 2 * t);
+      const uint32_t ba = *reinterpret_cast<const uint16_t*>(bot + 2 * t);
+      const uint32_t bb = *reinterpret_cast<const uint16_t*>(bot + 14 - 2 * t);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        // column j = 2t + e and its mirror 15 - j (byte 1 - e of the mirrored pair)
+        const int pj = (ta >> (8 * e)) & 0xff, pjb = (ba >> (8 * e)) & 0xff;
+        const int pm = (tb >> (8 * (1 - e))) & 0xff, pmb = (bb >> (8 * (1 - e))) & 0xff;
+        const int rj = pu ? pj - pjb : pj + pjb, rm = pu ? pm - pmb : pm + pmb;
+        q[0][i][e] = i32_to_f64(rj + rm);
+        q[1][i][e] = i32_to_f64(rj - rm);
+      }
+    }
+
+#pragma unroll
+    for (int pv = 0; pv < 2; ++pv) {
+      const int c = 2 * pu + pv;
+      const double2* gc = gs + c * (8 * 8 * 32);
+      double2 y[8];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) y[nt] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp) {
+        const double a0 = pv ? q[1][sp][0] : q[0][sp][0], a1 = pv ? q[1][sp][1] : q[0][sp][1];
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          const double2 bq = gc[(nt * 8 + sp) * 32 + lane];
+          dmma(y[nt], a0, bq.x);
+          dmma(y[nt], a1, bq.y);
+        }
+      }
+      if (COEF) {
+        const int bx = bx0 + g;
+        if (bx < bw) {
+          double* dst = coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 256;
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt) {
+            dst[(2 * nt + pu) * 16 + 2 * (2 * t) + pv] = y[nt].x;
+            dst[(2 * nt + pu) * 16 + 2 * (2 * t + 1) + pv] = y[nt].y;
+          }
+        }
+      }
+      // T[u' = nt][j = 2t + e] = sum_v' Y[u'][v'] C[2v' + pv][j]
+      double2 tt[8];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        tt[nt] = make_double2(0.0, 0.0);
+        dmma(tt[nt], y[nt].x, cb[pv][0]);
+        dmma(tt[nt], y[nt].y, cb[pv][1]);
+      }
+      // Z[i][e] = sum_u' C[2u' + pu][i] T[u'][e]  (+0.5 in the (0, 0) class)
+      double z[8][2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) z[i][0] = z[i][1] = (c == 0) ? 0.5 : 0.0;
+#pragma unroll
+      for (int u1 = 0; u1 < 8; ++u1) {
+        const double2* crow = reinterpret_cast<const double2*>(cs + (2 * u1 + pu) * 16);
+#pragma unroll
+        for (int ip = 0; ip < 4; ++ip) {
+          const double2 cc = crow[ip];
+          z[2 * ip][0] = fma(cc.x, tt[u1].x, z[2 * ip][0]);
+          z[2 * ip][1] = fma(cc.x, tt[u1].y, z[2 * ip][1]);
+          z[2 * ip + 1][0] = fma(cc.y, tt[u1].x, z[2 * ip + 1][0]);
+          z[2 * ip + 1][1] = fma(cc.y, tt[u1].y, z[2 * ip + 1][1]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<double2*>(zb + zoff(c, g, i, t)) = make_double2(z[i][0], z[i][1]);
+    }
+    bar_pair(pair);  // all four Z_c of the m-tile are in; the input pixels are consumed
+
+    // butterfly: this warp takes rows i = 4pu .. 4pu + 3 (and their mirrors)
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int i = 4 * pu + ii;
+      const double2 zee = *reinterpret_cast<const double2*>(zb + zoff(0, g, i, t));
+      const double2 zeo = *reinterpret_cast<const double2*>(zb + zoff(1, g, i, t));
+      const double2 zoe = *reinterpret_cast<const double2*>(zb + zoff(2, g, i, t));
+      const double2 zoo = *reinterpret_cast<const double2*>(zb + zoff(3, g, i, t));
+      uint32_t o_ij[2], o_rj[2], o_im[2], o_rm[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double ee = e ? zee.y : zee.x, eo = e ? zeo.y : zeo.x;
+        const double oe = e ? zoe.y : zoe.x, oo = e ? zoo.y : zoo.x;
+        const double a = ee + eo, b = ee - eo, cq = oe + oo, d = oe - oo;
+        o_ij[e] = floor_to_u8(a + cq);  // (i, j)
+        o_rj[e] = floor_to_u8(a - cq);  // (15-i, j)
+        o_im[e] = floor_to_u8(b + d);   // (i, 15-j)
+        o_rm[e] = floor_to_u8(b - d);   // (15-i, 15-j)
+      }
+      uint8_t* top = pix + i * PS + 16 * g;
+      uint8_t* bot = pix + (15 - i) * PS + 16 * g;
+      *reinterpret_cast<uint16_t*>(top + 2 * t) = static_cast<uint16_t>(o_ij[0] | (o_ij[1] << 8));
+      *reinterpret_cast<uint16_t*>(bot + 2 * t) = static_cast<uint16_t>(o_rj[0] | (o_rj[1] << 8));
+      *reinterpret_cast<uint16_t*>(top + 14 - 2 * t) = static_cast<uint16_t>(o_im[1] | (o_im[0] << 8));
+      *reinterpret_cast<uint16_t*>(bot + 14 - 2 * t) = static_cast<uint16_t>(o_rm[1] | (o_rm[0] << 8));
+    }
+    bar_pair(pair);  // the strip's output pixels are complete
+
+    uint8_t* ob = out + f * frame_stride;
+    if (fast) {
+      uint8_t* p = ob + static_cast<size_t>(by * 16) * pitch + bx0 * 16 + pc;
+      stg_stream(p + pr * pitch, *reinterpret_cast<const uint4*>(pix + pr * PS + pc));
+      stg_stream(p + (pr + 8) * pitch, *reinterpret_cast<const uint4*>(pix + (pr + 8) * PS + pc));
+    } else {
+      for (int e = pt; e < 16 * 128; e += 64) {
+        const int r = e >> 7, c = e & 127;
+        const int y = by * 16 + r, x = bx0 * 16 + c;
+        if (y < h && x < w) ob[static_cast<size_t>(y) * pitch + x] = pix[r * PS + c];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_spatial: convolve (spatial.hpp:41-68) per block, one thread per sample,
 // correlation orientation, zero-drop or clamp padding at the block edge; the
 // accumulation order (r, c ascending) and separately rounded multiply/add
@@ -1836,6 +2073,26 @@ dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, 
   return DCTF_OK;
 }
 
+dctf_status launch_fused16_sym(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
+                               size_t pitch, long long frame_stride, int nframes, double* coef_out,
+                               cudaStream_t st) {
+  auto kernel = coef_out ? k_fused16_sym<true> : k_fused16_sym<false>;
+  {
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(kernel), f16s::SMEM, "k_fused16_sym");
+    if (sa != DCTF_OK) return sa;
+  }
+  const int bw = (w + 15) / 16, bh = (h + 15) / 16, nsx = (bw + f16s::TB - 1) / f16s::TB;
+  const long long ntiles = static_cast<long long>(bh) * nsx * nframes;
+  if (ntiles <= 0) return DCTF_OK;
+  if (ntiles >= (1LL << 31)) return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
+  const long long ctas = std::min<long long>(sm_count(p->device), (ntiles + f16s::PAIRS - 1) / f16s::PAIRS);
+  kernel<<<static_cast<unsigned>(ctas), f16s::WARPS * 32, f16s::SMEM, st>>>(
+      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hsym, p->d_basis, coef_out);
+  dctf::add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
 // filter_image on device buffers, one frame or a strided frame batch.
 dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
@@ -1846,6 +2103,8 @@ dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* 
   const bool split = p->precision == DCTF_PREC_TF32X3;
   if (p->n == 8 && p->sym) return launch_fused8_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+  if (p->n == 16 && p->sym && !std::getenv("DCTF_N16_UNFUSED"))
+    return launch_fused16_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (!split && !std::getenv("DCTF_N16_UNFUSED"))
     return launch_fused16(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   // Unfused: forward (exact) -> H (split-precision tensor cores, or FP64 when
@@ -1921,6 +2180,13 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
       e = cudaMemcpy(p->d_hfused, hfused.data(), hfused.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
   p->sym = precision == DCTF_PREC_FP64 && dctf::parity_block_diagonal(p->op, n);
+  if (e == cudaSuccess && p->sym && n == 16) {
+    std::vector<double> gsym;
+    dctf::layout_gsym16(p->op, p->basis, gsym);
+    e = cudaMalloc(&p->d_hsym, gsym.size() * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_hsym, gsym.data(), gsym.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess && p->sym && n == 16) {
     std::vector<double> hcsym;
     dctf::layout_coefsym16(p->op, hcsym);
@@ -2119,7 +2385,8 @@ const char* dctf_plan_image_kernel(const dctf_plan* p) {
   if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT) return "k_fused8_i8";
   if (p->precision == DCTF_PREC_TF32X3) return "unfused";
   if (p->n == 8) return p->sym ? "k_fused8_sym" : "k_fused8";
-  return std::getenv("DCTF_N16_UNFUSED") ? "unfused" : "k_fused16";
+  if (std::getenv("DCTF_N16_UNFUSED")) return "unfused";
+  return p->sym ? "k_fused16_sym" : "k_fused16";
 }
 
 dctf_status dctf_plan_basis(const dctf_plan* p, double* h_c) {

@@ -570,6 +570,47 @@ void layout_coefsym16(const std::vector<double>& op, std::vector<double>& out) {
           }
 }
 
+// N = 16 fused-path image of the parity classes (k_fused16_sym, 128 KB):
+// G_c = H_c (C_c (x) C_c) maps the quad butterflies q_c(i, j) (i, j < 8) of a
+// block's pixels to its class-c filtered coefficients; class-local output
+// o = 8u' + v' <-> coefficient (2u' + pu, 2v' + pv); DMMA B fragments
+// [c][nt < 8][sp < 8][lane][e] = G_c[o = 8nt + g][(i = sp, j = 2t + e)].
+void layout_gsym16(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out) {
+  out.assign(4 * 8 * 8 * 64, 0.0);
+  auto C = [&](int u, int i) { return static_cast<long double>(basis[u * 16 + i]); };
+  for (int c = 0; c < 4; ++c) {
+    const int pu = c >> 1, pv = c & 1;
+    // T[o][(u2', j)] = sum_v2' H[o][(u2, v2)] C[v2][j], then contract u2' with C[u2][i]
+    std::vector<long double> g(64 * 64, 0.0L);
+    for (int o = 0; o < 64; ++o) {
+      const int row = (2 * (o >> 3) + pu) * 16 + 2 * (o & 7) + pv;
+      long double tmp[8][8];
+      for (int u1 = 0; u1 < 8; ++u1)
+        for (int j = 0; j < 8; ++j) {
+          long double acc = 0.0L;
+          for (int v1 = 0; v1 < 8; ++v1)
+            acc += static_cast<long double>(op[size_t(row) * 256 + (2 * u1 + pu) * 16 + 2 * v1 + pv]) *
+                   C(2 * v1 + pv, j);
+          tmp[u1][j] = acc;
+        }
+      for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) {
+          long double acc = 0.0L;
+          for (int u1 = 0; u1 < 8; ++u1) acc += tmp[u1][j] * C(2 * u1 + pu, i);
+          g[o * 64 + i * 8 + j] = acc;
+        }
+    }
+    size_t w = static_cast<size_t>(c) * 8 * 8 * 64;
+    for (int nt = 0; nt < 8; ++nt)
+      for (int sp = 0; sp < 8; ++sp)
+        for (int lane = 0; lane < 32; ++lane)
+          for (int e = 0; e < 2; ++e) {
+            const int gg = lane >> 2, t = lane & 3;
+            out[w++] = static_cast<double>(g[(8 * nt + gg) * 64 + sp * 8 + 2 * t + e]);
+          }
+  }
+}
+
 // Exact INT8 slicing of the forward-DCT-composed operator for k_fused8_i8.
 // G = H (C (x) C) maps a block's 64 pixels p (index i*8+j) straight to its
 // filtered DCT coefficients Y (index u*8+v). G is scaled by 2^-e (e: smallest

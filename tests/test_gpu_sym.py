@@ -141,3 +141,55 @@ def test_coef_sym_ragged_and_guarded(cuda, ref, n, nblocks):
     assert np.abs(y - r).max() <= 1e-9 * np.abs(r).max()
     yd = dense.filter_coeffs(x).cpu().numpy()
     assert np.abs(y - yd).max() <= 1e-12 * np.abs(yd).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wh", [(512, 512), (333, 200), (1000, 77), (2048, 48)])
+def test_sym16_matches_reference_and_dense(cuda, ref, wh):
+    """k_fused16_sym (N = 16 image path for symmetric masks): reference parity
+    (coefficients 1e-9 rel, u8 except near-ties), dense-kernel agreement,
+    ragged sizes and both paddings."""
+    torch = cuda
+    wd, h = wh
+    img = synth.uniform_image(41, wd, h)
+    d = torch.from_numpy(img).cuda()
+    nb = ((wd + 15) // 16) * ((h + 15) // 16)
+    masks = [("gaussian7", synth.gaussian_mask(7, 2.0), 7), ("average3", np.full(9, 1.0 / 9.0), 3),
+             ("gaussian3", None, 3)]
+    for name, w, k in masks:
+        if w is None:
+            w, k = ref.mask_preset(name)
+        for pad in (0, 1):
+            sym = P.FilterPlan(P.Mask(k, w), 16, P.PaddingMode(pad))
+            dense = P.FilterPlan(P.Mask(k, w), 16, P.PaddingMode(pad), precision=P.Precision.kFp64Dense)
+            assert sym.image_kernel == "k_fused16_sym" and dense.image_kernel == "k_fused16", name
+            cs = torch.empty((nb, 16, 16), dtype=torch.float64, device="cuda")
+            cd = torch.empty_like(cs)
+            os_, od = sym.filter_image(d, cs), dense.filter_image(d, cd)
+            r_out, _, r_co, r_pq = ref.filter_image(img, w, k, pad, 16, threads=nthreads(),
+                                                    side_outputs=True)
+            ours = os_.cpu().numpy()
+            mism, excused, _ = tie_report(ours, r_out, blocks_to_image(r_pq, wd, h))
+            assert mism == excused, (name, pad, mism)
+            scale = np.abs(r_co).max()
+            assert np.abs(cs.cpu().numpy() - r_co).max() <= 1e-9 * scale, (name, pad)
+            assert (cs - cd).abs().max().item() <= 1e-12 * scale, (name, pad)
+            m2, e2, _ = tie_report(ours, od.cpu().numpy(), blocks_to_image(r_pq, wd, h))
+            assert m2 == e2, (name, pad)
+
+
+@pytest.mark.gpu
+def test_sym16_frames(cuda, ref):
+    torch = cuda
+    w, k = synth.gaussian_mask(7, 2.0), 7
+    plan = P.FilterPlan(P.Mask(k, w), 16, P.PaddingMode.kReplicate)
+    frames = np.stack([synth.sinusoid_image(60 + f, 272, 144) for f in range(3)])
+    d = torch.from_numpy(frames).cuda()
+    outs = P.filter_frames(d, [plan], [0, 0, 0])
+    for f in range(3):
+        r_out, _, _, r_pq = ref.filter_image(frames[f], w, k, 1, 16, threads=nthreads(),
+                                             side_outputs=True)
+        got = outs[f].cpu().numpy()
+        mism, excused, _ = tie_report(got, r_out, blocks_to_image(r_pq, 272, 144))
+        assert mism == excused, f
+        assert torch.equal(outs[f], plan.filter_image(d[f].contiguous()))
