@@ -852,13 +852,14 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
 
   const long long spf = static_cast<long long>(bh) * nsx;
   const long long nstrips = spf * nframes;
-  const long long total = static_cast<long long>(gridDim.x) * WARPS;
+  const int nwarps = blockDim.x >> 5;  // < WARPS for small images (launcher)
+  const long long total = static_cast<long long>(gridDim.x) * nwarps;
   const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
   const int r0 = lane >> 3, c16 = (lane & 7) * 16;
 
   uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
-  long long s = static_cast<long long>(blockIdx.x) * WARPS + warp;
+  long long s = static_cast<long long>(blockIdx.x) * nwarps + warp;
   const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
                       fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
   auto strip_at = [&](long long si, int& f, int& by, int& bx0) {  // si < 2^31 (launcher)
@@ -1052,13 +1053,14 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
 
   const long long spf = static_cast<long long>(bh) * nsx;
   const long long nstrips = spf * nframes;
-  const long long total = static_cast<long long>(gridDim.x) * WARPS;
+  const int nwarps = blockDim.x >> 5;  // < WARPS for small images (launcher)
+  const long long total = static_cast<long long>(gridDim.x) * nwarps;
   const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
   const int r0 = lane >> 3, c16 = (lane & 7) * 16;
 
   uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
-  long long s = static_cast<long long>(blockIdx.x) * WARPS + warp;
+  long long s = static_cast<long long>(blockIdx.x) * nwarps + warp;
   const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
                       fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
   auto strip_at = [&](long long si, int& f, int& by, int& bx0) {  // si < 2^31 (launcher)
@@ -2018,12 +2020,13 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
   }
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8::SB - 1) / f8::SB;
   const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
-  const long long ctas =
-      std::min<long long>(2LL * sm_count(p->device), (nstrips + f8::WARPS - 1) / f8::WARPS);
+  const long long slots = 2LL * sm_count(p->device);
+  const int nw = static_cast<int>(std::max<long long>(1, std::min<long long>(f8::WARPS, nstrips / slots)));
+  const long long ctas = std::min<long long>(slots, (nstrips + nw - 1) / nw);
   if (ctas <= 0) return DCTF_OK;
   if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
     return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  kernel<<<static_cast<unsigned>(ctas), f8::WARPS * 32, f8::SMEM, st>>>(
+  kernel<<<static_cast<unsigned>(ctas), nw * 32, 32768 + nw * f8::WARP_BYTES, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
@@ -2040,12 +2043,14 @@ dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* ou
   }
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8s::SB - 1) / f8s::SB;
   const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
-  const long long ctas = std::min<long long>(static_cast<long long>(F8S_MINB) * sm_count(p->device),
-                                             (nstrips + f8s::WARPS - 1) / f8s::WARPS);
+  // small images: fewer warps per CTA so the strips spread over all SMs
+  const long long slots = static_cast<long long>(F8S_MINB) * sm_count(p->device);
+  const int nw = static_cast<int>(std::max<long long>(1, std::min<long long>(f8s::WARPS, nstrips / slots)));
+  const long long ctas = std::min<long long>(slots, (nstrips + nw - 1) / nw);
   if (ctas <= 0) return DCTF_OK;
   if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
     return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  kernel<<<static_cast<unsigned>(ctas), f8s::WARPS * 32, f8s::SMEM, st>>>(
+  kernel<<<static_cast<unsigned>(ctas), nw * 32, 16384 + nw * f8s::PIX_BYTES, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hsym, coef_out);
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
