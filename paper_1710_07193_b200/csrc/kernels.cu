@@ -1177,7 +1177,8 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
           dmma(z[1][c][nt2], y[1][nt].y, bb.y);
         }
     }
-    __syncwarp();
+    // (no __syncwarp: every lane's pixel reads fed the mma.sync.aligned DMMAs
+    // above, so they are complete before any lane overwrites the strip)
     // un-butterfly, quantise, write the four reflections of each position
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
