@@ -130,6 +130,7 @@ def cpu_reference_baseline(img, mask, budget_s=10.0):
     in place): filter_image's per-tile loop split over all host threads
     (filter.hpp:47-51 thread-safety contract), on the full config-2 image,
     repeated until ~budget_s of CPU time."""
+    import numpy as np
     from oracle import Reference
     ref = Reference()
     threads = os.cpu_count() or 1
@@ -139,10 +140,29 @@ def cpu_reference_baseline(img, mask, budget_s=10.0):
         t0 = time.perf_counter()
         ref.filter_image(img, mask, 5, 1, N, threads=threads)
         times.append(time.perf_counter() - t0)
-    return {"value": NBLOCKS / statistics.median(times), "unit": UNIT, "cores": threads,
-            "kind": "reference",
-            "sample": f"full 4096x4096 config-2 image x {len(times)} passes (median), "
-                      f"filter_image DCT path, tiles split over {threads} threads"}
+    out = {"value": NBLOCKS / statistics.median(times), "unit": UNIT, "cores": threads,
+           "kind": "reference",
+           "sample": f"full 4096x4096 config-2 image x {len(times)} passes (median), "
+                     f"filter_image DCT path, tiles split over {threads} threads"}
+    # SURVEY 8(d) CPU legs (i) and (iii): the reference exactly as shipped
+    # (one thread, whole filter_image) and its coefficient-only filter
+    # (cmd_bench, dctfilter_main.cc:420-425), each on a bounded band
+    band = img[:256]
+    nbb = (256 // N) * (W // N)
+    t0 = time.perf_counter()
+    ref.filter_image(band, mask, 5, 1, N, threads=1)
+    t1 = time.perf_counter() - t0
+    x = ref.forward_blocks(np.ascontiguousarray(
+        band.reshape(256 // N, N, W // N, N).transpose(0, 2, 1, 3).reshape(-1, N, N), np.float64))
+    t0 = time.perf_counter()
+    ref.filter_coeffs(mask, 5, N, 1, x, threads=threads)
+    tc = time.perf_counter() - t0
+    out["single_thread_filter_image"] = {"value": nbb / t1, "unit": UNIT, "cores": 1,
+                                         "sample": "256x4096 band, reference filter_image, 1 thread"}
+    out["coef_only_filter_coeffs"] = {"value": nbb / tc, "unit": UNIT, "cores": threads,
+                                      "sample": f"256x4096 band's blocks, reference filter_coeffs, "
+                                                f"{threads} threads"}
+    return out
 
 
 def run_reference_arm(args, rank):
