@@ -8,8 +8,23 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-O3 -Xptxas -v --ex
 
 all: $(PKG)/libdctf_b200.so $(PKG)/libdctf_synth.so oracle cpp-test cli
 
-$(PKG)/libdctf_b200.so: $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/ozaki.cu $(CSRC)/plan.cc $(CSRC)/internal.h include/dctf.h
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/kernels.cu $(CSRC)/tc.cu $(CSRC)/ozaki.cu $(CSRC)/plan.cc 2> build_ptxas.log || (cat build_ptxas.log; false)
+# one object per translation unit (built in parallel under make -j), linked
+# into the product library; ptxas -v reports are concatenated in build_ptxas.log
+CU_SRCS := capi coef fused tc ozaki
+CU_OBJS := $(patsubst %,build/%.o,$(CU_SRCS)) build/plan.o
+HDRS := $(CSRC)/internal.h $(CSRC)/device.cuh $(CSRC)/fastdiv.cuh include/dctf.h
+
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+build/plan.o: $(CSRC)/plan.cc $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(PKG)/libdctf_b200.so: $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS)
+	@cat build/*.ptxas.log > build_ptxas.log
 
 $(PKG)/libdctf_synth.so: $(CSRC)/synth.cc
 	g++ -O3 -std=c++17 -fPIC -shared -pthread -o $@ $<

@@ -1,5 +1,6 @@
 // Internal declarations shared by plan.cc (host operator compiler) and
-// kernels.cu (sm_100a kernels + C-ABI launchers).
+// the CUDA translation units (capi.cu: C ABI, transforms, plan upload; coef.cu;
+// fused.cu; tc.cu; ozaki.cu).
 #pragma once
 
 #include <cstddef>
@@ -23,7 +24,7 @@ struct dctf_plan {
   // merge_symmetric) and DCT-domain, npairs x n*n each (OperatorSet::pairs).
   std::vector<double> sp_left, sp_right, dct_left, dct_right;
 
-  // Device-resident copies (owned). Layouts: see kernels.cu.
+  // Device-resident copies (owned). Layouts: see plan.cc (layout_*).
   double* d_basis = nullptr;     // C, n*n
   double* d_hcoef = nullptr;     // H in coefficient-kernel fragment order
   double* d_hfused = nullptr;    // H in fused-kernel fragment order
@@ -47,11 +48,28 @@ struct dctf_plan {
 
 namespace dctf {
 
-// Thread-local error / launch bookkeeping (kernels.cu).
+// Thread-local error / launch bookkeeping (capi.cu).
 dctf_status set_error(dctf_status s, const std::string& msg);
 void add_launches(int k);
-// Dynamic shared-memory opt-in, once per (kernel, device), thread-safe (kernels.cu).
+// Dynamic shared-memory opt-in, once per (kernel, device), thread-safe (capi.cu).
 dctf_status ensure_dyn_smem(const void* func, int bytes, const char* name);
+// SM count of a device, cached (capi.cu).
+int sm_count(int device);
+inline bool misaligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; }
+
+// Launchers shared across the kernel translation units (all enqueue on `st`).
+// coef.cu: filter_coeffs on device buffers (dense / parity-class / 3xTF32).
+dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, long long nb, cudaStream_t st);
+// capi.cu: forward_2d of a u8 image into block-major coefficients, and the
+// inverse + quantize back to u8 (reference operation order).
+dctf_status launch_forward_u8(const dctf_plan* p, const uint8_t* img, int w, int h, size_t pitch,
+                              double* coeffs, cudaStream_t st);
+dctf_status launch_inverse_u8(const dctf_plan* p, const double* coeffs, uint8_t* img, int w, int h,
+                              size_t pitch, cudaStream_t st);
+// fused.cu: filter_image on device buffers, one frame or a strided frame batch.
+dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
+                                size_t pitch, long long frame_stride, int nframes, double* coef_out,
+                                cudaStream_t st);
 void reset_launches();
 
 // Host operator compiler (plan.cc).
@@ -85,7 +103,7 @@ void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>
 void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>& basis,
                        std::vector<int8_t>& bimg, std::vector<double>& scales);
 
-// TMA tensor map over block-major FP64 coefficients (kernels.cu): 2-D
+// TMA tensor map over block-major FP64 coefficients (capi.cu): 2-D
 // [nblocks rows x nn cols], box [box_rows x 16 cols], 128B swizzle.
 dctf_status make_xmap(void* map, const double* d, long long nblocks, int nn, int box_rows, int l2promo = 3);
 
@@ -99,3 +117,12 @@ dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d
                                cudaStream_t st, int sms);
 
 }  // namespace dctf
+
+// Returns DCTF_CUDA_ERROR (with the failing expression and CUDA's message)
+// from the enclosing dctf_status function when a runtime call fails.
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return set_error(DCTF_CUDA_ERROR, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)

@@ -401,7 +401,7 @@ void layout_hcoef(int n, const std::vector<double>& op, std::vector<double>& out
 // and the contraction index of k-step s = 2q+e for lane t is coefficient
 // (u = 2t+e, v = q). Both permutations are chosen so the per-warp shared
 // staging of X and Y is written and read with conflict-free 16-byte accesses
-// (see kernels.cu, fused8).
+// (see fused.cu, k_fused8).
 void layout_hfused8(const std::vector<double>& op, std::vector<double>& out) {
   out.assign(64 * 64, 0.0);
   size_t o = 0;
@@ -419,7 +419,7 @@ void layout_hfused8(const std::vector<double>& op, std::vector<double>& out) {
 // Fused n=16 kernel layout: [kc < 16][J < 32][q < 2][lane < 32][e < 2]
 //   = H[out(J, g)][in(kc, q, t, e)].
 // Staging word w of a block holds coefficients (u = 2a + e, v) with
-// v = w >> 3, a = (w & 7) ^ 4(v & 1) (see kernels.cu, k_fused16). K-step pair
+// v = w >> 3, a = (w & 7) ^ 4(v & 1) (see fused.cu, k_fused16). K-step pair
 // q of chunk kc for lane t reads word 8kc + 4q + t; column c of n-tile J is
 // word 4J + (c >> 1), element c & 1.
 void layout_hfused16(const std::vector<double>& op, std::vector<double>& out) {
