@@ -77,6 +77,11 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
 }
 
 
+// compute warps run the inverse chain on OZG blocks at once (independent
+// DMMA chains; all CB = 16 of a warp's blocks: +7 % over groups of 4)
+#ifndef OZG
+#define OZG 16
+#endif
 namespace oz {
 constexpr int TILE = 128;
 constexpr int S = 7;
@@ -309,24 +314,24 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       const int yb = static_cast<int>(tl & 1);
       const uint8_t* yt = ysm + yb * YBYTES;
       mbar_wait(&y_full[yb], static_cast<uint32_t>((tl >> 1) & 1));
-#pragma unroll 2
-      for (int bb = 0; bb < CB; bb += 4) {
-        double2 yv[4], z[4], o[4];
+#pragma unroll 1
+      for (int bb = 0; bb < CB; bb += OZG) {
+        double2 yv[OZG], z[OZG], o[OZG];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < OZG; ++i) {
           const int b = CB * cw + bb + i;
           yv[i] = *reinterpret_cast<const double2*>(yt + b * 512 + t * 128 + ((g ^ (2 * t) ^ fsw(b)) << 4));
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { z[i] = make_double2(0.0, 0.0); dmma(z[i], ai0, yv[i].x); }
+        for (int i = 0; i < OZG; ++i) { z[i] = make_double2(0.0, 0.0); dmma(z[i], ai0, yv[i].x); }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dmma(z[i], ai1, yv[i].y);
+        for (int i = 0; i < OZG; ++i) dmma(z[i], ai1, yv[i].y);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { o[i] = make_double2(0.5, 0.5); dmma(o[i], z[i].x, bi0); }
+        for (int i = 0; i < OZG; ++i) { o[i] = make_double2(0.5, 0.5); dmma(o[i], z[i].x, bi0); }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dmma(o[i], z[i].y, bi1);
+        for (int i = 0; i < OZG; ++i) dmma(o[i], z[i].y, bi1);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < OZG; ++i) {
           const uint32_t qv = floor_to_u8(o[i].x) | (floor_to_u8(o[i].y) << 8);
           *reinterpret_cast<uint16_t*>(pix + g * PS + 8 * (bb + i) + 2 * t) = static_cast<uint16_t>(qv);
         }
