@@ -514,7 +514,41 @@ def main():
                 "graph_us_per_call": graph1_us, "graph": "20 calls captured per CUDA graph",
                 "blocks_per_s_graph": 4096 / (graph1_us / 1e6)}
         del g1
+        # config 5: 64 frames of 3840x2160, 4 masks round-robin (Laplacian, Gaussian
+        # 5x5, 1x9 motion blur on 8x8 blocks, random asymmetric 5x5), one batched
+        # dctf_filter_frames_u8 call = one GPU's whole share at N=1 (8 unique
+        # S(f) frames generated on the host, tiled to 64 on the device)
+        FW, FH, FF = 3840, 2160, 64
+        rnd5, _ = synth.random_mask(1005, 5)
+        m5 = [(synth.LAPLACIAN3, 3, 3), (synth.gaussian_mask(5, 1.0), 5, 5), (synth.MOTION_1x9, 1, 9),
+              (rnd5, 5, 5)]
+        plans5 = [P.FilterPlan(P.Mask(k, w) if k == kc else P.Mask.rect(k, kc, w), 8,
+                               P.PaddingMode.kReplicate) for w, k, kc in m5]
+        uniq = np.stack([synth.sinusoid_image(f, FW, FH) for f in range(8)])
+        frames5 = torch.from_numpy(uniq).cuda().repeat(FF // 8, 1, 1).contiguous()
+        del uniq
+        idx5 = [f % 4 for f in range(FF)]
+        P.filter_frames(frames5, plans5, idx5)
+        torch.cuda.synchronize()
+        a5, b5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t5 = []
+        for _ in range(5):
+            a5.record()
+            out5 = P.filter_frames(frames5, plans5, idx5)
+            b5.record()
+            torch.cuda.synchronize()
+            t5.append(a5.elapsed_time(b5))
+            del out5
+        ms5 = statistics.median(t5)
+        nb5 = FF * (FW // 8) * (FH // 8)
+        cfg5 = {"workload": "config5: 64 x 3840x2160 S(f) frames, masks f mod 4 = Laplacian 3x3, "
+                "Gaussian 5x5 s=1, 1x9 motion blur, random asymmetric 5x5; replicate; FP64; one "
+                "dctf_filter_frames_u8 call", "blocks": nb5, "ms": ms5,
+                "blocks_per_s": nb5 / (ms5 / 1e3),
+                "kernels": [pl.image_kernel for pl in plans5]}
+        del frames5
         aux = {"n8_fused_dense": dense8, "n8_fused_int8exact": int8exact, "cfg1_graph": cfg1,
+               "cfg5_video": cfg5,
                "n16_coef_fp64": coefline(plan16.coef_kernel, ms_c16, 262144, 256, "fp64"),
                "n16_coef_fp64_dense": coefline(plan16d.coef_kernel, ms_c16d, 262144, 256, "fp64"),
                "n16_coef_tf32x3": coefline("k_coef_tf32x3<256>", ms_t16, 262144, 256, "3xtf32", err_t16),
