@@ -416,6 +416,10 @@ def main():
         ms_c16d = time_coef(plan16d, x16, y16, 262144)
         ms_t16 = time_coef(plan16t, x16, y16, 262144)
         err_t16 = float((y16 - ref16).abs().max() / ref16.abs().max())
+        plan16b = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate,
+                               precision=P.Precision.kBf16x3)
+        ms_b16 = time_coef(plan16b, x16, y16, 262144)
+        err_b16 = float((y16 - ref16).abs().max() / ref16.abs().max())
         y8t = torch.empty((NBLOCKS, 8, 8), dtype=torch.float64, device="cuda")
         plan8t = P.FilterPlan(P.Mask(5, mask), N, P.PaddingMode.kReplicate, precision=P.Precision.kTf32x3)
         coeffs8 = plan.forward_image(d_in)
@@ -552,6 +556,7 @@ def main():
                "n16_coef_fp64": coefline(plan16.coef_kernel, ms_c16, 262144, 256, "fp64"),
                "n16_coef_fp64_dense": coefline(plan16d.coef_kernel, ms_c16d, 262144, 256, "fp64"),
                "n16_coef_tf32x3": coefline("k_coef_tf32x3<256>", ms_t16, 262144, 256, "3xtf32", err_t16),
+               "n16_coef_bf16x3": coefline(plan16b.coef_kernel, ms_b16, 262144, 256, "3xbf16", err_b16),
                "n8_coef_tf32x3": coefline("k_coef_tf32x3<64>", ms_t8, NBLOCKS, 64, "3xtf32", err_t8),
                "n16_fused": {
             "kernel": plan16.image_kernel, "workload": "config4: 8192x8192 U(4), 16x16 blocks, "

@@ -53,7 +53,8 @@ typedef enum { DCTF_PAD_ZERO = 0, DCTF_PAD_REPLICATE = 1 } dctf_padding; /* spat
 typedef enum {
   DCTF_PREC_FP64 = 0,    /* FP64 DMMA tensor pipe; coefficients within 1e-9 rel. */
   DCTF_PREC_TF32X3 = 1,  /* split-precision tcgen05 kind::tf32, 3 passes          */
-  DCTF_PREC_BF16X3 = 2,  /* split-precision tcgen05 kind::f16 (bf16), 3 passes     */
+  DCTF_PREC_BF16X3 = 2,  /* split-precision tcgen05 kind::f16 (bf16), 3 passes;
+                            coefficients within ~1e-4 rel. (16-bit split)     */
   DCTF_PREC_INT8_EXACT = 3, /* n = 8 image path: DCT-domain contraction as exact INT8
                               tcgen05 slices (FP64-class accuracy); other entry
                               points of such a plan run the FP64 kernels        */

@@ -420,10 +420,6 @@ namespace {
 // operator in every layout the kernels use. Takes ownership of p.
 dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
   const int n = p->n, device = p->device, precision = p->precision;
-  if (precision == DCTF_PREC_BF16X3) {
-    delete p;
-    return set_error(DCTF_UNSUPPORTED, "BF16x3 is not built; use DCTF_PREC_TF32X3 or DCTF_PREC_FP64");
-  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -486,6 +482,13 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     dctf::layout_hsplit_tf32(n, p->op, hs);
     e = cudaMalloc(&p->d_hsplit, hs.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(p->d_hsplit, hs.data(), hs.size() * sizeof(float), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess && precision == DCTF_PREC_BF16X3) {
+    std::vector<uint16_t> hs;
+    dctf::layout_hsplit_bf16(n, p->op, hs);
+    e = cudaMalloc(&p->d_hsplit, hs.size() * sizeof(uint16_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_hsplit, hs.data(), hs.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) {
     const std::string msg = cudaGetErrorString(e);
@@ -651,6 +654,7 @@ dctf_status dctf_plan_info(const dctf_plan* p, int* n, int* npairs, int* merged)
 const char* dctf_plan_coef_kernel(const dctf_plan* p) {
   if (!p) return nullptr;
   if (p->precision == DCTF_PREC_TF32X3) return "k_coef_tf32x3";
+  if (p->precision == DCTF_PREC_BF16X3) return "k_coef_bf16x3";
   if (p->n == 8) return p->sym ? "k_coef8_sym" : "k_coef8";
   return p->sym ? "k_coef16_sym" : "k_coef16";
 }
@@ -658,7 +662,7 @@ const char* dctf_plan_coef_kernel(const dctf_plan* p) {
 const char* dctf_plan_image_kernel(const dctf_plan* p) {
   if (!p) return nullptr;
   if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT) return "k_fused8_i8";
-  if (p->precision == DCTF_PREC_TF32X3) return "unfused";
+  if (p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3) return "unfused";
   if (p->n == 8) return p->sym ? "k_fused8_sym" : "k_fused8";
   if (std::getenv("DCTF_N16_UNFUSED")) return "unfused";
   return p->sym ? "k_fused16_sym" : "k_fused16";
@@ -901,7 +905,7 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   cudaGetLastError();
   // zero-copy needs a single fused kernel (every precision except the
   // split-precision path, which runs forward/filter/inverse as three kernels)
-  const bool fused = p->precision != DCTF_PREC_TF32X3;
+  const bool fused = p->precision != DCTF_PREC_TF32X3 && p->precision != DCTF_PREC_BF16X3;
   int mode = (in_pinned && out_pinned && fused) ? 2 : (out_pinned && fused ? 1 : 0);
   if (const char* env = std::getenv("DCTF_E2E_MODE")) {
     const int m = std::atoi(env);

@@ -545,7 +545,7 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
   if (misaligned16(d_in) || misaligned16(d_out))
     return set_error(DCTF_INVALID_ARGUMENT, "coefficient buffers must be 16-byte aligned");
   if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in-place filter_coeffs not supported");
-  if (p->precision == DCTF_PREC_TF32X3) return dctf::launch_coef_tf32x3(p, d_in, d_out, nb, st, sm_count(p->device));
+  if (p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3) return dctf::launch_coef_tf32x3(p, d_in, d_out, nb, st, sm_count(p->device));
   if (p->sym) return p->n == 8 ? launch_coef8_sym(p, d_in, d_out, nb, st) : launch_coef16_sym(p, d_in, d_out, nb, st);
   CUtensorMap map;
   const int nn = p->n * p->n;

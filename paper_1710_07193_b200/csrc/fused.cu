@@ -1038,7 +1038,7 @@ dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* 
   if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT)
     return dctf::launch_fused8_i8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st,
                                   sm_count(p->device));
-  const bool split = p->precision == DCTF_PREC_TF32X3;
+  const bool split = p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3;
   if (p->n == 8 && p->sym) return launch_fused8_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (p->n == 16 && p->sym && !std::getenv("DCTF_N16_UNFUSED"))

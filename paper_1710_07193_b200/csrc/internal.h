@@ -28,7 +28,7 @@ struct dctf_plan {
   double* d_basis = nullptr;     // C, n*n
   double* d_hcoef = nullptr;     // H in coefficient-kernel fragment order
   double* d_hfused = nullptr;    // H in fused-kernel fragment order
-  void* d_hsplit = nullptr;      // TF32 hi/lo split of H, swizzled (precision TF32X3)
+  void* d_hsplit = nullptr;      // TF32 / BF16 hi/lo split of H in UMMA core layout (TF32X3, BF16X3)
   void* d_gimg = nullptr;        // INT8 digit slices of H (C (x) C), swizzled (INT8_EXACT)
   double* d_gscale = nullptr;    // per-row scales of those slices
   int* d_nan = nullptr;          // NaN flag
@@ -100,6 +100,7 @@ std::vector<long double> compose_forward_ld(const std::vector<double>& op, const
 std::vector<double> compose_forward(const std::vector<double>& op, const std::vector<double>& basis, int n);
 void layout_hfused16(const std::vector<double>& op, std::vector<double>& out);
 void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>& out);
+void layout_hsplit_bf16(int n, const std::vector<double>& op, std::vector<uint16_t>& out);
 void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>& basis,
                        std::vector<int8_t>& bimg, std::vector<double>& scales);
 

@@ -25,6 +25,7 @@
 // TMEM holds two accumulators (tile parity) so the epilogue of tile i
 // overlaps the MMAs of tile i+1; shared memory holds two K-chunk stages.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -66,25 +67,55 @@ __device__ __forceinline__ void split_tf32(double x, float& hi, float& lo) {
   lo = __uint_as_float(l);
 }
 
+// bf16 hi/lo split, same scheme: x ~= hi + lo, both bf16 (8 significant bits
+// each), after one rounding of x to float.
+__device__ __forceinline__ void split_bf16(double x, uint32_t& hi, uint32_t& lo) {
+  const float xf = __double2float_rn(x);
+  const __nv_bfloat16 h = __float2bfloat16_rn(xf);
+  const __nv_bfloat16 l = __float2bfloat16_rn(xf - __bfloat162float(h));
+  hi = __bfloat16_as_ushort(h);
+  lo = __bfloat16_as_ushort(l);
+}
+
+// Instruction descriptor: kind::f16 with BF16 A/B (K-major), D FP32, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // UMMA shared-memory descriptor, K-major, no swizzle: 8-row x 16-byte core
-// matrices, LBO = 128 B between K-adjacent cores, SBO = 512 B between 8-row
-// groups (a 16-wide TF32 K chunk per 64-byte row), version 1, layout type 0.
+// matrices, LBO = 128 B between K-adjacent cores, SBO = 8 rows x (bytes of a
+// 16-wide K chunk row) between 8-row groups — 512 B for TF32, 256 B for
+// BF16 — version 1, layout type 0.
+template <int SBO>
 __device__ __forceinline__ uint64_t umma_desc_k16(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>(128u >> 4) << 16;   // LBO
-  d |= static_cast<uint64_t>(512u >> 4) << 32;   // SBO
-  d |= static_cast<uint64_t>(1u) << 46;          // version
+  d |= static_cast<uint64_t>(128u >> 4) << 16;            // LBO
+  d |= static_cast<uint64_t>(static_cast<uint32_t>(SBO) >> 4) << 32;  // SBO
+  d |= static_cast<uint64_t>(1u) << 46;                   // version
   return d;
 }
 
-template <int NN>
+template <int NN, bool BF>
 struct TcCfg {
   static constexpr int TILE = 128;          // MMA M (blocks per tile)
-  static constexpr int KCH = NN / 16;       // K chunks of 16 (64-byte TF32 rows)
+  static constexpr int KCH = NN / 16;       // K chunks of 16
+  static constexpr int ROWB = BF ? 32 : 64; // bytes of one operand row of a chunk
+  static constexpr int SBO = 8 * ROWB;      // 8-row group stride
+  static constexpr int KSTEPS = BF ? 1 : 2; // MMAs per chunk and pass (K = 16 bf16 / 8 tf32)
   static constexpr int XBYTES = TILE * 128; // FP64 chunk staging (TMA box 128 rows x 16 doubles, SW128)
-  static constexpr int ABYTES = TILE * 64;  // one TF32 part of A
-  static constexpr int BBYTES = NN * 64;    // one TF32 part of B
+  static constexpr int ABYTES = TILE * ROWB;  // one split part of A
+  static constexpr int BBYTES = NN * ROWB;    // one split part of B
   static constexpr int XS = NN == 64 ? 8 : 5;  // FP64 staging stages (HBM latency cover)
   static constexpr int AS = NN == 64 ? 3 : 2;  // operand stages
   static constexpr int OPBYTES = 2 * ABYTES + 2 * BBYTES;
@@ -99,11 +130,11 @@ struct TcCfg {
   static constexpr int SMEM = 1024 + XS * XBYTES + AS * OPBYTES + EPI_WARPS * EPI_BYTES;
 };
 
-template <int NN>
-__global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
-    k_coef_tf32x3(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ hsplit,
+template <int NN, bool BF>
+__global__ void __launch_bounds__(TcCfg<NN, BF>::THREADS, 1)
+    k_coef_split3(const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ hsplit,
                   double* __restrict__ y, long long nblocks) {
-  using Cfg = TcCfg<NN>;
+  using Cfg = TcCfg<NN, BF>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
   uint8_t* xst = base;                               // FP64 staging ring
@@ -162,7 +193,7 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
         const long long tile = blockIdx.x + (c / Cfg::KCH) * gridDim.x;
         const int kc = static_cast<int>((c + tile) % Cfg::KCH), as = static_cast<int>(c % Cfg::AS);
         if (c >= Cfg::AS) mbar_wait(&a_empty[as], static_cast<uint32_t>(((c / Cfg::AS) - 1) & 1));
-        const float* hs = hsplit + static_cast<size_t>(kc) * 2 * (Cfg::BBYTES / 4);
+        const uint8_t* hs = hsplit + static_cast<size_t>(kc) * 2 * Cfg::BBYTES;
         mbar_expect_tx(&b_full[as], 2 * Cfg::BBYTES);
         bulk_load(ops + as * Cfg::OPBYTES + 2 * Cfg::ABYTES, hs, 2 * Cfg::BBYTES, &b_full[as]);
       }
@@ -170,7 +201,7 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
   } else if (warp == Cfg::MMA_WARP) {
     // ---------------- single-thread MMA issue
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(128, NN);
+      constexpr uint32_t idesc = BF ? idesc_bf16(128, NN) : idesc_tf32(128, NN);
       for (long long c = 0; c < nchunks; ++c) {
         const long long ti = c / Cfg::KCH;
         const int j = static_cast<int>(c % Cfg::KCH), as = static_cast<int>(c % Cfg::AS);
@@ -183,29 +214,51 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
         const uint32_t so = smem_u32(ops + as * Cfg::OPBYTES);
         const uint32_t d = tmem_base + static_cast<uint32_t>(ab * NN);
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
+        for (int ks = 0; ks < Cfg::KSTEPS; ++ks) {
           const uint32_t koff = 256u * ks;  // two 16-byte cores per K step
-          const uint64_t ah = umma_desc_k16(so + koff);
-          const uint64_t al = umma_desc_k16(so + Cfg::ABYTES + koff);
-          const uint64_t bh = umma_desc_k16(so + 2 * Cfg::ABYTES + koff);
-          const uint64_t bl = umma_desc_k16(so + 2 * Cfg::ABYTES + Cfg::BBYTES + koff);
-          mma_tf32(d, ah, bh, idesc, (j | ks) != 0);
-          mma_tf32(d, ah, bl, idesc, 1);
-          mma_tf32(d, al, bh, idesc, 1);
+          const uint64_t ah = umma_desc_k16<Cfg::SBO>(so + koff);
+          const uint64_t al = umma_desc_k16<Cfg::SBO>(so + Cfg::ABYTES + koff);
+          const uint64_t bh = umma_desc_k16<Cfg::SBO>(so + 2 * Cfg::ABYTES + koff);
+          const uint64_t bl = umma_desc_k16<Cfg::SBO>(so + 2 * Cfg::ABYTES + Cfg::BBYTES + koff);
+          if (BF) {
+            mma_bf16(d, ah, bh, idesc, (j | ks) != 0);
+            mma_bf16(d, ah, bl, idesc, 1);
+            mma_bf16(d, al, bh, idesc, 1);
+          } else {
+            mma_tf32(d, ah, bh, idesc, (j | ks) != 0);
+            mma_tf32(d, ah, bl, idesc, 1);
+            mma_tf32(d, al, bh, idesc, 1);
+          }
         }
         mma_commit(&a_empty[as]);
         if (j == Cfg::KCH - 1) mma_commit(&acc_full[ab]);
       }
     }
   } else if (warp < Cfg::CONV_WARPS) {
-    // ---------------- converters: FP64 staging -> TF32 hi/lo operand cores
-    const int r = threadIdx.x & (Cfg::TILE - 1), kp = threadIdx.x >> 7;  // row, K-core pair
+    // ---------------- converters: FP64 staging -> TF32 / BF16 hi/lo operand cores
+    const int r = threadIdx.x & (Cfg::TILE - 1), kp = threadIdx.x >> 7;  // row, K-core pair (TF32) / core (BF16)
     for (long long c = 0; c < nchunks; ++c) {
       const int xs = static_cast<int>(c % Cfg::XS), as = static_cast<int>(c % Cfg::AS);
       mbar_wait(&x_full[xs], static_cast<uint32_t>((c / Cfg::XS) & 1));
       if (c >= Cfg::AS) mbar_wait(&a_empty[as], static_cast<uint32_t>(((c / Cfg::AS) - 1) & 1));
       const uint8_t* xrow = xst + xs * Cfg::XBYTES + r * 128;
       uint8_t* op = ops + as * Cfg::OPBYTES;
+      if (BF) {
+        // one 16-byte core = 8 bf16 = K 8kp .. 8kp+7 (FP64 chunks 4kp .. 4kp+3)
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double2 v = *reinterpret_cast<const double2*>(xrow + (((4 * kp + m) ^ (r & 7)) << 4));
+          uint32_t h0, l0, h1, l1;
+          split_bf16(v.x, h0, l0);
+          split_bf16(v.y, h1, l1);
+          hw[m] = h0 | (h1 << 16);
+          lw[m] = l0 | (l1 << 16);
+        }
+        const int off = (r >> 3) * Cfg::SBO + kp * 128 + (r & 7) * 16;
+        *reinterpret_cast<uint4*>(op + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(op + Cfg::ABYTES + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      } else
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int kk = 2 * kp + i;  // 16-byte TF32 core column = K 4kk..4kk+3
@@ -216,7 +269,7 @@ __global__ void __launch_bounds__(TcCfg<NN>::THREADS, 1)
         split_tf32(v0.y, h4.y, l4.y);
         split_tf32(v1.x, h4.z, l4.z);
         split_tf32(v1.y, h4.w, l4.w);
-        const int off = (r >> 3) * 512 + kk * 128 + (r & 7) * 16;
+        const int off = (r >> 3) * Cfg::SBO + kk * 128 + (r & 7) * 16;
         *reinterpret_cast<float4*>(op + off) = h4;
         *reinterpret_cast<float4*>(op + Cfg::ABYTES + off) = l4;
       }
@@ -313,6 +366,37 @@ void layout_hsplit_tf32(int n, const std::vector<double>& op, std::vector<float>
       }
 }
 
+// BF16 version of the same image: rows of 32 B (16 bf16), core (n/8, kk) at
+// byte (n/8)*256 + kk*128, row n%8 at +16*(n%8), element k%8 at +2*(k%8).
+void layout_hsplit_bf16(int n, const std::vector<double>& op, std::vector<uint16_t>& out) {
+  const int nn = n * n, kch = nn / 16;
+  out.assign(static_cast<size_t>(kch) * 2 * nn * 16, 0);
+  auto bf16_rn = [](float f) -> uint16_t {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return static_cast<uint16_t>(u >> 16);
+    u += 0x7fffu + ((u >> 16) & 1u);  // round to nearest even
+    return static_cast<uint16_t>(u >> 16);
+  };
+  auto bf16_f = [](uint16_t h) {
+    const uint32_t u = static_cast<uint32_t>(h) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+  };
+  for (int kc = 0; kc < kch; ++kc)
+    for (int row = 0; row < nn; ++row)
+      for (int k = 0; k < 16; ++k) {
+        const double v = op[static_cast<size_t>(row) * nn + 16 * kc + k];
+        const float vf = static_cast<float>(v);
+        const uint16_t hi = bf16_rn(vf);
+        const uint16_t lo = bf16_rn(vf - bf16_f(hi));
+        const size_t pos = static_cast<size_t>(row >> 3) * 128 + (k >> 3) * 64 + (row & 7) * 8 + (k & 7);
+        out[(static_cast<size_t>(kc) * 2 + 0) * nn * 16 + pos] = hi;
+        out[(static_cast<size_t>(kc) * 2 + 1) * nn * 16 + pos] = lo;
+      }
+}
+
 dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
                                cudaStream_t st, int sms) {
   if (nb == 0) return DCTF_OK;
@@ -321,20 +405,25 @@ dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d
   const dctf_status s = make_xmap(&map, d_in, nb, nn, 128);
   if (s != DCTF_OK) return s;
   auto run = [&](auto kernel, int smem, int threads) -> dctf_status {
-    static_cast<void>(0);
-    const dctf_status sa = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), smem, "k_coef_tf32x3");
+    const dctf_status sa = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), smem, "k_coef_split3");
     if (sa != DCTF_OK) return sa;
     const long long ntiles = (nb + 127) / 128;
     kernel<<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), threads, smem, st>>>(
-        map, static_cast<const float*>(p->d_hsplit), d_out, nb);
+        map, static_cast<const uint8_t*>(p->d_hsplit), d_out, nb);
     return DCTF_OK;
   };
-  const dctf_status r = p->n == 8 ? run(k_coef_tf32x3<64>, TcCfg<64>::SMEM, TcCfg<64>::THREADS)
-                                  : run(k_coef_tf32x3<256>, TcCfg<256>::SMEM, TcCfg<256>::THREADS);
+  const bool bf = p->precision == DCTF_PREC_BF16X3;
+  dctf_status r;
+  if (p->n == 8)
+    r = bf ? run(k_coef_split3<64, true>, TcCfg<64, true>::SMEM, TcCfg<64, true>::THREADS)
+           : run(k_coef_split3<64, false>, TcCfg<64, false>::SMEM, TcCfg<64, false>::THREADS);
+  else
+    r = bf ? run(k_coef_split3<256, true>, TcCfg<256, true>::SMEM, TcCfg<256, true>::THREADS)
+           : run(k_coef_split3<256, false>, TcCfg<256, false>::SMEM, TcCfg<256, false>::THREADS);
   if (r != DCTF_OK) return r;
   add_launches(1);
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_coef_tf32x3: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_coef_split3: ") + cudaGetErrorString(e));
   return DCTF_OK;
 }
 
