@@ -48,18 +48,26 @@ for rep in sys.argv[3:]:
                          text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     hh, units, vals = rr[0], rr[1], rr[2]
-    name = vals[hh.index("Kernel Name")].split("(")[0].split("::")[-1].replace("<", "_").replace(">", "")
+    full = vals[hh.index("Kernel Name")].replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
+    if full.startswith("void "):
+        full = full[5:]
+    cut = min([i for i in (full.find("<"), full.find("(")) if i >= 0] or [len(full)])
+    base = full[:cut].split("::")[-1].strip()
+    rest = full[cut:]
+    targs = rest[1:rest.index(">(")] if rest.startswith("<") and ">(" in rest else ""
+    targs = "".join(ch if ch.isalnum() else "_" for ch in targs.replace("(bool)", "")).strip("_")
+    name = base + ("_" + targs if targs else "")
     m = {k: {"value": vals[hh.index(k)], "unit": units[hh.index(k)]} for k in KEYS if k in hh}
     json.dump({"report": os.path.basename(rep), "kernel": name, "metrics": m},
               open(os.path.join(out, f"ncu_{name}.json"), "w"), indent=1)
-    if name in ("k_fused8", "k_fused8_sym"):
+    if base in ("k_fused8", "k_fused8_sym"):
         def tobytes(e):
             s = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[e["unit"]]
             return float(e["value"].replace(",", "")) * s
         traffic = tobytes(m["dram__bytes_read.sum"]) + tobytes(m["dram__bytes_write.sum"])
-        json.dump({"kernel": name, "dram_bytes_per_launch": traffic,
+        json.dump({"kernel": base, "dram_bytes_per_launch": traffic,
                    "source": f"profiles/{tag}/ncu_{name}.json (ncu --set full, bench config 2, one launch)"},
-                  open(os.path.join(ROOT, "profiles", f"ncu_{name}_config2.json"), "w"), indent=1)
+                  open(os.path.join(ROOT, "profiles", f"ncu_{base}_config2.json"), "w"), indent=1)
 # the bench headline kernel's traffic file (bench.py: ncu_traffic)
 hp = os.path.join(ROOT, "profiles", "ncu_k_fused8_sym_config2.json")
 if os.path.exists(hp):
