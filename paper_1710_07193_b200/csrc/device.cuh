@@ -135,6 +135,15 @@ __device__ __forceinline__ void stg_stream(void* p, uint4 v) {
                : "memory");
 }
 
+// 16-byte global -> shared copy that bypasses L1 and registers (Ampere-style
+// cp.async; each thread waits for its own copies, then a warp/CTA barrier
+// publishes them)
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // small signed integer (|v| < 2^20) -> double, exactly, on the integer pipes
 __device__ __forceinline__ double i32_to_f64(int v) {
   const uint32_t m = static_cast<uint32_t>(v < 0 ? -v : v);

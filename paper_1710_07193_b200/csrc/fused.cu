@@ -250,7 +250,7 @@ constexpr int WARPS = 8;
 constexpr int SB = 16;
 constexpr int PS = 192;  // adjacent rows 16 banks apart: conflict-free u16 output stores
 constexpr int PIX_BYTES = 8 * PS;
-constexpr int SMEM = 16384 + WARPS * PIX_BYTES;
+constexpr int SMEM = 16384 + WARPS * 2 * PIX_BYTES;  // double-buffered strip tiles
 }  // namespace f8s
 
 template <bool COEF>
@@ -263,7 +263,8 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
   const double2* gs = reinterpret_cast<const double2*>(smem);          // [c][nt][sp][lane]
   const double2* ws = reinterpret_cast<const double2*>(smem + 8192);   // [c][nt2][nt][lane]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  uint8_t* pix = smem + 16384 + warp * PIX_BYTES;
+  uint8_t* pix = smem + 16384 + warp * 2 * PIX_BYTES;   // strip being filtered
+  uint8_t* pixn = pix + PIX_BYTES;                        // next strip (cp.async in flight)
 
   const long long spf = static_cast<long long>(bh) * nsx;
   const long long nstrips = spf * nframes;
@@ -273,7 +274,6 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
   const int r0 = lane >> 3, c16 = (lane & 7) * 16;
 
-  uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
   long long s = static_cast<long long>(blockIdx.x) * nwarps + warp;
   const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
                       fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
@@ -285,16 +285,21 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
     bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * SB;
   };
   auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && bx0 * 8 + 128 <= w; };
-  auto prefetch = [&](long long si) {
+  // strip si's pixels -> buf asynchronously (cp.async, no registers held);
+  // returns false when the strip needs the clamped path instead
+  auto fetch = [&](long long si, uint8_t* buf) {
     int f, by, bx0;
     strip_at(si, f, by, bx0);
-    if (is_fast(by, bx0)) {
+    const bool ok = is_fast(by, bx0);
+    if (ok) {
       const uint8_t* p = in + f * frame_stride + static_cast<size_t>(by * 8) * pitch + bx0 * 8 + c16;
-      pf0 = ldg_stream(p + r0 * pitch);
-      pf1 = ldg_stream(p + (r0 + 4) * pitch);
+      cp_async16(buf + r0 * PS + c16, p + r0 * pitch);
+      cp_async16(buf + (r0 + 4) * PS + c16, p + (r0 + 4) * pitch);
     }
+    cp_async_commit();
+    return ok;
   };
-  if (s < nstrips) prefetch(s);  // first strip's pixels in flight during the operator copy
+  bool fast = s < nstrips ? fetch(s, pix) : false;  // first strip in flight during the operator copy
   {
     const double2* src = reinterpret_cast<const double2*>(hsym);
     double2* dst = reinterpret_cast<double2*>(smem);
@@ -305,11 +310,8 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
   for (; s < nstrips; s += total) {
     int f, by, bx0;
     strip_at(s, f, by, bx0);
-    const bool fast = is_fast(by, bx0);
-    if (fast) {
-      *reinterpret_cast<uint4*>(pix + r0 * PS + c16) = pf0;
-      *reinterpret_cast<uint4*>(pix + (r0 + 4) * PS + c16) = pf1;
-    } else {
+    cp_async_wait_all();
+    if (!fast) {
       const uint8_t* ib = in + f * frame_stride;
       for (int e = lane; e < 8 * 128; e += 32) {
         const int r = e >> 7, c = e & 127;
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
       }
     }
     __syncwarp();
-    if (s + total < nstrips) prefetch(s + total);
+    const bool fast_next = s + total < nstrips ? fetch(s + total, pixn) : false;
 
     // quad butterflies of both m-tiles (blocks g and 8 + g) at positions
     // (sq, t), sq = 0..3, all four classes
@@ -432,7 +434,12 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
       }
     }
     __syncwarp();
+    uint8_t* tmp = pix;
+    pix = pixn;
+    pixn = tmp;
+    fast = fast_next;
   }
+  cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -979,7 +986,7 @@ dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* ou
   if (ctas <= 0) return DCTF_OK;
   if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
     return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  kernel<<<static_cast<unsigned>(ctas), nw * 32, 16384 + nw * f8s::PIX_BYTES, st>>>(
+  kernel<<<static_cast<unsigned>(ctas), nw * 32, 16384 + nw * 2 * f8s::PIX_BYTES, st>>>(
       in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hsym, coef_out);
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
