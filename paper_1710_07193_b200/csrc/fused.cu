@@ -266,18 +266,19 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
   uint8_t* pix = smem + 16384 + warp * 2 * PIX_BYTES;   // strip being filtered
   uint8_t* pixn = pix + PIX_BYTES;                        // next strip (cp.async in flight)
 
-  const long long spf = static_cast<long long>(bh) * nsx;
-  const long long nstrips = spf * nframes;
+  // strip counts < 2^31 (launcher): 32-bit strip arithmetic
+  const int spf = bh * nsx;
+  const int nstrips = spf * nframes;
   const int nwarps = blockDim.x >> 5;  // < WARPS for small images (launcher)
-  const long long total = static_cast<long long>(gridDim.x) * nwarps;
+  const int total = static_cast<int>(gridDim.x) * nwarps;
   const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
   const int r0 = lane >> 3, c16 = (lane & 7) * 16;
 
-  long long s = static_cast<long long>(blockIdx.x) * nwarps + warp;
+  int s = static_cast<int>(blockIdx.x) * nwarps + warp;
   const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
                       fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
-  auto strip_at = [&](long long si, int& f, int& by, int& bx0) {  // si < 2^31 (launcher)
+  auto strip_at = [&](int si, int& f, int& by, int& bx0) {
     const uint32_t u = static_cast<uint32_t>(si);
     f = static_cast<int>(dctf::fdiv(fd_spf, u));
     const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(spf);
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
   auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && bx0 * 8 + 128 <= w; };
   // strip si's pixels -> buf asynchronously (cp.async, no registers held);
   // returns false when the strip needs the clamped path instead
-  auto fetch = [&](long long si, uint8_t* buf) {
+  auto fetch = [&](int si, uint8_t* buf) {
     int f, by, bx0;
     strip_at(si, f, by, bx0);
     const bool ok = is_fast(by, bx0);
