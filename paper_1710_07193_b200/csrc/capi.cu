@@ -917,7 +917,7 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   if (mode == 2) {
     s = filter_image_device(p, static_cast<const uint8_t*>(ai.devicePointer),
                             static_cast<uint8_t*>(ao.devicePointer), w, h, pitch, 0, 1, nullptr,
-                            s_run);
+                            s_run, /*host_mapped=*/true);
     launches = dctf::t_launches;
   } else {
     const size_t chunk_target = mode == 1 ? (size_t(4) << 20) : (size_t(2) << 20);

@@ -253,7 +253,7 @@ constexpr int PIX_BYTES = 8 * PS;
 constexpr int SMEM = 16384 + WARPS * 2 * PIX_BYTES;  // double-buffered strip tiles
 }  // namespace f8s
 
-template <bool COEF>
+template <bool COEF, bool ASYNC>
 __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
     k_fused8_sym(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
                  long long frame_stride, int nframes, int bw, int bh, int nsx,
@@ -286,18 +286,26 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
     bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * SB;
   };
   auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && bx0 * 8 + 128 <= w; };
-  // strip si's pixels -> buf asynchronously (cp.async, no registers held);
-  // returns false when the strip needs the clamped path instead
+  // strip si's pixels -> buf: asynchronously (cp.async, no registers held;
+  // device-resident images) or into registers staged at the top of the next
+  // iteration (ld.global.cs; host-mapped zero-copy input, where it reads PCIe
+  // faster). Returns false when the strip needs the clamped path instead.
+  uint4 pf0 = make_uint4(0, 0, 0, 0), pf1 = pf0;
   auto fetch = [&](int si, uint8_t* buf) {
     int f, by, bx0;
     strip_at(si, f, by, bx0);
     const bool ok = is_fast(by, bx0);
     if (ok) {
       const uint8_t* p = in + f * frame_stride + static_cast<size_t>(by * 8) * pitch + bx0 * 8 + c16;
-      cp_async16(buf + r0 * PS + c16, p + r0 * pitch);
-      cp_async16(buf + (r0 + 4) * PS + c16, p + (r0 + 4) * pitch);
+      if constexpr (ASYNC) {
+        cp_async16(buf + r0 * PS + c16, p + r0 * pitch);
+        cp_async16(buf + (r0 + 4) * PS + c16, p + (r0 + 4) * pitch);
+      } else {
+        pf0 = ldg_stream(p + r0 * pitch);
+        pf1 = ldg_stream(p + (r0 + 4) * pitch);
+      }
     }
-    cp_async_commit();
+    if constexpr (ASYNC) cp_async_commit();
     return ok;
   };
   bool fast = s < nstrips ? fetch(s, pix) : false;  // first strip in flight during the operator copy
@@ -311,7 +319,12 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
   for (; s < nstrips; s += total) {
     int f, by, bx0;
     strip_at(s, f, by, bx0);
-    cp_async_wait_all();
+    if constexpr (ASYNC) {
+      cp_async_wait_all();
+    } else if (fast) {
+      *reinterpret_cast<uint4*>(pix + r0 * PS + c16) = pf0;
+      *reinterpret_cast<uint4*>(pix + (r0 + 4) * PS + c16) = pf1;
+    }
     if (!fast) {
       const uint8_t* ib = in + f * frame_stride;
       for (int e = lane; e < 8 * 128; e += 32) {
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
     pixn = tmp;
     fast = fast_next;
   }
-  cp_async_wait_all();
+  if constexpr (ASYNC) cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -972,8 +985,9 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
 
 dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                               size_t pitch, long long frame_stride, int nframes, double* coef_out,
-                              cudaStream_t st) {
-  auto kernel = coef_out ? k_fused8_sym<true> : k_fused8_sym<false>;
+                              cudaStream_t st, bool host_mapped) {
+  auto kernel = host_mapped ? (coef_out ? k_fused8_sym<true, false> : k_fused8_sym<false, false>)
+                            : (coef_out ? k_fused8_sym<true, true> : k_fused8_sym<false, true>);
   {
     const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(kernel), f8s::SMEM, "k_fused8_sym");
     if (sa != DCTF_OK) return sa;
@@ -1042,12 +1056,13 @@ namespace dctf {
 // filter_image on device buffers, one frame or a strided frame batch.
 dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
-                                cudaStream_t st) {
+                                cudaStream_t st, bool host_mapped) {
   if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT)
     return dctf::launch_fused8_i8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st,
                                   sm_count(p->device));
   const bool split = p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3;
-  if (p->n == 8 && p->sym) return launch_fused8_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+  if (p->n == 8 && p->sym)
+    return launch_fused8_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st, host_mapped);
   if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (p->n == 16 && p->sym && !std::getenv("DCTF_N16_UNFUSED"))
     return launch_fused16_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);

@@ -67,9 +67,10 @@ dctf_status launch_forward_u8(const dctf_plan* p, const uint8_t* img, int w, int
 dctf_status launch_inverse_u8(const dctf_plan* p, const double* coeffs, uint8_t* img, int w, int h,
                               size_t pitch, cudaStream_t st);
 // fused.cu: filter_image on device buffers, one frame or a strided frame batch.
+// host_mapped: `in` is UVA-mapped pinned host memory (zero-copy host entry).
 dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
-                                cudaStream_t st);
+                                cudaStream_t st, bool host_mapped = false);
 void reset_launches();
 
 // Host operator compiler (plan.cc).
