@@ -24,6 +24,7 @@
 
 #include "device.cuh"
 #include "fastdiv.cuh"
+#include "hostpool.h"
 #include "internal.h"
 
 // ---------------------------------------------------------------------------
@@ -634,6 +635,8 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_weights);
     cudaFree(p->io_in);
     cudaFree(p->io_out);
+    p->copy_pool.reset();
+    if (p->bounce) cudaFreeHost(p->bounce);
     for (void* s : p->streams)
       if (s) cudaStreamDestroy(as_stream(s));
     for (void* e : p->events)
@@ -895,7 +898,10 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   //          results to h_out itself (one launch, both link directions busy);
   //   mode 1 "copy-in + zero-copy out": H2D by the copy engine in a few large
   //          chunks, each chunk's kernel writes straight to h_out;
-  //   mode 0 "copy": H2D / compute / D2H in three streams (pageable buffers).
+  //   mode 3 "bounce": pageable buffers — a host thread pool copies row
+  //          chunks into pinned, mapped bounce buffers and back while the
+  //          fused kernel streams the previous chunk over PCIe (zero-copy);
+  //   mode 0 "copy": H2D / compute / D2H in three streams (split precision).
   // DCTF_E2E_MODE overrides the choice (measurement).
   cudaPointerAttributes ai{}, ao{};
   const bool in_pinned = cudaPointerGetAttributes(&ai, h_in) == cudaSuccess &&
@@ -906,10 +912,12 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   // zero-copy needs a single fused kernel (every precision except the
   // split-precision path, which runs forward/filter/inverse as three kernels)
   const bool fused = p->precision != DCTF_PREC_TF32X3 && p->precision != DCTF_PREC_BF16X3;
-  int mode = (in_pinned && out_pinned && fused) ? 2 : (out_pinned && fused ? 1 : 0);
+  int mode = (in_pinned && out_pinned && fused) ? 2 : (fused ? 3 : 0);
   if (const char* env = std::getenv("DCTF_E2E_MODE")) {
     const int m = std::atoi(env);
-    if (m == 0 || (m == 1 && out_pinned && fused) || (m == 2 && in_pinned && out_pinned && fused)) mode = m;
+    if (m == 0 || (m == 1 && out_pinned && fused) || (m == 2 && in_pinned && out_pinned && fused) ||
+        (m == 3 && fused))
+      mode = m;
   }
   if (p->n != 8) CUDA_TRY(cudaMemsetAsync(p->d_nan, 0, sizeof(int), s_run));
   const int n = p->n, bh = (h + n - 1) / n;
@@ -919,6 +927,50 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
                             static_cast<uint8_t*>(ao.devicePointer), w, h, pitch, 0, 1, nullptr,
                             s_run, /*host_mapped=*/true);
     launches = dctf::t_launches;
+  } else if (mode == 3) {
+    // chunks of whole block rows (~2 MiB), double-buffered pinned bounce buffers
+    const int crows = std::max(1, static_cast<int>((size_t(2) << 20) / (dpitch * n))) * n;
+    const size_t chunk_bytes = dpitch * static_cast<size_t>(crows);
+    if (p->bounce_chunk < chunk_bytes) {
+      if (p->bounce) cudaFreeHost(p->bounce);
+      p->bounce = nullptr;
+      p->bounce_chunk = 0;
+      CUDA_TRY(cudaHostAlloc(&p->bounce, 4 * chunk_bytes, cudaHostAllocMapped));
+      p->bounce_chunk = chunk_bytes;
+    }
+    if (!p->copy_pool) {
+      const int nt = static_cast<int>(std::max(1u, std::min(8u, std::thread::hardware_concurrency())));
+      p->copy_pool = std::shared_ptr<void>(new dctf::HostCopyPool(nt),
+                                           [](void* q) { delete static_cast<dctf::HostCopyPool*>(q); });
+    }
+    auto* pool = static_cast<dctf::HostCopyPool*>(p->copy_pool.get());
+    auto* hb = static_cast<uint8_t*>(p->bounce);
+    void* dbv = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(&dbv, p->bounce, 0));
+    auto* db = static_cast<uint8_t*>(dbv);
+    const size_t cb = p->bounce_chunk;
+    cudaEvent_t done[2] = {static_cast<cudaEvent_t>(p->events[0]), static_cast<cudaEvent_t>(p->events[1])};
+    const int nch = (h + crows - 1) / crows;
+    auto drain = [&](int c) {  // chunk c's result: bounce -> user output
+      const int b = c & 1, y0 = c * crows, rows = std::min(crows, h - y0);
+      const cudaError_t e = cudaEventSynchronize(done[b]);
+      if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("bounce drain: ") + cudaGetErrorString(e));
+      pool->copy2d(h_out + y0 * pitch, pitch, hb + (2 + b) * cb, dpitch, w, rows);
+      return DCTF_OK;
+    };
+    for (int c = 0; c < nch && s == DCTF_OK; ++c) {
+      const int b = c & 1, y0 = c * crows, rows = std::min(crows, h - y0);
+      if (c >= 2) CUDA_TRY(cudaEventSynchronize(done[b]));  // chunk c-2 has left both bounce buffers b
+      pool->copy2d(hb + b * cb, dpitch, h_in + y0 * pitch, pitch, w, rows);
+      dctf::reset_launches();
+      s = filter_image_device(p, db + b * cb, db + (2 + b) * cb, w, rows, dpitch, 0, 1, nullptr, s_run,
+                              /*host_mapped=*/true);
+      launches += dctf::t_launches;
+      if (s != DCTF_OK) break;
+      CUDA_TRY(cudaEventRecord(done[b], s_run));
+      if (c >= 1) s = drain(c - 1);  // overlaps chunk c's kernel
+    }
+    if (s == DCTF_OK && nch >= 1) s = drain(nch - 1);
   } else {
     const size_t chunk_target = mode == 1 ? (size_t(4) << 20) : (size_t(2) << 20);
     const int nchunks = std::max(1, std::min(bh, static_cast<int>((static_cast<size_t>(h) * w + chunk_target - 1) / chunk_target)));

@@ -5,6 +5,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -44,6 +45,11 @@ struct dctf_plan {
   mutable size_t io_bytes = 0;
   mutable void* streams[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
   mutable void* events[64] = {};                              // per-chunk ordering
+  // Pageable host buffers: pinned, UVA-mapped bounce buffers (2 input + 2
+  // output chunks) filled / drained by a host thread pool (capi.cu).
+  mutable void* bounce = nullptr;
+  mutable size_t bounce_chunk = 0;
+  mutable std::shared_ptr<void> copy_pool;
 };
 
 namespace dctf {
