@@ -96,13 +96,6 @@ __device__ __forceinline__ uint32_t quantize(double v, int* nan_flag) {
   return static_cast<uint32_t>(r);
 }
 
-// Exact double of an integer 0..255 built with integer ops only, so the FP64
-// pipe stays free for DMMA: 2^e (1 + m) with e = msb(p).
-__device__ __forceinline__ double u8_to_f64(uint32_t p) {
-  const int e = 31 - __clz(p);
-  const uint32_t hi = (static_cast<uint32_t>(1022 + e) << 20) + (p << (20 - e));
-  return p ? __hiloint2double(static_cast<int>(hi), 0) : 0.0;
-}
 
 // floor(t) clamped to [0,255] with a single conversion instruction. Callers
 // pass t = v + 0.5 (the 0.5 rides in the DMMA accumulator), which equals
@@ -144,14 +137,6 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// small signed integer (|v| < 2^20) -> double, exactly, on the integer pipes
-__device__ __forceinline__ double i32_to_f64(int v) {
-  const uint32_t m = static_cast<uint32_t>(v < 0 ? -v : v);
-  const int e = 31 - __clz(m);
-  const uint32_t hi = ((static_cast<uint32_t>(1022 + e) << 20) + (m << (20 - e))) |
-                      (static_cast<uint32_t>(v) & 0x80000000u);
-  return m ? __hiloint2double(static_cast<int>(hi), 0) : 0.0;
-}
 
 // tcgen05 (5th-gen tensor core) ordering fences and MMA completion -> mbarrier
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }

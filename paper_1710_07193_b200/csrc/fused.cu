@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
       const uint32_t q0 = pix[(2 * t) * PS + 8 * b + g];
       const uint32_t q1 = pix[(2 * t + 1) * PS + 8 * b + g];
       *reinterpret_cast<double2*>(xy + b * 512 + t * 128 + ((g ^ (2 * t) ^ fsw(b)) << 4)) =
-          make_double2(u8_to_f64(q0), u8_to_f64(q1));
+          make_double2(__uint2double_rn(q0), __uint2double_rn(q1));
     }
     __syncwarp();
 
@@ -349,10 +349,10 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
         const int p00 = (top.x >> (8 * t)) & 0xff, p01 = (top.y >> (24 - 8 * t)) & 0xff;
         const int p10 = (bot.x >> (8 * t)) & 0xff, p11 = (bot.y >> (24 - 8 * t)) & 0xff;
         const int rs0 = p00 + p10, ra0 = p00 - p10, rs1 = p01 + p11, ra1 = p01 - p11;
-        q[mt][0][sq] = i32_to_f64(rs0 + rs1);
-        q[mt][1][sq] = i32_to_f64(rs0 - rs1);
-        q[mt][2][sq] = i32_to_f64(ra0 + ra1);
-        q[mt][3][sq] = i32_to_f64(ra0 - ra1);
+        q[mt][0][sq] = __int2double_rn(rs0 + rs1);
+        q[mt][1][sq] = __int2double_rn(rs0 - rs1);
+        q[mt][2][sq] = __int2double_rn(ra0 + ra1);
+        q[mt][3][sq] = __int2double_rn(ra0 - ra1);
       }
     }
     // per class: filter Y_c^T = q_c^T G_c^T and inverse Z_c^T = Y_c^T W_c^T
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
         const int wd = lane + 32 * i, v = wd >> 3, a = (wd & 7) ^ (4 * (v & 1));
         const uint32_t q0 = pix[(2 * a) * PS + b * 16 + v];
         const uint32_t q1 = pix[(2 * a + 1) * PS + b * 16 + v];
-        *reinterpret_cast<double2*>(xy + xw(b, wd)) = make_double2(u8_to_f64(q0), u8_to_f64(q1));
+        *reinterpret_cast<double2*>(xy + xw(b, wd)) = make_double2(__uint2double_rn(q0), __uint2double_rn(q1));
       }
     }
     bar_mma();
@@ -854,8 +854,8 @@ __global__ void __launch_bounds__(f16s::WARPS * 32, 1)
         const int pj = (ta >> (8 * e)) & 0xff, pjb = (ba >> (8 * e)) & 0xff;
         const int pm = (tb >> (8 * (1 - e))) & 0xff, pmb = (bb >> (8 * (1 - e))) & 0xff;
         const int rj = pu ? pj - pjb : pj + pjb, rm = pu ? pm - pmb : pm + pmb;
-        q[0][i][e] = i32_to_f64(rj + rm);
-        q[1][i][e] = i32_to_f64(rj - rm);
+        q[0][i][e] = __int2double_rn(rj + rm);
+        q[1][i][e] = __int2double_rn(rj - rm);
       }
     }
 
