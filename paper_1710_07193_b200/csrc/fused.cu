@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
   const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
   const int r0 = lane >> 3, c16 = (lane & 7) * 16;
+  const uint32_t selL = 0x4440u + t, selR = 0x4440u + (3 - t);  // __byte_perm selectors
 
   int s = static_cast<int>(blockIdx.x) * nwarps + warp;
   const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
@@ -346,8 +347,9 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
       for (int sq = 0; sq < 4; ++sq) {
         const uint2 top = *reinterpret_cast<const uint2*>(pb + sq * PS);
         const uint2 bot = *reinterpret_cast<const uint2*>(pb + (7 - sq) * PS);
-        const int p00 = (top.x >> (8 * t)) & 0xff, p01 = (top.y >> (24 - 8 * t)) & 0xff;
-        const int p10 = (bot.x >> (8 * t)) & 0xff, p11 = (bot.y >> (24 - 8 * t)) & 0xff;
+        // byte t of the left half, byte 3-t of the right half (one PRMT each)
+        const int p00 = __byte_perm(top.x, 0, selL), p01 = __byte_perm(top.y, 0, selR);
+        const int p10 = __byte_perm(bot.x, 0, selL), p11 = __byte_perm(bot.y, 0, selR);
         const int rs0 = p00 + p10, ra0 = p00 - p10, rs1 = p01 + p11, ra1 = p01 - p11;
         q[mt][0][sq] = __int2double_rn(rs0 + rs1);
         q[mt][1][sq] = __int2double_rn(rs0 - rs1);
