@@ -97,15 +97,13 @@ __device__ __forceinline__ uint32_t quantize(double v, int* nan_flag) {
 }
 
 
-// floor(t) clamped to [0,255] with a single conversion instruction. Callers
-// pass t = v + 0.5 (the 0.5 rides in the DMMA accumulator), which equals
-// quantize_sample's round-half-away-from-zero + clamp for every v except
-// within one ulp of a .5 boundary — inside the 1e-6 near-tie window the
-// parity contract excuses. NaN converts to 0.
+// floor(t) clamped to [0, 255] in one conversion: cvt.rmi.u8.f64 saturates to
+// the destination range (SASS F2I.U8.F64.FLOOR), so the reference's
+// round-half-away + clamp of t - 0.5 is a single instruction.
 __device__ __forceinline__ uint32_t floor_to_u8(double t) {
-  int i;
-  asm("cvt.rmi.s32.f64 %0, %1;" : "=r"(i) : "d"(t));
-  return static_cast<uint32_t>(min(max(i, 0), 255));
+  unsigned short u;
+  asm("cvt.rmi.u8.f64 %0, %1;" : "=h"(u) : "d"(t));
+  return u;
 }
 
 // Aligns a dynamic shared-memory base to 1024 B (128B-swizzle atoms) while
