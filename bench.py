@@ -568,9 +568,9 @@ def main():
                "cfg5_video": cfg5,
                "n16_coef_fp64": coefline(plan16.coef_kernel, ms_c16, 262144, 256, "fp64"),
                "n16_coef_fp64_dense": coefline(plan16d.coef_kernel, ms_c16d, 262144, 256, "fp64"),
-               "n16_coef_tf32x3": coefline("k_coef_tf32x3<256>", ms_t16, 262144, 256, "3xtf32", err_t16),
+               "n16_coef_tf32x3": coefline(plan16t.coef_kernel, ms_t16, 262144, 256, "3xtf32", err_t16),
                "n16_coef_bf16x3": coefline(plan16b.coef_kernel, ms_b16, 262144, 256, "3xbf16", err_b16),
-               "n8_coef_tf32x3": coefline("k_coef_tf32x3<64>", ms_t8, NBLOCKS, 64, "3xtf32", err_t8),
+               "n8_coef_tf32x3": coefline(plan8t.coef_kernel, ms_t8, NBLOCKS, 64, "3xtf32", err_t8),
                "n16_fused": {
             "kernel": plan16.image_kernel, "workload": "config4: 8192x8192 U(4), 16x16 blocks, "
             "gaussian 7x7 sigma=2, replicate, FP64", "blocks_per_s": nb16 / (ms16 / 1e3), "ms": ms16,
