@@ -564,7 +564,31 @@ def main():
                 "blocks_per_s": nb5 / (ms5 / 1e3),
                 "kernels": [pl.image_kernel for pl in plans5]}
         del frames5
+        # config 3: 8192^2 U(3), random asymmetric 3x3 (dense operator), zero and
+        # replicate padding, fused u8 FP64 (1,048,576 blocks per launch)
+        img3 = torch.from_numpy(synth.uniform_image(3, 8192, 8192)).cuda()
+        out3 = torch.empty_like(img3)
+        r3, _ = synth.random_mask(1003, 3)
+        cfg3 = {"workload": "config3: 8192x8192 U(3), random asymmetric 3x3, FP64, fused u8",
+                "blocks": 1048576}
+        for padname, pad in (("zero", P.PaddingMode.kZero), ("replicate", P.PaddingMode.kReplicate)):
+            pl3 = P.FilterPlan(P.Mask(3, r3), N, pad)
+            ev3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(10)]
+            for i in range(13):
+                flush.fill_(6)
+                if i >= 3:
+                    ev3[i - 3][0].record(stream)
+                _lib.check(lib.dctf_filter_image_u8(pl3.handle, img3.data_ptr(), out3.data_ptr(), 8192,
+                                                    8192, 8192, None, sp))
+                if i >= 3:
+                    ev3[i - 3][1].record(stream)
+            torch.cuda.synchronize()
+            ms3 = statistics.mean(a.elapsed_time(b) for a, b in ev3)
+            cfg3[padname] = {"kernel": pl3.image_kernel, "ms": ms3, "blocks_per_s": 1048576 / (ms3 / 1e3)}
+        del img3, out3
         aux = {"n8_fused_dense": dense8, "n8_fused_int8exact": int8exact, "cfg1_graph": cfg1,
+               "cfg3_asymmetric": cfg3,
                "cfg5_video": cfg5,
                "n16_coef_fp64": coefline(plan16.coef_kernel, ms_c16, 262144, 256, "fp64"),
                "n16_coef_fp64_dense": coefline(plan16d.coef_kernel, ms_c16d, 262144, 256, "fp64"),
