@@ -56,11 +56,8 @@ __global__ void __launch_bounds__(c8::WARPS * 32, 1)
     for (int i = 0; i < WARPS * STAGES; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
-  {
-    const double2* src = reinterpret_cast<const double2*>(hc);
-    double2* dst = reinterpret_cast<double2*>(base);
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) dst[i] = src[i];
-  }
+  cta_copy_async(base, hc, 32768);
+  cp_async_wait_all();
   __syncthreads();
 
   const long long ntiles = (nblocks + TILE - 1) / TILE;
@@ -176,11 +173,8 @@ __global__ void __launch_bounds__(c8s::WARPS * 32, 1)
     for (int i = 0; i < WARPS * STAGES; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
-  {
-    const double2* src = reinterpret_cast<const double2*>(hc);
-    double2* dst = reinterpret_cast<double2*>(base);
-    for (int i = threadIdx.x; i < 512; i += blockDim.x) dst[i] = src[i];
-  }
+  cta_copy_async(base, hc, 8192);
+  cp_async_wait_all();
   __syncthreads();
 
   const long long ntiles = (nblocks + TILE - 1) / TILE;
@@ -322,11 +316,8 @@ __global__ void __launch_bounds__(c16s::WARPS * 32, 1)
     for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
-  {
-    const double2* src = reinterpret_cast<const double2*>(hc);
-    double2* dst = reinterpret_cast<double2*>(base);
-    for (int i = threadIdx.x; i < HBYTES / 16; i += blockDim.x) dst[i] = src[i];
-  }
+  cta_copy_async(base, hc, HBYTES);
+  cp_async_wait_all();
   __syncthreads();
 
   const long long ntiles = (nblocks + TILE - 1) / TILE;

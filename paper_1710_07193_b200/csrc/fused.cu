@@ -103,11 +103,8 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
     }
   };
   if (s < nstrips) prefetch(s);  // first strip's pixels in flight during the operator copy
-  {
-    const double2* src = reinterpret_cast<const double2*>(hf);
-    double2* dst = reinterpret_cast<double2*>(smem);
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) dst[i] = src[i];
-  }
+  cta_copy_async(smem, hf, 32768);
+  cp_async_wait_all();
   __syncthreads();
 
   for (; s < nstrips; s += total) {
@@ -310,11 +307,8 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
     return ok;
   };
   bool fast = s < nstrips ? fetch(s, pix) : false;  // first strip in flight during the operator copy
-  {
-    const double2* src = reinterpret_cast<const double2*>(hsym);
-    double2* dst = reinterpret_cast<double2*>(smem);
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) dst[i] = src[i];
-  }
+  cta_copy_async(smem, hsym, 16384);
+  cp_async_wait_all();
   __syncthreads();
 
   for (; s < nstrips; s += total) {
@@ -804,13 +798,9 @@ __global__ void __launch_bounds__(f16s::WARPS * 32, 1)
   };
   long long tile = static_cast<long long>(blockIdx.x) * PAIRS + pair;
   if (tile < ntiles) prefetch(tile);
-  {
-    const double2* src = reinterpret_cast<const double2*>(gsym);
-    double2* dst = reinterpret_cast<double2*>(smem);
-    for (int i = threadIdx.x; i < GBYTES / 16; i += blockDim.x) dst[i] = src[i];
-    double* cdst = reinterpret_cast<double*>(smem + GBYTES);
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) cdst[i] = basis[i];
-  }
+  cta_copy_async(smem, gsym, GBYTES);
+  cta_copy_async(smem + GBYTES, basis, CBYTES);
+  cp_async_wait_all();
   __syncthreads();
   // first inverse pass B fragments: C[2(2t + e) + pv][g], per class parity pv
   double cb[2][2];

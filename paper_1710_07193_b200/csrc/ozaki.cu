@@ -118,12 +118,8 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   __shared__ double sc_s[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(gimg);
-    uint4* dst = reinterpret_cast<uint4*>(bsm);
-    for (int i = threadIdx.x; i < BBYTES / 16; i += blockDim.x) dst[i] = src[i];
-    if (threadIdx.x < 64) sc_s[threadIdx.x] = gscale[threadIdx.x];
-  }
+  cta_copy_async(bsm, gimg, BBYTES);
+  if (threadIdx.x < 64) sc_s[threadIdx.x] = gscale[threadIdx.x];
   if (warp == PROD) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_s)),
@@ -143,6 +139,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  cp_async_wait_all();
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
