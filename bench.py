@@ -26,6 +26,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -208,6 +210,250 @@ def run_reference_arm(args, rank):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# auxiliary measurements (bench line "aux"): each function times one kernel
+# family on its BASELINE config with the same protocol as the headline
+# (device-resident inputs, L2 flushed before every launch, untimed).
+class AuxContext:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def timed_ms(c, launch, reps, warm=3):
+    """Mean device time (ms) of launch() over reps launches, L2 flushed before each."""
+    torch = c.torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    for i in range(reps + warm):
+        c.flush.fill_(i & 0xFF)
+        if i >= warm:
+            evs[i - warm][0].record(c.stream)
+        launch()
+        if i >= warm:
+            evs[i - warm][1].record(c.stream)
+    torch.cuda.synchronize()
+    return statistics.mean(a.elapsed_time(b) for a, b in evs)
+
+
+def image_launcher(c, pl, img, out, w, h):
+    return lambda: c.check(c.lib.dctf_filter_image_u8(pl.handle, img.data_ptr(), out.data_ptr(),
+                                                         w, h, w, None, c.sp))
+
+
+def coef_launcher(c, pl, x, y, nb):
+    return lambda: c.check(c.lib.dctf_filter_coeffs(pl.handle, x.data_ptr(), y.data_ptr(), nb,
+                                                       c.sp))
+
+
+def coefline(c, kernel, ms, nbk, nn, prec, err=None):
+    gbs = nbk * 16 * nn / (ms / 1e3) / 1e9
+    d = {"kernel": kernel, "precision": prec, "blocks_per_s": nbk / (ms / 1e3), "ms": ms,
+         "gb_per_s": gbs, "hbm_frac": gbs / (c.hbm_peak or 1.0),
+         "fp64_tflops_dense_count": 2 * nn * nn * nbk / (ms / 1e3) / 1e12}
+    if err is not None:
+        d["max_rel_err_vs_fp64"] = err
+    return d
+
+
+def aux_image8_variants(c):
+    """Config 2 image through the dense FP64 and the exact-INT8 kernels."""
+    P, torch = c.P, c.torch
+    out = {}
+    pd = P.FilterPlan(P.Mask(5, c.mask), N, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dense)
+    od = torch.empty_like(c.d_in)
+    msd = timed_ms(c, image_launcher(c, pd, c.d_in, od, W, H), 50)
+    out["n8_fused_dense"] = {
+        "kernel": pd.image_kernel, "precision": "fp64 (DCTF_PREC_FP64_DENSE)",
+        "blocks_per_s": NBLOCKS / (msd / 1e3), "ms": msd,
+        "u8_identical_to_headline": bool(torch.equal(od, c.d_out)),
+        "frac_dense_count": FLOP_PER_BLOCK_FUSED * NBLOCKS / (msd / 1e3) / 1e12 / c.peak_dmma,
+        "pipe_frac": PIPE_FLOP_PER_BLOCK["k_fused8"] * NBLOCKS / (msd / 1e3) / 1e12 / c.peak_dmma}
+    px = P.FilterPlan(P.Mask(5, c.mask), N, P.PaddingMode.kReplicate, precision=P.Precision.kInt8Exact)
+    ox = torch.empty_like(c.d_in)
+    msx = timed_ms(c, image_launcher(c, px, c.d_in, ox, W, H), 50)
+    out["n8_fused_int8exact"] = {
+        "kernel": "k_fused8_i8 (tcgen05 kind::i8 + DMMA inverse)", "precision": "int8-exact",
+        "blocks_per_s": NBLOCKS / (msx / 1e3), "ms": msx,
+        "speedup_vs_fp64_dmma": c.ms / msx, "u8_identical_to_fp64_path": bool(torch.equal(ox, c.d_out)),
+        "fp64_pipe_flop_per_block": 2 * (1024 + 128),
+        "fp64_pipe_frac": 2 * (1024 + 128) * NBLOCKS / (msx / 1e3) / 1e12 / c.peak_dmma,
+        "int8_macs_per_block": 7 * 64 * 64}
+    return out
+
+
+def aux_cfg1(c):
+    """Config 1 (512^2 U(1), average3, zero, coef dump + u8): 4,096 blocks, so
+    one eager call is launch bound; CUDA graph replay of 20 captured calls."""
+    P, torch, synth = c.P, c.torch, c.synth
+    img = torch.from_numpy(synth.uniform_image(1, 512, 512)).cuda()
+    out = torch.empty_like(img)
+    coef = torch.empty((4096, 8, 8), dtype=torch.float64, device="cuda")
+    pl = P.FilterPlan(P.Mask(3, np.full(9, 1.0 / 9.0)), 8, P.PaddingMode.kZero)
+
+    def call():
+        c.check(c.lib.dctf_filter_image_u8(pl.handle, img.data_ptr(), out.data_ptr(), 512, 512, 512,
+                                              coef.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(200):
+        call()
+    b.record()
+    torch.cuda.synchronize()
+    eager_us = a.elapsed_time(b) * 1e3 / 200
+    gs = torch.cuda.Stream()
+    gs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(gs):
+        call()
+    torch.cuda.current_stream().wait_stream(gs)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(20):
+            call()
+    g.replay()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(10):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    graph_us = a.elapsed_time(b) * 1e3 / 200
+    return {"kernel": pl.image_kernel + " (coef dump on)", "workload": "config1: 512x512 U(1), "
+            "average3, zero padding, FP64, u8 out + FP64 coefficients out", "blocks": 4096,
+            "eager_us_per_call": eager_us, "graph_us_per_call": graph_us,
+            "graph": "20 calls captured per CUDA graph", "blocks_per_s_graph": 4096 / (graph_us / 1e6)}
+
+
+def aux_cfg3(c):
+    """Config 3: 8192^2 U(3), random asymmetric 3x3 (dense operator), zero and
+    replicate padding, fused u8 FP64 (1,048,576 blocks per launch)."""
+    P, torch, synth = c.P, c.torch, c.synth
+    img = torch.from_numpy(synth.uniform_image(3, 8192, 8192)).cuda()
+    out = torch.empty_like(img)
+    r3, _ = synth.random_mask(1003, 3)
+    res = {"workload": "config3: 8192x8192 U(3), random asymmetric 3x3, FP64, fused u8", "blocks": 1048576}
+    for name, pad in (("zero", P.PaddingMode.kZero), ("replicate", P.PaddingMode.kReplicate)):
+        pl = P.FilterPlan(P.Mask(3, r3), N, pad)
+        ms = timed_ms(c, image_launcher(c, pl, img, out, 8192, 8192), 10)
+        res[name] = {"kernel": pl.image_kernel, "ms": ms, "blocks_per_s": 1048576 / (ms / 1e3)}
+    return res
+
+
+def aux_cfg5(c):
+    """Config 5: 64 frames of 3840x2160, 4 masks round-robin (Laplacian,
+    Gaussian 5x5, 1x9 motion blur on 8x8 blocks, random asymmetric 5x5), one
+    batched dctf_filter_frames_u8 call = one GPU's whole share at N=1 (8 unique
+    S(f) frames generated on the host, tiled to 64 on the device; 531 MB >> L2)."""
+    P, torch, synth = c.P, c.torch, c.synth
+    FW, FH, FF = 3840, 2160, 64
+    rnd5, _ = synth.random_mask(1005, 5)
+    masks = [(synth.LAPLACIAN3, 3, 3), (synth.gaussian_mask(5, 1.0), 5, 5), (synth.MOTION_1x9, 1, 9),
+             (rnd5, 5, 5)]
+    plans = [P.FilterPlan(P.Mask(k, w) if k == kc else P.Mask.rect(k, kc, w), 8, P.PaddingMode.kReplicate)
+             for w, k, kc in masks]
+    uniq = np.stack([synth.sinusoid_image(f, FW, FH) for f in range(8)])
+    frames = torch.from_numpy(uniq).cuda().repeat(FF // 8, 1, 1).contiguous()
+    idx = [f % 4 for f in range(FF)]
+    P.filter_frames(frames, plans, idx)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(5):
+        a.record()
+        out = P.filter_frames(frames, plans, idx)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+        del out
+    ms = statistics.median(ts)
+    nb = FF * (FW // 8) * (FH // 8)
+    return {"workload": "config5: 64 x 3840x2160 S(f) frames, masks f mod 4 = Laplacian 3x3, Gaussian "
+            "5x5 s=1, 1x9 motion blur, random asymmetric 5x5; replicate; FP64; one "
+            "dctf_filter_frames_u8 call", "blocks": nb, "ms": ms, "blocks_per_s": nb / (ms / 1e3),
+            "kernels": [pl.image_kernel for pl in plans]}
+
+
+def aux_n16(c):
+    """Config 4 shapes (8192^2 U(4), 16x16 blocks, Gaussian 7x7 sigma 2): the
+    fused image path (parity-class vs dense) and the coefficient path (FP64
+    parity-class / dense, 3xTF32, 3xBF16)."""
+    P, torch, synth = c.P, c.torch, c.synth
+    g7 = synth.gaussian_mask(7, 2.0)
+
+    def plan16(prec=P.Precision.kFp64):
+        return P.FilterPlan(P.Mask(7, g7), 16, P.PaddingMode.kReplicate, precision=prec)
+    img = torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda()
+    out = torch.empty_like(img)
+    ps, pd = plan16(), plan16(P.Precision.kFp64Dense)
+    ms_s = timed_ms(c, image_launcher(c, ps, img, out, 8192, 8192), 10)
+    out_s = out.clone()
+    ms_d = timed_ms(c, image_launcher(c, pd, img, out, 8192, 8192), 10)
+    same = bool(torch.equal(out_s, out))
+    nb, flop = 262144, 2 * 16 ** 4 + 8 * 16 ** 3
+    # executed FP64 flop per block: k_fused16 = G p + inverse; k_fused16_sym =
+    # 4 classes x (64x64 filter + 8x8 first inverse pass) DMMA + 4 x 512 DFMA
+    pipe_of = {"k_fused16": 2 * 16 ** 4 + 4 * 16 ** 3, "k_fused16_sym": 72 * 512 + 4 * 512 * 2}
+    pipe = pipe_of[ps.image_kernel]
+    res = {"n16_fused": {
+        "kernel": ps.image_kernel, "workload": "config4: 8192x8192 U(4), 16x16 blocks, gaussian 7x7 "
+        "sigma=2, replicate, FP64", "blocks_per_s": nb / (ms_s / 1e3), "ms": ms_s,
+        "fp64_tflops_dense_count": flop * nb / (ms_s / 1e3) / 1e12,
+        "frac_dense_count": flop * nb / (ms_s / 1e3) / 1e12 / c.peak_dmma,
+        "pipe_flop_per_block": pipe, "pipe_frac": pipe * nb / (ms_s / 1e3) / 1e12 / c.peak_dmma,
+        "dense_kernel": pd.image_kernel, "dense_blocks_per_s": nb / (ms_d / 1e3),
+        "dense_pipe_frac": pipe_of["k_fused16"] * nb / (ms_d / 1e3) / 1e12 / c.peak_dmma,
+        "u8_identical_to_dense": same}}
+    del img, out, out_s
+    x = ps.forward_image(torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda())
+    y = torch.empty_like(x)
+    ms_c = timed_ms(c, coef_launcher(c, ps, x, y, nb), 10)
+    ref = y.clone()
+    res["n16_coef_fp64"] = coefline(c, ps.coef_kernel, ms_c, nb, 256, "fp64")
+    ms_cd = timed_ms(c, coef_launcher(c, pd, x, y, nb), 10)
+    res["n16_coef_fp64_dense"] = coefline(c, pd.coef_kernel, ms_cd, nb, 256, "fp64")
+    for key, prec, tag in (("n16_coef_tf32x3", P.Precision.kTf32x3, "3xtf32"),
+                           ("n16_coef_bf16x3", P.Precision.kBf16x3, "3xbf16")):
+        pl = plan16(prec)
+        msp = timed_ms(c, coef_launcher(c, pl, x, y, nb), 10)
+        err = float((y - ref).abs().max() / ref.abs().max())
+        res[key] = coefline(c, pl.coef_kernel, msp, nb, 256, tag, err)
+    return res
+
+
+def aux_coef8(c):
+    """Config 2's coefficient path (forward once, then filter_coeffs timed):
+    parity-class, dense and 3xTF32 (the last reported under n8_coef_tf32x3)."""
+    P, torch = c.P, c.torch
+    coeffs = c.plan.forward_image(c.d_in)
+    y = torch.empty_like(coeffs)
+    ka = max(3, min(c.steps, 200))
+    ms_c = timed_ms(c, coef_launcher(c, c.plan, coeffs, y, NBLOCKS), ka)
+    pd = P.FilterPlan(P.Mask(5, c.mask), N, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dense)
+    ms_cd = timed_ms(c, coef_launcher(c, pd, coeffs, y, NBLOCKS), ka)
+    hbm = c.hbm_peak
+    return {
+        "kernel": c.plan.coef_kernel, "blocks_per_s": NBLOCKS / (ms_c / 1e3), "ms": ms_c,
+        "gb_per_s": NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9,
+        "hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9) / hbm if hbm else None,
+        "fp64_tflops_dense_count": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_c / 1e3) / 1e12,
+        "dense_kernel": pd.coef_kernel, "dense_blocks_per_s": NBLOCKS / (ms_cd / 1e3),
+        "dense_fp64_frac": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_cd / 1e3) / 1e12 / c.peak_dmma,
+        "dense_hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_cd / 1e3) / 1e9) / hbm if hbm else None}
+
+
+def aux_coef8_tf32(c):
+    P, torch = c.P, c.torch
+    coeffs = c.plan.forward_image(c.d_in)
+    y = torch.empty_like(coeffs)
+    pl = P.FilterPlan(P.Mask(5, c.mask), N, P.PaddingMode.kReplicate, precision=P.Precision.kTf32x3)
+    ms = timed_ms(c, coef_launcher(c, pl, coeffs, y, NBLOCKS), 50)
+    ref = c.plan.filter_coeffs(coeffs)
+    err = float((y - ref).abs().max() / ref.abs().max())
+    return coefline(c, pl.coef_kernel, ms, NBLOCKS, 64, "3xtf32", err)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -348,273 +594,20 @@ def main():
                "pageable_api": "the same call on pageable numpy buffers (pinned bounce buffers "
                                "filled/drained by host threads, overlapped with the kernel)"}
 
-    # auxiliary: the coefficient path on the same config (forward once,
-    # then filter_coeffs timed), FP64 in/out through HBM
+    # auxiliary measurements: the other kernels and BASELINE configs (aux_*)
     aux = None
     if not args.no_aux:
-        coeffs = plan.forward_image(d_in)
-        y = torch.empty_like(coeffs)
-        ka = max(3, min(args.steps, 200))
-
-        def time_coeffs(pl):
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                  for _ in range(ka)]
-            for i in range(ka + 3):
-                flush.fill_(2)
-                if i >= 3:
-                    ev[i - 3][0].record(stream)
-                _lib.check(lib.dctf_filter_coeffs(pl.handle, coeffs.data_ptr(), y.data_ptr(),
-                                                  NBLOCKS, sp))
-                if i >= 3:
-                    ev[i - 3][1].record(stream)
-            torch.cuda.synchronize()
-            return statistics.mean(a.elapsed_time(b) for a, b in ev)
-        ms_c = time_coeffs(plan)
-        plan_cd = P.FilterPlan(P.Mask(5, mask), N, P.PaddingMode.kReplicate,
-                               precision=P.Precision.kFp64Dense)
-        ms_cd = time_coeffs(plan_cd)
-        # n = 16 fused path on BASELINE config 4 (8192^2 U(4), gaussian 7x7 s=2)
-        img16 = torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda()
-        out16 = torch.empty_like(img16)
-        plan16 = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate)
-        plan16fd = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate,
-                                precision=P.Precision.kFp64Dense)
-
-        def time_image16(pl):
-            ev16 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                    for _ in range(10)]
-            for i in range(13):
-                flush.fill_(3)
-                if i >= 3:
-                    ev16[i - 3][0].record(stream)
-                _lib.check(lib.dctf_filter_image_u8(pl.handle, img16.data_ptr(), out16.data_ptr(),
-                                                    8192, 8192, 8192, None, sp))
-                if i >= 3:
-                    ev16[i - 3][1].record(stream)
-            torch.cuda.synchronize()
-            return statistics.mean(a.elapsed_time(b) for a, b in ev16)
-        ms16 = time_image16(plan16)
-        out16s = out16.clone()
-        ms16d = time_image16(plan16fd)
-        same16 = bool(torch.equal(out16s, out16))
-        del out16s
-        nb16, flop16 = 262144, 2 * 16 ** 4 + 8 * 16 ** 3
-        # executed FP64 flop per block: k_fused16 = G p + inverse; k_fused16_sym =
-        # 4 classes x (64x64 filter + 8x8 first inverse pass) DMMA + 4 x 512 DFMA
-        pipe_of = {"k_fused16": 2 * 16 ** 4 + 4 * 16 ** 3, "k_fused16_sym": 72 * 512 + 4 * 512 * 2}
-        pipe16 = pipe_of[plan16.image_kernel]
-        del img16, out16
-        # coefficient path at n = 16 (config 4 shapes): FP64 DMMA vs 3xTF32 tcgen05
-        x16 = plan16.forward_image(torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda())
-        y16 = torch.empty_like(x16)
-        plan16t = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate,
-                               precision=P.Precision.kTf32x3)
-
-        def time_coef(pl, xx, yy, nbk, reps=10):
-            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(reps)]
-            for i in range(reps + 3):
-                flush.fill_(4)
-                if i >= 3:
-                    evs[i - 3][0].record(stream)
-                _lib.check(lib.dctf_filter_coeffs(pl.handle, xx.data_ptr(), yy.data_ptr(), nbk, sp))
-                if i >= 3:
-                    evs[i - 3][1].record(stream)
-            torch.cuda.synchronize()
-            return statistics.mean(a.elapsed_time(b) for a, b in evs)
-        ms_c16 = time_coef(plan16, x16, y16, 262144)
-        ref16 = y16.clone()
-        plan16d = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate,
-                               precision=P.Precision.kFp64Dense)
-        ms_c16d = time_coef(plan16d, x16, y16, 262144)
-        ms_t16 = time_coef(plan16t, x16, y16, 262144)
-        err_t16 = float((y16 - ref16).abs().max() / ref16.abs().max())
-        plan16b = P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate,
-                               precision=P.Precision.kBf16x3)
-        ms_b16 = time_coef(plan16b, x16, y16, 262144)
-        err_b16 = float((y16 - ref16).abs().max() / ref16.abs().max())
-        y8t = torch.empty((NBLOCKS, 8, 8), dtype=torch.float64, device="cuda")
-        plan8t = P.FilterPlan(P.Mask(5, mask), N, P.PaddingMode.kReplicate, precision=P.Precision.kTf32x3)
-        coeffs8 = plan.forward_image(d_in)
-        ms_t8 = time_coef(plan8t, coeffs8, y8t, NBLOCKS, reps=50)
-        y8r = plan.filter_coeffs(coeffs8)
-        err_t8 = float((y8t - y8r).abs().max() / y8r.abs().max())
-        del x16, y16, ref16
-        hbm = hbm_peak or 1.0
-
-        def coefline(kernel, ms, nbk, nn, prec, err=None):
-            gbs_c = nbk * 16 * nn / (ms / 1e3) / 1e9
-            d = {"kernel": kernel, "precision": prec, "blocks_per_s": nbk / (ms / 1e3), "ms": ms,
-                 "gb_per_s": gbs_c, "hbm_frac": gbs_c / hbm,
-                 "fp64_tflops_dense_count": 2 * nn * nn * nbk / (ms / 1e3) / 1e12}
-            if err is not None:
-                d["max_rel_err_vs_fp64"] = err
-            return d
-        def time_image(pl, out_t, reps=50):
-            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(reps)]
-            for i in range(reps + 3):
-                flush.fill_(5)
-                if i >= 3:
-                    evs[i - 3][0].record(stream)
-                _lib.check(lib.dctf_filter_image_u8(pl.handle, d_in.data_ptr(), out_t.data_ptr(), W,
-                                                    H, W, None, sp))
-                if i >= 3:
-                    evs[i - 3][1].record(stream)
-            torch.cuda.synchronize()
-            return statistics.mean(a.elapsed_time(b) for a, b in evs)
-        # exact INT8 tensor-core fused path on the same config-2 image
-        plan8x = P.FilterPlan(P.Mask(5, mask), N, P.PaddingMode.kReplicate,
-                              precision=P.Precision.kInt8Exact)
-        out8 = torch.empty_like(d_in)
-        ms8x = time_image(plan8x, out8)
-        # the dense FP64 kernel on the same image (structure not exploited)
-        plan8d = P.FilterPlan(P.Mask(5, mask), N, P.PaddingMode.kReplicate,
-                              precision=P.Precision.kFp64Dense)
-        out8d = torch.empty_like(d_in)
-        ms8d = time_image(plan8d, out8d)
-        dense8 = {"kernel": plan8d.image_kernel, "precision": "fp64 (DCTF_PREC_FP64_DENSE)",
-                  "blocks_per_s": NBLOCKS / (ms8d / 1e3), "ms": ms8d,
-                  "u8_identical_to_headline": bool(torch.equal(out8d, d_out)),
-                  "frac_dense_count": FLOP_PER_BLOCK_FUSED * NBLOCKS / (ms8d / 1e3) / 1e12 / peak_dmma,
-                  "pipe_frac": PIPE_FLOP_PER_BLOCK["k_fused8"] * NBLOCKS / (ms8d / 1e3) / 1e12
-                  / peak_dmma}
-        same8x = bool(torch.equal(out8, d_out))
-        int8exact = {
-            "kernel": "k_fused8_i8 (tcgen05 kind::i8 + DMMA inverse)", "precision": "int8-exact",
-            "blocks_per_s": NBLOCKS / (ms8x / 1e3), "ms": ms8x,
-            "speedup_vs_fp64_dmma": ms / ms8x, "u8_identical_to_fp64_path": same8x,
-            "fp64_pipe_flop_per_block": 2 * (1024 + 128),
-            "fp64_pipe_frac": 2 * (1024 + 128) * NBLOCKS / (ms8x / 1e3) / 1e12 / peak_dmma,
-            "int8_macs_per_block": 7 * 64 * 64}
-        # config 1 (512^2 U(1), average3, zero, coef dump + u8): 4,096 blocks, so
-        # one eager call is launch bound; CUDA graph replay of 20 captured calls
-        img1 = torch.from_numpy(synth.uniform_image(1, 512, 512)).cuda()
-        out1 = torch.empty_like(img1)
-        coef1 = torch.empty((4096, 8, 8), dtype=torch.float64, device="cuda")
-        plan1 = P.FilterPlan(P.Mask(3, np.full(9, 1.0 / 9.0)), 8, P.PaddingMode.kZero)
-
-        def call1():
-            _lib.check(lib.dctf_filter_image_u8(plan1.handle, img1.data_ptr(), out1.data_ptr(),
-                                                512, 512, 512, coef1.data_ptr(),
-                                                torch.cuda.current_stream().cuda_stream))
-        for _ in range(3):
-            call1()
-        torch.cuda.synchronize()
-        a1, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a1.record()
-        for _ in range(200):
-            call1()
-        b1.record()
-        torch.cuda.synchronize()
-        eager1_us = a1.elapsed_time(b1) * 1e3 / 200
-        gs = torch.cuda.Stream()
-        gs.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(gs):
-            call1()
-        torch.cuda.current_stream().wait_stream(gs)
-        g1 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g1):
-            for _ in range(20):
-                call1()
-        g1.replay()
-        torch.cuda.synchronize()
-        a1.record()
-        for _ in range(10):
-            g1.replay()
-        b1.record()
-        torch.cuda.synchronize()
-        graph1_us = a1.elapsed_time(b1) * 1e3 / 200
-        cfg1 = {"kernel": plan1.image_kernel + " (coef dump on)", "workload": "config1: 512x512 U(1), "
-                "average3, zero padding, FP64, u8 out + FP64 coefficients out",
-                "blocks": 4096, "eager_us_per_call": eager1_us,
-                "graph_us_per_call": graph1_us, "graph": "20 calls captured per CUDA graph",
-                "blocks_per_s_graph": 4096 / (graph1_us / 1e6)}
-        del g1
-        # config 5: 64 frames of 3840x2160, 4 masks round-robin (Laplacian, Gaussian
-        # 5x5, 1x9 motion blur on 8x8 blocks, random asymmetric 5x5), one batched
-        # dctf_filter_frames_u8 call = one GPU's whole share at N=1 (8 unique
-        # S(f) frames generated on the host, tiled to 64 on the device)
-        FW, FH, FF = 3840, 2160, 64
-        rnd5, _ = synth.random_mask(1005, 5)
-        m5 = [(synth.LAPLACIAN3, 3, 3), (synth.gaussian_mask(5, 1.0), 5, 5), (synth.MOTION_1x9, 1, 9),
-              (rnd5, 5, 5)]
-        plans5 = [P.FilterPlan(P.Mask(k, w) if k == kc else P.Mask.rect(k, kc, w), 8,
-                               P.PaddingMode.kReplicate) for w, k, kc in m5]
-        uniq = np.stack([synth.sinusoid_image(f, FW, FH) for f in range(8)])
-        frames5 = torch.from_numpy(uniq).cuda().repeat(FF // 8, 1, 1).contiguous()
-        del uniq
-        idx5 = [f % 4 for f in range(FF)]
-        P.filter_frames(frames5, plans5, idx5)
-        torch.cuda.synchronize()
-        a5, b5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t5 = []
-        for _ in range(5):
-            a5.record()
-            out5 = P.filter_frames(frames5, plans5, idx5)
-            b5.record()
-            torch.cuda.synchronize()
-            t5.append(a5.elapsed_time(b5))
-            del out5
-        ms5 = statistics.median(t5)
-        nb5 = FF * (FW // 8) * (FH // 8)
-        cfg5 = {"workload": "config5: 64 x 3840x2160 S(f) frames, masks f mod 4 = Laplacian 3x3, "
-                "Gaussian 5x5 s=1, 1x9 motion blur, random asymmetric 5x5; replicate; FP64; one "
-                "dctf_filter_frames_u8 call", "blocks": nb5, "ms": ms5,
-                "blocks_per_s": nb5 / (ms5 / 1e3),
-                "kernels": [pl.image_kernel for pl in plans5]}
-        del frames5
-        # config 3: 8192^2 U(3), random asymmetric 3x3 (dense operator), zero and
-        # replicate padding, fused u8 FP64 (1,048,576 blocks per launch)
-        img3 = torch.from_numpy(synth.uniform_image(3, 8192, 8192)).cuda()
-        out3 = torch.empty_like(img3)
-        r3, _ = synth.random_mask(1003, 3)
-        cfg3 = {"workload": "config3: 8192x8192 U(3), random asymmetric 3x3, FP64, fused u8",
-                "blocks": 1048576}
-        for padname, pad in (("zero", P.PaddingMode.kZero), ("replicate", P.PaddingMode.kReplicate)):
-            pl3 = P.FilterPlan(P.Mask(3, r3), N, pad)
-            ev3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(10)]
-            for i in range(13):
-                flush.fill_(6)
-                if i >= 3:
-                    ev3[i - 3][0].record(stream)
-                _lib.check(lib.dctf_filter_image_u8(pl3.handle, img3.data_ptr(), out3.data_ptr(), 8192,
-                                                    8192, 8192, None, sp))
-                if i >= 3:
-                    ev3[i - 3][1].record(stream)
-            torch.cuda.synchronize()
-            ms3 = statistics.mean(a.elapsed_time(b) for a, b in ev3)
-            cfg3[padname] = {"kernel": pl3.image_kernel, "ms": ms3, "blocks_per_s": 1048576 / (ms3 / 1e3)}
-        del img3, out3
-        aux = {"n8_fused_dense": dense8, "n8_fused_int8exact": int8exact, "cfg1_graph": cfg1,
-               "cfg3_asymmetric": cfg3,
-               "cfg5_video": cfg5,
-               "n16_coef_fp64": coefline(plan16.coef_kernel, ms_c16, 262144, 256, "fp64"),
-               "n16_coef_fp64_dense": coefline(plan16d.coef_kernel, ms_c16d, 262144, 256, "fp64"),
-               "n16_coef_tf32x3": coefline(plan16t.coef_kernel, ms_t16, 262144, 256, "3xtf32", err_t16),
-               "n16_coef_bf16x3": coefline(plan16b.coef_kernel, ms_b16, 262144, 256, "3xbf16", err_b16),
-               "n8_coef_tf32x3": coefline(plan8t.coef_kernel, ms_t8, NBLOCKS, 64, "3xtf32", err_t8),
-               "n16_fused": {
-            "kernel": plan16.image_kernel, "workload": "config4: 8192x8192 U(4), 16x16 blocks, "
-            "gaussian 7x7 sigma=2, replicate, FP64", "blocks_per_s": nb16 / (ms16 / 1e3), "ms": ms16,
-            "fp64_tflops_dense_count": flop16 * nb16 / (ms16 / 1e3) / 1e12,
-            "frac_dense_count": flop16 * nb16 / (ms16 / 1e3) / 1e12 / peak_dmma,
-            "pipe_flop_per_block": pipe16,
-            "pipe_frac": pipe16 * nb16 / (ms16 / 1e3) / 1e12 / peak_dmma,
-            "dense_kernel": plan16fd.image_kernel, "dense_blocks_per_s": nb16 / (ms16d / 1e3),
-            "dense_pipe_frac": pipe_of["k_fused16"] * nb16 / (ms16d / 1e3) / 1e12 / peak_dmma,
-            "u8_identical_to_dense": same16},
-            "coef_path": {
-            "kernel": plan.coef_kernel, "blocks_per_s": NBLOCKS / (ms_c / 1e3), "ms": ms_c,
-            "gb_per_s": NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9,
-            "hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9) / hbm_peak
-            if hbm_peak else None,
-            "fp64_tflops_dense_count": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_c / 1e3) / 1e12,
-            "dense_kernel": plan_cd.coef_kernel, "dense_blocks_per_s": NBLOCKS / (ms_cd / 1e3),
-            "dense_fp64_frac": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_cd / 1e3) / 1e12 / peak_dmma,
-            "dense_hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_cd / 1e3) / 1e9) / hbm_peak
-            if hbm_peak else None}}
+        ctx = AuxContext(torch=torch, P=P, synth=synth, lib=lib, check=_lib.check, stream=stream,
+                         sp=sp, flush=flush, plan=plan, mask=mask, d_in=d_in, d_out=d_out,
+                         peak_dmma=peak_dmma, hbm_peak=hbm_peak, ms=ms, steps=args.steps)
+        aux = {}
+        aux.update(aux_image8_variants(ctx))
+        aux["cfg1_graph"] = aux_cfg1(ctx)
+        aux["cfg3_asymmetric"] = aux_cfg3(ctx)
+        aux["cfg5_video"] = aux_cfg5(ctx)
+        aux.update(aux_n16(ctx))
+        aux["n8_coef_tf32x3"] = aux_coef8_tf32(ctx)
+        aux["coef_path"] = aux_coef8(ctx)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
