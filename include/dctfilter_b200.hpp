@@ -268,6 +268,10 @@ class FilterPlan {
   int npairs() const { return npairs_; }
   bool symmetric_merged() const { return merged_ != 0; }
   const dctf_plan* handle() const { return plan_.get(); }
+  // Kernels the image / coefficient paths run for this plan (dctf_plan_image_kernel,
+  // dctf_plan_coef_kernel), e.g. "k_fused8_sym" for a symmetric mask.
+  std::string image_kernel() const { return dctf_plan_image_kernel(plan_.get()); }
+  std::string coef_kernel() const { return dctf_plan_coef_kernel(plan_.get()); }
 
   // Dense N^2 x N^2 DCT-domain operator (row (u*n+v), column (a*n+b)).
   std::vector<double> dct_operator() const {
@@ -345,6 +349,17 @@ struct GrayImage {
   std::uint8_t at(int x, int y) const { return samples[size_t(y) * width + x]; }
   std::uint8_t& at(int x, int y) { return samples[size_t(y) * width + x]; }
 };
+
+// filter_image with a prebuilt plan (any precision; the plan is reusable
+// across images and threads): the DCT path, fused on the device.
+inline GrayImage filter_image(const FilterPlan& plan, const GrayImage& img) {
+  if (img.samples.size() != size_t(img.width) * img.height)
+    throw std::invalid_argument("GrayImage: sample count must be width*height");
+  GrayImage out{img.width, img.height, std::vector<std::uint8_t>(img.samples.size())};
+  check(dctf_filter_image_host(plan.handle(), img.samples.data(), out.samples.data(), img.width,
+                               img.height, size_t(img.width)));
+  return out;
+}
 
 // filter_image (image.hpp:210-225): the DCT path, fused on the device.
 inline GrayImage filter_image(const GrayImage& img, const Mask& mask, PaddingMode padding,

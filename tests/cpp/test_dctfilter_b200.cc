@@ -101,6 +101,42 @@ int main() {
     for (auto s : o.samples) all = all && s == 77;
     CHECK(all, "constant image stays constant under averaging (n=16)");
   }
+  // precision modes through the drop-in: structured / dense / exact-INT8 image
+  // kernels give identical u8; split-precision coefficients within their bounds
+  {
+    GrayImage img{1000, 600, std::vector<std::uint8_t>(1000 * 600)};
+    for (auto& s : img.samples) s = std::uint8_t(rng() & 255);
+    const Mask g = Mask::gaussian3();
+    const FilterPlan sym(g, 8, PaddingMode::kReplicate);
+    const FilterPlan dense(g, 8, PaddingMode::kReplicate, Precision::kFp64Dense);
+    const FilterPlan i8(g, 8, PaddingMode::kReplicate, Precision::kInt8Exact);
+    CHECK(sym.image_kernel() == "k_fused8_sym" && dense.image_kernel() == "k_fused8" &&
+              i8.image_kernel() == "k_fused8_i8",
+          "image kernel selection by mask structure / precision");
+    const GrayImage a = filter_image(sym, img), b = filter_image(dense, img), c = filter_image(i8, img);
+    CHECK(a.samples == b.samples && a.samples == c.samples, "parity-class, dense and INT8-exact u8 identical");
+    std::vector<BlockMatrix> blocks;
+    std::uniform_real_distribution<double> u(-300, 300);
+    for (int i = 0; i < 500; ++i) {
+      BlockMatrix m(16);
+      for (double& v : m.data()) v = u(rng);
+      blocks.push_back(m);
+    }
+    const FilterPlan f64(g, 16, PaddingMode::kZero);
+    const FilterPlan t32(g, 16, PaddingMode::kZero, Precision::kTf32x3);
+    const FilterPlan b16(g, 16, PaddingMode::kZero, Precision::kBf16x3);
+    const auto ref = f64.filter_coeffs(blocks), yt = t32.filter_coeffs(blocks), yb = b16.filter_coeffs(blocks);
+    double et = 0, eb = 0, mx = 0;
+    for (size_t i = 0; i < ref.size(); ++i) {
+      et = std::max(et, max_abs_diff(yt[i], ref[i]));
+      eb = std::max(eb, max_abs_diff(yb[i], ref[i]));
+      for (double v : ref[i].data()) mx = std::max(mx, std::abs(v));
+    }
+    CHECK(f64.coef_kernel() == "k_coef16_sym" && t32.coef_kernel() == "k_coef_tf32x3" &&
+              b16.coef_kernel() == "k_coef_bf16x3",
+          "coefficient kernel selection");
+    CHECK(et <= 5e-6 * mx && eb <= 1e-4 * mx, "3xTF32 / 3xBF16 coefficients within their stated bounds");
+  }
   CHECK(quantize_sample(127.5) == 128 && quantize_sample(0.5) == 1 && quantize_sample(-3) == 0, "quantize KATs");
   std::printf("%s\n", failures ? "FAILED" : "ALL PASSED");
   return failures ? 1 : 0;
