@@ -1,11 +1,13 @@
 // The C ABI of include/dctf.h (plan lifecycle, device and host-buffer entry
 // points, kernel naming, NaN check, FP64 peak probe) plus the reference-order
 // transforms and the spatial path:
-//   k_forward<N,U8>   forward_2d (dct.hpp:59-62) per block, reference
-//                     operation order (mul then add, no FMA, zero-skip), so
-//                     coefficients are bit-identical to the reference.
-//   k_inverse<N,U8>   inverse_2d (dct.hpp:65-68) [+ quantize_sample +
-//                     assemble crop (spatial.hpp:71-75, image.hpp:188-203)].
+//   k_transform<N,FWD,U8>  forward_2d (dct.hpp:59-62) / inverse_2d
+//                     (dct.hpp:65-68) per block in the reference operation
+//                     order (mul then add, no FMA, zero-skip), so results are
+//                     bit-identical to the reference; u8 variants read tiles
+//                     (image.hpp:164-184) or quantize + assemble
+//                     (spatial.hpp:71-75, image.hpp:188-203). Persistent,
+//                     next batch staged during the current one.
 //   k_spatial<U8>     convolve (spatial.hpp:41-68), bit-identical samples.
 // The filter kernels live in coef.cu (filter_coeffs: k_coef8, k_coef16 and the
 // parity-class k_coef8_sym / k_coef16_sym), fused.cu (filter_image: k_fused8,
@@ -21,6 +23,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "device.cuh"
 #include "fastdiv.cuh"
@@ -56,123 +59,140 @@ namespace {
 // separately rounded multiply and add (the reference has no FMA
 // contraction), so results are bit-identical to forward_2d / inverse_2d.
 
-template <int N, bool FROM_U8>
-__global__ void __launch_bounds__(256) k_forward(const uint8_t* __restrict__ img, int w, int h,
-                                                 size_t pitch, int bw,
-                                                 const double* __restrict__ blocks,
-                                                 double* __restrict__ out, long long nblocks,
-                                                 const double* __restrict__ cb) {
-  constexpr int NN = N * N, BPC = 256 / N, STR = NN + 1;
-  __shared__ double xs[BPC * STR];
+// Persistent, double-buffered reference-order transforms: a CTA of 256
+// threads handles batches of 256/N blocks (thread (lb, r) = row r of block
+// lb); the next batch is staged while the current one is transformed (FP64
+// input by cp.async, u8 pixels by a register prefetch), so global latency
+// overlaps the FP64 work. The arithmetic is exactly the reference's matmul
+// (block_matrix.hpp:67-81): k ascending, a == 0 skipped, separately rounded
+// multiply and add.
+template <int N>
+struct TrCfg {
+  static constexpr int NN = N * N, BPC = 256 / N, STR = NN + 2;  // 16-byte aligned block rows
+  static constexpr int TILE = BPC * STR;                         // doubles per buffer
+  static constexpr int SMEM = 2 * TILE * 8;
+};
+
+template <int N, bool FWD, bool U8>
+__global__ void __launch_bounds__(256) k_transform(const uint8_t* __restrict__ img_in,
+                                                   uint8_t* __restrict__ img_out, int w, int h,
+                                                   size_t pitch, int bw,
+                                                   const double* __restrict__ blocks_in,
+                                                   double* __restrict__ blocks_out, long long nblocks,
+                                                   const double* __restrict__ cb, int* nan_flag) {
+  using Cfg = TrCfg<N>;
+  constexpr int NN = Cfg::NN, BPC = Cfg::BPC, STR = Cfg::STR;
+  extern __shared__ __align__(16) double tbuf[];
   __shared__ double cs[NN];
   for (int i = threadIdx.x; i < NN; i += 256) cs[i] = cb[i];
-  const long long b0 = static_cast<long long>(blockIdx.x) * BPC;
-  for (int e = threadIdx.x; e < BPC * NN; e += 256) {
-    const int lb = e / NN, idx = e % NN;
-    const long long blk = b0 + lb;
-    double v = 0.0;
-    if (blk < nblocks) {
-      if (FROM_U8) {
+  const int lb = threadIdx.x / N, r = threadIdx.x % N;
+  const long long nbatch = (nblocks + BPC - 1) / BPC;
+  constexpr bool U8IN = FWD && U8;
+  const bool async_in = !U8IN && (reinterpret_cast<uintptr_t>(blocks_in) & 15) == 0;
+  const bool u8_vec = U8IN && (pitch % N) == 0 && (reinterpret_cast<uintptr_t>(img_in) % N) == 0;
+  using Row = typename std::conditional<N == 8, uint2, uint4>::type;
+  Row pre{};
+  bool pre_fast = false;
+  // stage batch `bt` into buffer `buf` (FP64: cp.async / loads; u8: registers)
+  auto stage = [&](long long bt, double* buf) {
+    const long long b0 = bt * BPC;
+    if constexpr (U8IN) {
+      const long long blk = b0 + lb;
+      pre_fast = false;
+      if (blk < nblocks) {
         const int by = static_cast<int>(blk / bw), bx = static_cast<int>(blk % bw);
-        const int y = min(by * N + idx / N, h - 1), x = min(bx * N + idx % N, w - 1);
-        v = static_cast<double>(img[static_cast<size_t>(y) * pitch + x]);
-      } else {
-        v = blocks[blk * NN + idx];
+        if (u8_vec && by * N + N <= h && bx * N + N <= w) {
+          pre = *reinterpret_cast<const Row*>(img_in + static_cast<size_t>(by * N + r) * pitch + bx * N);
+          pre_fast = true;
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < BPC * NN / 2; e += 256) {
+        const int l = e / (NN / 2), c = e % (NN / 2);
+        const long long blk = b0 + l;
+        double* dst = buf + l * STR + 2 * c;
+        if (blk >= nblocks) {
+          dst[0] = dst[1] = 0.0;
+        } else if (async_in) {
+          cp_async16(dst, blocks_in + blk * NN + 2 * c);
+        } else {
+          dst[0] = blocks_in[blk * NN + 2 * c];
+          dst[1] = blocks_in[blk * NN + 2 * c + 1];
+        }
+      }
+      cp_async_commit();
+    }
+  };
+  // u8: this thread's row of batch bt (prefetched, or clamped per byte) -> buf
+  auto land_u8 = [&](long long bt, double* buf) {
+    const long long blk = bt * BPC + lb;
+    double* dst = buf + lb * STR + r * N;
+    if (pre_fast) {
+      const uint8_t* bytes = reinterpret_cast<const uint8_t*>(&pre);
+#pragma unroll
+      for (int j = 0; j < N; ++j) dst[j] = static_cast<double>(bytes[j]);
+    } else if (blk < nblocks) {
+      const int by = static_cast<int>(blk / bw), bx = static_cast<int>(blk % bw);
+      const int y = min(by * N + r, h - 1);
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+        dst[j] = static_cast<double>(img_in[static_cast<size_t>(y) * pitch + min(bx * N + j, w - 1)]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < N; ++j) dst[j] = 0.0;
+    }
+  };
+
+  long long bt = blockIdx.x;
+  if (bt < nbatch) stage(bt, tbuf);
+  for (int it = 0; bt < nbatch; bt += gridDim.x, ++it) {
+    double* cur = tbuf + (it & 1) * Cfg::TILE;
+    if constexpr (U8IN) land_u8(bt, cur);
+    cp_async_wait_all();
+    __syncthreads();
+    if (bt + gridDim.x < nbatch) stage(bt + gridDim.x, tbuf + ((it + 1) & 1) * Cfg::TILE);
+    const long long blk = bt * BPC + lb;
+    const double* x = cur + lb * STR;
+    double cv[N], trow[N], o[N];
+    // forward: T = C X (row r: C[r][k]), out = T C^t;  inverse: T = C^t Y (C[k][r]), out = T C
+#pragma unroll
+    for (int k = 0; k < N; ++k) cv[k] = FWD ? cs[r * N + k] : cs[k * N + r];
+#pragma unroll
+    for (int j = 0; j < N; ++j) trow[j] = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const double a = cv[k];
+      if (a != 0.0) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) trow[j] = __dadd_rn(trow[j], __dmul_rn(a, x[k * N + j]));
       }
     }
-    xs[lb * STR + idx] = v;
-  }
-  __syncthreads();
-  const int lb = threadIdx.x / N, r = threadIdx.x % N;
-  const long long blk = b0 + lb;
-  const double* x = xs + lb * STR;
-  double crow[N], trow[N], o[N];
 #pragma unroll
-  for (int k = 0; k < N; ++k) crow[k] = cs[r * N + k];
+    for (int j = 0; j < N; ++j) o[j] = 0.0;
 #pragma unroll
-  for (int j = 0; j < N; ++j) trow[j] = 0.0;
+    for (int k = 0; k < N; ++k) {
+      const double a = trow[k];
+      if (a != 0.0) {
 #pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const double a = crow[k];
-    if (a != 0.0) {
+        for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, FWD ? cs[j * N + k] : cs[k * N + j]));
+      }
+    }
+    if (blk >= nblocks) continue;
+    if (!U8 || FWD) {
+      double* dst = blocks_out + blk * NN + r * N;
 #pragma unroll
-      for (int j = 0; j < N; ++j) trow[j] = __dadd_rn(trow[j], __dmul_rn(a, x[k * N + j]));
+      for (int j = 0; j < N; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(o[j], o[j + 1]);
+    } else {
+      const int by = static_cast<int>(blk / bw), bx = static_cast<int>(blk % bw);
+      const int yy = by * N + r;
+      if (yy >= h) continue;
+      uint8_t* dst = img_out + static_cast<size_t>(yy) * pitch + bx * N;
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+        if (bx * N + j < w) dst[j] = static_cast<uint8_t>(quantize(o[j], nan_flag));
     }
   }
-#pragma unroll
-  for (int j = 0; j < N; ++j) o[j] = 0.0;
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const double a = trow[k];
-    if (a != 0.0) {
-#pragma unroll
-      for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, cs[j * N + k]));
-    }
-  }
-  if (blk < nblocks) {
-    double* dst = out + blk * NN + r * N;
-#pragma unroll
-    for (int j = 0; j < N; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(o[j], o[j + 1]);
-  }
-}
-
-template <int N, bool TO_U8>
-__global__ void __launch_bounds__(256) k_inverse(const double* __restrict__ coeffs,
-                                                 double* __restrict__ blocks_out,
-                                                 uint8_t* __restrict__ img, int w, int h,
-                                                 size_t pitch, int bw, long long nblocks,
-                                                 const double* __restrict__ cb, int* nan_flag) {
-  constexpr int NN = N * N, BPC = 256 / N, STR = NN + 1;
-  __shared__ double ys[BPC * STR];
-  __shared__ double cs[NN];
-  for (int i = threadIdx.x; i < NN; i += 256) cs[i] = cb[i];
-  const long long b0 = static_cast<long long>(blockIdx.x) * BPC;
-  for (int e = threadIdx.x; e < BPC * NN; e += 256) {
-    const int lb = e / NN, idx = e % NN;
-    const long long blk = b0 + lb;
-    ys[lb * STR + idx] = blk < nblocks ? coeffs[blk * NN + idx] : 0.0;
-  }
-  __syncthreads();
-  const int lb = threadIdx.x / N, r = threadIdx.x % N;
-  const long long blk = b0 + lb;
-  const double* y = ys + lb * STR;
-  double ccol[N], trow[N], o[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) ccol[k] = cs[k * N + r];  // C^t[r][k]
-#pragma unroll
-  for (int j = 0; j < N; ++j) trow[j] = 0.0;
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const double a = ccol[k];
-    if (a != 0.0) {
-#pragma unroll
-      for (int j = 0; j < N; ++j) trow[j] = __dadd_rn(trow[j], __dmul_rn(a, y[k * N + j]));
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < N; ++j) o[j] = 0.0;
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const double a = trow[k];
-    if (a != 0.0) {
-#pragma unroll
-      for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, cs[k * N + j]));
-    }
-  }
-  if (blk >= nblocks) return;
-  if (!TO_U8) {
-    double* dst = blocks_out + blk * NN + r * N;
-#pragma unroll
-    for (int j = 0; j < N; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(o[j], o[j + 1]);
-  } else {
-    const int by = static_cast<int>(blk / bw), bx = static_cast<int>(blk % bw);
-    const int yy = by * N + r;
-    if (yy >= h) return;
-    uint8_t* dst = img + static_cast<size_t>(yy) * pitch + bx * N;
-#pragma unroll
-    for (int j = 0; j < N; ++j)
-      if (bx * N + j < w) dst[j] = static_cast<uint8_t>(quantize(o[j], nan_flag));
-  }
+  cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -366,34 +386,44 @@ dctf_status check_image(int w, int h, size_t pitch) {
 
 namespace dctf {
 
+// Launch of k_transform: persistent grid (batches of 256/n blocks).
+template <int N, bool FWD, bool U8>
+dctf_status launch_transform_n(const dctf_plan* p, const uint8_t* img_in, uint8_t* img_out, int w,
+                               int h, size_t pitch, int bw, const double* bin, double* bout,
+                               long long nb, cudaStream_t st) {
+  if (nb == 0) return DCTF_OK;
+  auto kernel = k_transform<N, FWD, U8>;
+  const dctf_status sa = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), TrCfg<N>::SMEM, "k_transform");
+  if (sa != DCTF_OK) return sa;
+  const long long nbatch = (nb + TrCfg<N>::BPC - 1) / TrCfg<N>::BPC;
+  const long long grid = std::min<long long>(nbatch, 4LL * sm_count(p->device));
+  kernel<<<static_cast<unsigned>(grid), 256, TrCfg<N>::SMEM, st>>>(img_in, img_out, w, h, pitch, bw, bin,
+                                                                   bout, nb, p->d_basis, p->d_nan);
+  add_launches(1);
+  CUDA_TRY(cudaGetLastError());
+  return DCTF_OK;
+}
+
+template <bool FWD, bool U8>
+dctf_status launch_transform(const dctf_plan* p, const uint8_t* img_in, uint8_t* img_out, int w, int h,
+                             size_t pitch, int bw, const double* bin, double* bout, long long nb,
+                             cudaStream_t st) {
+  return p->n == 8 ? launch_transform_n<8, FWD, U8>(p, img_in, img_out, w, h, pitch, bw, bin, bout, nb, st)
+                   : launch_transform_n<16, FWD, U8>(p, img_in, img_out, w, h, pitch, bw, bin, bout, nb, st);
+}
+
 dctf_status launch_forward_u8(const dctf_plan* p, const uint8_t* img, int w, int h, size_t pitch,
                               double* coeffs, cudaStream_t st) {
   const int n = p->n, bw = (w + n - 1) / n, bh = (h + n - 1) / n;
-  const long long nb = static_cast<long long>(bw) * bh;
-  const int bpc = 256 / n;
-  const unsigned grid = static_cast<unsigned>((nb + bpc - 1) / bpc);
-  if (n == 8)
-    k_forward<8, true><<<grid, 256, 0, st>>>(img, w, h, pitch, bw, nullptr, coeffs, nb, p->d_basis);
-  else
-    k_forward<16, true><<<grid, 256, 0, st>>>(img, w, h, pitch, bw, nullptr, coeffs, nb, p->d_basis);
-  dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
-  return DCTF_OK;
+  return launch_transform<true, true>(p, img, nullptr, w, h, pitch, bw, nullptr, coeffs,
+                                      static_cast<long long>(bw) * bh, st);
 }
 
 dctf_status launch_inverse_u8(const dctf_plan* p, const double* coeffs, uint8_t* img, int w, int h,
                               size_t pitch, cudaStream_t st) {
   const int n = p->n, bw = (w + n - 1) / n, bh = (h + n - 1) / n;
-  const long long nb = static_cast<long long>(bw) * bh;
-  const int bpc = 256 / n;
-  const unsigned grid = static_cast<unsigned>((nb + bpc - 1) / bpc);
-  if (n == 8)
-    k_inverse<8, true><<<grid, 256, 0, st>>>(coeffs, nullptr, img, w, h, pitch, bw, nb, p->d_basis, p->d_nan);
-  else
-    k_inverse<16, true><<<grid, 256, 0, st>>>(coeffs, nullptr, img, w, h, pitch, bw, nb, p->d_basis, p->d_nan);
-  dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
-  return DCTF_OK;
+  return launch_transform<false, true>(p, nullptr, img, w, h, pitch, bw, coeffs, nullptr,
+                                       static_cast<long long>(bw) * bh, st);
 }
 
 }  // namespace dctf
@@ -703,16 +733,8 @@ dctf_status dctf_forward_blocks(const dctf_plan* p, const double* d_blocks, doub
   if (!d_blocks || !d_coeffs) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   if (misaligned16(d_coeffs)) return set_error(DCTF_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
   DeviceGuard guard(p->device);
-  const long long nb = static_cast<long long>(nblocks);
-  const int bpc = 256 / p->n;
-  const unsigned grid = static_cast<unsigned>((nb + bpc - 1) / bpc);
-  if (p->n == 8)
-    k_forward<8, false><<<grid, 256, 0, as_stream(stream)>>>(nullptr, 0, 0, 0, 1, d_blocks, d_coeffs, nb, p->d_basis);
-  else
-    k_forward<16, false><<<grid, 256, 0, as_stream(stream)>>>(nullptr, 0, 0, 0, 1, d_blocks, d_coeffs, nb, p->d_basis);
-  dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
-  return DCTF_OK;
+  return dctf::launch_transform<true, false>(p, nullptr, nullptr, 0, 0, 0, 1, d_blocks, d_coeffs,
+                                             static_cast<long long>(nblocks), as_stream(stream));
 }
 
 dctf_status dctf_inverse_blocks(const dctf_plan* p, const double* d_coeffs, double* d_blocks,
@@ -724,16 +746,8 @@ dctf_status dctf_inverse_blocks(const dctf_plan* p, const double* d_coeffs, doub
   if (!d_blocks || !d_coeffs) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   if (misaligned16(d_blocks)) return set_error(DCTF_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
   DeviceGuard guard(p->device);
-  const long long nb = static_cast<long long>(nblocks);
-  const int bpc = 256 / p->n;
-  const unsigned grid = static_cast<unsigned>((nb + bpc - 1) / bpc);
-  if (p->n == 8)
-    k_inverse<8, false><<<grid, 256, 0, as_stream(stream)>>>(d_coeffs, d_blocks, nullptr, 0, 0, 0, 1, nb, p->d_basis, nullptr);
-  else
-    k_inverse<16, false><<<grid, 256, 0, as_stream(stream)>>>(d_coeffs, d_blocks, nullptr, 0, 0, 0, 1, nb, p->d_basis, nullptr);
-  dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
-  return DCTF_OK;
+  return dctf::launch_transform<false, false>(p, nullptr, nullptr, 0, 0, 0, 1, d_coeffs, d_blocks,
+                                              static_cast<long long>(nblocks), as_stream(stream));
 }
 
 dctf_status dctf_filter_coeffs(const dctf_plan* p, const double* d_in, double* d_out,
