@@ -83,8 +83,12 @@ __global__ void __launch_bounds__(256) k_transform(const uint8_t* __restrict__ i
   using Cfg = TrCfg<N>;
   constexpr int NN = Cfg::NN, BPC = Cfg::BPC, STR = Cfg::STR;
   extern __shared__ __align__(16) double tbuf[];
-  __shared__ double cs[NN];
-  for (int i = threadIdx.x; i < NN; i += 256) cs[i] = cb[i];
+  __shared__ __align__(16) double cs[NN];
+  __shared__ __align__(16) double ct[NN];  // C transposed: the forward's second product reads rows
+  for (int i = threadIdx.x; i < NN; i += 256) {
+    cs[i] = cb[i];
+    ct[(i % N) * N + i / N] = cb[i];
+  }
   const int lb = threadIdx.x / N, r = threadIdx.x % N;
   const long long nbatch = (nblocks + BPC - 1) / BPC;
   constexpr bool U8IN = FWD && U8;
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(256) k_transform(const uint8_t* __restrict__ i
       const double a = trow[k];
       if (a != 0.0) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, FWD ? cs[j * N + k] : cs[k * N + j]));
+        for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, FWD ? ct[k * N + j] : cs[k * N + j]));
       }
     }
     if (blk >= nblocks) continue;
