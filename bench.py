@@ -443,6 +443,34 @@ def aux_coef8(c):
         "dense_hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_cd / 1e3) / 1e9) / hbm if hbm else None}
 
 
+def aux_transforms(c):
+    """forward_2d / inverse_2d in the reference's operation
+    order (bit-identical), 262,144 FP64 blocks, n = 8 and 16; the binding bound is
+    HBM at n = 8 (16 N^2 bytes) and the FP64 pipe at n = 16 (separately rounded
+    multiply and add: 4 N^3 FP64 instructions per block)."""
+    P, torch = c.P, c.torch
+    res = {}
+    for n in (8, 16):
+        pl = P.FilterPlan(P.Mask(3, np.full(9, 1.0 / 9.0)), n, P.PaddingMode.kZero)
+        nb = 262144
+        x = torch.randn((nb, n, n), dtype=torch.float64, device="cuda") * 100
+        y = torch.empty_like(x)
+        fwd = timed_ms(c, lambda: c.check(c.lib.dctf_forward_blocks(pl.handle, x.data_ptr(), y.data_ptr(),
+                                                                     nb, c.sp)), 20)
+        inv = timed_ms(c, lambda: c.check(c.lib.dctf_inverse_blocks(pl.handle, x.data_ptr(), y.data_ptr(),
+                                                                     nb, c.sp)), 20)
+        for name, ms in (("forward_2d", fwd), ("inverse_2d", inv)):
+            gbs = nb * 16 * n * n / (ms / 1e3) / 1e9
+            ops = 4 * n ** 3 * nb / (ms / 1e3) / 1e12
+            res[f"n{n}_{name}"] = {"kernel": f"k_transform<{n}>", "blocks_per_s": nb / (ms / 1e3), "ms": ms,
+                                   "gb_per_s": gbs, "hbm_frac": gbs / (c.hbm_peak or 1.0),
+                                   "fp64_tera_ops": ops,
+                                   # the pipe retires one FP64 op (or one FMA = 2 flop) per lane-cycle
+                                   "fp64_pipe_frac": ops / (c.peak_dfma / 2)}
+        del x, y
+    return res
+
+
 def aux_coef8_tf32(c):
     P, torch = c.P, c.torch
     coeffs = c.plan.forward_image(c.d_in)
@@ -599,7 +627,8 @@ def main():
     if not args.no_aux:
         ctx = AuxContext(torch=torch, P=P, synth=synth, lib=lib, check=_lib.check, stream=stream,
                          sp=sp, flush=flush, plan=plan, mask=mask, d_in=d_in, d_out=d_out,
-                         peak_dmma=peak_dmma, hbm_peak=hbm_peak, ms=ms, steps=args.steps)
+                         peak_dmma=peak_dmma, peak_dfma=peak_dfma, hbm_peak=hbm_peak, ms=ms,
+                         steps=args.steps)
         aux = {}
         aux.update(aux_image8_variants(ctx))
         aux["cfg1_graph"] = aux_cfg1(ctx)
@@ -608,6 +637,7 @@ def main():
         aux.update(aux_n16(ctx))
         aux["n8_coef_tf32x3"] = aux_coef8_tf32(ctx)
         aux["coef_path"] = aux_coef8(ctx)
+        aux["transforms"] = aux_transforms(ctx)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
