@@ -471,6 +471,35 @@ def aux_transforms(c):
     return res
 
 
+def aux_spatial(c):
+    """The spatial path (convolve in the reference's order,
+    bit-identical): k_spatial_rows on config 2's image with the headline
+    Gaussian 5x5 and with average3, and on config 4's 16x16 blocks with the
+    Gaussian 7x7. 2 FP64 instructions (DMUL + DADD) per tap, k^2 N^2 taps per
+    block; the FP64 pipe retires one instruction per lane-cycle."""
+    P, torch, synth = c.P, c.torch, c.synth
+    res = {}
+    img4 = torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda()
+    cases = (("n8_gaussian5", c.mask, 5, 8, c.d_in, W, H),
+             ("n8_average3", np.full(9, 1.0 / 9.0), 3, 8, c.d_in, W, H),
+             ("n16_gaussian7", synth.gaussian_mask(7, 2.0), 7, 16, img4, 8192, 8192))
+    for key, wm, k, n, img, w, h in cases:
+        pl = P.FilterPlan(P.Mask(k, wm), n, P.PaddingMode.kReplicate)
+        out = torch.empty_like(img)
+        ms = timed_ms(c, lambda: c.check(c.lib.dctf_filter_image_spatial_u8(
+            pl.handle, img.data_ptr(), out.data_ptr(), w, h, w, c.sp)), 20)
+        nb = (w // n) * (h // n)
+        ops = 2 * k * k * n * n * nb / (ms / 1e3) / 1e12
+        d = {"kernel": f"k_spatial_rows<{n},{k},{k}>", "blocks_per_s": nb / (ms / 1e3), "ms": ms,
+             "fp64_tera_ops": ops, "fp64_pipe_frac": ops / (c.peak_dfma / 2),
+             "gb_per_s": 2 * n * n * nb / (ms / 1e3) / 1e9}
+        if key == "n8_gaussian5":
+            d["pixels_differing_from_dct_path"] = int((out != c.d_out).sum().item())
+        res[key] = d
+    del img4
+    return res
+
+
 def aux_coef8_tf32(c):
     P, torch = c.P, c.torch
     coeffs = c.plan.forward_image(c.d_in)
@@ -638,6 +667,7 @@ def main():
         aux["n8_coef_tf32x3"] = aux_coef8_tf32(ctx)
         aux["coef_path"] = aux_coef8(ctx)
         aux["transforms"] = aux_transforms(ctx)
+        aux["spatial"] = aux_spatial(ctx)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -799,9 +799,11 @@ dctf_status dctf_filter_image_spatial_u8(const dctf_plan* p, const uint8_t* d_in
   DeviceGuard guard(p->device);
   const int n = p->n, bw = (w + n - 1) / n, bh = (h + n - 1) / n;
   const long long nb = static_cast<long long>(bw) * bh;
-  const unsigned grid = static_cast<unsigned>((nb * n * n + 255) / 256);
-  k_spatial<true><<<grid, 256, 0, as_stream(stream)>>>(d_in, w, h, pitch, bw, nullptr, d_out, nullptr, nb, n,
-                                                       p->d_weights, p->kr, p->kc, p->padding);
+  if (!dctf::launch_spatial_rows(p, d_in, w, h, pitch, bw, nullptr, d_out, nullptr, nb, as_stream(stream))) {
+    const unsigned grid = static_cast<unsigned>((nb * n * n + 255) / 256);
+    k_spatial<true><<<grid, 256, 0, as_stream(stream)>>>(d_in, w, h, pitch, bw, nullptr, d_out, nullptr, nb, n,
+                                                         p->d_weights, p->kr, p->kc, p->padding);
+  }
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
@@ -818,9 +820,11 @@ dctf_status dctf_convolve_blocks(const dctf_plan* p, const double* d_blocks, dou
   DeviceGuard guard(p->device);
   const int n = p->n;
   const long long nb = static_cast<long long>(nblocks);
-  const unsigned grid = static_cast<unsigned>((nb * n * n + 255) / 256);
-  k_spatial<false><<<grid, 256, 0, as_stream(stream)>>>(nullptr, 0, 0, 0, 1, d_blocks, nullptr, d_out, nb, n,
-                                                        p->d_weights, p->kr, p->kc, p->padding);
+  if (!dctf::launch_spatial_rows(p, nullptr, 0, 0, 0, 1, d_blocks, nullptr, d_out, nb, as_stream(stream))) {
+    const unsigned grid = static_cast<unsigned>((nb * n * n + 255) / 256);
+    k_spatial<false><<<grid, 256, 0, as_stream(stream)>>>(nullptr, 0, 0, 0, 1, d_blocks, nullptr, d_out, nb, n,
+                                                          p->d_weights, p->kr, p->kc, p->padding);
+  }
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
   return DCTF_OK;

@@ -63,6 +63,13 @@ dctf_status ensure_dyn_smem(const void* func, int bytes, const char* name);
 int sm_count(int device);
 inline bool misaligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; }
 
+// Register-tiled spatial path (spatial.cu): n in {8, 16}, square 3/5/7 masks.
+// Returns false (nothing launched) for other shapes; the caller then runs the
+// generic k_spatial. Exactly one of img / blocks is non-null.
+bool launch_spatial_rows(const dctf_plan* p, const uint8_t* img, int w, int h, size_t pitch, int bw,
+                         const double* blocks, uint8_t* out_img, double* out_blocks, long long nblocks,
+                         cudaStream_t st);
+
 // Launchers shared across the kernel translation units (all enqueue on `st`).
 // coef.cu: filter_coeffs on device buffers (dense / parity-class / 3xTF32).
 dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, long long nb, cudaStream_t st);

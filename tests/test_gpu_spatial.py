@@ -73,3 +73,31 @@ def test_paths_agree_c7(P, ref):
                 assert np.array_equal(
                     P.filter_image(img, P.Mask(k, wm), P.PaddingMode(pad), P.Domain.kSpatial),
                     ref.filter_image_spatial(img, wm, k, pad, 8))
+
+
+@pytest.mark.parametrize("n", [8, 16])
+def test_tiled_kernel_equals_generic(P, n, monkeypatch):
+    """k_spatial_rows (register-tiled, square 3/5/7 masks) against the
+    generic one-thread-per-sample k_spatial (DCTF_SPATIAL_GENERIC=1): images
+    with ragged edges and a padded, odd pitch, FP64 blocks at an 8-byte
+    offset, bit for bit."""
+    import torch
+    from paper_1710_07193_b200 import synth
+    rng = np.random.default_rng(n)
+    img = synth.uniform_image(17, 1001, 333)
+    d = torch.from_numpy(img).cuda()
+    big = torch.zeros((333, 1001 + 11), dtype=torch.uint8, device="cuda")
+    big[:, 3:1004] = d
+    view = big[:, 3:1004]
+    blocks = torch.from_numpy(rng.uniform(-300, 300, (1 + 4099 * n * n,))).cuda()
+    xb = blocks[1:].view(4099, n, n)          # 8-byte aligned, not 16
+    for k in (3, 5, 7):
+        wm = rng.uniform(-1, 1, k * k)
+        for pad in (0, 1):
+            plan = P.FilterPlan(P.Mask(k, wm), n, P.PaddingMode(pad))
+            monkeypatch.setenv("DCTF_SPATIAL_GENERIC", "0")
+            a, av, ab = plan.filter_image_spatial(d), plan.filter_image_spatial(view), plan.convolve(xb)
+            monkeypatch.setenv("DCTF_SPATIAL_GENERIC", "1")
+            g, gb = plan.filter_image_spatial(d), plan.convolve(xb.contiguous())
+            assert torch.equal(a, g) and torch.equal(av, g), (k, pad)
+            assert torch.equal(ab, gb), (k, pad)
