@@ -338,6 +338,14 @@ int sm_count(int device) {
   return cached[device];
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DCTF_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Opts `func` into `bytes` of dynamic shared memory on the current device,
 // once per (kernel, device); safe under concurrent first calls and across
 // several devices in one process.

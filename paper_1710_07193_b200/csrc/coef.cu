@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(c8::WARPS * 32, 1)
     for (int i = 0; i < WARPS * STAGES; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
-  cta_copy_async(base, hc, 32768);
+  pdl_trigger();
+  cta_copy_async(base, hc, 32768);  // plan-owned operator
+  pdl_wait();
   cp_async_wait_all();
   __syncthreads();
 
@@ -173,7 +175,9 @@ __global__ void __launch_bounds__(c8s::WARPS * 32, 1)
     for (int i = 0; i < WARPS * STAGES; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
-  cta_copy_async(base, hc, 8192);
+  pdl_trigger();
+  cta_copy_async(base, hc, 8192);  // plan-owned operator
+  pdl_wait();
   cp_async_wait_all();
   __syncthreads();
 
@@ -316,7 +320,9 @@ __global__ void __launch_bounds__(c16s::WARPS * 32, 1)
     for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
-  cta_copy_async(base, hc, HBYTES);
+  pdl_trigger();
+  cta_copy_async(base, hc, HBYTES);  // plan-owned operator
+  pdl_wait();
   cp_async_wait_all();
   __syncthreads();
 
@@ -440,6 +446,8 @@ __global__ void __launch_bounds__(c16::CWARPS * 32, 1)
     tma_load_2d(dst, &xmap, &full[s], kc * 16, static_cast<int>(tile * TILE));
     bulk_load(dst + XBYTES, hc + static_cast<size_t>(kc) * (HBYTES / 8), HBYTES, &full[s]);
   };
+  pdl_trigger();
+  pdl_wait();
   if (warp == 0 && lane == 0)
     for (long long c = 0; c < STAGES && c < nchunks; ++c) refill(c);
 
@@ -504,9 +512,9 @@ dctf_status launch_coef8_sym(const dctf_plan* p, const double* d_in, double* d_o
   if (s != DCTF_OK) return s;
   const long long ntiles = (nb + c8s::TILE - 1) / c8s::TILE;
   const long long ctas = std::min<long long>(sm_count(p->device), (ntiles + c8s::WARPS - 1) / c8s::WARPS);
-  k_coef8_sym<<<static_cast<unsigned>(ctas), c8s::WARPS * 32, c8s::SMEM, st>>>(xmap, ymap, p->d_hcsym, nb);
+  CUDA_TRY(dctf::launch_pdl(k_coef8_sym, static_cast<unsigned>(ctas), c8s::WARPS * 32, c8s::SMEM, st, xmap, ymap,
+                            static_cast<const double*>(p->d_hcsym), nb));
   dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
 }
 
@@ -520,9 +528,9 @@ dctf_status launch_coef16_sym(const dctf_plan* p, const double* d_in, double* d_
   if (s != DCTF_OK) return s;
   const long long ntiles = (nb + c16s::TILE - 1) / c16s::TILE;
   const long long ctas = std::min<long long>(sm_count(p->device), ntiles);
-  k_coef16_sym<<<static_cast<unsigned>(ctas), c16s::WARPS * 32, c16s::SMEM, st>>>(xmap, ymap, p->d_hcsym, nb);
+  CUDA_TRY(dctf::launch_pdl(k_coef16_sym, static_cast<unsigned>(ctas), c16s::WARPS * 32, c16s::SMEM, st, xmap, ymap,
+                            static_cast<const double*>(p->d_hcsym), nb));
   dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
 }
 
@@ -550,7 +558,8 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
     }
     const long long ntiles = (nb + c8::TILE - 1) / c8::TILE;
     const long long ctas = std::min<long long>(sms, (ntiles + c8::WARPS - 1) / c8::WARPS);
-    k_coef8<<<static_cast<unsigned>(ctas), c8::WARPS * 32, c8::SMEM, st>>>(map, p->d_hcoef, d_out, nb);
+    CUDA_TRY(dctf::launch_pdl(k_coef8, static_cast<unsigned>(ctas), c8::WARPS * 32, c8::SMEM, st, map,
+                              static_cast<const double*>(p->d_hcoef), d_out, nb));
   } else {
     {
       const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_coef16), c16::SMEM, "k_coef16");
@@ -558,8 +567,8 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
     }
     const long long ntiles = (nb + c16::TILE - 1) / c16::TILE;
     const long long ctas = std::min<long long>(sms, ntiles);
-    k_coef16<<<static_cast<unsigned>(ctas), c16::CWARPS * 32, c16::SMEM, st>>>(map, p->d_hcoef,
-                                                                                   d_out, nb);
+    CUDA_TRY(dctf::launch_pdl(k_coef16, static_cast<unsigned>(ctas), c16::CWARPS * 32, c16::SMEM, st, map,
+                              static_cast<const double*>(p->d_hcoef), d_out, nb));
   }
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());

@@ -147,6 +147,16 @@ __device__ __forceinline__ void cta_copy_async(void* dst, const void* src, int b
 }
 
 
+// Programmatic dependent launch (launch_pdl in internal.h). A grid calls
+// pdl_trigger() once it no longer needs exclusive SMs, so the next grid on the
+// stream can be scheduled onto SMs as this one's CTAs retire; pdl_wait() blocks
+// until the preceding grid has completed and its memory is visible. Kernels
+// read only plan-owned operators (uploaded synchronously at plan creation)
+// before pdl_wait() and touch caller buffers only after it. Both are no-ops
+// when the grid was launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // tcgen05 (5th-gen tensor core) ordering fences and MMA completion -> mbarrier
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

@@ -102,8 +102,10 @@ __global__ void __launch_bounds__(f8::WARPS * 32, 2)
       pf1 = ldg_stream(p + (r0 + 4) * pitch);
     }
   };
+  pdl_trigger();
+  cta_copy_async(smem, hf, 32768);  // plan-owned operator: staged before the dependency wait
+  pdl_wait();
   if (s < nstrips) prefetch(s);  // first strip's pixels in flight during the operator copy
-  cta_copy_async(smem, hf, 32768);
   cp_async_wait_all();
   __syncthreads();
 
@@ -306,8 +308,10 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
     if constexpr (ASYNC) cp_async_commit();
     return ok;
   };
+  pdl_trigger();                       // the next grid may take SMs as ours retire
+  cta_copy_async(smem, hsym, 16384);   // plan-owned: staged before the dependency wait
+  pdl_wait();                          // caller buffers: after the preceding grid
   bool fast = s < nstrips ? fetch(s, pix) : false;  // first strip in flight during the operator copy
-  cta_copy_async(smem, hsym, 16384);
   cp_async_wait_all();
   __syncthreads();
 
@@ -500,6 +504,7 @@ __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
   uint8_t* xy = base;
   uint8_t* hst = base + XY_BYTES;
   uint8_t* pix = hst + STAGES * HBYTES;
+  pdl_trigger();
   __shared__ uint64_t full[STAGES], empty[STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -523,7 +528,8 @@ __global__ void __launch_bounds__(f16::CWARPS * 32, 1)
     bulk_load(hst + s * HBYTES, hf + static_cast<size_t>(chunk % 16) * (HBYTES / 8), HBYTES, &full[s]);
   };
   if (warp == 0 && lane == 0)
-    for (long long c = 0; c < STAGES && c < nchunks; ++c) refill(c);
+    for (long long c = 0; c < STAGES && c < nchunks; ++c) refill(c);  // plan-owned operator
+  pdl_wait();
 
   const int g = lane >> 2, t = lane & 3, mg = warp & 3, ng = warp >> 2;
   const int tid = threadIdx.x;  // 0..511
@@ -797,9 +803,11 @@ __global__ void __launch_bounds__(f16s::WARPS * 32, 1)
     }
   };
   long long tile = static_cast<long long>(blockIdx.x) * PAIRS + pair;
-  if (tile < ntiles) prefetch(tile);
-  cta_copy_async(smem, gsym, GBYTES);
+  pdl_trigger();
+  cta_copy_async(smem, gsym, GBYTES);  // plan-owned operators: staged before the dependency wait
   cta_copy_async(smem + GBYTES, basis, CBYTES);
+  pdl_wait();
+  if (tile < ntiles) prefetch(tile);
   cp_async_wait_all();
   __syncthreads();
   // first inverse pass B fragments: C[2(2t + e) + pv][g], per class parity pv
@@ -968,10 +976,11 @@ dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, i
   if (ctas <= 0) return DCTF_OK;
   if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
     return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  kernel<<<static_cast<unsigned>(ctas), nw * 32, 32768 + nw * f8::WARP_BYTES, st>>>(
-      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
+  CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), nw * 32, 32768 + nw * f8::WARP_BYTES, st,
+                            in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx,
+                            static_cast<const double*>(p->d_hfused), static_cast<const double*>(p->d_basis),
+                            coef_out));
   dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
 }
 
@@ -993,10 +1002,10 @@ dctf_status launch_fused8_sym(const dctf_plan* p, const uint8_t* in, uint8_t* ou
   if (ctas <= 0) return DCTF_OK;
   if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
     return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  kernel<<<static_cast<unsigned>(ctas), nw * 32, 16384 + nw * 2 * f8s::PIX_BYTES, st>>>(
-      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hsym, coef_out);
+  CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), nw * 32, 16384 + nw * 2 * f8s::PIX_BYTES, st,
+                            in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx,
+                            static_cast<const double*>(p->d_hsym), coef_out));
   dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
 }
 
@@ -1014,10 +1023,11 @@ dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, 
   if (ctas <= 0) return DCTF_OK;
   if (static_cast<long long>(bh) * nsx * nframes >= (1LL << 31))
     return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  kernel<<<static_cast<unsigned>(ctas), f16::CWARPS * 32, f16::SMEM, st>>>(
-      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hfused, p->d_basis, coef_out);
+  CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), f16::CWARPS * 32, f16::SMEM, st,
+                            in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx,
+                            static_cast<const double*>(p->d_hfused), static_cast<const double*>(p->d_basis),
+                            coef_out));
   dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
 }
 
@@ -1034,10 +1044,11 @@ dctf_status launch_fused16_sym(const dctf_plan* p, const uint8_t* in, uint8_t* o
   if (ntiles <= 0) return DCTF_OK;
   if (ntiles >= (1LL << 31)) return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
   const long long ctas = std::min<long long>(sm_count(p->device), (ntiles + f16s::PAIRS - 1) / f16s::PAIRS);
-  kernel<<<static_cast<unsigned>(ctas), f16s::WARPS * 32, f16s::SMEM, st>>>(
-      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, p->d_hsym, p->d_basis, coef_out);
+  CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), f16s::WARPS * 32, f16s::SMEM, st,
+                            in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx,
+                            static_cast<const double*>(p->d_hsym), static_cast<const double*>(p->d_basis),
+                            coef_out));
   dctf::add_launches(1);
-  CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
 }
 

@@ -8,6 +8,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -130,6 +131,29 @@ dctf_status launch_fused8_i8(const dctf_plan* p, const uint8_t* in, uint8_t* out
 // 3xTF32 tcgen05 coefficient filter (tc.cu).
 dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
                                cudaStream_t st, int sms);
+
+// Programmatic dependent launch: kernels written for it (pdl_wait() before
+// their first access to caller buffers, device.cuh) are launched with
+// programmatic stream serialisation, so a launch overlaps the tail of the
+// preceding grid on the stream (its CTAs start as SMs free up and stage their
+// operators; their image work still waits for the predecessor to complete).
+// DCTF_PDL=0 in the environment launches them conventionally.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace dctf
 

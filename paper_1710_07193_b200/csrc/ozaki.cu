@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   __shared__ double sc_s[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  cta_copy_async(bsm, gimg, BBYTES);
+  pdl_trigger();
+  cta_copy_async(bsm, gimg, BBYTES);  // plan-owned operator: staged before the dependency wait
   if (threadIdx.x < 64) sc_s[threadIdx.x] = gscale[threadIdx.x];
   if (warp == PROD) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  pdl_wait();
 
   const long long spf = static_cast<long long>(bh) * nsx;
   const long long ntiles = spf * nframes;
@@ -390,11 +392,11 @@ dctf_status launch_fused8_i8(const dctf_plan* p, const uint8_t* in, uint8_t* out
   const long long ntiles = static_cast<long long>(bh) * nsx * nframes;
   if (ntiles <= 0) return DCTF_OK;
   if (ntiles >= (1LL << 31)) return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  k_fused8_i8<<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), oz::THREADS, oz::SMEM, st>>>(
-      in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx, static_cast<const int8_t*>(p->d_gimg),
-      p->d_gscale, p->d_basis, coef_out);
+  const cudaError_t e = launch_pdl(k_fused8_i8, static_cast<unsigned>(std::min<long long>(sms, ntiles)), oz::THREADS,
+                                   oz::SMEM, st, in, out, w, h, pitch, frame_stride, nframes, bw, bh, nsx,
+                                   static_cast<const int8_t*>(p->d_gimg), static_cast<const double*>(p->d_gscale),
+                                   static_cast<const double*>(p->d_basis), coef_out);
   add_launches(1);
-  const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_fused8_i8: ") + cudaGetErrorString(e));
   return DCTF_OK;
 }

@@ -134,6 +134,7 @@ template <int NN, bool BF>
 __global__ void __launch_bounds__(TcCfg<NN, BF>::THREADS, 1)
     k_coef_split3(const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ hsplit,
                   double* __restrict__ y, long long nblocks) {
+  pdl_trigger();
   using Cfg = TcCfg<NN, BF>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(TcCfg<NN, BF>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  pdl_wait();
   const long long ntiles = (nblocks + Cfg::TILE - 1) / Cfg::TILE;
   const long long my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const long long nchunks = my_tiles * Cfg::KCH;
@@ -408,8 +410,9 @@ dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d
     const dctf_status sa = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), smem, "k_coef_split3");
     if (sa != DCTF_OK) return sa;
     const long long ntiles = (nb + 127) / 128;
-    kernel<<<static_cast<unsigned>(std::min<long long>(sms, ntiles)), threads, smem, st>>>(
-        map, static_cast<const uint8_t*>(p->d_hsplit), d_out, nb);
+    const cudaError_t e = launch_pdl(kernel, static_cast<unsigned>(std::min<long long>(sms, ntiles)), threads, smem,
+                                     st, map, static_cast<const uint8_t*>(p->d_hsplit), d_out, nb);
+    if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_coef_split3: ") + cudaGetErrorString(e));
     return DCTF_OK;
   };
   const bool bf = p->precision == DCTF_PREC_BF16X3;
