@@ -258,6 +258,22 @@ def stream_ms(c, pl, reps=200):
     return a.elapsed_time(b) / reps
 
 
+def ring_ms(c, launches, reps=60):
+    """Mean device time (ms) per launch with the launches cycling over
+    distinct buffer sets whose total exceeds L2, back to back (the headline's
+    streaming protocol); launches[i] is a closure over buffer set i."""
+    torch = c.torch
+    for i in range(2 * len(launches)):
+        launches[i % len(launches)]()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(c.stream)
+    for i in range(reps):
+        launches[i % len(launches)]()
+    b.record(c.stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
 def image_launcher(c, pl, img, out, w, h):
     return lambda: c.check(c.lib.dctf_filter_image_u8(pl.handle, img.data_ptr(), out.data_ptr(),
                                                          w, h, w, None, c.sp))
@@ -366,6 +382,11 @@ def aux_cfg3(c):
         pl = P.FilterPlan(P.Mask(3, r3), N, pad)
         ms = timed_ms(c, image_launcher(c, pl, img, out, 8192, 8192), 10)
         res[name] = {"kernel": pl.image_kernel, "ms": ms, "blocks_per_s": 1048576 / (ms / 1e3)}
+        ref_out = out.clone()
+        px = P.FilterPlan(P.Mask(3, r3), N, pad, precision=P.Precision.kInt8Exact)
+        ms = timed_ms(c, image_launcher(c, px, img, out, 8192, 8192), 10)
+        res[name + "_int8exact"] = {"kernel": px.image_kernel, "ms": ms, "blocks_per_s": 1048576 / (ms / 1e3),
+                                    "u8_identical_to_fp64": bool(torch.equal(out, ref_out))}
     return res
 
 
@@ -384,23 +405,38 @@ def aux_cfg5(c):
     uniq = np.stack([synth.sinusoid_image(f, FW, FH) for f in range(8)])
     frames = torch.from_numpy(uniq).cuda().repeat(FF // 8, 1, 1).contiguous()
     idx = [f % 4 for f in range(FF)]
-    P.filter_frames(frames, plans, idx)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ts = []
-    for _ in range(5):
-        a.record()
-        out = P.filter_frames(frames, plans, idx)
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-        del out
-    ms = statistics.median(ts)
     nb = FF * (FW // 8) * (FH // 8)
-    return {"workload": "config5: 64 x 3840x2160 S(f) frames, masks f mod 4 = Laplacian 3x3, Gaussian "
-            "5x5 s=1, 1x9 motion blur, random asymmetric 5x5; replicate; FP64; one "
-            "dctf_filter_frames_u8 call", "blocks": nb, "ms": ms, "blocks_per_s": nb / (ms / 1e3),
-            "kernels": [pl.image_kernel for pl in plans]}
+
+    def run(pls):
+        first = P.filter_frames(frames, pls, idx)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(5):
+            a.record()
+            out = P.filter_frames(frames, pls, idx)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+            del out
+        return statistics.median(ts), first
+
+    ms, ref_out = run(plans)
+    res = {"workload": "config5: 64 x 3840x2160 S(f) frames, masks f mod 4 = Laplacian 3x3, Gaussian "
+           "5x5 s=1, 1x9 motion blur, random asymmetric 5x5; replicate; FP64; one "
+           "dctf_filter_frames_u8 call", "blocks": nb, "ms": ms, "blocks_per_s": nb / (ms / 1e3),
+           "kernels": [pl.image_kernel for pl in plans]}
+    # the frames whose mask is asymmetric (dense FP64 kernel) through the
+    # exact-INT8 tensor-core kernel instead; u8 must not change
+    mixed = [pl if pl.image_kernel == "k_fused8_sym" else
+             P.FilterPlan(P.Mask(k, w) if k == kc else P.Mask.rect(k, kc, w), 8, P.PaddingMode.kReplicate,
+                          precision=P.Precision.kInt8Exact)
+             for pl, (w, k, kc) in zip(plans, masks)]
+    ms_m, out_m = run(mixed)
+    res["asymmetric_frames_int8exact"] = {"ms": ms_m, "blocks_per_s": nb / (ms_m / 1e3),
+                                          "kernels": [pl.image_kernel for pl in mixed],
+                                          "u8_identical_to_fp64": bool(torch.equal(out_m, ref_out))}
+    return res
 
 
 def aux_n16(c):
@@ -419,6 +455,8 @@ def aux_n16(c):
     out_s = out.clone()
     ms_d = timed_ms(c, image_launcher(c, pd, img, out, 8192, 8192), 10)
     same = bool(torch.equal(out_s, out))
+    imgs, outs = [img, img.clone()], [out, torch.empty_like(out)]   # 4 x 64 MiB > L2
+    ms_ss = ring_ms(c, [image_launcher(c, ps, a, b, 8192, 8192) for a, b in zip(imgs, outs)], 20)
     nb, flop = 262144, 2 * 16 ** 4 + 8 * 16 ** 3
     # executed FP64 flop per block: k_fused16 = G p + inverse; k_fused16_sym =
     # 4 classes x (64x64 filter + 8x8 first inverse pass) DMMA + 4 x 512 DFMA
@@ -432,13 +470,20 @@ def aux_n16(c):
         "pipe_flop_per_block": pipe, "pipe_frac": pipe * nb / (ms_s / 1e3) / 1e12 / c.peak_dmma,
         "dense_kernel": pd.image_kernel, "dense_blocks_per_s": nb / (ms_d / 1e3),
         "dense_pipe_frac": pipe_of["k_fused16"] * nb / (ms_d / 1e3) / 1e12 / c.peak_dmma,
-        "u8_identical_to_dense": same}}
-    del img, out, out_s
+        "u8_identical_to_dense": same, "streaming_blocks_per_s": nb / (ms_ss / 1e3),
+        "streaming_pipe_frac": pipe * nb / (ms_ss / 1e3) / 1e12 / c.peak_dmma}}
+    del img, out, out_s, imgs, outs
     x = ps.forward_image(torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda())
     y = torch.empty_like(x)
+    xs, ys = [x, x.clone()], [y, torch.empty_like(y)]   # streaming ring: 4 x 537 MB
+
+    def stream(pl, tag):
+        return coefline(c, pl.coef_kernel, ring_ms(c, [coef_launcher(c, pl, a, b, nb) for a, b in zip(xs, ys)],
+                                                   20), nb, 256, tag)
     ms_c = timed_ms(c, coef_launcher(c, ps, x, y, nb), 10)
     ref = y.clone()
     res["n16_coef_fp64"] = coefline(c, ps.coef_kernel, ms_c, nb, 256, "fp64")
+    res["n16_coef_fp64"]["streaming"] = stream(ps, "fp64")
     ms_cd = timed_ms(c, coef_launcher(c, pd, x, y, nb), 10)
     res["n16_coef_fp64_dense"] = coefline(c, pd.coef_kernel, ms_cd, nb, 256, "fp64")
     for key, prec, tag in (("n16_coef_tf32x3", P.Precision.kTf32x3, "3xtf32"),
@@ -447,6 +492,7 @@ def aux_n16(c):
         msp = timed_ms(c, coef_launcher(c, pl, x, y, nb), 10)
         err = float((y - ref).abs().max() / ref.abs().max())
         res[key] = coefline(c, pl.coef_kernel, msp, nb, 256, tag, err)
+        res[key]["streaming"] = stream(pl, tag)
     return res
 
 
@@ -461,7 +507,19 @@ def aux_coef8(c):
     pd = P.FilterPlan(P.Mask(5, c.mask), N, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dense)
     ms_cd = timed_ms(c, coef_launcher(c, pd, coeffs, y, NBLOCKS), ka)
     hbm = c.hbm_peak
+    # streaming: 2 input + 2 output coefficient buffers (4 x 134 MB > L2)
+    xs, ys = [coeffs, coeffs.clone()], [y, torch.empty_like(y)]
+    ring = lambda pl: [coef_launcher(c, pl, a, b, NBLOCKS) for a, b in zip(xs, ys)]
+    ms_s, ms_sd = ring_ms(c, ring(c.plan)), ring_ms(c, ring(pd))
+    gb = NBLOCKS * BYTES_PER_BLOCK_COEF / 1e9
     return {
+        "streaming": {"blocks_per_s": NBLOCKS / (ms_s / 1e3), "ms": ms_s, "gb_per_s": gb / (ms_s / 1e3),
+                      "hbm_frac": gb / (ms_s / 1e3) / hbm if hbm else None,
+                      "dense_blocks_per_s": NBLOCKS / (ms_sd / 1e3),
+                      "dense_fp64_frac": FLOP_PER_BLOCK_COEF * NBLOCKS / (ms_sd / 1e3) / 1e12 / c.peak_dmma,
+                      "protocol": "back to back over 2 input + 2 output buffers (536 MB > L2)"},
+        "cold_protocol": "fields below: one launch after a 256 MiB L2-flush write (the flush leaves "
+                         "~126 MB of dirty lines that this launch's traffic evicts)",
         "kernel": c.plan.coef_kernel, "blocks_per_s": NBLOCKS / (ms_c / 1e3), "ms": ms_c,
         "gb_per_s": NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9,
         "hbm_frac": (NBLOCKS * BYTES_PER_BLOCK_COEF / (ms_c / 1e3) / 1e9) / hbm if hbm else None,
@@ -487,15 +545,22 @@ def aux_transforms(c):
                                                                      nb, c.sp)), 20)
         inv = timed_ms(c, lambda: c.check(c.lib.dctf_inverse_blocks(pl.handle, x.data_ptr(), y.data_ptr(),
                                                                      nb, c.sp)), 20)
-        for name, ms in (("forward_2d", fwd), ("inverse_2d", inv)):
+        xs, ys = [x, x.clone()], [y, torch.empty_like(y)]
+        sfwd = ring_ms(c, [lambda a=a, b=b: c.check(c.lib.dctf_forward_blocks(pl.handle, a.data_ptr(), b.data_ptr(),
+                                                                              nb, c.sp)) for a, b in zip(xs, ys)])
+        sinv = ring_ms(c, [lambda a=a, b=b: c.check(c.lib.dctf_inverse_blocks(pl.handle, a.data_ptr(), b.data_ptr(),
+                                                                              nb, c.sp)) for a, b in zip(xs, ys)])
+        for name, ms, sms in (("forward_2d", fwd, sfwd), ("inverse_2d", inv, sinv)):
             gbs = nb * 16 * n * n / (ms / 1e3) / 1e9
             ops = 4 * n ** 3 * nb / (ms / 1e3) / 1e12
             res[f"n{n}_{name}"] = {"kernel": f"k_transform<{n}>", "blocks_per_s": nb / (ms / 1e3), "ms": ms,
                                    "gb_per_s": gbs, "hbm_frac": gbs / (c.hbm_peak or 1.0),
                                    "fp64_tera_ops": ops,
                                    # the pipe retires one FP64 op (or one FMA = 2 flop) per lane-cycle
-                                   "fp64_pipe_frac": ops / (c.peak_dfma / 2)}
-        del x, y
+                                   "fp64_pipe_frac": ops / (c.peak_dfma / 2),
+                                   "streaming_blocks_per_s": nb / (sms / 1e3),
+                                   "streaming_hbm_frac": nb * 16 * n * n / (sms / 1e3) / 1e9 / (c.hbm_peak or 1.0)}
+        del x, y, xs, ys
     return res
 
 
@@ -536,7 +601,11 @@ def aux_coef8_tf32(c):
     ms = timed_ms(c, coef_launcher(c, pl, coeffs, y, NBLOCKS), 50)
     ref = c.plan.filter_coeffs(coeffs)
     err = float((y - ref).abs().max() / ref.abs().max())
-    return coefline(c, pl.coef_kernel, ms, NBLOCKS, 64, "3xtf32", err)
+    d = coefline(c, pl.coef_kernel, ms, NBLOCKS, 64, "3xtf32", err)
+    xs, ys = [coeffs, coeffs.clone()], [y, torch.empty_like(y)]
+    d["streaming"] = coefline(c, pl.coef_kernel, ring_ms(c, [coef_launcher(c, pl, a, b, NBLOCKS)
+                                                             for a, b in zip(xs, ys)]), NBLOCKS, 64, "3xtf32")
+    return d
 
 
 def main():
