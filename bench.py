@@ -633,9 +633,17 @@ def main():
     import paper_1710_07193_b200 as P
     from paper_1710_07193_b200 import _lib, synth
 
+    # DCTF_BENCH_BACKEND=gloo runs the multi-rank code path with ranks sharing
+    # the visible GPUs (code-path check only: such timings are not valid)
+    backend = os.environ.get("DCTF_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -644,7 +652,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
