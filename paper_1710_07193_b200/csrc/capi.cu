@@ -66,6 +66,14 @@ namespace {
 // overlaps the FP64 work. The arithmetic is exactly the reference's matmul
 // (block_matrix.hpp:67-81): k ascending, a == 0 skipped, separately rounded
 // multiply and add.
+// The basis travels by value in the kernel parameters (constant bank): the
+// second product's C operand has a compile-time index, so every DMUL reads it
+// straight from the constant bank instead of shared memory (the kernel is
+// shared-memory-bandwidth bound otherwise).
+template <int N>
+struct BasisParam {
+  double c[N * N];
+};
 template <int N>
 struct TrCfg {
   static constexpr int NN = N * N, BPC = 256 / N, STR = NN + 2;  // 16-byte aligned block rows
@@ -79,17 +87,15 @@ __global__ void __launch_bounds__(256) k_transform(const uint8_t* __restrict__ i
                                                    size_t pitch, int bw,
                                                    const double* __restrict__ blocks_in,
                                                    double* __restrict__ blocks_out, long long nblocks,
-                                                   const double* __restrict__ cb, int* nan_flag) {
+                                                   const __grid_constant__ BasisParam<N> bp, int* nan_flag) {
   using Cfg = TrCfg<N>;
   constexpr int NN = Cfg::NN, BPC = Cfg::BPC, STR = Cfg::STR;
   extern __shared__ __align__(16) double tbuf[];
-  __shared__ __align__(16) double cs[NN];
-  __shared__ __align__(16) double ct[NN];  // C transposed: the forward's second product reads rows
-  for (int i = threadIdx.x; i < NN; i += 256) {
-    cs[i] = cb[i];
-    ct[(i % N) * N + i / N] = cb[i];
-  }
   const int lb = threadIdx.x / N, r = threadIdx.x % N;
+  // forward: T = C X (row r: C[r][k]), out = T C^t;  inverse: T = C^t Y (C[k][r]), out = T C
+  double cv[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) cv[k] = FWD ? bp.c[r * N + k] : bp.c[k * N + r];
   const long long nbatch = (nblocks + BPC - 1) / BPC;
   constexpr bool U8IN = FWD && U8;
   const bool async_in = !U8IN && (reinterpret_cast<uintptr_t>(blocks_in) & 15) == 0;
@@ -157,10 +163,7 @@ __global__ void __launch_bounds__(256) k_transform(const uint8_t* __restrict__ i
     if (bt + gridDim.x < nbatch) stage(bt + gridDim.x, tbuf + ((it + 1) & 1) * Cfg::TILE);
     const long long blk = bt * BPC + lb;
     const double* x = cur + lb * STR;
-    double cv[N], trow[N], o[N];
-    // forward: T = C X (row r: C[r][k]), out = T C^t;  inverse: T = C^t Y (C[k][r]), out = T C
-#pragma unroll
-    for (int k = 0; k < N; ++k) cv[k] = FWD ? cs[r * N + k] : cs[k * N + r];
+    double trow[N], o[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) trow[j] = 0.0;
 #pragma unroll
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(256) k_transform(const uint8_t* __restrict__ i
       const double a = trow[k];
       if (a != 0.0) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, FWD ? ct[k * N + j] : cs[k * N + j]));
+        for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, FWD ? bp.c[j * N + k] : bp.c[k * N + j]));
       }
     }
     if (blk >= nblocks) continue;
@@ -409,8 +412,10 @@ dctf_status launch_transform_n(const dctf_plan* p, const uint8_t* img_in, uint8_
   if (sa != DCTF_OK) return sa;
   const long long nbatch = (nb + TrCfg<N>::BPC - 1) / TrCfg<N>::BPC;
   const long long grid = std::min<long long>(nbatch, 4LL * sm_count(p->device));
+  BasisParam<N> bp;
+  std::copy(p->basis.begin(), p->basis.begin() + N * N, bp.c);
   kernel<<<static_cast<unsigned>(grid), 256, TrCfg<N>::SMEM, st>>>(img_in, img_out, w, h, pitch, bw, bin,
-                                                                   bout, nb, p->d_basis, p->d_nan);
+                                                                   bout, nb, bp, p->d_nan);
   add_launches(1);
   CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
