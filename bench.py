@@ -455,12 +455,20 @@ def aux_n16(c):
     out_s = out.clone()
     ms_d = timed_ms(c, image_launcher(c, pd, img, out, 8192, 8192), 10)
     same = bool(torch.equal(out_s, out))
+    # the parity-class kernel without the separable form (DCTF_NO_SEP at plan creation)
+    os.environ["DCTF_NO_SEP"] = "1"
+    pn = plan16()
+    del os.environ["DCTF_NO_SEP"]
+    ms_n = timed_ms(c, image_launcher(c, pn, img, out, 8192, 8192), 10)
+    same = same and bool(torch.equal(out_s, out))
     imgs, outs = [img, img.clone()], [out, torch.empty_like(out)]   # 4 x 64 MiB > L2
     ms_ss = ring_ms(c, [image_launcher(c, ps, a, b, 8192, 8192) for a, b in zip(imgs, outs)], 20)
     nb, flop = 262144, 2 * 16 ** 4 + 8 * 16 ** 3
     # executed FP64 flop per block: k_fused16 = G p + inverse; k_fused16_sym =
-    # 4 classes x (64x64 filter + 8x8 first inverse pass) DMMA + 4 x 512 DFMA
-    pipe_of = {"k_fused16": 2 * 16 ** 4 + 4 * 16 ** 3, "k_fused16_sym": 72 * 512 + 4 * 512 * 2}
+    # 4 classes x (64x64 filter + 8x8 first inverse pass) DMMA + 4 x 512 DFMA;
+    # k_fused16_sep (one separable pair) = 4 classes x 8 DMMA (8x8 factors)
+    pipe_of = {"k_fused16": 2 * 16 ** 4 + 4 * 16 ** 3, "k_fused16_sym": 72 * 512 + 4 * 512 * 2,
+               "k_fused16_sep": 32 * 512}
     pipe = pipe_of[ps.image_kernel]
     res = {"n16_fused": {
         "kernel": ps.image_kernel, "workload": "config4: 8192x8192 U(4), 16x16 blocks, gaussian 7x7 "
@@ -468,9 +476,11 @@ def aux_n16(c):
         "fp64_tflops_dense_count": flop * nb / (ms_s / 1e3) / 1e12,
         "frac_dense_count": flop * nb / (ms_s / 1e3) / 1e12 / c.peak_dmma,
         "pipe_flop_per_block": pipe, "pipe_frac": pipe * nb / (ms_s / 1e3) / 1e12 / c.peak_dmma,
+        "parity_class_kernel": pn.image_kernel, "parity_class_blocks_per_s": nb / (ms_n / 1e3),
+        "parity_class_pipe_frac": pipe_of[pn.image_kernel] * nb / (ms_n / 1e3) / 1e12 / c.peak_dmma,
         "dense_kernel": pd.image_kernel, "dense_blocks_per_s": nb / (ms_d / 1e3),
         "dense_pipe_frac": pipe_of["k_fused16"] * nb / (ms_d / 1e3) / 1e12 / c.peak_dmma,
-        "u8_identical_to_dense": same, "streaming_blocks_per_s": nb / (ms_ss / 1e3),
+        "u8_identical_to_dense_and_parity_class": same, "streaming_blocks_per_s": nb / (ms_ss / 1e3),
         "streaming_pipe_frac": pipe * nb / (ms_ss / 1e3) / 1e12 / c.peak_dmma}}
     del img, out, out_s, imgs, outs
     x = ps.forward_image(torch.from_numpy(synth.uniform_image(4, 8192, 8192)).cuda())

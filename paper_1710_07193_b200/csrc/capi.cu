@@ -506,6 +506,14 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_hsym, gsym.data(), gsym.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess && p->sym && n == 16 && !std::getenv("DCTF_NO_SEP")) {
+    std::vector<double> frag;
+    if (dctf::layout_sep16(*p, frag, p->sep_rank)) {
+      e = cudaMalloc(&p->d_sep, frag.size() * sizeof(double));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_sep, frag.data(), frag.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+  }
   if (e == cudaSuccess && p->sym && n == 16) {
     std::vector<double> hcsym;
     dctf::layout_coefsym16(p->op, hcsym);
@@ -675,6 +683,7 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_hfused);
     cudaFree(p->d_hsym);
     cudaFree(p->d_hcsym);
+    cudaFree(p->d_sep);
     cudaFree(p->d_hsplit);
     cudaFree(p->d_gimg);
     cudaFree(p->d_gscale);
@@ -715,6 +724,7 @@ const char* dctf_plan_image_kernel(const dctf_plan* p) {
   if (p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3) return "unfused";
   if (p->n == 8) return p->sym ? "k_fused8_sym" : "k_fused8";
   if (std::getenv("DCTF_N16_UNFUSED")) return "unfused";
+  if (p->sep_rank > 0) return "k_fused16_sep";
   return p->sym ? "k_fused16_sym" : "k_fused16";
 }
 

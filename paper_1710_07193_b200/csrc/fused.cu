@@ -960,6 +960,202 @@ __global__ void __launch_bounds__(f16s::WARPS * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_fused16_sep: the n = 16 image path for masks that are symmetric in both
+// axes and a sum of P <= 2 separable terms (Gaussians, box, 1xK motion blur,
+// Laplacian-like; layout_sep16 in plan.cc) — config 4's masks. The paper's
+// sandwich form with the fewest pairs: per parity class c = (pu, pv) and block
+//   Y_c = sum_p V_p,pu Q_c M_p,pv^T     (8x8 factors, forward DCT composed in)
+//   Z_c = C_pu^T Y_c C_pv               (inverse DCT, 8x8 factors)
+// with Q_c the butterflied quad (exact integers) and the output pixels +/-
+// sums of the four Z_c (+0.5 in Z_ee, floor -> u8). Every product is a DMMA
+// m8n8k4 pair (K = 8) chained fragment to fragment with no shuffles: each
+// step's D fragment (lane (g,t): row g, columns 2t, 2t+1) is the next step's
+// B operand with the contraction index permuted to k(s, t) = 2t + s, the
+// constant factor on the A side (fragment image from layout_sep16):
+//   A: T^T = M_pv Q^T   (B = Q^T: lane (g,t) holds q_c(g, 4s+t), from pixels)
+//   B: Y   = V_pu T     (B = T^T fragments of A)
+//   C: W^T = C_pv^T Y^T (B = Y fragments)
+//   D: Z   = C_pu^T W   (B = W^T fragments; Z_c[g][2t], Z_c[g][2t+1])
+// 4 classes x (4 P + 4) DMMA per block: 32 for P = 1 (8,192 FMA) against
+// k_fused16_sym's 72 DMMA + 2,048 DFMA and k_fused16's 288 DMMA. All four
+// classes of a block live in one lane, so the reflection butterfly is
+// lane-local. A warp owns a strip of 8 blocks (16 rows x 128 px), staged by
+// cp.async into a double-buffered per-warp tile; outputs overwrite the block's
+// own pixels (every lane has read them before the block's first DMMA).
+namespace f16p {
+constexpr int WARPS = 8;
+constexpr int TB = 8;                  // blocks per strip
+constexpr int PS = 144;                // pixel row stride (bytes)
+constexpr int PIX_BYTES = 16 * PS;
+constexpr int SMEM = WARPS * 2 * PIX_BYTES;
+}  // namespace f16p
+
+template <int P, bool COEF>
+__global__ void __launch_bounds__(f16p::WARPS * 32, 2)
+    k_fused16_sep(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
+                  long long frame_stride, int nframes, int bw, int bh, int nsx,
+                  const double* __restrict__ frag, double* __restrict__ coef_out) {
+  using namespace f16p;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  uint8_t* pix = smem + warp * 2 * PIX_BYTES;
+  uint8_t* pixn = pix + PIX_BYTES;
+  // constant A fragments: fm = M_p,pv (step A), fv = V_p,pu (step B), fc = C_par (inverse)
+  double fm[P][2][2], fv[P][2][2], fc[2][2];
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+#pragma unroll
+    for (int par = 0; par < 2; ++par)
+#pragma unroll
+      for (int sk = 0; sk < 2; ++sk) {
+        fm[q][par][sk] = frag[(((q * 2 + 0) * 2 + par) * 2 + sk) * 32 + lane];
+        fv[q][par][sk] = frag[(((q * 2 + 1) * 2 + par) * 2 + sk) * 32 + lane];
+      }
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int sk = 0; sk < 2; ++sk) fc[par][sk] = frag[P * 256 + (par * 2 + sk) * 32 + lane];
+
+  const int spf = bh * nsx;        // strip counts < 2^31 (launcher)
+  const int nstrips = spf * nframes;
+  const int nwarps = blockDim.x >> 5;
+  const int total = static_cast<int>(gridDim.x) * nwarps;
+  const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
+  const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
+                      fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
+  auto strip_at = [&](int si, int& f, int& by, int& bx0) {
+    const uint32_t u = static_cast<uint32_t>(si);
+    f = static_cast<int>(dctf::fdiv(fd_spf, u));
+    const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(spf);
+    by = static_cast<int>(dctf::fdiv(fd_nsx, rem));
+    bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * TB;
+  };
+  auto is_fast = [&](int by, int bx0) { return aligned && by * 16 + 16 <= h && (bx0 + TB) * 16 <= w; };
+  // strip si's 16 rows x 128 bytes -> buf by cp.async (4 x 16 B per lane)
+  auto fetch = [&](int si, uint8_t* buf) {
+    int f, by, bx0;
+    strip_at(si, f, by, bx0);
+    if (is_fast(by, bx0)) {
+      const uint8_t* src = in + f * frame_stride + static_cast<size_t>(by * 16) * pitch + bx0 * 16;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = 32 * k + lane, row = e >> 3, col = (e & 7) * 16;
+        cp_async16(buf + row * PS + col, src + row * pitch + col);
+      }
+    }
+    cp_async_commit();
+  };
+  pdl_trigger();
+  pdl_wait();
+  int si = static_cast<int>(blockIdx.x) * nwarps + warp;
+  if (si < nstrips) fetch(si, pix);
+  for (; si < nstrips; si += total) {
+    int f, by, bx0;
+    strip_at(si, f, by, bx0);
+    const bool fast = is_fast(by, bx0);
+    cp_async_wait_all();
+    if (!fast) {  // tile()'s edge replication, byte by byte
+      const uint8_t* ib = in + f * frame_stride;
+      for (int e = lane; e < 16 * 128; e += 32) {
+        const int r = e >> 7, c = e & 127;
+        const int y = min(by * 16 + r, h - 1), x = min(bx0 * 16 + c, w - 1);
+        pix[r * PS + c] = ib[static_cast<size_t>(y) * pitch + x];
+      }
+    }
+    __syncwarp();
+    if (si + total < nstrips) fetch(si + total, pixn);
+
+#pragma unroll 1
+    for (int b = 0; b < TB; ++b) {
+      uint8_t* pb = pix + 16 * b;
+      const uint4 top = *reinterpret_cast<const uint4*>(pb + g * PS);
+      const uint4 bot = *reinterpret_cast<const uint4*>(pb + (15 - g) * PS);
+      // q[pu][pv][s] at quad position (g, 4s + t); j = 4s + t, mirror 15 - j
+      double q[2][2][2];
+#pragma unroll
+      for (int sk = 0; sk < 2; ++sk) {
+        const uint32_t tw = sk ? top.y : top.x, tm = sk ? top.z : top.w;  // bytes j and 15 - j
+        const uint32_t bw2 = sk ? bot.y : bot.x, bm = sk ? bot.z : bot.w;
+        const int a = (tw >> (8 * t)) & 0xff, am = (tm >> (8 * (3 - t))) & 0xff;
+        const int c = (bw2 >> (8 * t)) & 0xff, cm = (bm >> (8 * (3 - t))) & 0xff;
+        const int rp = a + c, rm = a - c, rpm = am + cm, rmm = am - cm;
+        q[0][0][sk] = __int2double_rn(rp + rpm);
+        q[0][1][sk] = __int2double_rn(rp - rpm);
+        q[1][0][sk] = __int2double_rn(rm + rmm);
+        q[1][1][sk] = __int2double_rn(rm - rmm);
+      }
+      double2 z[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int pu = c >> 1, pv = c & 1;
+        double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int qq = 0; qq < P; ++qq) {
+          double2 tt = make_double2(0.0, 0.0);
+          dmma(tt, fm[qq][pv][0], q[pu][pv][0]);
+          dmma(tt, fm[qq][pv][1], q[pu][pv][1]);
+          dmma(y, fv[qq][pu][0], tt.x);
+          dmma(y, fv[qq][pu][1], tt.y);
+        }
+        if (COEF) {
+          const int bx = bx0 + b;
+          if (bx < bw) {
+            double* dst = coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 256 + (2 * g + pu) * 16;
+            dst[2 * (2 * t) + pv] = y.x;
+            dst[2 * (2 * t + 1) + pv] = y.y;
+          }
+        }
+        double2 wt = make_double2(0.0, 0.0);
+        dmma(wt, fc[pv][0], y.x);
+        dmma(wt, fc[pv][1], y.y);
+        z[c] = c == 0 ? make_double2(0.5, 0.5) : make_double2(0.0, 0.0);
+        dmma(z[c], fc[pu][0], wt.x);
+        dmma(z[c], fc[pu][1], wt.y);
+      }
+      // reflections of quad positions (g, 2t + e): Z_(pu,pv)
+      uint32_t o_ij[2], o_rj[2], o_im[2], o_rm[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double ee = e ? z[0].y : z[0].x, eo = e ? z[1].y : z[1].x;
+        const double oe = e ? z[2].y : z[2].x, oo = e ? z[3].y : z[3].x;
+        const double a = ee + eo, bq = ee - eo, cq = oe + oo, d = oe - oo;
+        o_ij[e] = floor_to_u8(a + cq);   // (g, j)
+        o_rj[e] = floor_to_u8(a - cq);   // (15-g, j)
+        o_im[e] = floor_to_u8(bq + d);   // (g, 15-j)
+        o_rm[e] = floor_to_u8(bq - d);   // (15-g, 15-j)
+      }
+      *reinterpret_cast<uint16_t*>(pb + g * PS + 2 * t) = static_cast<uint16_t>(o_ij[0] | (o_ij[1] << 8));
+      *reinterpret_cast<uint16_t*>(pb + (15 - g) * PS + 2 * t) = static_cast<uint16_t>(o_rj[0] | (o_rj[1] << 8));
+      *reinterpret_cast<uint16_t*>(pb + g * PS + 14 - 2 * t) = static_cast<uint16_t>(o_im[1] | (o_im[0] << 8));
+      *reinterpret_cast<uint16_t*>(pb + (15 - g) * PS + 14 - 2 * t) =
+          static_cast<uint16_t>(o_rm[1] | (o_rm[0] << 8));
+    }
+    __syncwarp();
+    uint8_t* ob = out + f * frame_stride;
+    if (fast) {
+      uint8_t* dst = ob + static_cast<size_t>(by * 16) * pitch + bx0 * 16;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = 32 * k + lane, row = e >> 3, col = (e & 7) * 16;
+        stg_stream(dst + row * pitch + col, *reinterpret_cast<const uint4*>(pix + row * PS + col));
+      }
+    } else {
+      for (int e = lane; e < 16 * 128; e += 32) {
+        const int r = e >> 7, c = e & 127;
+        const int y = by * 16 + r, x = bx0 * 16 + c;
+        if (y < h && x < w) ob[static_cast<size_t>(y) * pitch + x] = pix[r * PS + c];
+      }
+    }
+    __syncwarp();
+    uint8_t* tmp = pix;
+    pix = pixn;
+    pixn = tmp;
+  }
+  cp_async_wait_all();
+}
+
 dctf_status launch_fused8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                           size_t pitch, long long frame_stride, int nframes, double* coef_out,
                           cudaStream_t st) {
@@ -1031,6 +1227,26 @@ dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, 
   return DCTF_OK;
 }
 
+template <int P>
+dctf_status launch_fused16_sep_p(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
+                                 long long frame_stride, int nframes, double* coef_out, cudaStream_t st) {
+  auto kernel = coef_out ? k_fused16_sep<P, true> : k_fused16_sep<P, false>;
+  {
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(kernel), f16p::SMEM, "k_fused16_sep");
+    if (sa != DCTF_OK) return sa;
+  }
+  const int bw = (w + 15) / 16, bh = (h + 15) / 16, nsx = (bw + f16p::TB - 1) / f16p::TB;
+  const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
+  if (nstrips <= 0) return DCTF_OK;
+  if (nstrips >= (1LL << 31)) return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
+  const long long ctas = std::min<long long>(2LL * sm_count(p->device), (nstrips + f16p::WARPS - 1) / f16p::WARPS);
+  CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), f16p::WARPS * 32, f16p::SMEM, st, in, out, w, h,
+                            pitch, frame_stride, nframes, bw, bh, nsx, static_cast<const double*>(p->d_sep),
+                            coef_out));
+  dctf::add_launches(1);
+  return DCTF_OK;
+}
+
 dctf_status launch_fused16_sym(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                size_t pitch, long long frame_stride, int nframes, double* coef_out,
                                cudaStream_t st) {
@@ -1067,6 +1283,10 @@ dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* 
   if (p->n == 8 && p->sym)
     return launch_fused8_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st, host_mapped);
   if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+  if (p->n == 16 && p->sep_rank > 0 && !std::getenv("DCTF_N16_UNFUSED"))
+    return p->sep_rank == 1
+               ? launch_fused16_sep_p<1>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st)
+               : launch_fused16_sep_p<2>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (p->n == 16 && p->sym && !std::getenv("DCTF_N16_UNFUSED"))
     return launch_fused16_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (!split && !std::getenv("DCTF_N16_UNFUSED"))

@@ -38,6 +38,8 @@ struct dctf_plan {
   bool sym = false;              // H parity-block-diagonal and precision FP64 (k_fused8_sym, k_coef*_sym)
   double* d_hsym = nullptr;      // layout_sym8 (n = 8) / layout_gsym16 (n = 16) image (sym)
   double* d_hcsym = nullptr;     // layout_coefsym8 / layout_coefsym16 image (sym)
+  int sep_rank = 0;              // > 0: k_fused16_sep applies (layout_sep16), pairs
+  double* d_sep = nullptr;       // its DMMA fragment image
 
   // Device staging of the host-buffer entry (copy mode), guarded by io_mu.
   mutable std::mutex io_mu;
@@ -106,6 +108,7 @@ void layout_hfused8(const std::vector<double>& op, std::vector<double>& out);
 // Parity-class structure of H (symmetric masks) and the k_fused8_sym image.
 bool parity_block_diagonal(const std::vector<double>& op, int n);
 void layout_sym8(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out);
+bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank);
 void layout_coefsym8(const std::vector<double>& op, std::vector<double>& out);
 void layout_coefsym16(const std::vector<double>& op, std::vector<double>& out);
 void layout_gsym16(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out);

@@ -651,4 +651,132 @@ void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>&
   }
 }
 
+
+// Separable parity-class form of the n = 16 path (k_fused16_sep). The paper's
+// sandwich form Y = sum_p L_p X R_p^T (filter.hpp:30-38) with the fewest
+// pairs: the mask is split into P <= 2 separable terms w = sum_p a_p b_p^T by
+// cross approximation with full pivoting (long double). A_p / B_p are the 1-D
+// vertical / horizontal operators of the taps a_p / b_p under the plan's
+// padding (zero-drop or clamp-fold, as build_band_matrix, operators.hpp:80-98),
+// so L_p = C A_p C^t and R_p = C B_p C^t, and with the forward DCT composed in
+// per direction Y = sum_p V_p x M_p^T, V_p = C A_p, M_p = C B_p. For even taps
+// V_p[u][n-1-i] = (-1)^u V_p[u][i], so per parity class c = (pu, pv)
+//   Y_c = sum_p V_p,pu Q_c M_p,pv^T,  V_p,pu[u'][i] = V_p[2u'+pu][i] (i < n/2),
+// with Q_c the butterflied quad (exact integers): 8x8 factors at n = 16, the
+// DMMA m8n8k4 shape. Accepted only when the operator the kernel applies (the
+// half-width blocks with the exact reflection signs) equals the plan's H to
+// 1e-13 max|H|. Fragment image (DMMA A operands, lane l = 4g + t, k-step s):
+//   [p][0][pv][s][l] = M_p[2g+pv][4s+t]   (step A: T^T = M_pv Q^T)
+//   [p][1][pu][s][l] = V_p[2g+pu][2t+s]   (step B: Y = V_pu T)
+//   then [par][s][l] = C[2(2t+s)+par][g]  (inverse: W^T = C_pv^T Y^T, Z = C_pu^T W)
+bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
+  rank = 0;
+  out.clear();
+  const int n = p.n, hn = n / 2;
+  if (n != 16) return false;
+  const int kr = p.kr, kc = p.kc, hr = (kr - 1) / 2, hc = (kc - 1) / 2;
+  const bool rep = p.padding == DCTF_PAD_REPLICATE;
+  std::vector<long double> res(p.weights.begin(), p.weights.end());
+  long double wmax = 0.0L;
+  for (long double v : res) wmax = std::max(wmax, std::fabs(v));
+  if (wmax == 0.0L) return false;
+  std::vector<std::vector<long double>> as, bs;
+  for (int it = 0; it < 3; ++it) {
+    int r0 = 0, c0 = 0;
+    long double best = -1.0L;
+    for (int r = 0; r < kr; ++r)
+      for (int c = 0; c < kc; ++c)
+        if (std::fabs(res[r * kc + c]) > best) best = std::fabs(res[r * kc + c]), r0 = r, c0 = c;
+    if (best <= 1e-15L * wmax) break;
+    if (it == 2) return false;  // rank > 2
+    std::vector<long double> a(kr), b(kc);
+    for (int r = 0; r < kr; ++r) a[r] = res[r * kc + c0];
+    for (int c = 0; c < kc; ++c) b[c] = res[r0 * kc + c] / res[r0 * kc + c0];
+    for (int r = 0; r < kr; ++r)
+      for (int c = 0; c < kc; ++c) res[r * kc + c] -= a[r] * b[c];
+    as.push_back(a);
+    bs.push_back(b);
+  }
+  const int np = static_cast<int>(as.size());
+  if (np == 0) return false;
+  // 1-D operator of taps t (k long, centre h): out[i] = sum_src m[i][src] x[src]
+  auto band = [&](const std::vector<long double>& taps, int k, int h, std::vector<long double>& m) {
+    m.assign(size_t(n) * n, 0.0L);
+    for (int i = 0; i < n; ++i)
+      for (int r = 0; r < k; ++r) {
+        int src = i + r - h;
+        if (!rep) {
+          if (src < 0 || src >= n) continue;
+        } else {
+          src = clampi(src, 0, n - 1);
+        }
+        m[size_t(i) * n + src] += taps[r];
+      }
+  };
+  const double* C = p.basis.data();
+  // half-width factors: F[q][0 = V, 1 = M][u][i] = (C A_q)[u][i] / (C B_q)[u][i], i < n/2
+  std::vector<long double> F(size_t(np) * 2 * n * hn);
+  auto Fq = [&](int q, int dir, int u, int i) -> long double& { return F[((size_t(q) * 2 + dir) * n + u) * hn + i]; };
+  for (int q = 0; q < np; ++q)
+    for (int dir = 0; dir < 2; ++dir) {
+      std::vector<long double> m;
+      if (dir == 0) band(as[q], kr, hr, m);
+      else band(bs[q], kc, hc, m);
+      for (int u = 0; u < n; ++u)
+        for (int i = 0; i < hn; ++i) {
+          long double acc = 0.0L;
+          for (int k = 0; k < n; ++k) acc += static_cast<long double>(C[u * n + k]) * m[size_t(k) * n + i];
+          Fq(q, dir, u, i) = acc;
+        }
+    }
+  // the operator the kernel applies: L'_q = V'_q C^t, R'_q = M'_q C^t with
+  // V'[u][i] = F[u][i] (i < n/2), (-1)^u F[u][n-1-i] (i >= n/2)
+  auto full = [&](int q, int dir, int u, int i) {
+    const long double v = Fq(q, dir, u, i < hn ? i : n - 1 - i);
+    return (i >= hn && (u & 1)) ? -v : v;
+  };
+  std::vector<long double> L(size_t(np) * n * n), R(size_t(np) * n * n);
+  for (int q = 0; q < np; ++q)
+    for (int u = 0; u < n; ++u)
+      for (int a = 0; a < n; ++a) {
+        long double l = 0.0L, r = 0.0L;
+        for (int i = 0; i < n; ++i) {
+          l += full(q, 0, u, i) * C[a * n + i];
+          r += full(q, 1, u, i) * C[a * n + i];
+        }
+        L[(size_t(q) * n + u) * n + a] = l;
+        R[(size_t(q) * n + u) * n + a] = r;
+      }
+  const size_t nn = size_t(n) * n;
+  double hmax = 0.0, diff = 0.0;
+  for (int u = 0; u < n; ++u)
+    for (int v = 0; v < n; ++v)
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+          long double acc = 0.0L;
+          for (int q = 0; q < np; ++q) acc += L[(size_t(q) * n + u) * n + a] * R[(size_t(q) * n + v) * n + b];
+          const double h = p.op[(size_t(u) * n + v) * nn + size_t(a) * n + b];
+          hmax = std::max(hmax, std::fabs(h));
+          diff = std::max(diff, static_cast<double>(std::fabs(acc - static_cast<long double>(h))));
+        }
+  if (!(hmax > 0.0) || diff > 1e-13 * hmax) return false;
+  for (int q = 0; q < np; ++q)
+    for (int mat = 0; mat < 2; ++mat)
+      for (int par = 0; par < 2; ++par)
+        for (int sk = 0; sk < 2; ++sk)
+          for (int l = 0; l < 32; ++l) {
+            const int g = l >> 2, t = l & 3;
+            const long double v = mat == 0 ? Fq(q, 1, 2 * g + par, 4 * sk + t)    // M_pv[v'=g][j=4s+t]
+                                            : Fq(q, 0, 2 * g + par, 2 * t + sk);  // V_pu[u'=g][i=2t+s]
+            out.push_back(static_cast<double>(v));
+          }
+  for (int par = 0; par < 2; ++par)
+    for (int sk = 0; sk < 2; ++sk)
+      for (int l = 0; l < 32; ++l) {
+        const int g = l >> 2, t = l & 3;
+        out.push_back(C[(2 * (2 * t + sk) + par) * n + g]);
+      }
+  rank = np;
+  return true;
+}
 }  // namespace dctf

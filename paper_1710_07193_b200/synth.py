@@ -71,3 +71,16 @@ def motion_9x9() -> np.ndarray:
     w = np.zeros((9, 9))
     w[4, :] = 1.0 / 9.0
     return w.reshape(-1)
+
+
+def symmetric_mask(seed: int, k: int) -> np.ndarray:
+    """k x k mask symmetric in both axes with entries drawn from U(0.1, 1) on
+    one quadrant and normalised to sum 1: rank (k + 1) / 2 in general, so
+    for k >= 5 it has no separable form with <= 2 pairs (the parity-class
+    kernels without the separable path)."""
+    h = (k + 1) // 2
+    q = np.random.default_rng(seed).uniform(0.1, 1.0, (h, h))
+    idx = [min(r, k - 1 - r) for r in range(k)]
+    w = q[np.ix_(idx, idx)]
+    return (w / w.sum()).reshape(-1)
+

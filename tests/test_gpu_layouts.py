@@ -1,5 +1,5 @@
 """Memory-layout edge cases of the image entry points, for every image kernel
-(k_fused8_sym, k_fused8, k_fused16_sym, k_fused16, k_fused8_i8, the
+(k_fused8_sym, k_fused8, k_fused16_sep, k_fused16_sym, k_fused16, k_fused8_i8, the
 unfused 3xTF32 route): views whose base pointer or pitch is not 16-byte
 aligned (the kernels fall back from 16-byte vector loads to the clamped
 per-byte path), padded pitches, and the host-buffer entry on pinned and
@@ -19,7 +19,9 @@ def _plans():
     r5, _ = synth.random_mask(77, 5)
     yield "k_fused8_sym", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate)
     yield "k_fused8", P.FilterPlan(P.Mask(5, r5), 8, P.PaddingMode.kZero)
-    yield "k_fused16_sym", P.FilterPlan(P.Mask(5, g5), 16, P.PaddingMode.kZero)
+    yield "k_fused16_sep", P.FilterPlan(P.Mask(5, g5), 16, P.PaddingMode.kZero)
+    yield "k_fused16_sep", P.FilterPlan(P.Mask(3, synth.LAPLACIAN3), 16, P.PaddingMode.kReplicate)
+    yield "k_fused16_sym", P.FilterPlan(P.Mask(5, synth.symmetric_mask(5, 5)), 16, P.PaddingMode.kZero)
     yield "k_fused16", P.FilterPlan(P.Mask(5, r5), 16, P.PaddingMode.kReplicate)
     yield "k_fused8_i8", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate,
                                       precision=P.Precision.kInt8Exact)

@@ -146,23 +146,28 @@ def test_coef_sym_ragged_and_guarded(cuda, ref, n, nblocks):
 @pytest.mark.gpu
 @pytest.mark.parametrize("wh", [(512, 512), (333, 200), (1000, 77), (2048, 48)])
 def test_sym16_matches_reference_and_dense(cuda, ref, wh):
-    """k_fused16_sym (N = 16 image path for symmetric masks): reference parity
-    (coefficients 1e-9 rel, u8 except near-ties), dense-kernel agreement,
-    ragged sizes and both paddings."""
+    """k_fused16_sep / k_fused16_sym (N = 16 image paths for symmetric masks:
+    separable with <= 2 pairs / any): reference parity (coefficients 1e-9 rel,
+    u8 except near-ties), dense-kernel agreement, ragged sizes and both
+    paddings."""
     torch = cuda
     wd, h = wh
     img = synth.uniform_image(41, wd, h)
     d = torch.from_numpy(img).cuda()
     nb = ((wd + 15) // 16) * ((h + 15) // 16)
-    masks = [("gaussian7", synth.gaussian_mask(7, 2.0), 7), ("average3", np.full(9, 1.0 / 9.0), 3),
-             ("gaussian3", None, 3)]
-    for name, w, k in masks:
+    # separable masks (rank 1, 2) take k_fused16_sep, the rank-3 symmetric one k_fused16_sym
+    masks = [("gaussian7", synth.gaussian_mask(7, 2.0), 7, "k_fused16_sep"),
+             ("average3", np.full(9, 1.0 / 9.0), 3, "k_fused16_sep"),
+             ("gaussian3", None, 3, "k_fused16_sep"),
+             ("laplacian3", synth.LAPLACIAN3, 3, "k_fused16_sep"),
+             ("sym5_rank3", synth.symmetric_mask(3, 5), 5, "k_fused16_sym")]
+    for name, w, k, kernel in masks:
         if w is None:
             w, k = ref.mask_preset(name)
         for pad in (0, 1):
             sym = P.FilterPlan(P.Mask(k, w), 16, P.PaddingMode(pad))
             dense = P.FilterPlan(P.Mask(k, w), 16, P.PaddingMode(pad), precision=P.Precision.kFp64Dense)
-            assert sym.image_kernel == "k_fused16_sym" and dense.image_kernel == "k_fused16", name
+            assert sym.image_kernel == kernel and dense.image_kernel == "k_fused16", name
             cs = torch.empty((nb, 16, 16), dtype=torch.float64, device="cuda")
             cd = torch.empty_like(cs)
             os_, od = sym.filter_image(d, cs), dense.filter_image(d, cd)
@@ -193,3 +198,26 @@ def test_sym16_frames(cuda, ref):
         mism, excused, _ = tie_report(got, r_out, blocks_to_image(r_pq, 272, 144))
         assert mism == excused, f
         assert torch.equal(outs[f], plan.filter_image(d[f].contiguous()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [16])
+def test_sep16_matches_sym16(cuda, n, monkeypatch):
+    """The separable path against the parity-class path on the same masks
+    (DCTF_NO_SEP=1 at plan creation forces the latter): coefficients within
+    1e-12 x max, u8 identical; config 4's two masks and a rank-2 one."""
+    torch = cuda
+    img = torch.from_numpy(synth.uniform_image(4, 2048, 1024)).cuda()
+    nb = (2048 // 16) * (1024 // 16)
+    for k, w in ((7, synth.gaussian_mask(7, 2.0)), (9, synth.motion_9x9()), (3, synth.LAPLACIAN3)):
+        sep = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        monkeypatch.setenv("DCTF_NO_SEP", "1")
+        sym = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        monkeypatch.delenv("DCTF_NO_SEP")
+        assert sep.image_kernel == "k_fused16_sep" and sym.image_kernel == "k_fused16_sym", k
+        ca = torch.empty((nb, n, n), dtype=torch.float64, device="cuda")
+        cb = torch.empty_like(ca)
+        a, b = sep.filter_image(img, ca), sym.filter_image(img, cb)
+        assert (ca - cb).abs().max().item() <= 1e-12 * cb.abs().max().item(), k
+        assert torch.equal(a, b), k
+
