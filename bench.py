@@ -494,6 +494,9 @@ def aux_n16(c):
     ref = y.clone()
     res["n16_coef_fp64"] = coefline(c, ps.coef_kernel, ms_c, nb, 256, "fp64")
     res["n16_coef_fp64"]["streaming"] = stream(ps, "fp64")
+    ms_cn = timed_ms(c, coef_launcher(c, pn, x, y, nb), 10)
+    res["n16_coef_fp64_parity_class"] = coefline(c, pn.coef_kernel, ms_cn, nb, 256, "fp64")
+    res["n16_coef_fp64_parity_class"]["streaming"] = stream(pn, "fp64")
     ms_cd = timed_ms(c, coef_launcher(c, pd, x, y, nb), 10)
     res["n16_coef_fp64_dense"] = coefline(c, pd.coef_kernel, ms_cd, nb, 256, "fp64")
     for key, prec, tag in (("n16_coef_tf32x3", P.Precision.kTf32x3, "3xtf32"),

@@ -513,6 +513,11 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
       if (e == cudaSuccess)
         e = cudaMemcpy(p->d_sep, frag.data(), frag.size() * sizeof(double), cudaMemcpyHostToDevice);
     }
+    if (e == cudaSuccess && dctf::layout_csep16(*p, frag, p->csep_rank)) {
+      e = cudaMalloc(&p->d_csep, frag.size() * sizeof(double));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_csep, frag.data(), frag.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
   }
   if (e == cudaSuccess && p->sym && n == 16) {
     std::vector<double> hcsym;
@@ -684,6 +689,7 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_hsym);
     cudaFree(p->d_hcsym);
     cudaFree(p->d_sep);
+    cudaFree(p->d_csep);
     cudaFree(p->d_hsplit);
     cudaFree(p->d_gimg);
     cudaFree(p->d_gscale);
@@ -715,6 +721,7 @@ const char* dctf_plan_coef_kernel(const dctf_plan* p) {
   if (p->precision == DCTF_PREC_TF32X3) return "k_coef_tf32x3";
   if (p->precision == DCTF_PREC_BF16X3) return "k_coef_bf16x3";
   if (p->n == 8) return p->sym ? "k_coef8_sym" : "k_coef8";
+  if (p->csep_rank > 0) return "k_coef16_sep";
   return p->sym ? "k_coef16_sym" : "k_coef16";
 }
 

@@ -538,6 +538,145 @@ dctf_status launch_coef16_sym(const dctf_plan* p, const double* d_in, double* d_
 
 namespace dctf {
 
+// ---------------------------------------------------------------------------
+// k_coef16_sep: filter_coeffs (filter.hpp:65-67) at n = 16 for masks that are
+// symmetric in both axes and a sum of P <= 2 separable terms (layout_csep16):
+// the paper's sandwich form Y = sum_p L_p X R_p^T with the fewest pairs, per
+// parity class Y_c = sum_p L_p,pu X_c R_p,pv^T with 8x8 factors — 4 DMMA per
+// class and pair (16 per block for P = 1, against 64 in k_coef16_sym), so the
+// kernel is HBM-bound. Chain per class: U = L_pu X_c (A = L fragments, B = X_c
+// from shared memory: lane (g,t) holds X[2(4s+t)+pu][2g+pv]), then Y_c = U R^T
+// (A = U's D fragment, k = 2t + s; B = R fragments); the (pu, 0) and (pu, 1)
+// classes share each 16-byte load and store.
+// Stage = 16 blocks as ONE TMA box of 256 rows (block, u) x 16 coefficients
+// (v) with 128B swizzle (chunk v>>1 at position (v>>1) ^ (row & 7)): the
+// loads above hit 8 distinct chunks per quarter-warp. A 6-stage ring; the
+// filtered tile goes back through the same stage and a TMA store.
+namespace c16p {
+constexpr int WARPS = 8;
+constexpr int TILE = 16;
+constexpr int STAGE_BYTES = TILE * 256 * 8;  // 32 KB
+constexpr int STAGES = 6;
+constexpr int SMEM = 1024 + STAGES * STAGE_BYTES;
+}  // namespace c16p
+
+template <int P>
+__global__ void __launch_bounds__(c16p::WARPS * 32, 1)
+    k_coef16_sep(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                 const double* __restrict__ frag, long long nblocks) {
+  using namespace c16p;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* stages = align1024(smem_raw);
+  __shared__ uint64_t full[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double fl[P][2][2], fr[P][2][2];  // [pair][parity][k-step]
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+#pragma unroll
+    for (int par = 0; par < 2; ++par)
+#pragma unroll
+      for (int sk = 0; sk < 2; ++sk) {
+        fl[q][par][sk] = frag[(((q * 2 + 0) * 2 + par) * 2 + sk) * 32 + lane];
+        fr[q][par][sk] = frag[(((q * 2 + 1) * 2 + par) * 2 + sk) * 32 + lane];
+      }
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&xmap);
+    prefetch_tmap(&ymap);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  pdl_trigger();
+  __syncthreads();
+  pdl_wait();
+
+  const long long ntiles = (nblocks + TILE - 1) / TILE;
+  auto issue = [&](int s, long long tile) {
+    mbar_expect_tx(&full[s], STAGE_BYTES);
+    tma_load_2d(stages + s * STAGE_BYTES, &xmap, &full[s], 0, static_cast<int>(tile * TILE * 16));
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < STAGES - 1; ++k) {
+      const long long tile = blockIdx.x + static_cast<long long>(k) * gridDim.x;
+      if (tile < ntiles) issue(k, tile);
+    }
+
+  long long i = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+    const int s = static_cast<int>(i % STAGES);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / STAGES) & 1));
+    uint8_t* st = stages + s * STAGE_BYTES;
+#pragma unroll
+    for (int bb = 0; bb < TILE / WARPS; ++bb) {
+      uint8_t* rb = st + (2 * warp + bb) * 16 * 128;  // the block's 16 rows (u)
+      // X[2(4s+t)+pu][2g + {0,1}]: row u = 2(4s+t)+pu, chunk g
+      double2 x[2][2];
+#pragma unroll
+      for (int pu = 0; pu < 2; ++pu)
+#pragma unroll
+        for (int sk = 0; sk < 2; ++sk) {
+          const int u = 2 * (4 * sk + t) + pu;
+          x[pu][sk] = *reinterpret_cast<const double2*>(rb + u * 128 + ((g ^ (u & 7)) << 4));
+        }
+      double2 y[2][2];  // [pu][pv]: Y_c[u' = g][v' = 2t, 2t+1]
+#pragma unroll
+      for (int pu = 0; pu < 2; ++pu)
+#pragma unroll
+        for (int pv = 0; pv < 2; ++pv) {
+          y[pu][pv] = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            double2 uu = make_double2(0.0, 0.0);
+            dmma(uu, fl[q][pu][0], pv ? x[pu][0].y : x[pu][0].x);
+            dmma(uu, fl[q][pu][1], pv ? x[pu][1].y : x[pu][1].x);
+            dmma(y[pu][pv], uu.x, fr[q][pv][0]);
+            dmma(y[pu][pv], uu.y, fr[q][pv][1]);
+          }
+        }
+      // Y[2g+pu][2(2t+e) + pv]: row 2g+pu, chunk 2t+e holds pv = 0, 1
+#pragma unroll
+      for (int pu = 0; pu < 2; ++pu)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int u = 2 * g + pu, c = 2 * t + e;
+          *reinterpret_cast<double2*>(rb + u * 128 + ((c ^ (u & 7)) << 4)) =
+              e ? make_double2(y[pu][0].y, y[pu][1].y) : make_double2(y[pu][0].x, y[pu][1].x);
+        }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store_2d(&ymap, st, 0, static_cast<int>(tile * TILE * 16));
+      bulk_commit();
+      const long long nxt = tile + static_cast<long long>(STAGES - 1) * gridDim.x;
+      if (nxt < ntiles) {
+        bulk_wait_read<1>();  // the store of the previous tile (this stage's successor slot) has read it
+        issue(static_cast<int>((i + STAGES - 1) % STAGES), nxt);
+      }
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+template <int P>
+dctf_status launch_coef16_sep(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
+                              cudaStream_t st) {
+  CUtensorMap xmap, ymap;
+  dctf_status s = dctf::make_xmap(&xmap, d_in, nb * 16, 16, 256);
+  if (s == DCTF_OK) s = dctf::make_xmap(&ymap, d_out, nb * 16, 16, 256);
+  if (s != DCTF_OK) return s;
+  {
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_coef16_sep<P>), c16p::SMEM,
+                                                 "k_coef16_sep");
+    if (sa != DCTF_OK) return sa;
+  }
+  const long long ntiles = (nb + c16p::TILE - 1) / c16p::TILE;
+  const long long ctas = std::min<long long>(sm_count(p->device), ntiles);
+  CUDA_TRY(dctf::launch_pdl(k_coef16_sep<P>, static_cast<unsigned>(ctas), c16p::WARPS * 32, c16p::SMEM, st, xmap,
+                            ymap, static_cast<const double*>(p->d_csep), nb));
+  dctf::add_launches(1);
+  return DCTF_OK;
+}
+
 dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
                         cudaStream_t st) {
   if (nb == 0) return DCTF_OK;
@@ -545,6 +684,8 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
     return set_error(DCTF_INVALID_ARGUMENT, "coefficient buffers must be 16-byte aligned");
   if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in-place filter_coeffs not supported");
   if (p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3) return dctf::launch_coef_tf32x3(p, d_in, d_out, nb, st, sm_count(p->device));
+  if (p->n == 16 && p->csep_rank > 0)
+    return p->csep_rank == 1 ? launch_coef16_sep<1>(p, d_in, d_out, nb, st) : launch_coef16_sep<2>(p, d_in, d_out, nb, st);
   if (p->sym) return p->n == 8 ? launch_coef8_sym(p, d_in, d_out, nb, st) : launch_coef16_sym(p, d_in, d_out, nb, st);
   CUtensorMap map;
   const int nn = p->n * p->n;

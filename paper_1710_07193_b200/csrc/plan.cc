@@ -669,18 +669,18 @@ void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>&
 //   [p][0][pv][s][l] = M_p[2g+pv][4s+t]   (step A: T^T = M_pv Q^T)
 //   [p][1][pu][s][l] = V_p[2g+pu][2t+s]   (step B: Y = V_pu T)
 //   then [par][s][l] = C[2(2t+s)+par][g]  (inverse: W^T = C_pv^T Y^T, Z = C_pu^T W)
-bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
-  rank = 0;
-  out.clear();
-  const int n = p.n, hn = n / 2;
-  if (n != 16) return false;
-  const int kr = p.kr, kc = p.kc, hr = (kr - 1) / 2, hc = (kc - 1) / 2;
-  const bool rep = p.padding == DCTF_PAD_REPLICATE;
+namespace {
+// Cross approximation with full pivoting (long double): w = sum_p a_p b_p^T
+// with P <= 2 terms, or false (rank > 2, or w = 0).
+bool separable_taps(const dctf_plan& p, std::vector<std::vector<long double>>& as,
+                    std::vector<std::vector<long double>>& bs) {
+  const int kr = p.kr, kc = p.kc;
   std::vector<long double> res(p.weights.begin(), p.weights.end());
   long double wmax = 0.0L;
   for (long double v : res) wmax = std::max(wmax, std::fabs(v));
   if (wmax == 0.0L) return false;
-  std::vector<std::vector<long double>> as, bs;
+  as.clear();
+  bs.clear();
   for (int it = 0; it < 3; ++it) {
     int r0 = 0, c0 = 0;
     long double best = -1.0L;
@@ -697,22 +697,57 @@ bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
     as.push_back(a);
     bs.push_back(b);
   }
+  return !as.empty();
+}
+
+// 1-D operator of taps (k long, centre h) on n samples under the plan's
+// padding: out[i] = sum_src m[i][src] x[src] (zero-drop / clamp-fold, as
+// build_band_matrix, operators.hpp:80-98).
+void band_operator(const std::vector<long double>& taps, int k, int h, int n, bool rep, std::vector<long double>& m) {
+  m.assign(size_t(n) * n, 0.0L);
+  for (int i = 0; i < n; ++i)
+    for (int r = 0; r < k; ++r) {
+      int src = i + r - h;
+      if (!rep) {
+        if (src < 0 || src >= n) continue;
+      } else {
+        src = clampi(src, 0, n - 1);
+      }
+      m[size_t(i) * n + src] += taps[r];
+    }
+}
+
+// max |sum_q L_q (x) R_q - H| / max |H| in the reference's H orientation
+// (H[(u,v),(a,b)] = sum_q L_q[u][a] R_q[v][b] with R_q here = R_ref^T).
+double kron_mismatch(const dctf_plan& p, const std::vector<long double>& L, const std::vector<long double>& R, int np) {
+  const int n = p.n;
+  const size_t nn = size_t(n) * n;
+  double hmax = 0.0, diff = 0.0;
+  for (int u = 0; u < n; ++u)
+    for (int v = 0; v < n; ++v)
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+          long double acc = 0.0L;
+          for (int q = 0; q < np; ++q) acc += L[(size_t(q) * n + u) * n + a] * R[(size_t(q) * n + v) * n + b];
+          const double h = p.op[(size_t(u) * n + v) * nn + size_t(a) * n + b];
+          hmax = std::max(hmax, std::fabs(h));
+          diff = std::max(diff, static_cast<double>(std::fabs(acc - static_cast<long double>(h))));
+        }
+  return hmax > 0.0 ? diff / hmax : 1.0;
+}
+}  // namespace
+
+bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
+  rank = 0;
+  out.clear();
+  const int n = p.n, hn = n / 2;
+  if (n != 16) return false;
+  const int kr = p.kr, kc = p.kc, hr = (kr - 1) / 2, hc = (kc - 1) / 2;
+  const bool rep = p.padding == DCTF_PAD_REPLICATE;
+  std::vector<std::vector<long double>> as, bs;
+  if (!separable_taps(p, as, bs)) return false;
   const int np = static_cast<int>(as.size());
   if (np == 0) return false;
-  // 1-D operator of taps t (k long, centre h): out[i] = sum_src m[i][src] x[src]
-  auto band = [&](const std::vector<long double>& taps, int k, int h, std::vector<long double>& m) {
-    m.assign(size_t(n) * n, 0.0L);
-    for (int i = 0; i < n; ++i)
-      for (int r = 0; r < k; ++r) {
-        int src = i + r - h;
-        if (!rep) {
-          if (src < 0 || src >= n) continue;
-        } else {
-          src = clampi(src, 0, n - 1);
-        }
-        m[size_t(i) * n + src] += taps[r];
-      }
-  };
   const double* C = p.basis.data();
   // half-width factors: F[q][0 = V, 1 = M][u][i] = (C A_q)[u][i] / (C B_q)[u][i], i < n/2
   std::vector<long double> F(size_t(np) * 2 * n * hn);
@@ -720,8 +755,8 @@ bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
   for (int q = 0; q < np; ++q)
     for (int dir = 0; dir < 2; ++dir) {
       std::vector<long double> m;
-      if (dir == 0) band(as[q], kr, hr, m);
-      else band(bs[q], kc, hc, m);
+      if (dir == 0) band_operator(as[q], kr, hr, n, rep, m);
+      else band_operator(bs[q], kc, hc, n, rep, m);
       for (int u = 0; u < n; ++u)
         for (int i = 0; i < hn; ++i) {
           long double acc = 0.0L;
@@ -747,19 +782,7 @@ bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
         L[(size_t(q) * n + u) * n + a] = l;
         R[(size_t(q) * n + u) * n + a] = r;
       }
-  const size_t nn = size_t(n) * n;
-  double hmax = 0.0, diff = 0.0;
-  for (int u = 0; u < n; ++u)
-    for (int v = 0; v < n; ++v)
-      for (int a = 0; a < n; ++a)
-        for (int b = 0; b < n; ++b) {
-          long double acc = 0.0L;
-          for (int q = 0; q < np; ++q) acc += L[(size_t(q) * n + u) * n + a] * R[(size_t(q) * n + v) * n + b];
-          const double h = p.op[(size_t(u) * n + v) * nn + size_t(a) * n + b];
-          hmax = std::max(hmax, std::fabs(h));
-          diff = std::max(diff, static_cast<double>(std::fabs(acc - static_cast<long double>(h))));
-        }
-  if (!(hmax > 0.0) || diff > 1e-13 * hmax) return false;
+  if (kron_mismatch(p, L, R, np) > 1e-13) return false;
   for (int q = 0; q < np; ++q)
     for (int mat = 0; mat < 2; ++mat)
       for (int par = 0; par < 2; ++par)
@@ -776,6 +799,59 @@ bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
         const int g = l >> 2, t = l & 3;
         out.push_back(C[(2 * (2 * t + sk) + par) * n + g]);
       }
+  rank = np;
+  return true;
+}
+
+// Coefficient path of the same separable form (k_coef16_sep): per class
+// Y_c = sum_p L_p,pu X_c R_p,pv^T with L_p = C A_p C^t, R_p = C B_p C^t
+// restricted to their parity blocks (the off-parity entries are rounding
+// residue; accepted when the class-block operator equals H to 1e-13 max|H|).
+// Fragment image, lane l = 4g + t, k-step s:
+//   [p][0][pu][s][l] = L_p[2g+pu][2(4s+t)+pu]   (A of U = L_pu X_c)
+//   [p][1][pv][s][l] = R_p[2g+pv][2(2t+s)+pv]   (B of Y_c = U R_pv^T)
+bool layout_csep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
+  rank = 0;
+  out.clear();
+  const int n = p.n;
+  if (n != 16) return false;
+  const int kr = p.kr, kc = p.kc, hr = (kr - 1) / 2, hc = (kc - 1) / 2;
+  const bool rep = p.padding == DCTF_PAD_REPLICATE;
+  std::vector<std::vector<long double>> as, bs;
+  if (!separable_taps(p, as, bs)) return false;
+  const int np = static_cast<int>(as.size());
+  const double* C = p.basis.data();
+  std::vector<long double> L(size_t(np) * n * n), R(size_t(np) * n * n);
+  for (int q = 0; q < np; ++q)
+    for (int dir = 0; dir < 2; ++dir) {
+      std::vector<long double> m, cm(size_t(n) * n);
+      if (dir == 0) band_operator(as[q], kr, hr, n, rep, m);
+      else band_operator(bs[q], kc, hc, n, rep, m);
+      for (int u = 0; u < n; ++u)  // cm = C m
+        for (int i = 0; i < n; ++i) {
+          long double acc = 0.0L;
+          for (int k = 0; k < n; ++k) acc += static_cast<long double>(C[u * n + k]) * m[size_t(k) * n + i];
+          cm[size_t(u) * n + i] = acc;
+        }
+      long double* dst = (dir == 0 ? L.data() : R.data()) + size_t(q) * n * n;
+      for (int u = 0; u < n; ++u)  // (C m) C^t, parity blocks only
+        for (int a = 0; a < n; ++a) {
+          long double acc = 0.0L;
+          for (int i = 0; i < n; ++i) acc += cm[size_t(u) * n + i] * C[a * n + i];
+          dst[size_t(u) * n + a] = ((u ^ a) & 1) ? 0.0L : acc;
+        }
+    }
+  if (kron_mismatch(p, L, R, np) > 1e-13) return false;
+  for (int q = 0; q < np; ++q)
+    for (int mat = 0; mat < 2; ++mat)
+      for (int par = 0; par < 2; ++par)
+        for (int sk = 0; sk < 2; ++sk)
+          for (int l = 0; l < 32; ++l) {
+            const int g = l >> 2, t = l & 3;
+            const long double v = mat == 0 ? L[(size_t(q) * n + 2 * g + par) * n + 2 * (4 * sk + t) + par]
+                                            : R[(size_t(q) * n + 2 * g + par) * n + 2 * (2 * t + sk) + par];
+            out.push_back(static_cast<double>(v));
+          }
   rank = np;
   return true;
 }

@@ -132,7 +132,7 @@ int main() {
       eb = std::max(eb, max_abs_diff(yb[i], ref[i]));
       for (double v : ref[i].data()) mx = std::max(mx, std::abs(v));
     }
-    CHECK(f64.coef_kernel() == "k_coef16_sym" && t32.coef_kernel() == "k_coef_tf32x3" &&
+    CHECK(f64.coef_kernel() == "k_coef16_sep" && t32.coef_kernel() == "k_coef_tf32x3" &&
               b16.coef_kernel() == "k_coef_bf16x3",
           "coefficient kernel selection");
     CHECK(et <= 5e-6 * mx && eb <= 1e-4 * mx, "3xTF32 / 3xBF16 coefficients within their stated bounds");

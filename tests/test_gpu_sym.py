@@ -117,30 +117,35 @@ def test_sym_frames_and_pitch(cuda, ref):
 @pytest.mark.parametrize("n,nblocks", [(8, 1), (8, 15), (8, 16), (8, 17), (8, 129), (8, 4099),
                                        (8, 100003), (16, 1), (16, 17), (16, 4099), (16, 20011)])
 def test_coef_sym_ragged_and_guarded(cuda, ref, n, nblocks):
-    """k_coef8_sym / k_coef16_sym (TMA load/store of 16-block tiles): ragged
+    """k_coef8_sym / k_coef16_sep / k_coef16_sym (TMA load/store of 16-block tiles): ragged
     block counts, parity with the reference's filter_coeffs and the dense
     kernel, and no write past the last block (the TMA store clips the
     partial tile)."""
     torch = cuda
     from paper_1710_07193_b200 import _lib
-    w, k = (synth.gaussian_mask(5, 1.0), 5) if n == 8 else (synth.gaussian_mask(7, 2.0), 7)
-    plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
-    dense = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dense)
-    assert plan.coef_kernel == f"k_coef{n}_sym" and dense.coef_kernel == f"k_coef{n}"
+    if n == 8:
+        cases = [(synth.gaussian_mask(5, 1.0), 5, "k_coef8_sym")]
+    else:  # separable (1 and 2 pairs) -> k_coef16_sep; rank-3 symmetric -> k_coef16_sym
+        cases = [(synth.gaussian_mask(7, 2.0), 7, "k_coef16_sep"), (synth.LAPLACIAN3, 3, "k_coef16_sep"),
+                 (synth.symmetric_mask(5, 5), 5, "k_coef16_sym")]
     rng = np.random.default_rng(nblocks)
     xh = rng.uniform(-500, 500, (nblocks, n, n))
     x = torch.from_numpy(xh).cuda()
-    guard = 40
-    yb = torch.full((nblocks + guard, n, n), 12345.0, dtype=torch.float64, device="cuda")
-    _lib.check(_lib.lib.dctf_filter_coeffs(plan.handle, x.data_ptr(), yb.data_ptr(), nblocks,
-                                           torch.cuda.current_stream().cuda_stream))
-    torch.cuda.synchronize()
-    assert bool((yb[nblocks:] == 12345.0).all())
-    y = yb[:nblocks].cpu().numpy()
-    r = ref.filter_coeffs(w, k, n, 1, xh, threads=nthreads())
-    assert np.abs(y - r).max() <= 1e-9 * np.abs(r).max()
-    yd = dense.filter_coeffs(x).cpu().numpy()
-    assert np.abs(y - yd).max() <= 1e-12 * np.abs(yd).max()
+    for w, k, kernel in cases:
+        plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        dense = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dense)
+        assert plan.coef_kernel == kernel and dense.coef_kernel == f"k_coef{n}"
+        guard = 40
+        yb = torch.full((nblocks + guard, n, n), 12345.0, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib.dctf_filter_coeffs(plan.handle, x.data_ptr(), yb.data_ptr(), nblocks,
+                                               torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert bool((yb[nblocks:] == 12345.0).all()), kernel
+        y = yb[:nblocks].cpu().numpy()
+        r = ref.filter_coeffs(w, k, n, 1, xh, threads=nthreads())
+        assert np.abs(y - r).max() <= 1e-9 * np.abs(r).max(), kernel
+        yd = dense.filter_coeffs(x).cpu().numpy()
+        assert np.abs(y - yd).max() <= 1e-12 * np.abs(yd).max(), kernel
 
 
 @pytest.mark.gpu
