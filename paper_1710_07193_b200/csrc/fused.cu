@@ -991,8 +991,15 @@ constexpr int PIX_BYTES = 16 * PS;
 constexpr int SMEM = WARPS * 2 * PIX_BYTES;
 }  // namespace f16p
 
+#ifndef F16P_MINB
+#define F16P_MINB 3
+#endif
+#ifndef F16P_UNROLL
+#define F16P_UNROLL 2
+#endif
+constexpr int kF16pUnroll = F16P_UNROLL;
 template <int P, bool COEF>
-__global__ void __launch_bounds__(f16p::WARPS * 32, 2)
+__global__ void __launch_bounds__(f16p::WARPS * 32, F16P_MINB)
     k_fused16_sep(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
                   long long frame_stride, int nframes, int bw, int bh, int nsx,
                   const double* __restrict__ frag, double* __restrict__ coef_out) {
@@ -1067,7 +1074,7 @@ __global__ void __launch_bounds__(f16p::WARPS * 32, 2)
     __syncwarp();
     if (si + total < nstrips) fetch(si + total, pixn);
 
-#pragma unroll 1
+#pragma unroll kF16pUnroll
     for (int b = 0; b < TB; ++b) {
       uint8_t* pb = pix + 16 * b;
       const uint4 top = *reinterpret_cast<const uint4*>(pb + g * PS);
@@ -1239,7 +1246,8 @@ dctf_status launch_fused16_sep_p(const dctf_plan* p, const uint8_t* in, uint8_t*
   const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
   if (nstrips <= 0) return DCTF_OK;
   if (nstrips >= (1LL << 31)) return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  const long long ctas = std::min<long long>(2LL * sm_count(p->device), (nstrips + f16p::WARPS - 1) / f16p::WARPS);
+  const long long ctas = std::min<long long>(static_cast<long long>(F16P_MINB) * sm_count(p->device),
+                                            (nstrips + f16p::WARPS - 1) / f16p::WARPS);
   CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), f16p::WARPS * 32, f16p::SMEM, st, in, out, w, h,
                             pitch, frame_stride, nframes, bw, bh, nsx, static_cast<const double*>(p->d_sep),
                             coef_out));
