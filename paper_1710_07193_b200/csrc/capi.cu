@@ -506,6 +506,20 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_hsym, gsym.data(), gsym.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
+  // n = 8 sandwich kernel: worth it where it runs fewer DMMA per block than
+  // the alternative (4P + 4 against 8 parity-class / 20 dense): separable
+  // masks, and rank <= 3 when the operator has no parity structure
+  if (e == cudaSuccess && n == 8 && (precision == DCTF_PREC_FP64) && !std::getenv("DCTF_NO_SEP")) {
+    std::vector<double> frag;
+    const bool psym = dctf::parity_block_diagonal(p->op, 8);
+    if (dctf::layout_sep8(*p, frag, p->sep_rank) && (!psym || p->sep_rank == 1)) {
+      e = cudaMalloc(&p->d_sep, frag.size() * sizeof(double));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_sep, frag.data(), frag.size() * sizeof(double), cudaMemcpyHostToDevice);
+    } else {
+      p->sep_rank = 0;
+    }
+  }
   if (e == cudaSuccess && p->sym && n == 16 && !std::getenv("DCTF_NO_SEP")) {
     std::vector<double> frag;
     if (dctf::layout_sep16(*p, frag, p->sep_rank)) {
@@ -729,7 +743,7 @@ const char* dctf_plan_image_kernel(const dctf_plan* p) {
   if (!p) return nullptr;
   if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT) return "k_fused8_i8";
   if (p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3) return "unfused";
-  if (p->n == 8) return p->sym ? "k_fused8_sym" : "k_fused8";
+  if (p->n == 8) return p->sep_rank > 0 ? "k_fused8_sep" : (p->sym ? "k_fused8_sym" : "k_fused8");
   if (std::getenv("DCTF_N16_UNFUSED")) return "unfused";
   if (p->sep_rank > 0) return "k_fused16_sep";
   return p->sym ? "k_fused16_sym" : "k_fused16";

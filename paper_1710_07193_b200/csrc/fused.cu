@@ -457,6 +457,152 @@ __global__ void __launch_bounds__(f8s::WARPS * 32, F8S_MINB)
 }
 
 // ---------------------------------------------------------------------------
+// k_fused8_sep: the n = 8 image path for masks of rank P <= 3 (any symmetry;
+// layout_sep8 in plan.cc) as the paper's sandwich form with the fewest pairs,
+// Y = sum_p L_p X R_p^T (filter.hpp:30-38), forward DCT composed per direction
+// (V_p = C A_p, M_p = C B_p), then the inverse Z = C^t Y C — every product an
+// 8x8x8 DMMA pair chained fragment to fragment (see k_fused16_sep):
+//   T_p^T = M_p x^T  (B: lane (g,t) holds pixels x[g][t], x[g][t+4])
+//   Y     = sum_p V_p T_p,  W^T = C^t Y^T,  Z = C^t W + 0.5
+// 4P + 4 DMMA per block (8 for a separable mask, the parity-class kernel's
+// count, with no butterflies and no operator traffic: the 6P + 2 fragments
+// stay in registers; 16 for rank 3 against k_fused8's 20). A warp owns a strip
+// of 16 blocks (8 rows x 128 px) staged by cp.async into a double-buffered
+// per-warp tile; the output bytes overwrite their own pixels.
+namespace f8q {
+constexpr int WARPS = 8;
+constexpr int SB = 16;
+constexpr int PS = 144;  // row stride: 8-byte row loads and u16 stores conflict-free
+constexpr int PIX_BYTES = 8 * PS;
+constexpr int SMEM = WARPS * 2 * PIX_BYTES;
+}  // namespace f8q
+#ifndef F8Q_MINB
+#define F8Q_MINB 3
+#endif
+#ifndef F8Q_UNROLL
+#define F8Q_UNROLL 2
+#endif
+constexpr int kF8qUnroll = F8Q_UNROLL;
+
+template <int P, bool COEF>
+__global__ void __launch_bounds__(f8q::WARPS * 32, F8Q_MINB)
+    k_fused8_sep(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
+                 long long frame_stride, int nframes, int bw, int bh, int nsx,
+                 const double* __restrict__ frag, double* __restrict__ coef_out) {
+  using namespace f8q;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  uint8_t* pix = smem + warp * 2 * PIX_BYTES;
+  uint8_t* pixn = pix + PIX_BYTES;
+  double fm[P][2], fv[P][2], fc[2];
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+#pragma unroll
+    for (int sk = 0; sk < 2; ++sk) {
+      fm[q][sk] = frag[((q * 2 + 0) * 2 + sk) * 32 + lane];
+      fv[q][sk] = frag[((q * 2 + 1) * 2 + sk) * 32 + lane];
+    }
+#pragma unroll
+  for (int sk = 0; sk < 2; ++sk) fc[sk] = frag[P * 128 + sk * 32 + lane];
+
+  const int spf = bh * nsx;  // strip counts < 2^31 (launcher)
+  const int nstrips = spf * nframes;
+  const int nwarps = blockDim.x >> 5;
+  const int total = static_cast<int>(gridDim.x) * nwarps;
+  const bool aligned = ((pitch & 15) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((frame_stride & 15) == 0);
+  const dctf::FastDiv fd_spf = dctf::make_fastdiv(static_cast<uint32_t>(spf)),
+                      fd_nsx = dctf::make_fastdiv(static_cast<uint32_t>(nsx));
+  auto strip_at = [&](int si, int& f, int& by, int& bx0) {
+    const uint32_t u = static_cast<uint32_t>(si);
+    f = static_cast<int>(dctf::fdiv(fd_spf, u));
+    const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(spf);
+    by = static_cast<int>(dctf::fdiv(fd_nsx, rem));
+    bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(nsx)) * SB;
+  };
+  auto is_fast = [&](int by, int bx0) { return aligned && by * 8 + 8 <= h && (bx0 + SB) * 8 <= w; };
+  const int r0 = lane >> 3, c16 = (lane & 7) * 16;
+  auto fetch = [&](int si, uint8_t* buf) {
+    int f, by, bx0;
+    strip_at(si, f, by, bx0);
+    if (is_fast(by, bx0)) {
+      const uint8_t* src = in + f * frame_stride + static_cast<size_t>(by * 8) * pitch + bx0 * 8 + c16;
+      cp_async16(buf + r0 * PS + c16, src + r0 * pitch);
+      cp_async16(buf + (r0 + 4) * PS + c16, src + (r0 + 4) * pitch);
+    }
+    cp_async_commit();
+  };
+  pdl_trigger();
+  pdl_wait();
+  int si = static_cast<int>(blockIdx.x) * nwarps + warp;
+  if (si < nstrips) fetch(si, pix);
+  for (; si < nstrips; si += total) {
+    int f, by, bx0;
+    strip_at(si, f, by, bx0);
+    const bool fast = is_fast(by, bx0);
+    cp_async_wait_all();
+    if (!fast) {  // tile()'s edge replication, byte by byte
+      const uint8_t* ib = in + f * frame_stride;
+      for (int e = lane; e < 8 * 128; e += 32) {
+        const int r = e >> 7, c = e & 127;
+        const int y = min(by * 8 + r, h - 1), x = min(bx0 * 8 + c, w - 1);
+        pix[r * PS + c] = ib[static_cast<size_t>(y) * pitch + x];
+      }
+    }
+    __syncwarp();
+    if (si + total < nstrips) fetch(si + total, pixn);
+
+#pragma unroll kF8qUnroll
+    for (int b = 0; b < SB; ++b) {
+      uint8_t* pb = pix + g * PS + 8 * b;
+      const uint2 v = *reinterpret_cast<const uint2*>(pb);
+      const double a0 = __int2double_rn((v.x >> (8 * t)) & 0xff);  // x[g][t]
+      const double a1 = __int2double_rn((v.y >> (8 * t)) & 0xff);  // x[g][t + 4]
+      double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        double2 tt = make_double2(0.0, 0.0);
+        dmma(tt, fm[q][0], a0);
+        dmma(tt, fm[q][1], a1);
+        dmma(y, fv[q][0], tt.x);
+        dmma(y, fv[q][1], tt.y);
+      }
+      if (COEF) {
+        const int bx = bx0 + b;
+        if (bx < bw)
+          *reinterpret_cast<double2*>(coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 64 + g * 8 +
+                                      2 * t) = y;
+      }
+      double2 wt = make_double2(0.0, 0.0);
+      dmma(wt, fc[0], y.x);
+      dmma(wt, fc[1], y.y);
+      double2 z = make_double2(0.5, 0.5);
+      dmma(z, fc[0], wt.x);
+      dmma(z, fc[1], wt.y);
+      *reinterpret_cast<uint16_t*>(pb + 2 * t) = static_cast<uint16_t>(floor_to_u8(z.x) | (floor_to_u8(z.y) << 8));
+    }
+    __syncwarp();
+    uint8_t* ob = out + f * frame_stride;
+    if (fast) {
+      uint8_t* dst = ob + static_cast<size_t>(by * 8) * pitch + bx0 * 8 + c16;
+      stg_stream(dst + r0 * pitch, *reinterpret_cast<const uint4*>(pix + r0 * PS + c16));
+      stg_stream(dst + (r0 + 4) * pitch, *reinterpret_cast<const uint4*>(pix + (r0 + 4) * PS + c16));
+    } else {
+      for (int e = lane; e < 8 * 128; e += 32) {
+        const int r = e >> 7, c = e & 127;
+        const int y = by * 8 + r, x = bx0 * 8 + c;
+        if (y < h && x < w) ob[static_cast<size_t>(y) * pitch + x] = pix[r * PS + c];
+      }
+    }
+    __syncwarp();
+    uint8_t* tmp = pix;
+    pix = pixn;
+    pixn = tmp;
+  }
+  cp_async_wait_all();
+}
+
+// ---------------------------------------------------------------------------
 // k_fused16: the n = 16 chain fused, one HBM pass per pixel.
 //
 // CTA tile = a strip of 64 horizontally adjacent 16x16 blocks (16 rows x 1024
@@ -1235,6 +1381,29 @@ dctf_status launch_fused16(const dctf_plan* p, const uint8_t* in, uint8_t* out, 
 }
 
 template <int P>
+dctf_status launch_fused8_sep_p(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
+                                long long frame_stride, int nframes, double* coef_out, cudaStream_t st) {
+  auto kernel = coef_out ? k_fused8_sep<P, true> : k_fused8_sep<P, false>;
+  {
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(kernel), f8q::SMEM, "k_fused8_sep");
+    if (sa != DCTF_OK) return sa;
+  }
+  const int bw = (w + 7) / 8, bh = (h + 7) / 8, nsx = (bw + f8q::SB - 1) / f8q::SB;
+  const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
+  if (nstrips <= 0) return DCTF_OK;
+  if (nstrips >= (1LL << 31)) return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
+  // small images: fewer warps per CTA so the strips spread over all SMs
+  const long long slots = static_cast<long long>(F8Q_MINB) * sm_count(p->device);
+  const int nw = static_cast<int>(std::max<long long>(1, std::min<long long>(f8q::WARPS, nstrips / slots)));
+  const long long ctas = std::min<long long>(slots, (nstrips + nw - 1) / nw);
+  CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), nw * 32, nw * 2 * f8q::PIX_BYTES, st, in, out, w, h,
+                            pitch, frame_stride, nframes, bw, bh, nsx, static_cast<const double*>(p->d_sep),
+                            coef_out));
+  dctf::add_launches(1);
+  return DCTF_OK;
+}
+
+template <int P>
 dctf_status launch_fused16_sep_p(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
                                  long long frame_stride, int nframes, double* coef_out, cudaStream_t st) {
   auto kernel = coef_out ? k_fused16_sep<P, true> : k_fused16_sep<P, false>;
@@ -1246,9 +1415,10 @@ dctf_status launch_fused16_sep_p(const dctf_plan* p, const uint8_t* in, uint8_t*
   const long long nstrips = static_cast<long long>(bh) * nsx * nframes;
   if (nstrips <= 0) return DCTF_OK;
   if (nstrips >= (1LL << 31)) return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 work units)");
-  const long long ctas = std::min<long long>(static_cast<long long>(F16P_MINB) * sm_count(p->device),
-                                            (nstrips + f16p::WARPS - 1) / f16p::WARPS);
-  CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), f16p::WARPS * 32, f16p::SMEM, st, in, out, w, h,
+  const long long slots = static_cast<long long>(F16P_MINB) * sm_count(p->device);
+  const int nw = static_cast<int>(std::max<long long>(1, std::min<long long>(f16p::WARPS, nstrips / slots)));
+  const long long ctas = std::min<long long>(slots, (nstrips + nw - 1) / nw);
+  CUDA_TRY(dctf::launch_pdl(kernel, static_cast<unsigned>(ctas), nw * 32, nw * 2 * f16p::PIX_BYTES, st, in, out, w, h,
                             pitch, frame_stride, nframes, bw, bh, nsx, static_cast<const double*>(p->d_sep),
                             coef_out));
   dctf::add_launches(1);
@@ -1288,6 +1458,11 @@ dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* 
     return dctf::launch_fused8_i8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st,
                                   sm_count(p->device));
   const bool split = p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3;
+  if (p->n == 8 && p->sep_rank > 0 && !host_mapped) {
+    if (p->sep_rank == 1) return launch_fused8_sep_p<1>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+    if (p->sep_rank == 2) return launch_fused8_sep_p<2>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+    return launch_fused8_sep_p<3>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
+  }
   if (p->n == 8 && p->sym)
     return launch_fused8_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st, host_mapped);
   if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);

@@ -38,7 +38,7 @@ struct dctf_plan {
   bool sym = false;              // H parity-block-diagonal and precision FP64 (k_fused8_sym, k_coef*_sym)
   double* d_hsym = nullptr;      // layout_sym8 (n = 8) / layout_gsym16 (n = 16) image (sym)
   double* d_hcsym = nullptr;     // layout_coefsym8 / layout_coefsym16 image (sym)
-  int sep_rank = 0;              // > 0: k_fused16_sep applies (layout_sep16), pairs
+  int sep_rank = 0;              // > 0: k_fused16_sep / k_fused8_sep applies (layout_sep16 / 8), pairs
   double* d_sep = nullptr;       // its DMMA fragment image
   int csep_rank = 0;             // > 0: k_coef16_sep applies (layout_csep16), pairs
   double* d_csep = nullptr;      // its DMMA fragment image
@@ -111,6 +111,7 @@ void layout_hfused8(const std::vector<double>& op, std::vector<double>& out);
 bool parity_block_diagonal(const std::vector<double>& op, int n);
 void layout_sym8(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out);
 bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank);
+bool layout_sep8(const dctf_plan& p, std::vector<double>& out, int& rank);
 bool layout_csep16(const dctf_plan& p, std::vector<double>& out, int& rank);
 void layout_coefsym8(const std::vector<double>& op, std::vector<double>& out);
 void layout_coefsym16(const std::vector<double>& op, std::vector<double>& out);

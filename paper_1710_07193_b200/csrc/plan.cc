@@ -671,9 +671,9 @@ void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>&
 //   then [par][s][l] = C[2(2t+s)+par][g]  (inverse: W^T = C_pv^T Y^T, Z = C_pu^T W)
 namespace {
 // Cross approximation with full pivoting (long double): w = sum_p a_p b_p^T
-// with P <= 2 terms, or false (rank > 2, or w = 0).
+// with P <= max_rank terms, or false (higher rank, or w = 0).
 bool separable_taps(const dctf_plan& p, std::vector<std::vector<long double>>& as,
-                    std::vector<std::vector<long double>>& bs) {
+                    std::vector<std::vector<long double>>& bs, int max_rank = 2) {
   const int kr = p.kr, kc = p.kc;
   std::vector<long double> res(p.weights.begin(), p.weights.end());
   long double wmax = 0.0L;
@@ -681,14 +681,14 @@ bool separable_taps(const dctf_plan& p, std::vector<std::vector<long double>>& a
   if (wmax == 0.0L) return false;
   as.clear();
   bs.clear();
-  for (int it = 0; it < 3; ++it) {
+  for (int it = 0; it <= max_rank; ++it) {
     int r0 = 0, c0 = 0;
     long double best = -1.0L;
     for (int r = 0; r < kr; ++r)
       for (int c = 0; c < kc; ++c)
         if (std::fabs(res[r * kc + c]) > best) best = std::fabs(res[r * kc + c]), r0 = r, c0 = c;
     if (best <= 1e-15L * wmax) break;
-    if (it == 2) return false;  // rank > 2
+    if (it == max_rank) return false;  // rank > max_rank
     std::vector<long double> a(kr), b(kc);
     for (int r = 0; r < kr; ++r) a[r] = res[r * kc + c0];
     for (int c = 0; c < kc; ++c) b[c] = res[r0 * kc + c] / res[r0 * kc + c0];
@@ -852,6 +852,63 @@ bool layout_csep16(const dctf_plan& p, std::vector<double>& out, int& rank) {
                                             : R[(size_t(q) * n + 2 * g + par) * n + 2 * (2 * t + sk) + par];
             out.push_back(static_cast<double>(v));
           }
+  rank = np;
+  return true;
+}
+
+// n = 8 image path of the same sandwich form without parity classes
+// (k_fused8_sep): Y = sum_p V_p x M_p^T with the full 8x8 factors V_p = C A_p,
+// M_p = C B_p (any mask of rank P <= 3, symmetric or not), then the inverse
+// Z = C^t Y C, every product a DMMA pair chained fragment to fragment.
+// Accepted when sum_p (V_p C^t) (x) (M_p C^t) equals H to 1e-13 max|H|.
+// Fragment image, lane l = 4g + t, k-step s:
+//   [p][0][s][l] = M_p[g][4s+t]   (T^T = M_p x^T)
+//   [p][1][s][l] = V_p[g][2t+s]   (Y = sum_p V_p T_p)
+//   then [s][l] = C[2t+s][g]      (W^T = C^t Y^T, Z = C^t W)
+bool layout_sep8(const dctf_plan& p, std::vector<double>& out, int& rank) {
+  rank = 0;
+  out.clear();
+  const int n = p.n;
+  if (n != 8) return false;
+  const int kr = p.kr, kc = p.kc, hr = (kr - 1) / 2, hc = (kc - 1) / 2;
+  const bool rep = p.padding == DCTF_PAD_REPLICATE;
+  std::vector<std::vector<long double>> as, bs;
+  if (!separable_taps(p, as, bs, 3)) return false;
+  const int np = static_cast<int>(as.size());
+  const double* C = p.basis.data();
+  std::vector<long double> F(size_t(np) * 2 * 64), L(size_t(np) * 64), R(size_t(np) * 64);
+  for (int q = 0; q < np; ++q)
+    for (int dir = 0; dir < 2; ++dir) {
+      std::vector<long double> m;
+      if (dir == 0) band_operator(as[q], kr, hr, n, rep, m);
+      else band_operator(bs[q], kc, hc, n, rep, m);
+      long double* f = &F[(size_t(q) * 2 + dir) * 64];
+      for (int u = 0; u < n; ++u)  // f = C m
+        for (int i = 0; i < n; ++i) {
+          long double acc = 0.0L;
+          for (int k = 0; k < n; ++k) acc += static_cast<long double>(C[u * n + k]) * m[size_t(k) * n + i];
+          f[u * n + i] = acc;
+        }
+      long double* d = (dir == 0 ? L.data() : R.data()) + size_t(q) * 64;
+      for (int u = 0; u < n; ++u)  // (C m) C^t
+        for (int a = 0; a < n; ++a) {
+          long double acc = 0.0L;
+          for (int i = 0; i < n; ++i) acc += f[u * n + i] * C[a * n + i];
+          d[u * n + a] = acc;
+        }
+    }
+  if (kron_mismatch(p, L, R, np) > 1e-13) return false;
+  for (int q = 0; q < np; ++q)
+    for (int mat = 0; mat < 2; ++mat)
+      for (int sk = 0; sk < 2; ++sk)
+        for (int l = 0; l < 32; ++l) {
+          const int g = l >> 2, t = l & 3;
+          const long double v = mat == 0 ? F[(size_t(q) * 2 + 1) * 64 + g * 8 + 4 * sk + t]   // M_p[g][4s+t]
+                                          : F[(size_t(q) * 2 + 0) * 64 + g * 8 + 2 * t + sk];  // V_p[g][2t+s]
+          out.push_back(static_cast<double>(v));
+        }
+  for (int sk = 0; sk < 2; ++sk)
+    for (int l = 0; l < 32; ++l) out.push_back(C[(2 * (l & 3) + sk) * n + (l >> 2)]);
   rank = np;
   return true;
 }

@@ -56,3 +56,19 @@ def tie_report(ours, ref_u8, ref_prequant_img, window=1e-6):
     frac = np.abs(np.abs(ref_prequant_img - np.floor(ref_prequant_img)) - 0.5)
     near = frac < window
     return int(diff.sum()), int((diff & near).sum()), int(near.sum())
+
+
+def expected_n8_kernel(w, kr, kc=None):
+    """The n = 8 FP64 image kernel a plan picks for mask w (kr x kc): the
+    sandwich kernel when it runs fewer DMMA than the alternative (rank 1, or
+    rank <= 3 without parity structure), the parity-class kernel for other
+    masks symmetric in both axes, else the dense one."""
+    kc = kc or kr
+    m = np.asarray(w, dtype=np.float64).reshape(kr, kc)
+    sym = np.array_equal(m, m[::-1, :]) and np.array_equal(m, m[:, ::-1])
+    s = np.linalg.svd(m, compute_uv=False)
+    rank = int((s > 1e-13 * s[0]).sum())
+    if rank == 1 or (not sym and rank <= 3):
+        return "k_fused8_sep"
+    return "k_fused8_sym" if sym else "k_fused8"
+

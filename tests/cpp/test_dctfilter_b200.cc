@@ -110,7 +110,7 @@ int main() {
     const FilterPlan sym(g, 8, PaddingMode::kReplicate);
     const FilterPlan dense(g, 8, PaddingMode::kReplicate, Precision::kFp64Dense);
     const FilterPlan i8(g, 8, PaddingMode::kReplicate, Precision::kInt8Exact);
-    CHECK(sym.image_kernel() == "k_fused8_sym" && dense.image_kernel() == "k_fused8" &&
+    CHECK(sym.image_kernel() == "k_fused8_sep" && dense.image_kernel() == "k_fused8" &&
               i8.image_kernel() == "k_fused8_i8",
           "image kernel selection by mask structure / precision");
     const GrayImage a = filter_image(sym, img), b = filter_image(dense, img), c = filter_image(i8, img);

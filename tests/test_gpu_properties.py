@@ -63,11 +63,13 @@ def test_parity_class_kernel_equals_dense_config3_size(cuda):
     torch = cuda
     img = torch.from_numpy(synth.uniform_image(3, 8192, 8192)).cuda()
     nb = 1024 * 1024
-    for w, k in ((synth.gaussian_mask(5, 1.0), 5), (np.full(9, 1.0 / 9.0), 3)):
+    for w, k, kernel in ((synth.gaussian_mask(5, 1.0), 5, "k_fused8_sep"), (np.full(9, 1.0 / 9.0), 3, "k_fused8_sep"),
+                         (synth.symmetric_mask(5, 5), 5, "k_fused8_sym"), (synth.LAPLACIAN3, 3, "k_fused8_sym"),
+                         (synth.random_mask(1003, 3)[0], 3, "k_fused8_sep")):
         for pad in (P.PaddingMode.kZero, P.PaddingMode.kReplicate):
             sym = P.FilterPlan(P.Mask(k, w), 8, pad)
             dense = P.FilterPlan(P.Mask(k, w), 8, pad, precision=P.Precision.kFp64Dense)
-            assert sym.image_kernel == "k_fused8_sym" and dense.image_kernel == "k_fused8"
+            assert sym.image_kernel == kernel and dense.image_kernel == "k_fused8"
             cs = torch.empty((nb, 8, 8), dtype=torch.float64, device="cuda")
             cd = torch.empty_like(cs)
             os_, od = sym.filter_image(img, cs), dense.filter_image(img, cd)

@@ -14,7 +14,7 @@ import pytest
 
 import paper_1710_07193_b200 as P
 from paper_1710_07193_b200 import synth
-from conftest import blocks_to_image, nthreads, tie_report
+from conftest import blocks_to_image, expected_n8_kernel, nthreads, tie_report
 
 SYMMETRIC = {
     "average3": (np.full(9, 1.0 / 9.0), 3),
@@ -49,20 +49,31 @@ def _masks(ref):
 
 
 @pytest.mark.gpu
-def test_kernel_selection(cuda, ref):
+def test_kernel_selection(cuda, ref, monkeypatch):
     for name, w, k in _masks(ref):
-        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8_sym", name
+        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero).image_kernel == expected_n8_kernel(w, k), name
         assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero,
                             precision=P.Precision.kFp64Dense).image_kernel == "k_fused8", name
-    w, _ = synth.random_mask(3, 3)
-    assert P.FilterPlan(P.Mask(3, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8"
+        monkeypatch.setenv("DCTF_NO_SEP", "1")
+        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8_sym", name
+        monkeypatch.delenv("DCTF_NO_SEP")
+    w, _ = synth.random_mask(3, 3)   # rank 3, no parity structure: sandwich at n = 8, dense at 16
+    assert P.FilterPlan(P.Mask(3, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8_sep"
     assert P.FilterPlan(P.Mask(3, w), 16, P.PaddingMode.kZero).image_kernel == "k_fused16"
+    w, _ = synth.random_mask(5, 5)   # rank 5: dense
+    assert P.FilterPlan(P.Mask(5, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8"
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("nosep", [False, True])
 @pytest.mark.parametrize("wh", [(512, 512), (333, 200), (1000, 77)])
-def test_sym_matches_reference_and_dense(cuda, ref, wh):
+def test_sym_matches_reference_and_dense(cuda, ref, wh, nosep, monkeypatch):
+    """Every symmetric mask through the kernel its plan picks (k_fused8_sep
+    for the separable ones, k_fused8_sym otherwise) and, with DCTF_NO_SEP=1,
+    through k_fused8_sym."""
     torch = cuda
+    if nosep:
+        monkeypatch.setenv("DCTF_NO_SEP", "1")
     wd, h = wh
     img = synth.uniform_image(31, wd, h)
     d = torch.from_numpy(img).cuda()
@@ -95,7 +106,7 @@ def test_sym_frames_and_pitch(cuda, ref):
     wr, _ = synth.random_mask(5, 5)
     plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kReplicate)
     plan_r = P.FilterPlan(P.Mask(5, wr), 8, P.PaddingMode.kReplicate)
-    assert plan.image_kernel == "k_fused8_sym" and plan_r.image_kernel == "k_fused8"
+    assert plan.image_kernel == "k_fused8_sep" and plan_r.image_kernel == "k_fused8"
     frames = np.stack([synth.sinusoid_image(40 + f, 264, 136) for f in range(4)])
     d = torch.from_numpy(frames).cuda()
     outs = P.filter_frames(d, [plan, plan_r], [0, 1, 0, 1])
