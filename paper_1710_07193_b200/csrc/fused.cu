@@ -479,10 +479,9 @@ constexpr int SMEM = WARPS * 2 * PIX_BYTES;
 #ifndef F8Q_MINB
 #define F8Q_MINB 3
 #endif
-#ifndef F8Q_UNROLL
-#define F8Q_UNROLL 2
+#ifndef F8Q_ILP
+#define F8Q_ILP 4
 #endif
-constexpr int kF8qUnroll = F8Q_UNROLL;
 
 template <int P, bool COEF>
 __global__ void __launch_bounds__(f8q::WARPS * 32, F8Q_MINB)
@@ -552,34 +551,51 @@ __global__ void __launch_bounds__(f8q::WARPS * 32, F8Q_MINB)
     __syncwarp();
     if (si + total < nstrips) fetch(si + total, pixn);
 
-#pragma unroll kF8qUnroll
-    for (int b = 0; b < SB; ++b) {
-      uint8_t* pb = pix + g * PS + 8 * b;
-      const uint2 v = *reinterpret_cast<const uint2*>(pb);
-      const double a0 = __int2double_rn((v.x >> (8 * t)) & 0xff);  // x[g][t]
-      const double a1 = __int2double_rn((v.y >> (8 * t)) & 0xff);  // x[g][t + 4]
-      double2 y = make_double2(0.0, 0.0);
+    // F8Q_ILP blocks in lock step: their DMMA chains interleave (one chain
+    // of 4P + 4 dependent DMMAs per block)
+#pragma unroll 1
+    for (int b0 = 0; b0 < SB; b0 += F8Q_ILP) {
+      double2 y[F8Q_ILP], tt[F8Q_ILP], wt[F8Q_ILP], z[F8Q_ILP];
+      double a0[F8Q_ILP], a1[F8Q_ILP];
+#pragma unroll
+      for (int k = 0; k < F8Q_ILP; ++k) {
+        const uint2 v = *reinterpret_cast<const uint2*>(pix + g * PS + 8 * (b0 + k));
+        a0[k] = __int2double_rn((v.x >> (8 * t)) & 0xff);  // x[g][t]
+        a1[k] = __int2double_rn((v.y >> (8 * t)) & 0xff);  // x[g][t + 4]
+        y[k] = make_double2(0.0, 0.0);
+      }
 #pragma unroll
       for (int q = 0; q < P; ++q) {
-        double2 tt = make_double2(0.0, 0.0);
-        dmma(tt, fm[q][0], a0);
-        dmma(tt, fm[q][1], a1);
-        dmma(y, fv[q][0], tt.x);
-        dmma(y, fv[q][1], tt.y);
+#pragma unroll
+        for (int k = 0; k < F8Q_ILP; ++k) { tt[k] = make_double2(0.0, 0.0); dmma(tt[k], fm[q][0], a0[k]); }
+#pragma unroll
+        for (int k = 0; k < F8Q_ILP; ++k) dmma(tt[k], fm[q][1], a1[k]);
+#pragma unroll
+        for (int k = 0; k < F8Q_ILP; ++k) dmma(y[k], fv[q][0], tt[k].x);
+#pragma unroll
+        for (int k = 0; k < F8Q_ILP; ++k) dmma(y[k], fv[q][1], tt[k].y);
       }
       if (COEF) {
-        const int bx = bx0 + b;
-        if (bx < bw)
-          *reinterpret_cast<double2*>(coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 64 + g * 8 +
-                                      2 * t) = y;
+#pragma unroll
+        for (int k = 0; k < F8Q_ILP; ++k) {
+          const int bx = bx0 + b0 + k;
+          if (bx < bw)
+            *reinterpret_cast<double2*>(coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 64 + g * 8 +
+                                        2 * t) = y[k];
+        }
       }
-      double2 wt = make_double2(0.0, 0.0);
-      dmma(wt, fc[0], y.x);
-      dmma(wt, fc[1], y.y);
-      double2 z = make_double2(0.5, 0.5);
-      dmma(z, fc[0], wt.x);
-      dmma(z, fc[1], wt.y);
-      *reinterpret_cast<uint16_t*>(pb + 2 * t) = static_cast<uint16_t>(floor_to_u8(z.x) | (floor_to_u8(z.y) << 8));
+#pragma unroll
+      for (int k = 0; k < F8Q_ILP; ++k) { wt[k] = make_double2(0.0, 0.0); dmma(wt[k], fc[0], y[k].x); }
+#pragma unroll
+      for (int k = 0; k < F8Q_ILP; ++k) dmma(wt[k], fc[1], y[k].y);
+#pragma unroll
+      for (int k = 0; k < F8Q_ILP; ++k) { z[k] = make_double2(0.5, 0.5); dmma(z[k], fc[0], wt[k].x); }
+#pragma unroll
+      for (int k = 0; k < F8Q_ILP; ++k) dmma(z[k], fc[1], wt[k].y);
+#pragma unroll
+      for (int k = 0; k < F8Q_ILP; ++k)
+        *reinterpret_cast<uint16_t*>(pix + g * PS + 8 * (b0 + k) + 2 * t) =
+            static_cast<uint16_t>(floor_to_u8(z[k].x) | (floor_to_u8(z[k].y) << 8));
     }
     __syncwarp();
     uint8_t* ob = out + f * frame_stride;
