@@ -1255,34 +1255,50 @@ __global__ void __launch_bounds__(f16p::WARPS * 32, F16P_MINB)
         q[1][0][sk] = __int2double_rn(rm + rmm);
         q[1][1][sk] = __int2double_rn(rm - rmm);
       }
-      double2 z[4];
+      // the four class chains in lock step so their DMMAs interleave
+      double2 y[4], tt[4], wt[4], z[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int pu = c >> 1, pv = c & 1;
-        double2 y = make_double2(0.0, 0.0);
+      for (int c = 0; c < 4; ++c) y[c] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int qq = 0; qq < P; ++qq) {
-          double2 tt = make_double2(0.0, 0.0);
-          dmma(tt, fm[qq][pv][0], q[pu][pv][0]);
-          dmma(tt, fm[qq][pv][1], q[pu][pv][1]);
-          dmma(y, fv[qq][pu][0], tt.x);
-          dmma(y, fv[qq][pu][1], tt.y);
+      for (int qq = 0; qq < P; ++qq) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          tt[c] = make_double2(0.0, 0.0);
+          dmma(tt[c], fm[qq][c & 1][0], q[c >> 1][c & 1][0]);
         }
-        if (COEF) {
-          const int bx = bx0 + b;
-          if (bx < bw) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma(tt[c], fm[qq][c & 1][1], q[c >> 1][c & 1][1]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma(y[c], fv[qq][c >> 1][0], tt[c].x);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma(y[c], fv[qq][c >> 1][1], tt[c].y);
+      }
+      if (COEF) {
+        const int bx = bx0 + b;
+        if (bx < bw) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int pu = c >> 1, pv = c & 1;
             double* dst = coef_out + ((static_cast<long long>(f) * bh + by) * bw + bx) * 256 + (2 * g + pu) * 16;
-            dst[2 * (2 * t) + pv] = y.x;
-            dst[2 * (2 * t + 1) + pv] = y.y;
+            dst[2 * (2 * t) + pv] = y[c].x;
+            dst[2 * (2 * t + 1) + pv] = y[c].y;
           }
         }
-        double2 wt = make_double2(0.0, 0.0);
-        dmma(wt, fc[pv][0], y.x);
-        dmma(wt, fc[pv][1], y.y);
-        z[c] = c == 0 ? make_double2(0.5, 0.5) : make_double2(0.0, 0.0);
-        dmma(z[c], fc[pu][0], wt.x);
-        dmma(z[c], fc[pu][1], wt.y);
       }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        wt[c] = make_double2(0.0, 0.0);
+        dmma(wt[c], fc[c & 1][0], y[c].x);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dmma(wt[c], fc[c & 1][1], y[c].y);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        z[c] = c == 0 ? make_double2(0.5, 0.5) : make_double2(0.0, 0.0);
+        dmma(z[c], fc[c >> 1][0], wt[c].x);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dmma(z[c], fc[c >> 1][1], wt[c].y);
       // reflections of quad positions (g, 2t + e): Z_(pu,pv)
       uint32_t o_ij[2], o_rj[2], o_im[2], o_rm[2];
 #pragma unroll
