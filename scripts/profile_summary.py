@@ -60,7 +60,7 @@ for rep in sys.argv[3:]:
     m = {k: {"value": vals[hh.index(k)], "unit": units[hh.index(k)]} for k in KEYS if k in hh}
     json.dump({"report": os.path.basename(rep), "kernel": name, "metrics": m},
               open(os.path.join(out, f"ncu_{name}.json"), "w"), indent=1)
-    if base in ("k_fused8", "k_fused8_sym"):
+    if base in ("k_fused8", "k_fused8_sym", "k_fused8_sep"):
         def tobytes(e):
             s = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[e["unit"]]
             return float(e["value"].replace(",", "")) * s
@@ -69,7 +69,7 @@ for rep in sys.argv[3:]:
                    "source": f"profiles/{tag}/ncu_{name}.json (ncu --set full, bench config 2, one launch)"},
                   open(os.path.join(ROOT, "profiles", f"ncu_{base}_config2.json"), "w"), indent=1)
 # the bench headline kernel's traffic file (bench.py: ncu_traffic)
-hp = os.path.join(ROOT, "profiles", "ncu_k_fused8_sym_config2.json")
+hp = os.path.join(ROOT, "profiles", "ncu_k_fused8_sep_config2.json")
 if os.path.exists(hp):
     import shutil
     shutil.copy(hp, os.path.join(ROOT, "profiles", "ncu_headline_config2.json"))
