@@ -387,6 +387,16 @@ def aux_cfg3(c):
         ms = timed_ms(c, image_launcher(c, pl, img, out, 8192, 8192), 10)
         res[name] = {"kernel": pl.image_kernel, "ms": ms, "blocks_per_s": 1048576 / (ms / 1e3)}
         ref_out = out.clone()
+        if name == "replicate":  # the coefficient path on the same mask: sandwich vs dense kernel
+            x = pl.forward_image(img)
+            y = torch.empty_like(x)
+            pdn = P.FilterPlan(P.Mask(3, r3), N, pad, precision=P.Precision.kFp64Dense)
+            ms_s = timed_ms(c, coef_launcher(c, pl, x, y, 1048576), 10)
+            ms_dn = timed_ms(c, coef_launcher(c, pdn, x, y, 1048576), 10)
+            res["coef_path"] = {"kernel": pl.coef_kernel, **coefline(c, pl.coef_kernel, ms_s, 1048576, 64, "fp64"),
+                                "dense_kernel": pdn.coef_kernel,
+                                "dense_blocks_per_s": 1048576 / (ms_dn / 1e3)}
+            del x, y
         px = P.FilterPlan(P.Mask(3, r3), N, pad, precision=P.Precision.kInt8Exact)
         ms = timed_ms(c, image_launcher(c, px, img, out, 8192, 8192), 10)
         res[name + "_int8exact"] = {"kernel": px.image_kernel, "ms": ms, "blocks_per_s": 1048576 / (ms / 1e3),

@@ -519,6 +519,14 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     } else {
       p->sep_rank = 0;
     }
+    // coefficient path: the parity-class k_coef8_sym is already HBM-bound
+    if (e == cudaSuccess && !psym && dctf::layout_csep8(*p, frag, p->csep_rank)) {
+      e = cudaMalloc(&p->d_csep, frag.size() * sizeof(double));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_csep, frag.data(), frag.size() * sizeof(double), cudaMemcpyHostToDevice);
+    } else {
+      p->csep_rank = 0;
+    }
   }
   if (e == cudaSuccess && p->sym && n == 16 && !std::getenv("DCTF_NO_SEP")) {
     std::vector<double> frag;
@@ -734,8 +742,8 @@ const char* dctf_plan_coef_kernel(const dctf_plan* p) {
   if (!p) return nullptr;
   if (p->precision == DCTF_PREC_TF32X3) return "k_coef_tf32x3";
   if (p->precision == DCTF_PREC_BF16X3) return "k_coef_bf16x3";
+  if (p->csep_rank > 0) return p->n == 8 ? "k_coef8_sep" : "k_coef16_sep";
   if (p->n == 8) return p->sym ? "k_coef8_sym" : "k_coef8";
-  if (p->csep_rank > 0) return "k_coef16_sep";
   return p->sym ? "k_coef16_sym" : "k_coef16";
 }
 

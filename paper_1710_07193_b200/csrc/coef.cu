@@ -677,6 +677,122 @@ dctf_status launch_coef16_sep(const dctf_plan* p, const double* d_in, double* d_
   return DCTF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// k_coef8_sep: filter_coeffs (filter.hpp:65-67) at n = 8 for masks of rank
+// P <= 3 without parity structure (layout_csep8; the symmetric ones take the
+// HBM-bound k_coef8_sym): the sandwich form Y = sum_p L_p X R_p^T, per block
+// and pair U = L_p X (A = L fragments, B = X: lane (g,t) holds X[4s+t][g]),
+// Y += U R_p^T (A = U's D fragment with k = 2t + s, B = R fragments):
+// 4 DMMA per pair (12 for rank 3 against k_coef8's 16), so HBM-bound up to
+// rank 2. Blocks are contiguous 512-byte tiles, so a stage of 32 blocks moves
+// with ONE bulk copy each way (cp.async.bulk, no tensor map); the per-lane
+// accesses (8-byte loads X[4s+t][g], 16-byte stores of Y[g][2t..2t+1]) are
+// conflict-free in that natural layout. 8-stage ring, one CTA per SM.
+namespace c8p {
+constexpr int WARPS = 8;
+constexpr int TILE = 32;                     // blocks per stage
+constexpr int STAGE_BYTES = TILE * 64 * 8;   // 16 KB
+constexpr int STAGES = 8;
+constexpr int SMEM = 1024 + STAGES * STAGE_BYTES;
+}  // namespace c8p
+
+template <int P>
+__global__ void __launch_bounds__(c8p::WARPS * 32, 1)
+    k_coef8_sep(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ frag,
+                long long nblocks) {
+  using namespace c8p;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* stages = align1024(smem_raw);
+  __shared__ uint64_t full[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double fl[P][2], fr[P][2];
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+#pragma unroll
+    for (int sk = 0; sk < 2; ++sk) {
+      fl[q][sk] = frag[((q * 2 + 0) * 2 + sk) * 32 + lane];
+      fr[q][sk] = frag[((q * 2 + 1) * 2 + sk) * 32 + lane];
+    }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  pdl_trigger();
+  __syncthreads();
+  pdl_wait();
+  const long long ntiles = (nblocks + TILE - 1) / TILE;
+  auto tile_bytes = [&](long long tile) {
+    return static_cast<uint32_t>(min(static_cast<long long>(TILE), nblocks - tile * TILE) * 512);
+  };
+  auto issue = [&](int s, long long tile) {
+    const uint32_t bytes = tile_bytes(tile);
+    mbar_expect_tx(&full[s], bytes);
+    bulk_load(stages + s * STAGE_BYTES, x + tile * TILE * 64, bytes, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < STAGES - 1; ++k) {
+      const long long tile = blockIdx.x + static_cast<long long>(k) * gridDim.x;
+      if (tile < ntiles) issue(k, tile);
+    }
+  long long i = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+    const int s = static_cast<int>(i % STAGES);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / STAGES) & 1));
+    uint8_t* st = stages + s * STAGE_BYTES;
+    // warp w: blocks 4w .. 4w + 3 of the stage, in lock step
+    double a[4][2];
+    double2 acc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double* xb = reinterpret_cast<const double*>(st + (4 * warp + k) * 512);
+      a[k][0] = xb[t * 8 + g];
+      a[k][1] = xb[(4 + t) * 8 + g];
+      acc[k] = make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      double2 uu[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { uu[k] = make_double2(0.0, 0.0); dmma(uu[k], fl[q][0], a[k][0]); }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dmma(uu[k], fl[q][1], a[k][1]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dmma(acc[k], uu[k].x, fr[q][0]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dmma(acc[k], uu[k].y, fr[q][1]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)  // Y[g][2t], Y[g][2t+1]: every lane has read this block (mma.sync)
+      *reinterpret_cast<double2*>(st + (4 * warp + k) * 512 + g * 64 + 16 * t) = acc[k];
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_store(y + tile * TILE * 64, st, tile_bytes(tile));
+      bulk_commit();
+      const long long nxt = tile + static_cast<long long>(STAGES - 1) * gridDim.x;
+      if (nxt < ntiles) {
+        bulk_wait_read<1>();  // the previous tile's store (this slot's last user) has read it
+        issue(static_cast<int>((i + STAGES - 1) % STAGES), nxt);
+      }
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+template <int P>
+dctf_status launch_coef8_sep(const dctf_plan* p, const double* d_in, double* d_out, long long nb, cudaStream_t st) {
+  {
+    const dctf_status sa = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_coef8_sep<P>), c8p::SMEM, "k_coef8_sep");
+    if (sa != DCTF_OK) return sa;
+  }
+  const long long ntiles = (nb + c8p::TILE - 1) / c8p::TILE;
+  const long long ctas = std::min<long long>(sm_count(p->device), ntiles);
+  CUDA_TRY(dctf::launch_pdl(k_coef8_sep<P>, static_cast<unsigned>(ctas), c8p::WARPS * 32, c8p::SMEM, st, d_in, d_out,
+                            static_cast<const double*>(p->d_csep), nb));
+  dctf::add_launches(1);
+  return DCTF_OK;
+}
+
 dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, long long nb,
                         cudaStream_t st) {
   if (nb == 0) return DCTF_OK;
@@ -684,6 +800,11 @@ dctf_status launch_coef(const dctf_plan* p, const double* d_in, double* d_out, l
     return set_error(DCTF_INVALID_ARGUMENT, "coefficient buffers must be 16-byte aligned");
   if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in-place filter_coeffs not supported");
   if (p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3) return dctf::launch_coef_tf32x3(p, d_in, d_out, nb, st, sm_count(p->device));
+  if (p->n == 8 && p->csep_rank > 0) {
+    if (p->csep_rank == 1) return launch_coef8_sep<1>(p, d_in, d_out, nb, st);
+    if (p->csep_rank == 2) return launch_coef8_sep<2>(p, d_in, d_out, nb, st);
+    return launch_coef8_sep<3>(p, d_in, d_out, nb, st);
+  }
   if (p->n == 16 && p->csep_rank > 0)
     return p->csep_rank == 1 ? launch_coef16_sep<1>(p, d_in, d_out, nb, st) : launch_coef16_sep<2>(p, d_in, d_out, nb, st);
   if (p->sym) return p->n == 8 ? launch_coef8_sym(p, d_in, d_out, nb, st) : launch_coef16_sym(p, d_in, d_out, nb, st);

@@ -40,7 +40,7 @@ struct dctf_plan {
   double* d_hcsym = nullptr;     // layout_coefsym8 / layout_coefsym16 image (sym)
   int sep_rank = 0;              // > 0: k_fused16_sep / k_fused8_sep applies (layout_sep16 / 8), pairs
   double* d_sep = nullptr;       // its DMMA fragment image
-  int csep_rank = 0;             // > 0: k_coef16_sep applies (layout_csep16), pairs
+  int csep_rank = 0;             // > 0: k_coef16_sep / k_coef8_sep applies (layout_csep16 / 8), pairs
   double* d_csep = nullptr;      // its DMMA fragment image
 
   // Device staging of the host-buffer entry (copy mode), guarded by io_mu.
@@ -113,6 +113,7 @@ void layout_sym8(const std::vector<double>& op, const std::vector<double>& basis
 bool layout_sep16(const dctf_plan& p, std::vector<double>& out, int& rank);
 bool layout_sep8(const dctf_plan& p, std::vector<double>& out, int& rank);
 bool layout_csep16(const dctf_plan& p, std::vector<double>& out, int& rank);
+bool layout_csep8(const dctf_plan& p, std::vector<double>& out, int& rank);
 void layout_coefsym8(const std::vector<double>& op, std::vector<double>& out);
 void layout_coefsym16(const std::vector<double>& op, std::vector<double>& out);
 void layout_gsym16(const std::vector<double>& op, const std::vector<double>& basis, std::vector<double>& out);

@@ -912,4 +912,54 @@ bool layout_sep8(const dctf_plan& p, std::vector<double>& out, int& rank) {
   rank = np;
   return true;
 }
+
+// n = 8 coefficient path of the sandwich form (k_coef8_sep), for masks of rank
+// P <= 3: Y = sum_p L_p X R_p^T with the full 8x8 L_p = C A_p C^t,
+// R_p = C B_p C^t (4 DMMA per pair and block). Accepted when sum_p L_p (x) R_p
+// equals H to 1e-13 max|H|. Fragments, lane l = 4g + t, k-step s:
+//   [p][0][s][l] = L_p[g][4s+t]   (A of U = L_p X)
+//   [p][1][s][l] = R_p[g][2t+s]   (B of Y += U R_p^T)
+bool layout_csep8(const dctf_plan& p, std::vector<double>& out, int& rank) {
+  rank = 0;
+  out.clear();
+  const int n = p.n;
+  if (n != 8) return false;
+  const int kr = p.kr, kc = p.kc, hr = (kr - 1) / 2, hc = (kc - 1) / 2;
+  const bool rep = p.padding == DCTF_PAD_REPLICATE;
+  std::vector<std::vector<long double>> as, bs;
+  if (!separable_taps(p, as, bs, 3)) return false;
+  const int np = static_cast<int>(as.size());
+  const double* C = p.basis.data();
+  std::vector<long double> L(size_t(np) * 64), R(size_t(np) * 64);
+  for (int q = 0; q < np; ++q)
+    for (int dir = 0; dir < 2; ++dir) {
+      std::vector<long double> m, cm(64);
+      if (dir == 0) band_operator(as[q], kr, hr, n, rep, m);
+      else band_operator(bs[q], kc, hc, n, rep, m);
+      for (int u = 0; u < n; ++u)
+        for (int i = 0; i < n; ++i) {
+          long double acc = 0.0L;
+          for (int k = 0; k < n; ++k) acc += static_cast<long double>(C[u * n + k]) * m[size_t(k) * n + i];
+          cm[u * n + i] = acc;
+        }
+      long double* dst = (dir == 0 ? L.data() : R.data()) + size_t(q) * 64;
+      for (int u = 0; u < n; ++u)
+        for (int a = 0; a < n; ++a) {
+          long double acc = 0.0L;
+          for (int i = 0; i < n; ++i) acc += cm[u * n + i] * C[a * n + i];
+          dst[u * n + a] = acc;
+        }
+    }
+  if (kron_mismatch(p, L, R, np) > 1e-13) return false;
+  for (int q = 0; q < np; ++q)
+    for (int mat = 0; mat < 2; ++mat)
+      for (int sk = 0; sk < 2; ++sk)
+        for (int l = 0; l < 32; ++l) {
+          const int g = l >> 2, t = l & 3;
+          const long double v = mat == 0 ? L[size_t(q) * 64 + g * 8 + 4 * sk + t] : R[size_t(q) * 64 + g * 8 + 2 * t + sk];
+          out.push_back(static_cast<double>(v));
+        }
+  rank = np;
+  return true;
+}
 }  // namespace dctf

@@ -116,3 +116,32 @@ def test_sep16_rank2_and_coefficients(cuda, ref, wh):
         assert np.abs(co.cpu().numpy() - r_co).max() <= 1e-9 * scale, pad
         y = plan.filter_coeffs(torch.from_numpy(np.ascontiguousarray(r_x)).cuda()).cpu().numpy()
         assert np.abs(y - r_co).max() <= 1e-9 * scale, pad
+
+
+@pytest.mark.parametrize("nblocks", [1, 31, 32, 33, 4099, 100003])
+def test_coef8_sep_ragged_guarded(cuda, ref, nblocks):
+    """k_coef8_sep (whole-stage bulk copies, the last one partial): ranks 1-3
+    of asymmetric masks against the reference's filter_coeffs and the dense
+    kernel; nothing written past the last block."""
+    torch = cuda
+    from paper_1710_07193_b200 import _lib
+    rng = np.random.default_rng(nblocks)
+    xh = rng.uniform(-500, 500, (nblocks, 8, 8))
+    x = torch.from_numpy(xh).cuda()
+    for seed, k, rank in ((11, 3, 1), (12, 3, 2), (13, 5, 3)):
+        w = _rank_mask(seed, k, rank)
+        for pad in (0, 1):
+            plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad))
+            dense = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad), precision=P.Precision.kFp64Dense)
+            assert plan.coef_kernel == "k_coef8_sep" and dense.coef_kernel == "k_coef8", (rank, pad)
+            guard = 40
+            yb = torch.full((nblocks + guard, 8, 8), 12345.0, dtype=torch.float64, device="cuda")
+            _lib.check(_lib.lib.dctf_filter_coeffs(plan.handle, x.data_ptr(), yb.data_ptr(), nblocks,
+                                                   torch.cuda.current_stream().cuda_stream))
+            torch.cuda.synchronize()
+            assert bool((yb[nblocks:] == 12345.0).all()), (rank, pad)
+            y = yb[:nblocks].cpu().numpy()
+            r = ref.filter_coeffs(w, k, 8, pad, xh, threads=nthreads())
+            assert np.abs(y - r).max() <= 1e-9 * np.abs(r).max(), (rank, pad)
+            yd = dense.filter_coeffs(x).cpu().numpy()
+            assert np.abs(y - yd).max() <= 1e-12 * np.abs(yd).max(), (rank, pad)
