@@ -379,6 +379,46 @@ inline GrayImage filter_image(const GrayImage& img, const Mask& mask, PaddingMod
   return out;
 }
 
+// tile / assemble (image.hpp:155-203), for callers of the per-block API: an
+// image as n x n FP64 blocks in row-major block order, extended to a multiple
+// of n by edge replication (tile), and blocks back to u8 through
+// quantize_sample with the overhang cropped (assemble). Host-side layout
+// helpers only: the batched device entry points (filter_image, the batch
+// overloads of filter_block / forward_2d) never go through them.
+struct BlockTile {
+  int row0;
+  int col0;
+  BlockMatrix block;
+};
+
+inline std::vector<BlockTile> tile(const GrayImage& img, int n) {
+  if (n < 2) throw std::invalid_argument("tile: block side must be >= 2");
+  if (img.width < 1 || img.height < 1 || img.samples.size() != size_t(img.width) * img.height)
+    throw std::invalid_argument("GrayImage: sample count must be width*height");
+  const int bw = (img.width + n - 1) / n, bh = (img.height + n - 1) / n;
+  std::vector<BlockTile> out;
+  out.reserve(size_t(bw) * bh);
+  for (int by = 0; by < bh; ++by)
+    for (int bx = 0; bx < bw; ++bx) {
+      BlockTile t{by * n, bx * n, BlockMatrix(n)};
+      for (int i = 0; i < n; ++i) {
+        const int y = std::min(t.row0 + i, img.height - 1);
+        for (int j = 0; j < n; ++j) t.block(i, j) = double(img.at(std::min(t.col0 + j, img.width - 1), y));
+      }
+      out.push_back(std::move(t));
+    }
+  return out;
+}
+
+inline GrayImage assemble(const std::vector<BlockTile>& tiles, int width, int height) {
+  GrayImage img{width, height, std::vector<std::uint8_t>(size_t(width) * height, 0)};
+  for (const BlockTile& t : tiles)
+    for (int i = 0; i < t.block.n() && t.row0 + i < height; ++i)
+      for (int j = 0; j < t.block.n() && t.col0 + j < width; ++j)
+        img.at(t.col0 + j, t.row0 + i) = quantize_sample(t.block(i, j));
+  return img;
+}
+
 // ---------------------------------------------------------------------------
 // PGM I/O (image.hpp:45-152): binary P5 and ASCII P2 with maxval 255 in,
 // binary P5 out; malformed input throws PgmError.

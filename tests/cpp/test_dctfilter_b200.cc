@@ -2,6 +2,7 @@
 // reference's own GTest suites exercise dctfilter (filter_test.cc,
 // image_test.cc, dct_test.cc), on the GPU. Built by `make cpp-test`, run by
 // tests/test_gpu_cpp.py. Prints one line per check, exits non-zero on failure.
+#include <algorithm>
 #include <cstdio>
 #include <random>
 
@@ -136,6 +137,22 @@ int main() {
               b16.coef_kernel() == "k_coef_bf16x3",
           "coefficient kernel selection");
     CHECK(et <= 5e-6 * mx && eb <= 1e-4 * mx, "3xTF32 / 3xBF16 coefficients within their stated bounds");
+  }
+  // tile -> per-block filter in shuffled order -> assemble equals the fused
+  // whole-image path (image_test.cc BlockOrderIndependent pattern, ragged size)
+  {
+    GrayImage img{37, 29, std::vector<std::uint8_t>(37 * 29)};
+    for (auto& s : img.samples) s = std::uint8_t(rng() & 255);
+    const FilterPlan plan(Mask::gaussian3(), 8, PaddingMode::kReplicate);
+    std::vector<BlockTile> tiles = tile(img, 8);
+    std::shuffle(tiles.begin(), tiles.end(), rng);
+    std::vector<BlockMatrix> blocks;
+    for (const auto& t : tiles) blocks.push_back(t.block);
+    const std::vector<BlockMatrix> filtered = plan.filter_block(blocks);
+    for (size_t i = 0; i < tiles.size(); ++i) tiles[i].block = filtered[i];
+    const GrayImage a = assemble(tiles, img.width, img.height);
+    const GrayImage b = filter_image(img, Mask::gaussian3(), PaddingMode::kReplicate, Domain::kDct, 8);
+    CHECK(tiles.size() == 5 * 4 && a.samples == b.samples, "tile / shuffled filter_block / assemble == filter_image");
   }
   CHECK(quantize_sample(127.5) == 128 && quantize_sample(0.5) == 1 && quantize_sample(-3) == 0, "quantize KATs");
   std::printf("%s\n", failures ? "FAILED" : "ALL PASSED");
