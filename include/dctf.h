@@ -91,6 +91,15 @@ dctf_status dctf_plan_destroy(dctf_plan* plan);
  *     fingerprint and counts as read_operator_sets does (errors ->
  *     DCTF_INVALID_ARGUMENT with the reference's message text). */
 dctf_status dctf_plan_dump(const dctf_plan* plan, char* buf, size_t* len);
+/* A plan from an explicit sandwich set — the operand of apply(set, X)
+ * (filter.hpp:40-45) and apply_pairs (filter.hpp:30-38): npairs (left,
+ * right) factors, n*n doubles each, row-major; domain 0 = spatial (conjugated
+ * into the DCT domain as to_dct_domain does, operators.hpp:124-141),
+ * 1 = DCT. The k x k mask (OperatorSet::mask) drives the spatial path and the
+ * fingerprint; the DCT-domain filter follows the pairs. */
+dctf_status dctf_plan_create_from_pairs(const double* h_lefts, const double* h_rights, int npairs, int n,
+                                        int domain, const double* h_weights, int k, int padding, int precision,
+                                        int device, dctf_plan** out);
 dctf_status dctf_plan_create_from_dump(const char* text, size_t len, int precision, int device,
                                        dctf_plan** out);
 

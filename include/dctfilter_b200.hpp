@@ -170,6 +170,47 @@ inline std::vector<std::uint8_t> quantize_u8(const BlockMatrix& block) {
   return out;
 }
 
+// BlockMatrix arithmetic (block_matrix.hpp:61-101): i-k-j product with the
+// zero skip and separately rounded multiply / add, elementwise sum,
+// transpose. Host-side, used by the one-time operator construction below.
+inline void check_same_side(const BlockMatrix& a, const BlockMatrix& b) {
+  if (a.n() != b.n()) throw std::invalid_argument("BlockMatrix: dimension mismatch");
+}
+inline BlockMatrix matmul(const BlockMatrix& a, const BlockMatrix& b) {
+  check_same_side(a, b);
+  const int n = a.n();
+  BlockMatrix c(n);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) {
+      const double aik = a(i, k);
+      if (aik == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        const volatile double prod = aik * b(k, j);  // no contraction into an FMA
+        c(i, j) = c(i, j) + prod;
+      }
+    }
+  return c;
+}
+inline BlockMatrix add(const BlockMatrix& a, const BlockMatrix& b) {
+  check_same_side(a, b);
+  BlockMatrix c(a.n());
+  for (size_t i = 0; i < c.data().size(); ++i) c.data()[i] = a.data()[i] + b.data()[i];
+  return c;
+}
+inline BlockMatrix transpose(const BlockMatrix& a) {
+  BlockMatrix t(a.n());
+  for (int i = 0; i < a.n(); ++i)
+    for (int j = 0; j < a.n(); ++j) t(j, i) = a(i, j);
+  return t;
+}
+
+// A compiled filter as sandwich terms (operators.hpp:36-53): applying the set
+// sums left * X * right over the pairs.
+struct SandwichPair {
+  BlockMatrix left;
+  BlockMatrix right;
+};
+
 namespace detail {
 struct PlanDeleter {
   void operator()(dctf_plan* p) const { dctf_plan_destroy(p); }
@@ -249,6 +290,126 @@ inline BlockMatrix inverse_2d(const DctBasis& basis, const BlockMatrix& coeffs) 
   return inverse_2d(basis, std::vector<BlockMatrix>{coeffs})[0];
 }
 
+struct OperatorSet {
+  int n;
+  PaddingMode padding;
+  Domain domain;
+  bool symmetric_merged;
+  Mask mask;  // source kernel
+  std::vector<SandwichPair> pairs;
+  std::uint64_t mask_fingerprint() const { return mask.fingerprint(); }
+  // device copy made by the first apply() (sets are immutable once built)
+  mutable detail::PlanPtr device_plan = nullptr;
+};
+
+// Operator construction (operators.hpp:56-169), host-side and one-time like
+// the reference's: row shift (zero-drop or clamp), band matrix of one mask
+// row (zero-drop or clamp-fold), one (shift, band) pair per mask row,
+// conjugation into the DCT domain, merging of mirrored rows.
+inline BlockMatrix build_shift_matrix(int n, int offset, PaddingMode padding) {
+  if (std::abs(offset) >= n) throw std::invalid_argument("build_shift_matrix: |offset| must be < n");
+  BlockMatrix s(n);
+  for (int i = 0; i < n; ++i) {
+    const int src = i - offset;
+    if (padding == PaddingMode::kReplicate) s(i, std::min(std::max(src, 0), n - 1)) = 1.0;
+    else if (src >= 0 && src < n) s(i, src) = 1.0;
+  }
+  return s;
+}
+inline BlockMatrix build_band_matrix(const double* row, int k, int n, PaddingMode padding) {
+  if (k % 2 == 0) throw std::invalid_argument("build_band_matrix: row length must be odd");
+  if (k > n) throw std::invalid_argument("build_band_matrix: row longer than block side");
+  const int h = (k - 1) / 2;
+  BlockMatrix t(n);
+  for (int j = 0; j < n; ++j)
+    for (int c = 0; c < k; ++c) {
+      const int src = j + c - h;
+      if (padding == PaddingMode::kReplicate) t(std::min(std::max(src, 0), n - 1), j) += row[c];
+      else if (src >= 0 && src < n) t(src, j) += row[c];
+    }
+  return t;
+}
+inline BlockMatrix build_band_matrix(const std::vector<double>& row, int n, PaddingMode padding) {
+  return build_band_matrix(row.data(), int(row.size()), n, padding);
+}
+inline OperatorSet build_spatial_operator_set(const Mask& mask, int n, PaddingMode padding) {
+  if (mask.rows() != mask.cols()) throw std::invalid_argument("build_spatial_operator_set: square masks only");
+  if (mask.k() > n) throw std::invalid_argument("build_spatial_operator_set: mask larger than block");
+  const int k = mask.k(), h = mask.half();
+  OperatorSet set{n, padding, Domain::kSpatial, false, mask, {}};
+  for (int r = 0; r < k; ++r)
+    set.pairs.push_back({build_shift_matrix(n, h - r, padding),
+                         build_band_matrix(mask.weights().data() + size_t(r) * k, k, n, padding)});
+  return set;
+}
+inline OperatorSet to_dct_domain(const OperatorSet& set, const DctBasis& basis) {
+  if (set.domain == Domain::kDct) throw std::invalid_argument("to_dct_domain: set is already in the DCT domain");
+  if (basis.n() != set.n) throw std::invalid_argument("to_dct_domain: basis side mismatch");
+  const BlockMatrix ct = basis.ct();
+  OperatorSet out{set.n, set.padding, Domain::kDct, set.symmetric_merged, set.mask, {}};
+  for (const SandwichPair& p : set.pairs)
+    out.pairs.push_back({matmul(matmul(basis.c(), p.left), ct), matmul(matmul(basis.c(), p.right), ct)});
+  return out;
+}
+inline OperatorSet merge_symmetric(const OperatorSet& set) {
+  if (set.symmetric_merged) throw std::invalid_argument("merge_symmetric: set is already merged");
+  if (!row_symmetric(set.mask)) throw std::invalid_argument("merge_symmetric: mask rows are not symmetric");
+  const int k = set.mask.k();
+  if (set.pairs.size() != size_t(k)) throw std::invalid_argument("merge_symmetric: expected one pair per mask row");
+  OperatorSet out{set.n, set.padding, set.domain, true, set.mask, {}};
+  for (int r = 0; r < (k + 1) / 2; ++r) {
+    const int m = k - 1 - r;
+    out.pairs.push_back(r == m ? set.pairs[size_t(r)]
+                               : SandwichPair{add(set.pairs[size_t(r)].left, set.pairs[size_t(m)].left),
+                                              set.pairs[size_t(r)].right});
+  }
+  return out;
+}
+
+// apply / apply_pairs (filter.hpp:30-45) — the DCT-domain filter of a set, on
+// the device: the set becomes a plan (dctf_plan_create_from_pairs; spatial sets
+// are conjugated like to_dct_domain), made once per set and reused.
+namespace detail {
+inline const PlanPtr& set_plan(const OperatorSet& set, int device = 0) {
+  if (!set.device_plan) {
+    const size_t nn = size_t(set.n) * set.n;
+    std::vector<double> l(set.pairs.size() * nn), r(set.pairs.size() * nn);
+    for (size_t q = 0; q < set.pairs.size(); ++q) {
+      check_same_side(set.pairs[q].left, set.pairs[q].right);
+      if (set.pairs[q].left.n() != set.n) throw std::invalid_argument("apply: pair side does not match operator set");
+      std::memcpy(&l[q * nn], set.pairs[q].left.data().data(), nn * sizeof(double));
+      std::memcpy(&r[q * nn], set.pairs[q].right.data().data(), nn * sizeof(double));
+    }
+    dctf_plan* p = nullptr;
+    check(dctf_plan_create_from_pairs(l.data(), r.data(), int(set.pairs.size()), set.n,
+                                      set.domain == Domain::kDct ? 1 : 0, set.mask.weights().data(), set.mask.k(),
+                                      int(set.padding), int(Precision::kFp64), device, &p));
+    set.device_plan = PlanPtr(p, PlanDeleter());
+  }
+  return set.device_plan;
+}
+}  // namespace detail
+// A DCT-domain set filters coefficient blocks; a spatial set (sum of S x T)
+// filters spatial blocks, here through the transform: inverse(H forward(x)).
+// (Batch form named apply_batch: an unqualified apply(set, std::vector) would
+// also find std::apply by argument-dependent lookup.)
+inline std::vector<BlockMatrix> apply_batch(const OperatorSet& set, const std::vector<BlockMatrix>& xs) {
+  const detail::PlanPtr& p = detail::set_plan(set);
+  if (set.domain == Domain::kDct) return detail::run(p, set.n, xs, dctf_filter_coeffs_host);
+  return detail::run(p, set.n,
+                     detail::run(p, set.n, detail::run(p, set.n, xs, dctf_forward_blocks_host),
+                                 dctf_filter_coeffs_host),
+                     dctf_inverse_blocks_host);
+}
+inline BlockMatrix apply(const OperatorSet& set, const BlockMatrix& x) {
+  if (x.n() != set.n) throw std::invalid_argument("apply: block side does not match operator set");
+  return apply_batch(set, std::vector<BlockMatrix>{x})[0];
+}
+inline BlockMatrix apply_pairs(const std::vector<SandwichPair>& pairs, const BlockMatrix& x) {
+  OperatorSet set{x.n(), PaddingMode::kZero, Domain::kDct, false, Mask::identity(), pairs};
+  return dctfilter_b200::apply(set, x);
+}
+
 // FilterPlan (filter.hpp:52-87): compile once, filter many blocks.
 class FilterPlan {
  public:
@@ -272,6 +433,23 @@ class FilterPlan {
   // dctf_plan_coef_kernel), e.g. "k_fused8_sym" for a symmetric mask.
   std::string image_kernel() const { return dctf_plan_image_kernel(plan_.get()); }
   std::string coef_kernel() const { return dctf_plan_coef_kernel(plan_.get()); }
+
+  // The compiled DCT-domain sandwich set (FilterPlan::dct_set, filter.hpp:62);
+  // apply(plan.dct_set(), X) runs on this plan's device copy.
+  const OperatorSet& dct_set() const {
+    if (!dct_set_) {
+      const size_t nn = size_t(n_) * n_;
+      std::vector<double> l(size_t(npairs_) * nn), r(size_t(npairs_) * nn);
+      check(dctf_plan_pairs(plan_.get(), 1, l.data(), r.data()));
+      auto set = std::make_shared<OperatorSet>(OperatorSet{n_, padding_, Domain::kDct, merged_ != 0, mask_, {}});
+      for (int q = 0; q < npairs_; ++q)
+        set->pairs.push_back({BlockMatrix(n_, std::vector<double>(l.begin() + q * nn, l.begin() + (q + 1) * nn)),
+                              BlockMatrix(n_, std::vector<double>(r.begin() + q * nn, r.begin() + (q + 1) * nn))});
+      set->device_plan = plan_;
+      dct_set_ = set;
+    }
+    return *dct_set_;
+  }
 
   // Dense N^2 x N^2 DCT-domain operator (row (u*n+v), column (a*n+b)).
   std::vector<double> dct_operator() const {
@@ -340,6 +518,7 @@ class FilterPlan {
   DctBasis basis_;
   detail::PlanPtr plan_;
   int n_ = 0, npairs_ = 0, merged_ = 0;
+  mutable std::shared_ptr<OperatorSet> dct_set_;
 };
 
 struct GrayImage {

@@ -616,6 +616,31 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
   return finish_plan(p, out);
 }
 
+dctf_status dctf_plan_create_from_pairs(const double* h_lefts, const double* h_rights, int npairs, int n,
+                                        int domain, const double* h_weights, int k, int padding, int precision,
+                                        int device, dctf_plan** out) {
+  dctf::reset_launches();
+  if (!out || (npairs > 0 && (!h_lefts || !h_rights)) || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DENSE)
+    return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
+  if (domain != 0 && domain != 1) return set_error(DCTF_INVALID_ARGUMENT, "domain must be 0 (spatial) or 1 (DCT)");
+  if (k < 1 || (k % 2) == 0) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
+  auto* p = new dctf_plan();
+  p->n = n;
+  p->kr = p->kc = k;
+  p->padding = padding;
+  p->precision = precision;
+  p->device = device;
+  p->weights.assign(h_weights, h_weights + static_cast<size_t>(k) * k);
+  dctf_status s = dctf::compile_from_pairs(*p, h_lefts, h_rights, npairs, domain);
+  if (s != DCTF_OK) {
+    delete p;
+    return s;
+  }
+  return finish_plan(p, out);
+}
+
 dctf_status dctf_plan_create_from_dump(const char* text, size_t len, int precision, int device,
                                        dctf_plan** out) {
   dctf::reset_launches();

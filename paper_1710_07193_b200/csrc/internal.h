@@ -95,6 +95,8 @@ void reset_launches();
 // Builds C and the dense DCT-domain operator H for the mask.
 // Returns DCTF_INVALID_ARGUMENT with a message on bad input.
 dctf_status compile_operator(dctf_plan& p);
+// A plan from explicit sandwich pairs (domain 0 spatial, 1 DCT), plan.cc.
+dctf_status compile_from_pairs(dctf_plan& p, const double* lefts, const double* rights, int np, int domain);
 
 // Operator dump format (operator_io.hpp:105-217), plan.cc.
 std::string format_operator_dump(const dctf_plan& p);

@@ -357,6 +357,45 @@ dctf_status parse_operator_dump(const std::string& text, dctf_plan& p) {
   return DCTF_OK;
 }
 
+// A plan from an explicit sandwich set (OperatorSet, operators.hpp:43-53),
+// the operand of apply(set, X) (filter.hpp:40-45): spatial pairs are
+// conjugated into the DCT domain like to_dct_domain (operators.hpp:124-141,
+// C M C^t in matmul's order), then densified into H. The mask (weights)
+// is kept for the spatial path and the fingerprint.
+dctf_status compile_from_pairs(dctf_plan& p, const double* lefts, const double* rights, int np, int domain) {
+  if (p.n != 8 && p.n != 16) return set_error(DCTF_INVALID_ARGUMENT, "block side n must be 8 or 16");
+  if (np < 0) return set_error(DCTF_INVALID_ARGUMENT, "pair count must be >= 0");
+  if (p.padding != DCTF_PAD_ZERO && p.padding != DCTF_PAD_REPLICATE)
+    return set_error(DCTF_INVALID_ARGUMENT, "padding must be DCTF_PAD_ZERO or DCTF_PAD_REPLICATE");
+  const int n = p.n;
+  const size_t nn = size_t(n) * n;
+  for (size_t i = 0; i < nn * np; ++i)
+    if (!std::isfinite(lefts[i]) || !std::isfinite(rights[i]))
+      return set_error(DCTF_INVALID_ARGUMENT, "sandwich pairs must be finite");
+  p.basis.assign(nn, 0.0);
+  dct_basis(n, p.basis.data());
+  p.reference_domain = true;
+  p.npairs = np;
+  p.merged = 0;
+  std::vector<double> L(lefts, lefts + nn * np), R(rights, rights + nn * np);
+  if (domain == 0) {
+    p.sp_left = L;
+    p.sp_right = R;
+    std::vector<double> ct(nn), tmp(nn);
+    transpose(n, p.basis.data(), ct.data());
+    for (int q = 0; q < np; ++q) {
+      matmul(n, p.basis.data(), &p.sp_left[q * nn], tmp.data());
+      matmul(n, tmp.data(), ct.data(), &L[q * nn]);
+      matmul(n, p.basis.data(), &p.sp_right[q * nn], tmp.data());
+      matmul(n, tmp.data(), ct.data(), &R[q * nn]);
+    }
+  }
+  p.dct_left = L;
+  p.dct_right = R;
+  densify(p);
+  return DCTF_OK;
+}
+
 dctf_status compile_operator(dctf_plan& p) {
   if (p.n != 8 && p.n != 16) return set_error(DCTF_INVALID_ARGUMENT, "block side n must be 8 or 16");
   if (p.kr < 1 || p.kc < 1 || (p.kr % 2) == 0 || (p.kc % 2) == 0)

@@ -154,6 +154,52 @@ int main() {
     const GrayImage b = filter_image(img, Mask::gaussian3(), PaddingMode::kReplicate, Domain::kDct, 8);
     CHECK(tiles.size() == 5 * 4 && a.samples == b.samples, "tile / shuffled filter_block / assemble == filter_image");
   }
+  // operator construction (operators.hpp) and apply (filter.hpp) through the drop-in
+  {
+    const Mask g = Mask::gaussian3();
+    const FilterPlan plan(g, 8, PaddingMode::kReplicate);
+    const OperatorSet spatial = build_spatial_operator_set(g, 8, PaddingMode::kReplicate);
+    const OperatorSet merged = merge_symmetric(spatial);
+    const OperatorSet dct = to_dct_domain(merged, plan.basis());
+    const OperatorSet& own = plan.dct_set();
+    bool same = dct.pairs.size() == own.pairs.size() && own.pairs.size() == 2 && dct.symmetric_merged &&
+                own.symmetric_merged && dct.domain == Domain::kDct && spatial.pairs.size() == 3;
+    for (size_t q = 0; same && q < dct.pairs.size(); ++q)
+      same = dct.pairs[q].left.data() == own.pairs[q].left.data() &&
+             dct.pairs[q].right.data() == own.pairs[q].right.data();
+    CHECK(same, "build_spatial_operator_set -> merge_symmetric -> to_dct_domain == FilterPlan::dct_set (bitwise)");
+    std::vector<BlockMatrix> xs;
+    std::uniform_real_distribution<double> u(-300, 300);
+    for (int i = 0; i < 70; ++i) {
+      BlockMatrix m(8);
+      for (double& v : m.data()) v = u(rng);
+      xs.push_back(m);
+    }
+    const auto ref = plan.filter_coeffs(xs), a = apply_batch(dct, xs), b = apply_batch(own, xs);
+    double ea = 0, eb = 0, ep = 0, mx = 0;
+    for (size_t i = 0; i < xs.size(); ++i) {
+      ea = std::max(ea, max_abs_diff(a[i], ref[i]));
+      eb = std::max(eb, max_abs_diff(b[i], ref[i]));
+      ep = std::max(ep, max_abs_diff(i % 10 ? apply(dct, xs[i]) : apply_pairs(dct.pairs, xs[i]), ref[i]));
+      for (double v : ref[i].data()) mx = std::max(mx, std::abs(v));
+    }
+    CHECK(eb == 0.0 && ea <= 1e-12 * mx && ep <= 1e-12 * mx, "apply(set) / apply_pairs on the device == filter_coeffs");
+    // a spatial set filters spatial blocks: apply(spatial, x) == convolve(x)
+    const auto cs = apply_batch(spatial, xs), cv = plan.convolve(xs);
+    double es = 0, ms = 0;
+    for (size_t i = 0; i < xs.size(); ++i) {
+      es = std::max(es, max_abs_diff(cs[i], cv[i]));
+      for (double v : cv[i].data()) ms = std::max(ms, std::abs(v));
+    }
+    CHECK(es <= 1e-12 * ms, "apply(spatial set) == convolve");
+    bool threw = false;
+    try {
+      merge_symmetric(merged);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw, "merge_symmetric of a merged set throws invalid_argument");
+  }
   CHECK(quantize_sample(127.5) == 128 && quantize_sample(0.5) == 1 && quantize_sample(-3) == 0, "quantize KATs");
   std::printf("%s\n", failures ? "FAILED" : "ALL PASSED");
   return failures ? 1 : 0;
