@@ -36,6 +36,8 @@ _SIGS = {
     "dctf_plan_dump": (_st, [_vp, C.c_char_p, C.POINTER(C.c_size_t)]),
     "dctf_plan_create_from_dump": (_st, [C.c_char_p, C.c_size_t, C.c_int, C.c_int, C.POINTER(_vp)]),
     "dctf_plan_pairs": (_st, [_vp, C.c_int, _d, _d]),
+    "dctf_plan_create_from_pairs": (_st, [_d, _d, C.c_int, C.c_int, C.c_int, _d, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, C.POINTER(_vp)]),
     "dctf_format_operator_dump": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_size_t)]),
     "dctf_operator_from_dump": (_st, [C.c_char_p, C.c_size_t, _d, _i, _i, _i]),
     "dctf_plan_info": (_st, [_vp, _i, _i, _i]),

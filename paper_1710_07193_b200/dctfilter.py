@@ -213,6 +213,55 @@ class FilterPlan:
         self._mask = None
         return self
 
+    @classmethod
+    def from_pairs(cls, lefts, rights, mask: Mask, padding: PaddingMode, domain: "Domain" = None,
+                   device: int | None = None):
+        """Plan from an explicit sandwich set (OperatorSet, operators.hpp:43-53)
+        — what apply(set, X) (filter.hpp:40-45) filters with: lefts / rights
+        are (npairs, n, n); a spatial set (Domain.kSpatial) is conjugated into
+        the DCT domain as to_dct_domain does. The square mask drives the
+        spatial path and the fingerprint."""
+        if device is None:
+            import torch
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        lefts = np.ascontiguousarray(lefts, np.float64)
+        rights = np.ascontiguousarray(rights, np.float64)
+        if lefts.shape != rights.shape or lefts.ndim != 3 or lefts.shape[1] != lefts.shape[2]:
+            raise InvalidArgument("lefts / rights must both be (npairs, n, n)")
+        if mask.kr != mask.kc:
+            raise InvalidArgument("from_pairs: square masks only")
+        n = lefts.shape[1]
+        dom = Domain.kDct if domain is None else Domain(domain)
+        h = C.c_void_p()
+        check(_lib.lib.dctf_plan_create_from_pairs(
+            lefts.ctypes.data_as(_lib._d), rights.ctypes.data_as(_lib._d), lefts.shape[0], n,
+            1 if dom == Domain.kDct else 0, mask._w.ctypes.data_as(_lib._d), mask.kr, int(padding),
+            int(Precision.kFp64), int(device), C.byref(h)))
+        self = cls.__new__(cls)
+        self._h, self._device, self._mask, self._padding = h, int(device), mask, PaddingMode(padding)
+        nn, np_, mg = C.c_int(), C.c_int(), C.c_int()
+        check(_lib.lib.dctf_plan_info(h, C.byref(nn), C.byref(np_), C.byref(mg)))
+        self._n, self.npairs, self.symmetric_merged = nn.value, np_.value, bool(mg.value)
+        return self
+
+    def dct_set(self):
+        """The compiled DCT-domain sandwich pairs (FilterPlan::dct_set,
+        filter.hpp:62) as (lefts, rights), each (npairs, n, n)."""
+        return self._pairs(1)
+
+    def spatial_set(self):
+        """The spatial-domain pairs after merge_symmetric (the set to_dct_domain
+        conjugates), as (lefts, rights)."""
+        return self._pairs(0)
+
+    def _pairs(self, domain):
+        n = self._n
+        lefts = np.zeros((self.npairs, n, n))
+        rights = np.zeros((self.npairs, n, n))
+        check(_lib.lib.dctf_plan_pairs(self._h, domain, lefts.ctypes.data_as(_lib._d),
+                                       rights.ctypes.data_as(_lib._d)))
+        return lefts, rights
+
     def dump(self) -> str:
         """write_operator_sets of the plan's {spatial, dct} sets (byte-identical
         to the reference's build-operators output)."""

@@ -145,3 +145,22 @@ def test_coef8_sep_ragged_guarded(cuda, ref, nblocks):
             assert np.abs(y - r).max() <= 1e-9 * np.abs(r).max(), (rank, pad)
             yd = dense.filter_coeffs(x).cpu().numpy()
             assert np.abs(y - yd).max() <= 1e-12 * np.abs(yd).max(), (rank, pad)
+
+
+def test_operator_set_round_trip_through_pairs(cuda, ref):
+    """FilterPlan.dct_set() equals the reference's dct_set() bitwise; a plan
+    built from those pairs (the operand of apply(set, X)) and one built from
+    the spatial set both filter like the original plan."""
+    torch = cuda
+    w, k = ref.mask_preset("gaussian3")
+    for n in (8, 16):
+        plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        lefts, rights = plan.dct_set()
+        rl, rr, merged = ref.plan_pairs(w, k, n, 1)
+        assert merged and np.array_equal(lefts, rl) and np.array_equal(rights, rr), n
+        x = torch.randn((999, n, n), dtype=torch.float64, device="cuda") * 100
+        y = plan.filter_coeffs(x)
+        for dom, (ls, rs) in ((P.Domain.kDct, (lefts, rights)), (P.Domain.kSpatial, plan.spatial_set())):
+            other = P.FilterPlan.from_pairs(ls, rs, P.Mask(k, w), P.PaddingMode.kReplicate, domain=dom)
+            ys = other.filter_coeffs(x)
+            assert (ys - y).abs().max().item() <= 1e-13 * y.abs().max().item(), (n, dom)
