@@ -406,19 +406,23 @@ def aux_cfg3(c):
 
 def aux_cfg5(c):
     """Config 5: 64 frames of 3840x2160, 4 masks round-robin (Laplacian,
-    Gaussian 5x5, 1x9 motion blur on 8x8 blocks, random asymmetric 5x5), one
-    batched dctf_filter_frames_u8 call = one GPU's whole share at N=1 (8 unique
-    S(f) frames generated on the host, tiled to 64 on the device; 531 MB >> L2)."""
+    Gaussian 5x5, 1x9 motion blur on 8x8 blocks, random asymmetric 5x5). The
+    frame range is sharded across the ranks (rank r takes frames
+    [64 r / N, 64 (r + 1) / N), no data-path collective: SURVEY 8(e)); each
+    rank's share is one batched dctf_filter_frames_u8 call; time = max over
+    ranks, value = all 64 frames' blocks / that time (strong scaling). 8 unique
+    S(f) frames generated on the host, tiled on the device; 531 MB >> L2 at N=1."""
     P, torch, synth = c.P, c.torch, c.synth
     FW, FH, FF = 3840, 2160, 64
+    f0, f1 = FF * c.rank // c.world, FF * (c.rank + 1) // c.world
     rnd5, _ = synth.random_mask(1005, 5)
     masks = [(synth.LAPLACIAN3, 3, 3), (synth.gaussian_mask(5, 1.0), 5, 5), (synth.MOTION_1x9, 1, 9),
              (rnd5, 5, 5)]
     plans = [P.FilterPlan(P.Mask(k, w) if k == kc else P.Mask.rect(k, kc, w), 8, P.PaddingMode.kReplicate)
              for w, k, kc in masks]
-    uniq = np.stack([synth.sinusoid_image(f, FW, FH) for f in range(8)])
-    frames = torch.from_numpy(uniq).cuda().repeat(FF // 8, 1, 1).contiguous()
-    idx = [f % 4 for f in range(FF)]
+    uniq = torch.from_numpy(np.stack([synth.sinusoid_image(f, FW, FH) for f in range(8)])).cuda()
+    frames = torch.stack([uniq[f % 8] for f in range(f0, f1)]).contiguous()
+    idx = [f % 4 for f in range(f0, f1)]
     nb = FF * (FW // 8) * (FH // 8)
 
     def run(pls):
@@ -427,18 +431,20 @@ def aux_cfg5(c):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ts = []
         for _ in range(5):
+            c.barrier()
             a.record()
             out = P.filter_frames(frames, pls, idx)
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
             del out
-        return statistics.median(ts), first
+        return c.max_over_ranks(statistics.median(ts)), first
 
     ms, ref_out = run(plans)
     res = {"workload": "config5: 64 x 3840x2160 S(f) frames, masks f mod 4 = Laplacian 3x3, Gaussian "
            "5x5 s=1, 1x9 motion blur, random asymmetric 5x5; replicate; FP64; one "
-           "dctf_filter_frames_u8 call", "blocks": nb, "ms": ms, "blocks_per_s": nb / (ms / 1e3),
+           "dctf_filter_frames_u8 call per rank over its frame range", "blocks": nb, "ms": ms,
+           "blocks_per_s": nb / (ms / 1e3), "ranks": c.world, "frames_per_rank": f1 - f0,
            "kernels": [pl.image_kernel for pl in plans]}
     # the frames whose mask is asymmetric (dense FP64 kernel) through the
     # exact-INT8 tensor-core kernel instead; u8 must not change
@@ -808,8 +814,8 @@ def main():
                          sp=sp, flush=flush, plan=plan, mask=mask, d_in=d_in, d_out=d_out,
                          ring_in=ring_in, ring_out=ring_out,
                          peak_dmma=peak_dmma, peak_dfma=peak_dfma, hbm_peak=hbm_peak, ms=ms_cold,
-                         ms_stream=ms,
-                         steps=args.steps)
+                         ms_stream=ms, rank=rank, world=world, barrier=barrier,
+                         max_over_ranks=max_over_ranks, steps=args.steps)
         aux = {}
         aux.update(aux_image8_variants(ctx))
         aux["cfg1_graph"] = aux_cfg1(ctx)
