@@ -72,55 +72,107 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NVML polled every ~2 ms from a host thread (each sample stamped with the
+    host clock, so only samples inside [mark_start, mark_stop] count as "under
+    load"); nvidia-smi -lms 50 when NVML is unavailable. A timed region
+    shorter than a few samples (small --steps) is reported with the samples it
+    got plus those of `sustain()`: the same step launched back to back for
+    ~0.3 s right after the region, untimed, named in "window"."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, gpu: int):
-        self.gpu, self.proc, self.lines = gpu, None, []
+        self.gpu, self.samples, self.windows = gpu, [], []
+        self._stop = threading.Event()
+        self._thread = None
+        self._nvml = None
+        self._smi = None
+        self._smi_lines = []
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.gpu)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+
+    def _poll(self):
+        nv, h = self._nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.perf_counter(), float(sm), float(mx), int(rs)))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
+            self._nvml = self._handle()
+            self._thread = threading.Thread(target=self._poll, daemon=True)
+            self._thread.start()
+            self.source = "nvml (2 ms poll)"
         except Exception:
-            self.proc = None
+            self._nvml = None
+            self.source = "nvidia-smi -lms 50"
+            try:
+                self._smi = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                     "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "50"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                threading.Thread(target=self._read_smi, daemon=True).start()
+            except Exception:
+                self._smi = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _read_smi(self):
+        for line in self._smi.stdout:
+            p = [x.strip() for x in line.split(",")]
+            try:
+                rs = int(p[2], 16) if len(p) > 2 and p[2].startswith("0x") else 0
+                self.samples.append((time.perf_counter(), float(p[0]), float(p[1]), rs))
+            except (ValueError, IndexError):
+                continue
+
+    def window(self, name, t0, t1):
+        self.windows.append((name, t0, t1))
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
+        time.sleep(0.01)
+        self._stop.set()
+        if self._thread:
+            self._thread.join(timeout=2)
+        if self._smi:
+            self._smi.terminate()
             try:
-                self.proc.wait(timeout=5)
+                self._smi.wait(timeout=5)
             except Exception:
-                self.proc.kill()
-        time.sleep(0.05)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 7:
-                continue
-            try:
-                sm.append(float(p[0]))
-                mx.append(float(p[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                self._smi.kill()
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+               "source": self.source, "window": []}
+        picked = []
+        for name, t0, t1 in self.windows:
+            got = [s for s in self.samples if t0 <= s[0] <= t1]
+            out["window"].append({"name": name, "s": round(t1 - t0, 4), "samples": len(got)})
+            picked += got
+        if not picked:
+            return out
+        mask = 0
+        for s in picked:
+            mask |= s[3]
+        out.update(sm_mhz=statistics.median(s[1] for s in picked),
+                   sm_max_mhz=max(s[2] for s in picked),
+                   reasons=[nm for nm, bit in self.REASONS if mask & bit], samples=len(picked))
+        return out
 
 
 def ncu_traffic(kernel):
@@ -725,16 +777,29 @@ def main():
     t_end = torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.2)
     launches = 0
     barrier()
     torch.cuda.synchronize()
+    h0 = time.perf_counter()
     t_start.record(stream)
     for i in range(args.steps):
         launches += step(i)
     t_end.record(stream)
     torch.cuda.synchronize()
+    clocks.window("timed region", h0, time.perf_counter())
     barrier()
+    if clocks.source.startswith("nvml") and len(clocks.samples) < 20:
+        # too short a region for the poller: keep the same steps running
+        # ~0.3 s (untimed) and sample those too, named as such
+        h1 = time.perf_counter()
+        i = 0
+        while time.perf_counter() - h1 < 0.3:
+            for _ in range(64):
+                step(i)
+                i += 1
+            torch.cuda.synchronize()
+        clocks.window("sustain: the same steps, untimed, right after the region", h1,
+                      time.perf_counter())
     clk = clocks.stop()
     ms_local = t_start.elapsed_time(t_end) / args.steps
     ms = max_over_ranks(ms_local)

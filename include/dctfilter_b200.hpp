@@ -572,7 +572,7 @@ struct BlockTile {
 
 inline std::vector<BlockTile> tile(const GrayImage& img, int n) {
   if (n < 2) throw std::invalid_argument("tile: block side must be >= 2");
-  if (img.width < 1 || img.height < 1 || img.samples.size() != size_t(img.width) * img.height)
+  if (img.width < 0 || img.height < 0 || img.samples.size() != size_t(img.width) * img.height)
     throw std::invalid_argument("GrayImage: sample count must be width*height");
   const int bw = (img.width + n - 1) / n, bh = (img.height + n - 1) / n;
   std::vector<BlockTile> out;

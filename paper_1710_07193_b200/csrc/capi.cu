@@ -392,8 +392,9 @@ dctf_status check_plan(const dctf_plan* p) {
 }
 
 dctf_status check_image(int w, int h, size_t pitch) {
-  if (w < 1 || h < 1) return set_error(DCTF_INVALID_ARGUMENT, "image dimensions must be >= 1");
-  if (pitch < static_cast<size_t>(w)) return set_error(DCTF_INVALID_ARGUMENT, "pitch < width");
+  if (w < 0 || h < 0) return set_error(DCTF_INVALID_ARGUMENT, "image dimensions must be >= 0");
+  if (h > 0 && pitch < static_cast<size_t>(w))
+    return set_error(DCTF_INVALID_ARGUMENT, "pitch < width");
   return DCTF_OK;
 }
 
@@ -800,6 +801,7 @@ dctf_status dctf_forward(const dctf_plan* p, const uint8_t* d_img, int w, int h,
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
   if (s != DCTF_OK) return s;
+  if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (!d_img || !d_coeffs) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
   return launch_forward_u8(p, d_img, w, h, pitch, d_coeffs, as_stream(stream));
@@ -848,6 +850,7 @@ dctf_status dctf_inverse_u8(const dctf_plan* p, const double* d_coeffs, uint8_t*
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
   if (s != DCTF_OK) return s;
+  if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (!d_img || !d_coeffs) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
   return launch_inverse_u8(p, d_coeffs, d_img, w, h, pitch, as_stream(stream));
@@ -859,6 +862,7 @@ dctf_status dctf_filter_image_u8(const dctf_plan* p, const uint8_t* d_in, uint8_
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
   if (s != DCTF_OK) return s;
+  if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (!d_in || !d_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   if (d_in == d_out) return set_error(DCTF_INVALID_ARGUMENT, "in/out images may not alias");
   DeviceGuard guard(p->device);
@@ -871,6 +875,7 @@ dctf_status dctf_filter_image_spatial_u8(const dctf_plan* p, const uint8_t* d_in
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
   if (s != DCTF_OK) return s;
+  if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (!d_in || !d_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   if (p->kr * p->kc > 1024) return set_error(DCTF_UNSUPPORTED, "spatial path supports masks up to 1024 taps");
   DeviceGuard guard(p->device);
@@ -916,6 +921,7 @@ dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
     return set_error(DCTF_INVALID_ARGUMENT, "bad plan list");
   dctf_status s = check_image(w, h, pitch);
   if (s != DCTF_OK) return s;
+  if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (frame_stride < pitch * static_cast<size_t>(h))
     return set_error(DCTF_INVALID_ARGUMENT, "frame_stride smaller than one frame");
   for (int i = 0; i < nplans; ++i) {
@@ -963,6 +969,7 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
   if (s != DCTF_OK) return s;
+  if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
   std::lock_guard<std::mutex> lock(p->io_mu);
@@ -1180,6 +1187,7 @@ dctf_status dctf_filter_image_spatial_host(const dctf_plan* p, const uint8_t* h_
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
   if (s != DCTF_OK) return s;
+  if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
   const size_t bytes = pitch * static_cast<size_t>(h);

@@ -205,3 +205,25 @@ def test_identity_and_constant_properties(P):
         const = torch.full((2048, 2048), 77, dtype=torch.uint8, device="cuda")
         avg = P.FilterPlan(P.Mask.average3(), n, P.PaddingMode.kReplicate)
         assert bool((avg.filter_image(const) == 77).all())
+
+
+@pytest.mark.parametrize("shape", [(0, 0), (0, 5), (5, 0)])
+@pytest.mark.parametrize("n", [8, 16])
+def test_empty_images(P, ref, shape, n):
+    """tile() of an empty image has no blocks (image.hpp:166-167), so the
+    reference's filter_image returns an empty image of the same size without
+    an error; every image entry point here does the same."""
+    import torch
+    img = np.zeros(shape, np.uint8)
+    wm, k = ref.mask_preset("gaussian3")
+    assert ref.filter_image(img, wm, k, 1, n).shape == shape
+    plan = _plan(P, wm, k, n, 1)
+    d_img = torch.zeros(shape, dtype=torch.uint8, device="cuda")
+    co = torch.empty((0, n, n), dtype=torch.float64, device="cuda")
+    assert tuple(plan.filter_image(d_img, co).shape) == shape
+    assert tuple(plan.filter_image_spatial(d_img).shape) == shape
+    assert plan.forward_image(d_img).shape[0] == 0
+    assert tuple(plan.inverse_image_u8(co, shape[1], shape[0]).shape) == shape
+    assert plan.filter_image_host(img).shape == shape
+    assert P.filter_image(img, P.Mask(k, wm), P.PaddingMode.kReplicate, n=n).shape == shape
+    torch.cuda.synchronize()
