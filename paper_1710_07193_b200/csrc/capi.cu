@@ -1078,7 +1078,8 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
     }
     if (s == DCTF_OK && nch >= 1) s = drain(nch - 1);
   } else {
-    const size_t chunk_target = mode == 1 ? (size_t(4) << 20) : (size_t(2) << 20);
+    size_t chunk_target = mode == 1 ? (size_t(4) << 20) : (size_t(2) << 20);
+    if (const char* env = std::getenv("DCTF_E2E_CHUNK_KB")) chunk_target = std::max<size_t>(64, std::atoll(env)) << 10;
     const int nchunks = std::max(1, std::min(bh, static_cast<int>((static_cast<size_t>(h) * w + chunk_target - 1) / chunk_target)));
     const int brows = (bh + nchunks - 1) / nchunks;
     auto* din = static_cast<uint8_t*>(p->io_in);

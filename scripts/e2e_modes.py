@@ -28,3 +28,10 @@ for mode in ("0", "3"):
     run(f"pageable mode {mode}", pg_in, pg_out, K=30)
 os.environ.pop("DCTF_E2E_MODE")
 run("pageable default", pg_in, pg_out, K=30)
+# copy-engine modes against chunk size (DCTF_E2E_CHUNK_KB)
+for mode in ("0", "1"):
+    for kb in ("1024", "2048", "4096", "8192", "16384"):
+        os.environ["DCTF_E2E_MODE"] = mode
+        os.environ["DCTF_E2E_CHUNK_KB"] = kb
+        run(f"pinned mode {mode} {kb}K", h_in.numpy(), h_out.numpy())
+os.environ.pop("DCTF_E2E_CHUNK_KB")
