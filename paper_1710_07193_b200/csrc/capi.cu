@@ -973,8 +973,10 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
   std::lock_guard<std::mutex> lock(p->io_mu);
-  const size_t dpitch = (static_cast<size_t>(w) + 15) & ~size_t(15);
-  const size_t bytes = dpitch * static_cast<size_t>(h);
+  size_t dpitch = (static_cast<size_t>(w) + 15) & ~size_t(15);
+  // mode 1 stages the input with the caller's pitch (the kernel then reads
+  // the device copy and writes the mapped host output with one pitch)
+  const size_t bytes = std::max(dpitch, pitch) * static_cast<size_t>(h);
   if (p->io_bytes < bytes) {
     cudaFree(p->io_in);
     cudaFree(p->io_out);
@@ -1025,6 +1027,7 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
         (m == 3 && fused))
       mode = m;
   }
+  if (mode == 1) dpitch = pitch;
   if (p->n != 8) CUDA_TRY(cudaMemsetAsync(p->d_nan, 0, sizeof(int), s_run));
   const int n = p->n, bh = (h + n - 1) / n;
   int launches = 0;
@@ -1079,18 +1082,21 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
     if (s == DCTF_OK && nch >= 1) s = drain(nch - 1);
   } else {
     size_t chunk_target = mode == 1 ? (size_t(4) << 20) : (size_t(2) << 20);
-    if (const char* env = std::getenv("DCTF_E2E_CHUNK_KB")) chunk_target = std::max<size_t>(64, std::atoll(env)) << 10;
+    const char* chunk_env = std::getenv("DCTF_E2E_CHUNK_KB");
+    if (chunk_env) chunk_target = std::max<size_t>(64, std::atoll(chunk_env)) << 10;
     const int nchunks = std::max(1, std::min(bh, static_cast<int>((static_cast<size_t>(h) * w + chunk_target - 1) / chunk_target)));
     const int brows = (bh + nchunks - 1) / nchunks;
+    std::vector<int> cut{0};  // chunk boundaries in block rows
+    for (int c = 1; (c - 1) * brows < bh; ++c) cut.push_back(std::min(bh, c * brows));
     auto* din = static_cast<uint8_t*>(p->io_in);
     auto* dout = static_cast<uint8_t*>(p->io_out);
     auto* hout_dev = static_cast<uint8_t*>(ao.devicePointer);
-    for (int c = 0; c * brows < bh && s == DCTF_OK; ++c) {
-      const int y0 = c * brows * n;
-      const int rows = std::min(brows * n, h - y0);
+    for (size_t c = 0; c + 1 < cut.size() && s == DCTF_OK; ++c) {
+      const int y0 = cut[c] * n;
+      const int rows = std::min(cut[c + 1] * n, h) - y0;
       cudaEvent_t in_done = static_cast<cudaEvent_t>(p->events[(2 * c) % 64]);
       cudaEvent_t run_done = static_cast<cudaEvent_t>(p->events[(2 * c + 1) % 64]);
-      if (pitch == dpitch)
+      if (pitch == dpitch && pitch == static_cast<size_t>(w))  // else 2-D: the caller's row padding is not ours
         CUDA_TRY(cudaMemcpyAsync(din + y0 * dpitch, h_in + y0 * pitch, static_cast<size_t>(rows) * pitch,
                                  cudaMemcpyHostToDevice, s_in));
       else
@@ -1109,7 +1115,7 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
       if (s != DCTF_OK || mode == 1) continue;
       CUDA_TRY(cudaEventRecord(run_done, s_run));
       CUDA_TRY(cudaStreamWaitEvent(s_out, run_done, 0));
-      if (pitch == dpitch)
+      if (pitch == dpitch && pitch == static_cast<size_t>(w))  // else 2-D: the caller's row padding is not ours
         CUDA_TRY(cudaMemcpyAsync(h_out + y0 * pitch, dout + y0 * dpitch, static_cast<size_t>(rows) * pitch,
                                  cudaMemcpyDeviceToHost, s_out));
       else

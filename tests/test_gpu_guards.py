@@ -120,13 +120,32 @@ def test_entry_points_stay_in_bounds(cuda, n, name, prec, pad):
         img_ok(out, sp_t, "filter_image_spatial_u8")
         torch.cuda.synchronize()
         assert torch.equal(src, src_before), "an entry point wrote into its input"
-        # host entry on pitched host buffers (pageable and pinned)
-        for pinned in (False, True):
-            hs = src.cpu()
-            ho = torch.full((h + 3, pitch), CANARY_U8, dtype=torch.uint8)
-            if pinned:
-                hs, ho = hs.pin_memory(), ho.pin_memory()
-            hsn, hon = hs.numpy(), ho.numpy()
-            _lib.check(lib.dctf_filter_image_host(plan.handle, hsn.ctypes.data + pitch, hon.ctypes.data + pitch,
-                                                  wd, h, pitch))
-            img_ok(torch.from_numpy(hon), ref_img, f"filter_image_host pinned={pinned}")
+        # host entry on pitched host buffers (pageable and pinned), every
+        # transfer mode (DCTF_E2E_MODE; invalid ones fall back to the
+        # default), at this pitch and at the 16-byte-rounded width
+        import os
+        for hp in sorted({pitch, (wd + 15) // 16 * 16}):
+            hsrc = np.full((h + 3, hp), 0x3C, np.uint8)
+            hsrc[1:h + 1, :wd] = img
+            for mode in (None, "0", "1", "2", "3"):
+                for pinned in (False, True):
+                    hs = torch.from_numpy(hsrc.copy())
+                    ho = torch.full((h + 3, hp), CANARY_U8, dtype=torch.uint8)
+                    if pinned:
+                        hs, ho = hs.pin_memory(), ho.pin_memory()
+                    hsn, hon = hs.numpy(), ho.numpy()
+                    if mode is None:
+                        os.environ.pop("DCTF_E2E_MODE", None)
+                    else:
+                        os.environ["DCTF_E2E_MODE"] = mode
+                    try:
+                        _lib.check(lib.dctf_filter_image_host(plan.handle, hsn.ctypes.data + hp,
+                                                              hon.ctypes.data + hp, wd, h, hp))
+                    finally:
+                        os.environ.pop("DCTF_E2E_MODE", None)
+                    what = f"filter_image_host pitch={hp} mode={mode} pinned={pinned}"
+                    b = hon
+                    assert (b[0] == CANARY_U8).all() and (b[h + 1:] == CANARY_U8).all(), f"{what}: rows outside"
+                    assert (b[1:h + 1, wd:] == CANARY_U8).all(), f"{what}: bytes past the row end"
+                    assert np.array_equal(b[1:h + 1, :wd], ref_img), f"{what}: differs from the device path"
+                    assert np.array_equal(hsn, hsrc), f"{what}: wrote into its input"
