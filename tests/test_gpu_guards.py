@@ -149,3 +149,45 @@ def test_entry_points_stay_in_bounds(cuda, n, name, prec, pad):
                     assert (b[1:h + 1, wd:] == CANARY_U8).all(), f"{what}: bytes past the row end"
                     assert np.array_equal(b[1:h + 1, :wd], ref_img), f"{what}: differs from the device path"
                     assert np.array_equal(hsn, hsrc), f"{what}: wrote into its input"
+
+
+@pytest.mark.parametrize("n", [8, 16])
+def test_frame_batch_stays_in_bounds(cuda, n):
+    """dctf_filter_frames_u8 with pitch > width and frame_stride > pitch *
+    height: the gaps between rows and between frames are the caller's; every
+    frame equals the single-image call with its plan."""
+    import ctypes as C
+
+    import torch
+
+    import paper_1710_07193_b200 as P
+    from paper_1710_07193_b200 import _lib, synth
+    masks = _masks()
+    plans = [P.FilterPlan(P.Mask(kr, w) if kr == kc else P.Mask.rect(kr, kc, w), n, P.PaddingMode.kReplicate)
+             for (kr, kc, w) in (masks["gaussian5"], masks["laplacian"], masks["random5"], masks["motion1x9"])]
+    F, h, wd = 6, 3 * n + 3, 9 * n + 5
+    pitch = ((wd + 15) // 16) * 16 + 32
+    stride = pitch * (h + 3)
+    imgs = [synth.uniform_image(100 + f, wd, h) for f in range(F)]
+    src = torch.full((F * stride + pitch,), 0x3C, dtype=torch.uint8, device="cuda")
+    out = torch.full_like(src, CANARY_U8)
+    for f in range(F):
+        v = src[f * stride: f * stride + h * pitch].view(h, pitch)
+        v[:, :wd] = torch.from_numpy(imgs[f]).cuda()
+    before = src.clone()
+    of = [f % 4 for f in range(F)]
+    handles = (C.c_void_p * 4)(*[p.handle.value for p in plans])
+    idx = (C.c_int * F)(*of)
+    _lib.check(_lib.lib.dctf_filter_frames_u8(handles, 4, idx, src.data_ptr(), out.data_ptr(), F, wd, h, pitch,
+                                              stride, int(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(src, before), "frame batch wrote into its input"
+    o = out.cpu().numpy()
+    mask = np.ones(o.shape, bool)
+    for f in range(F):
+        blk = o[f * stride: f * stride + h * pitch].reshape(h, pitch)
+        ref = plans[of[f]].filter_image(torch.from_numpy(imgs[f]).cuda()).cpu().numpy()
+        assert np.array_equal(blk[:, :wd], ref), f"frame {f}"
+        m = mask[f * stride: f * stride + h * pitch].reshape(h, pitch)
+        m[:, :wd] = False
+    assert (o[mask] == CANARY_U8).all(), "frame batch wrote outside its frames"
