@@ -521,7 +521,7 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
       p->sep_rank = 0;
     }
     // coefficient path: the parity-class k_coef8_sym is already HBM-bound
-    if (e == cudaSuccess && !psym && dctf::layout_csep8(*p, frag, p->csep_rank)) {
+    if (e == cudaSuccess && (!psym || std::getenv("DCTF_COEF8_SEP_SYM")) && dctf::layout_csep8(*p, frag, p->csep_rank)) {
       e = cudaMalloc(&p->d_csep, frag.size() * sizeof(double));
       if (e == cudaSuccess)
         e = cudaMemcpy(p->d_csep, frag.data(), frag.size() * sizeof(double), cudaMemcpyHostToDevice);
