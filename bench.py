@@ -508,7 +508,42 @@ def aux_cfg5(c):
     res["asymmetric_frames_int8exact"] = {"ms": ms_m, "blocks_per_s": nb / (ms_m / 1e3),
                                           "kernels": [pl.image_kernel for pl in mixed],
                                           "u8_identical_to_fp64": bool(torch.equal(out_m, ref_out))}
+    if c.world > 1:
+        res["gather"] = aux_gather(c, ref_out, FF)
     return res
+
+
+def aux_gather(c, part, total_frames):
+    """The optional collective of SURVEY 8(e), timed apart from the filter:
+    every rank's filtered frames all-gathered (one all_gather_into_tensor of
+    equal slabs, as paper_1710_07193_b200/shard.py does; NCCL over
+    NVLink/NVSwitch), CUDA events on the launching stream, median of 5,
+    max over ranks. Under DCTF_BENCH_BACKEND=gloo the slabs go through host
+    memory (code-path check; not a timing)."""
+    import torch.distributed as dist
+    torch = c.torch
+    nccl = dist.get_backend() == "nccl"
+    slab = part.contiguous() if nccl else part.cpu()
+    full = torch.empty((slab.shape[0] * c.world,) + tuple(slab.shape[1:]), dtype=slab.dtype,
+                       device=slab.device)
+    ts = []
+    for _ in range(6):
+        c.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dist.all_gather_into_tensor(full, slab)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = c.max_over_ranks(statistics.median(ts[1:]))
+    own = slab.numel()
+    ok = bool(torch.equal(full[c.rank * slab.shape[0]:(c.rank + 1) * slab.shape[0]].to(slab.device), slab))
+    return {"collective": "all_gather_into_tensor of each rank's filtered frames",
+            "backend": dist.get_backend(), "frames": total_frames,
+            "bytes_per_rank_received": own * (c.world - 1), "ms": ms,
+            "gb_per_s_per_rank": own * (c.world - 1) / (ms / 1e3) / 1e9,
+            "own_slab_intact": ok,
+            "note": None if nccl else "gloo through host memory: code-path check, not a timing"}
 
 
 def aux_n16(c):
