@@ -71,15 +71,37 @@ def measured_peaks():
         return {}
 
 
+_POLL_SRC = r"""
+import sys, time, pynvml as nv
+nv.nvmlInit()
+bus, out = sys.argv[1], open(sys.argv[2], "w", buffering=1)
+try:
+    h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+except Exception:
+    h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[3]))
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+print("ready", file=sys.stdout, flush=True)
+while True:
+    try:
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        out.write(f"{time.perf_counter()!r},{sm},{mx},{rs}\n")
+    except Exception:
+        pass
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
     """SM clocks / throttle reasons sampled during the timed region.
 
-    NVML polled every ~2 ms from a host thread (each sample stamped with the
-    host clock, so only samples inside [mark_start, mark_stop] count as "under
-    load"); nvidia-smi -lms 50 when NVML is unavailable. A timed region
+    A separate process polls NVML every ~2 ms and appends samples stamped with
+    CLOCK_MONOTONIC (time.perf_counter, the same clock in every process) to a
+    file, so nothing runs in this interpreter during the timed region; only
+    samples inside a marked window count as "under load". A timed region
     shorter than a few samples (small --steps) is reported with the samples it
-    got plus those of `sustain()`: the same step launched back to back for
-    ~0.3 s right after the region, untimed, named in "window"."""
+    got plus those of a named, untimed window of the same steps right after it
+    (see main). nvidia-smi -lms 50 when NVML is unavailable."""
 
     REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
                ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
@@ -87,59 +109,56 @@ class ClockSampler:
 
     def __init__(self, gpu: int):
         self.gpu, self.samples, self.windows = gpu, [], []
-        self._stop = threading.Event()
-        self._thread = None
-        self._nvml = None
-        self._smi = None
-        self._smi_lines = []
+        self.proc, self.path, self.source = None, None, None
 
-    def _handle(self):
-        import pynvml
-        pynvml.nvmlInit()
+    def start(self):
+        import tempfile
+        fd, self.path = tempfile.mkstemp(prefix="dctf_clocks_", suffix=".csv")
+        os.close(fd)
         try:
+            import pynvml  # noqa: F401  (the poller needs it)
             import torch
             pr = torch.cuda.get_device_properties(self.gpu)
             bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
-            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            self.proc = subprocess.Popen([sys.executable, "-c", _POLL_SRC, bus, self.path, str(self.gpu)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            if self.proc.stdout.readline().strip() != "ready":
+                raise RuntimeError("NVML poller did not start")
+            self.source = "nvml (2 ms poll, separate process)"
         except Exception:
-            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-
-    def _poll(self):
-        nv, h = self._nvml
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        while not self._stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((time.perf_counter(), float(sm), float(mx), int(rs)))
-            except Exception:
-                pass
-            time.sleep(0.002)
-
-    def start(self):
-        try:
-            self._nvml = self._handle()
-            self._thread = threading.Thread(target=self._poll, daemon=True)
-            self._thread.start()
-            self.source = "nvml (2 ms poll)"
-        except Exception:
-            self._nvml = None
+            if self.proc:
+                self.proc.kill()
             self.source = "nvidia-smi -lms 50"
+            self._smi_out = open(self.path, "w")
             try:
-                self._smi = subprocess.Popen(
-                    ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=timestamp,clocks.sm,clocks.max.sm,"
                      "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "50"],
-                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-                threading.Thread(target=self._read_smi, daemon=True).start()
+                    stdout=self._smi_out, stderr=subprocess.DEVNULL, text=True)
             except Exception:
-                self._smi = None
+                self.proc = None
+            self._smi_t0 = time.perf_counter()
 
-    def _read_smi(self):
-        for line in self._smi.stdout:
-            p = [x.strip() for x in line.split(",")]
+    def sample_count(self, t0):
+        """Samples stamped after t0 so far (reads the poller's file)."""
+        self._load()
+        return sum(1 for s in self.samples if s[0] >= t0)
+
+    def _load(self):
+        self.samples = []
+        try:
+            lines = open(self.path).read().splitlines()
+        except OSError:
+            return
+        for ln in lines:
+            p = [x.strip() for x in ln.split(",")]
             try:
-                rs = int(p[2], 16) if len(p) > 2 and p[2].startswith("0x") else 0
-                self.samples.append((time.perf_counter(), float(p[0]), float(p[1]), rs))
+                if self.source.startswith("nvml"):
+                    self.samples.append((float(p[0]), float(p[1]), float(p[2]), int(p[3])))
+                else:  # nvidia-smi: no shared clock, stamp by arrival order (50 ms apart)
+                    rs = int(p[3], 16) if p[3].startswith("0x") else 0
+                    self.samples.append((self._smi_t0 + 0.05 * len(self.samples), float(p[1]),
+                                         float(p[2]), rs))
             except (ValueError, IndexError):
                 continue
 
@@ -148,15 +167,17 @@ class ClockSampler:
 
     def stop(self):
         time.sleep(0.01)
-        self._stop.set()
-        if self._thread:
-            self._thread.join(timeout=2)
-        if self._smi:
-            self._smi.terminate()
+        if self.proc:
+            self.proc.terminate()
             try:
-                self._smi.wait(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
-                self._smi.kill()
+                self.proc.kill()
+        self._load()
+        try:
+            os.unlink(self.path)
+        except OSError:
+            pass
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
                "source": self.source, "window": []}
         picked = []
@@ -823,7 +844,7 @@ def main():
     torch.cuda.synchronize()
     clocks.window("timed region", h0, time.perf_counter())
     barrier()
-    if clocks.source.startswith("nvml") and len(clocks.samples) < 20:
+    if clocks.source.startswith("nvml") and clocks.sample_count(h0) < 20:
         # too short a region for the poller: keep the same steps running
         # ~0.3 s (untimed) and sample those too, named as such
         h1 = time.perf_counter()
