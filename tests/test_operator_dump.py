@@ -59,7 +59,7 @@ def test_rejects_malformed_dumps(ref):
     bad_fp[pos] = "1" if text[pos] == "0" else "0"
     for bad, what in (("bogus 1\n", "expected 'dctfilter-operators'"),
                       ("dctfilter-operators 9\nsets 0\n", "unsupported version"),
-                      (text[: len(text) // 2], ""),
+                      (text[: len(text) // 2], None),  # truncated: any parse error
                       ("".join(bad_fp), "fingerprint mismatch"),
                       ("dctfilter-operators 1\nsets 0\n", "no operator set")):
         with pytest.raises(ValueError, match=what):
