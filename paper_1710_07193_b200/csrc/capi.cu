@@ -322,6 +322,28 @@ dctf_status make_xmap(void* vmap, const double* d, long long nblocks, int nn, in
   if (r != CUDA_SUCCESS) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   return DCTF_OK;
 }
+
+// 3-D u8 view [nframes][h][w] of a frame batch (pitch and frame_stride in
+// bytes, both multiples of 16, base 16-byte aligned); box [1][8][box_w], no
+// swizzle, OOB -> 0.
+dctf_status make_imap(void* vmap, const uint8_t* d, int w, int h, int nframes, size_t pitch,
+                      long long frame_stride, int box_w) {
+  CUtensorMap* map = static_cast<CUtensorMap*>(vmap);
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+                              static_cast<cuuint64_t>(nframes)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch),
+                                 static_cast<cuuint64_t>(nframes > 1 ? frame_stride : pitch * h)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), 8, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(d), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled (u8 image) failed (" + std::to_string(int(r)) + ")");
+  return DCTF_OK;
+}
 }  // namespace dctf
 
 namespace {
@@ -586,6 +608,16 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
       return s;
     }
   }
+  // n = 8 FP64 plans: the exact-integer composed-operator kernel serves the
+  // u8 image path (coefficient requests keep the FP64 kernels); DCTF_NO_Q=1
+  // at plan creation opts out.
+  if (precision == DCTF_PREC_FP64 && n == 8 && !std::getenv("DCTF_NO_Q")) {
+    const dctf_status s = dctf::upload_kq_operator(p);
+    if (s != DCTF_OK) {
+      dctf_plan_destroy(p);
+      return s;
+    }
+  }
   *out = p;
   return DCTF_OK;
 }
@@ -741,6 +773,8 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_hsplit);
     cudaFree(p->d_gimg);
     cudaFree(p->d_gscale);
+    cudaFree(p->d_kq);
+    cudaFree(p->d_refchain);
     cudaFree(p->d_nan);
     cudaFree(p->d_weights);
     cudaFree(p->io_in);
@@ -776,6 +810,7 @@ const char* dctf_plan_coef_kernel(const dctf_plan* p) {
 const char* dctf_plan_image_kernel(const dctf_plan* p) {
   if (!p) return nullptr;
   if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT) return "k_fused8_i8";
+  if (p->kq) return "k_fused8_q";
   if (p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3) return "unfused";
   if (p->n == 8) return p->sep_rank > 0 ? "k_fused8_sep" : (p->sym ? "k_fused8_sym" : "k_fused8");
   if (std::getenv("DCTF_N16_UNFUSED")) return "unfused";
@@ -935,6 +970,13 @@ dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
       return set_error(DCTF_INVALID_ARGUMENT, "plan_of_frame index out of range");
   DeviceGuard guard(plans[0]->device);
   const cudaStream_t st = as_stream(stream);
+  // Every plan on the exact-integer kernel: the whole batch is one launch
+  // (each plan's digit image resident in shared memory, per-frame selection).
+  bool all_kq = plans[0]->n == 8 && nplans <= dctf::KQ_MAX_PLANS && nframes <= dctf::KQ_MAX_FRAMES;
+  for (int i = 0; i < nplans && all_kq; ++i) all_kq = plans[i]->kq;
+  if (all_kq)
+    return dctf::launch_fused8_q(plans, nplans, h_plan_of_frame, d_in, d_out, w, h, pitch,
+                                 static_cast<long long>(frame_stride), nframes, st, false, nullptr);
   // Frames sharing a plan and evenly spaced go in one launch (round-robin
   // assignment -> one launch per plan); anything else falls back per frame.
   for (int pi = 0; pi < nplans && s == DCTF_OK; ++pi) {

@@ -1486,6 +1486,9 @@ namespace dctf {
 dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
                                 cudaStream_t st, bool host_mapped) {
+  if (p->kq && !coef_out)
+    return dctf::launch_fused8_q(&p, 1, nullptr, in, out, w, h, pitch, frame_stride, nframes, st, host_mapped,
+                                 p->d_nan);
   if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT)
     return dctf::launch_fused8_i8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st,
                                   sm_count(p->device));

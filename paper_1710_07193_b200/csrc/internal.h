@@ -42,6 +42,16 @@ struct dctf_plan {
   double* d_sep = nullptr;       // its DMMA fragment image
   int csep_rank = 0;             // > 0: k_coef16_sep / k_coef8_sep applies (layout_csep16 / 8), pairs
   double* d_csep = nullptr;      // its DMMA fragment image
+  // k_fused8_q (quant.cu): the composed operator as exact int8 digit slices
+  // (layout_kq8) and the reference-order fallback's data (refchain_image).
+  bool kq = false;               // the u8 image path of this plan runs k_fused8_q
+  int kq_F = 0;                  // fixed-point fraction bits of K_int
+  uint32_t kq_U = 0;             // uncertainty window, in units of 2^-32 of a pixel
+  double kq_ebound = 0.0;        // E + M of layout_kq8 (pixel units)
+  double kq_flag_rate = 0.0;     // expected flagged-block fraction (uniform fractions)
+  void* d_kq = nullptr;          // 16 KB digit image (SW64 K-major)
+  double* d_refchain = nullptr;  // C | C^t | lefts | rights (mode 1)
+  int ref_mode = 0, ref_npairs = 0;
 
   // Device staging of the host-buffer entry (copy mode), guarded by io_mu.
   mutable std::mutex io_mu;
@@ -129,14 +139,39 @@ void layout_hsplit_bf16(int n, const std::vector<double>& op, std::vector<uint16
 void layout_gslices_i8(const std::vector<double>& op, const std::vector<double>& basis,
                        std::vector<int8_t>& bimg, std::vector<double>& scales);
 
+// k_fused8_q operator (plan.cc): see layout_kq8.
+struct KqInfo {
+  bool ok = false;
+  int F = 0;
+  uint32_t U = 0;
+  double ebound = 0.0, flag_rate = 0.0;
+};
+bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info);
+void refchain_image(const dctf_plan& p, std::vector<double>& out, int& mode, int& npairs);
+
 // TMA tensor map over block-major FP64 coefficients (capi.cu): 2-D
 // [nblocks rows x nn cols], box [box_rows x 16 cols], 128B swizzle.
 dctf_status make_xmap(void* map, const double* d, long long nblocks, int nn, int box_rows, int l2promo = 3);
+// TMA tensor map over a u8 frame batch (capi.cu): 3-D [nframes][h][w], box
+// [1][8][box_w], no swizzle, OOB -> 0.
+dctf_status make_imap(void* map, const uint8_t* d, int w, int h, int nframes, size_t pitch,
+                      long long frame_stride, int box_w);
 
 // Exact-INT8 tcgen05 fused n=8 path (ozaki.cu).
 dctf_status upload_i8_operator(dctf_plan* p);
 dctf_status launch_fused8_i8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
                              long long frame_stride, int nframes, double* coef_out, cudaStream_t st, int sms);
+
+// Exact-integer composed-operator n = 8 image path (quant.cu): uploads the
+// plan's digit image and fallback data; launches the kernel for a batch of
+// frames whose plans are plans[plan_of_frame[f]] (all kq-enabled, n = 8, one
+// device), then the reference-order fallback over the flagged blocks.
+dctf_status upload_kq_operator(dctf_plan* p);
+dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int* plan_of_frame,
+                            const uint8_t* in, uint8_t* out, int w, int h, size_t pitch, long long frame_stride,
+                            int nframes, cudaStream_t st, bool host_mapped, int* d_nan_or_null);
+constexpr int KQ_MAX_PLANS = 4;
+constexpr int KQ_MAX_FRAMES = 1024;
 
 // 3xTF32 tcgen05 coefficient filter (tc.cu).
 dctf_status launch_coef_tf32x3(const dctf_plan* p, const double* d_in, double* d_out, long long nb,

@@ -1002,3 +1002,158 @@ bool layout_csep8(const dctf_plan& p, std::vector<double>& out, int& rank) {
   return true;
 }
 }  // namespace dctf
+
+namespace dctf {
+
+// Operator of k_fused8_q (quant.cu): the fused chain's three linear maps —
+// forward DCT, the DCT-domain filter, inverse DCT — composed into one 64 x 64
+// operator on pixels, K = (C (x) C)^t H (C (x) C), evaluated in long double
+// from the plan's own factors rather than from the rounded dense H:
+//   reference-domain plans (apply_pairs, filter.hpp:30-38):
+//     z = C^t (sum_p L_p (C P C^t) R_p) C = sum_p A_p P B_p,
+//     A_p = C^t L_p C, B_p = C^t R_p C, so K[(y,x),(a,b)] = sum_p A_p[y][a] B_p[b][x];
+//   convolve-formula plans (kr != kc or k > n; spatial.hpp:36-37):
+//     K[(y,x),(pad(y+r-hr), pad(x+c-hc))] += w[r][c].
+// K is then written as K_int = round(K 2^F) in four balanced base-256 digits
+// d_0..d_3 in [-128, 127] (K_int = sum_s d_s 256^(3-s)), F the largest
+// integer <= 32 with max|K| 2^F inside the digits' range. Pixels are exact
+// u8, so the tensor cores' int32 partials a_s = sum_j d_s[i][j] p_j are exact
+// and so is z_int = sum_s a_s 256^(3-s) = sum_j K_int[i][j] p_j. Against the
+// exact composed value z* the only error is the operator quantisation,
+//   |z_int 2^-F - z*| <= E_i = 255 sum_j |K[i][j] - K_int[i][j] 2^-F|,
+// and against the reference's own FP64 result z_ref (rounding in its
+// forward / apply / inverse chain, ~1e-13 relative in practice) the kernel
+// allows M_i = 2^-30 + 2^-36 * 255 sum_j |K[i][j]|. A pixel whose fixed-point
+// value lies more than T = (E + M) 2^F units of 2^-F away from every .5
+// rounding boundary therefore rounds exactly as the reference does; the
+// others (a ~1e-4 fraction of blocks at the BASELINE masks) are flagged and
+// recomputed in the reference's own operation order (k_fallback8).
+//
+// B-operand image: 256 rows x 64 bytes, K-major, 64-byte swizzle (UMMA
+// SWIZZLE_64B: 16-byte chunk c of row n stored at chunk c ^ ((n >> 1) & 3));
+// row n = 4 i + s holds digit s of output pixel i, so one 32-column
+// tcgen05.ld returns 8 whole pixels.
+bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
+  info = KqInfo{};
+  if (p.n != 8) return false;
+  constexpr int n = 8, nn = 64;
+  std::vector<long double> K(size_t(nn) * nn, 0.0L);
+  const double* C = p.basis.data();
+  if (!p.dct_left.empty() || (p.reference_domain && p.npairs == 0)) {
+    const int np = static_cast<int>(p.dct_left.size() / nn);
+    for (int q = 0; q < np; ++q) {
+      long double A[64], B[64];
+      for (int side = 0; side < 2; ++side) {
+        const double* M = (side == 0 ? p.dct_left.data() : p.dct_right.data()) + size_t(q) * nn;
+        long double t[64];
+        for (int u = 0; u < n; ++u)  // t = M C
+          for (int x = 0; x < n; ++x) {
+            long double acc = 0.0L;
+            for (int v = 0; v < n; ++v) acc += static_cast<long double>(M[u * n + v]) * C[v * n + x];
+            t[u * n + x] = acc;
+          }
+        long double* dst = side == 0 ? A : B;
+        for (int y = 0; y < n; ++y)  // C^t t
+          for (int x = 0; x < n; ++x) {
+            long double acc = 0.0L;
+            for (int u = 0; u < n; ++u) acc += static_cast<long double>(C[u * n + y]) * t[u * n + x];
+            dst[y * n + x] = acc;
+          }
+      }
+      for (int y = 0; y < n; ++y)
+        for (int x = 0; x < n; ++x)
+          for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) K[size_t(y * n + x) * nn + a * n + b] += A[y * n + a] * B[b * n + x];
+    }
+  } else {
+    const int kr = p.kr, kc = p.kc, hr = (kr - 1) / 2, hc = (kc - 1) / 2;
+    const bool rep = p.padding == DCTF_PAD_REPLICATE;
+    for (int y = 0; y < n; ++y)
+      for (int x = 0; x < n; ++x)
+        for (int r = 0; r < kr; ++r)
+          for (int c = 0; c < kc; ++c) {
+            int a = y + r - hr, b = x + c - hc;
+            if (rep) {
+              a = std::min(std::max(a, 0), n - 1);
+              b = std::min(std::max(b, 0), n - 1);
+            } else if (a < 0 || a >= n || b < 0 || b >= n) {
+              continue;
+            }
+            K[size_t(y * n + x) * nn + a * n + b] += static_cast<long double>(p.weights[size_t(r) * kc + c]);
+          }
+  }
+  long double kmax = 0.0L;
+  for (long double v : K) {
+    if (!std::isfinite(static_cast<double>(v))) return false;
+    kmax = std::max(kmax, std::fabs(v));
+  }
+  constexpr long double R = 16843009.0L;  // 256^3 + 256^2 + 256 + 1
+  const long double lim = 127.0L * R - 1.0L;
+  int F = 32;
+  if (kmax > 0.0L) F = std::min(32, static_cast<int>(std::floor(std::log2(lim / kmax))));
+  while (F > 0 && kmax * std::ldexp(1.0L, F) > lim) --F;  // log2 rounding guard
+  if (F < 17) return false;
+  const long double scale = std::ldexp(1.0L, F);
+  std::vector<long long> Ki(K.size());
+  long double emax = 0.0L;
+  for (int i = 0; i < nn; ++i) {
+    long double err = 0.0L, mag = 0.0L;
+    for (int j = 0; j < nn; ++j) {
+      const long double v = K[size_t(i) * nn + j] * scale;
+      const long long q = std::llroundl(v);
+      Ki[size_t(i) * nn + j] = q;
+      err += std::fabs(v - static_cast<long double>(q));
+      mag += std::fabs(K[size_t(i) * nn + j]);
+    }
+    const long double e = 255.0L * err / scale + std::ldexp(1.0L, -30) + std::ldexp(1.0L, -36) * 255.0L * mag;
+    emax = std::max(emax, e);
+  }
+  const long double T = std::ceil(emax * scale) + 1.0L;
+  const long double U = T * std::ldexp(1.0L, 32 - F);
+  if (U >= std::ldexp(1.0L, 30)) return false;
+  const double flag_rate = static_cast<double>(64.0L * 2.0L * T / scale);  // per block, uniform fractions
+  if (flag_rate > 0.02) return false;
+  bimg.assign(size_t(256) * 64, 0);
+  for (int i = 0; i < nn; ++i)
+    for (int j = 0; j < nn; ++j) {
+      long long v = Ki[size_t(i) * nn + j];
+      int d[4];
+      for (int s = 3; s >= 1; --s) {
+        d[s] = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(v & 255)));
+        v = (v - d[s]) / 256;
+      }
+      if (v < -128 || v > 127) return false;
+      d[0] = static_cast<int>(v);
+      for (int s = 0; s < 4; ++s) {
+        const int row = 4 * i + s;
+        bimg[size_t(row) * 64 + ((((j >> 4) ^ ((row >> 1) & 3)) << 4) | (j & 15))] = static_cast<int8_t>(d[s]);
+      }
+    }
+  info.ok = true;
+  info.F = F;
+  info.U = static_cast<uint32_t>(U);
+  info.ebound = static_cast<double>(emax);
+  info.flag_rate = flag_rate;
+  return true;
+}
+
+// Device data of the reference-order fallback (k_fallback8): C, C^t and the
+// DCT-domain pairs (mode 1), or nothing beyond the plan's weights (mode 2,
+// convolve formula).
+void refchain_image(const dctf_plan& p, std::vector<double>& out, int& mode, int& npairs) {
+  const int nn = p.n * p.n;
+  out.assign(p.basis.begin(), p.basis.end());
+  for (int i = 0; i < p.n; ++i)
+    for (int j = 0; j < p.n; ++j) out.push_back(p.basis[size_t(j) * p.n + i]);
+  if (!p.dct_left.empty() || (p.reference_domain && p.npairs == 0)) {
+    mode = 1;
+    npairs = static_cast<int>(p.dct_left.size() / nn);
+    out.insert(out.end(), p.dct_left.begin(), p.dct_left.end());
+    out.insert(out.end(), p.dct_right.begin(), p.dct_right.end());
+  } else {
+    mode = 2;
+    npairs = 0;
+  }
+}
+
+}  // namespace dctf

@@ -1,0 +1,612 @@
+// k_fused8_q: the 8x8 spatial-in/spatial-out DCT-domain filter
+// (filter_image, image.hpp:210-225; per block filter_block, filter.hpp:71-73,
+// then quantize_sample, spatial.hpp:71-75) as ONE exact integer contraction
+// on the 5th-generation tensor cores (tcgen05.mma kind::i8, int32
+// accumulators in TMEM), sm_100a.
+//
+// Math. The fused chain is three linear maps on a block's pixels p (forward
+// DCT, the DCT-domain operator H_dct, inverse DCT); plan.cc: layout_kq8
+// composes them on the host into one 64 x 64 operator K = (C (x) C)^t H (C (x) C)
+// (long double, from the plan's own DCT-domain pairs) and writes it as
+// K_int = round(K 2^F) in four balanced base-256 int8 digits. Pixels are
+// exact u8, so every tensor-core partial a_s = sum_j d_s[i][j] p_j is an
+// exact int32 and z_int = sum_s a_s 256^(3-s) is the exact fixed-point value
+// of K_int p. Its only error against the exact chain is the operator
+// quantisation, bounded per plan (E); together with a margin for the
+// reference's own FP64 rounding (M) this gives an uncertainty window T: a
+// pixel whose fixed-point value is more than T/2^F from every .5 rounding
+// boundary rounds exactly as the reference does (round half away, clamp).
+// The rest (~1e-4 of the blocks at the BASELINE masks) are recomputed in the
+// reference's own operation order (forward_2d -> apply_pairs -> inverse_2d,
+// block_matrix.hpp:67-81's i-k-j products with separately rounded multiply
+// and add, dct.hpp:59-68, filter.hpp:30-38; convolve's order for
+// convolve-formula plans) by a fallback warp of the same CTA, so the u8
+// output is the reference's on every pixel, not only outside near-ties.
+//
+// Epilogue arithmetic (per pixel, 32-bit integer ops only): with
+// h = a0*256 + a1, l = a2*256 + a3, the rounding offset 2^(F-1) folded in:
+//   S = h + (l >> 16) + 2^(F-17)          -> v = S*2^16 + (l & 0xffff)
+//   q = S >> (F-16)                        = floor(z + 0.5) (u8 after saturation)
+//   key = (v mod 2^F) << (32-F)            one funnel shift of (S : l << 16)
+//   uncertain  <=>  (key + U) mod 2^32 < 2U,  U = T 2^(32-F)
+// so the per-block test is a running unsigned min.
+//
+// CTA = 15 warps, one CTA per SM (TMEM: 2 x 256 columns), persistent over
+// tiles of up to 128 horizontally adjacent blocks (one block row, 8 x 1024 px):
+//   warp 0      TMA: 4 boxes [8 rows x 256 px] per tile into a 6-stage raw ring
+//               (48 KB of pixels in flight per SM); a 3-D tensor map covers
+//               the whole frame batch, out-of-range rows/columns read as 0.
+//   warp 1      MMA issuer: 2 x tcgen05.mma (M 128, N 256, K 32) per tile into
+//               a double-buffered TMEM accumulator.
+//   warps 2-5   converters: thread = block; the block's 8 pixel rows from the
+//               raw stage (tile()'s edge replication for ragged blocks) into the
+//               K-major 64-byte-swizzled A operand.
+//   warps 6-13  epilogue: two warps per TMEM lane quarter (pixel rows 0-3 /
+//               4-7); tcgen05.ld 32 columns = 8 whole pixels, the integer
+//               rounding above, cvt.pack.sat, 8-byte coalesced row stores.
+//               Blocks with an uncertain pixel are not stored here; they go
+//               to the fallback queue.
+//   warp 14     fallback: the reference-order chain on queued blocks (FP64).
+// The plans' digit images (16 KB each, up to 4 plans: one launch covers a
+// whole multi-mask frame batch) stay resident in shared memory.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <string>
+
+#include "device.cuh"
+#include "fastdiv.cuh"
+#include "internal.h"
+
+using dctf::KQ_MAX_FRAMES;
+using dctf::KQ_MAX_PLANS;
+using dctf::set_error;
+
+namespace {
+
+namespace q8 {
+constexpr int TILE = 128;                  // blocks per tile = MMA M = TMEM lanes
+constexpr int NCOL = 256;                  // accumulator columns: 64 pixels x 4 digits
+constexpr int BBYTES = NCOL * 64;          // one plan's digit image
+constexpr int ABYTES = TILE * 64;          // one A stage
+constexpr int RAWB = 8 * TILE * 8;         // one raw stage: 8 rows x 1024 px
+constexpr int NRAW = 6, NA = 2;
+constexpr int W_TMA = 0, W_MMA = 1, W_CONV = 2, NCONV = 4, W_EPI = 6, NEPI = 8, W_FB = 14;
+constexpr int THREADS = 32 * (W_FB + 1);
+constexpr int FQ = 256;                    // fallback queue slots
+constexpr int SMEM = 1024 + KQ_MAX_PLANS * BBYTES + NA * ABYTES + NRAW * RAWB;
+}  // namespace q8
+
+struct RefPlan {
+  const double* chain;    // C | C^t | lefts | rights (mode 1)
+  const double* weights;  // kr x kc (mode 2)
+  int mode, npairs, kr, kc, padding;
+};
+
+struct QArgs {
+  const int8_t* bimg[KQ_MAX_PLANS];
+  uint32_t U[KQ_MAX_PLANS], c17[KQ_MAX_PLANS];
+  int shS[KQ_MAX_PLANS], shK[KQ_MAX_PLANS];
+  RefPlan ref[KQ_MAX_PLANS];
+  int nplans;
+  uint8_t pof[KQ_MAX_FRAMES];  // plan of frame
+};
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_64B (8-row atoms of 64 B):
+// SBO = 512 B between 8-row groups, version 1 (sm_100).
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>(512u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(4u) << 61;
+  return d;
+}
+// kind::i8 instruction descriptor: D s32, A u8 (pixels), B s8 (digits), both K-major.
+__host__ __device__ constexpr uint32_t idesc_u8s8(int m, int n) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_u8s8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+        "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+        "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// {sat_u8(x0), sat_u8(x1), sat_u8(x2), sat_u8(x3)} little-endian
+__device__ __forceinline__ uint32_t pack4_sat(int x0, int x1, int x2, int x3) {
+  uint32_t r;
+  asm("{\n\t.reg .u32 t;\n\t"
+      "cvt.pack.sat.u8.s32.b32 t, %4, %3, 0;\n\t"
+      "cvt.pack.sat.u8.s32.b32 %0, %2, %1, t;\n\t}"
+      : "=r"(r)
+      : "r"(x0), "r"(x1), "r"(x2), "r"(x3));
+  return r;
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// The reference's per-block chain on one flagged block, one warp: lane owns
+// outputs e = lane and lane + 32. Every product is block_matrix.hpp:67-81's
+// (per output element: k ascending, a(i,k) == 0 skipped, separately rounded
+// multiply and add from +0.0); sums as add() (block_matrix.hpp:94-101).
+__device__ __forceinline__ double ref_mm(const double* a, const double* b, int i, int j) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double aik = a[i * 8 + k];
+    if (aik == 0.0) continue;
+    acc = __dadd_rn(acc, __dmul_rn(aik, b[k * 8 + j]));
+  }
+  return acc;
+}
+
+__device__ void fallback_block(const RefPlan& rp, const uint8_t* img, size_t pitch, int w, int h, int y0, int x0,
+                               uint8_t* dst, bool fast_out, double* sm, int* nan_flag, int lane) {
+  double* sx = sm;        // X (pixels, then forward coefficients)
+  double* st = sm + 64;   // products
+  double* sa = sm + 128;  // apply_pairs accumulator
+  double* s2 = sm + 192;
+  for (int e = lane; e < 64; e += 32) {
+    const int r = e >> 3, c = e & 7;
+    const int yy = min(y0 + r, h - 1), xx = min(x0 + c, w - 1);
+    sx[e] = static_cast<double>(img[static_cast<size_t>(yy) * pitch + xx]);
+  }
+  __syncwarp();
+  double z[2];
+  if (rp.mode == 1) {
+    const double* C = rp.chain;
+    const double* Ct = rp.chain + 64;
+    // forward_2d: (C X) C^t
+    for (int e = lane; e < 64; e += 32) st[e] = ref_mm(C, sx, e >> 3, e & 7);
+    __syncwarp();
+    for (int e = lane; e < 64; e += 32) s2[e] = ref_mm(st, Ct, e >> 3, e & 7);
+    __syncwarp();
+    // apply_pairs: acc = acc + (L_p X) R_p
+    double acc[2] = {0.0, 0.0};
+    for (int p = 0; p < rp.npairs; ++p) {
+      const double* L = rp.chain + 128 + 64 * p;
+      const double* R = rp.chain + 128 + 64 * (rp.npairs + p);
+      for (int e = lane; e < 64; e += 32) st[e] = ref_mm(L, s2, e >> 3, e & 7);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int e = lane + 32 * q;
+        acc[q] = __dadd_rn(acc[q], ref_mm(st, R, e >> 3, e & 7));
+      }
+      __syncwarp();
+    }
+    sa[lane] = acc[0];
+    sa[lane + 32] = acc[1];
+    __syncwarp();
+    // inverse_2d: (C^t Y) C
+    for (int e = lane; e < 64; e += 32) st[e] = ref_mm(Ct, sa, e >> 3, e & 7);
+    __syncwarp();
+    z[0] = ref_mm(st, C, lane >> 3, lane & 7);
+    z[1] = ref_mm(st, C, (lane + 32) >> 3, lane & 7);
+  } else {
+    // convolve (spatial.hpp:41-68): taps r ascending, c ascending
+    const int hr = (rp.kr - 1) / 2, hc = (rp.kc - 1) / 2;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = lane + 32 * q, i = e >> 3, j = e & 7;
+      double acc = 0.0;
+      for (int r = 0; r < rp.kr; ++r)
+        for (int c = 0; c < rp.kc; ++c) {
+          int si = i + r - hr, sj = j + c - hc;
+          if (rp.padding == DCTF_PAD_ZERO) {
+            if (si < 0 || si >= 8 || sj < 0 || sj >= 8) continue;
+          } else {
+            si = min(max(si, 0), 7);
+            sj = min(max(sj, 0), 7);
+          }
+          acc = __dadd_rn(acc, __dmul_rn(rp.weights[r * rp.kc + c], sx[si * 8 + sj]));
+        }
+      z[q] = acc;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int e = lane + 32 * q, r = e >> 3, c = e & 7;
+    const uint32_t v = quantize(z[q], nan_flag);
+    if (y0 + r < h && x0 + c < w) dst[static_cast<size_t>(r) * pitch + c] = static_cast<uint8_t>(v);
+  }
+  __syncwarp();
+  (void)fast_out;
+}
+
+template <bool TMA>
+__global__ void __launch_bounds__(q8::THREADS, 1)
+    k_fused8_q(const __grid_constant__ CUtensorMap imap, const __grid_constant__ QArgs args,
+               const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
+               long long frame_stride, int nframes, int bw, int bh, int ntx, bool fast_out, int* nan_flag) {
+  using namespace q8;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = align1024(smem_raw);
+  uint8_t* bsm = base;                                // digit images
+  uint8_t* asm_ = bsm + KQ_MAX_PLANS * BBYTES;        // A stages
+  uint8_t* raw = asm_ + NA * ABYTES;                  // raw pixel stages
+  __shared__ uint64_t raw_full[NRAW], raw_empty[NRAW], a_full[NA], a_empty[NA], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ uint32_t flagw[2][4][2];
+  __shared__ unsigned long long fq[FQ];
+  __shared__ uint32_t fq_tail, fq_done;
+  __shared__ __align__(16) double fb_sm[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  pdl_trigger();
+  for (int pi = 0; pi < args.nplans; ++pi) cta_copy_async(bsm + pi * BBYTES, args.bimg[pi], BBYTES);
+  for (int i = threadIdx.x; i < FQ; i += blockDim.x) fq[i] = 0ull;
+  if (warp == W_MMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NRAW; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], 32 * NCONV);
+    }
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(&a_full[i], 32 * NCONV);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 32 * NEPI);
+    }
+    fq_tail = 0;
+    fq_done = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cp_async_wait_all();
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+  pdl_wait();
+
+  const long long tpf = static_cast<long long>(bh) * ntx;  // tiles per frame
+  const long long ntiles = tpf * nframes;                  // < 2^31 (launcher)
+  const dctf::FastDiv fd_tpf = dctf::make_fastdiv(static_cast<uint32_t>(tpf)),
+                      fd_ntx = dctf::make_fastdiv(static_cast<uint32_t>(ntx));
+  auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {
+    const uint32_t u = static_cast<uint32_t>(ti);
+    f = static_cast<int>(dctf::fdiv(fd_tpf, u));
+    const uint32_t rem = u - static_cast<uint32_t>(f) * static_cast<uint32_t>(tpf);
+    by = static_cast<int>(dctf::fdiv(fd_ntx, rem));
+    bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(ntx)) * TILE;
+  };
+
+  if (warp == W_TMA) {
+    // ---------------- TMA producer: raw strips into the ring
+    if (TMA && lane == 0) {
+      prefetch_tmap(&imap);
+      long long tl = 0;
+      for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+        int f, by, bx0;
+        tile_at(ti, f, by, bx0);
+        const int r = static_cast<int>(tl % NRAW);
+        const uint32_t k = static_cast<uint32_t>(tl / NRAW);
+        mbar_wait(&raw_empty[r], (k & 1u) ^ 1u);
+        const int nbt = min(TILE, bw - bx0);
+        const int nbox = (nbt * 8 + 255) >> 8;
+        mbar_expect_tx(&raw_full[r], static_cast<uint32_t>(nbox * 2048));
+        for (int j = 0; j < nbox; ++j) tma_load_3d(raw + r * RAWB + j * 2048, &imap, &raw_full[r], bx0 * 8 + 256 * j, by * 8, f);
+      }
+    }
+  } else if (warp == W_MMA) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_u8s8(128, 256);
+      long long tl = 0;
+      for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+        int f, by, bx0;
+        tile_at(ti, f, by, bx0);
+        const int pi = args.pof[f];
+        const int s = static_cast<int>(tl % NA);
+        const int buf = static_cast<int>(tl & 1);
+        mbar_wait(&a_full[s], static_cast<uint32_t>((tl / NA) & 1));
+        mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t sa = smem_u32(asm_ + s * ABYTES), sb = smem_u32(bsm + pi * BBYTES);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+          mma_u8s8(tmem_base + 256 * buf, desc_sw64(sa + 32 * ks), desc_sw64(sb + 32 * ks), idesc, ks);
+        mma_commit(&acc_full[buf]);
+        mma_commit(&a_empty[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp < W_EPI) {
+    // ---------------- converters: thread = block b of the tile
+    const int b = threadIdx.x - 32 * W_CONV;
+    long long tl = 0;
+    for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+      int f, by, bx0;
+      tile_at(ti, f, by, bx0);
+      const int nbt = min(TILE, bw - bx0);
+      const int y0 = by * 8, x0 = (bx0 + b) * 8;
+      uint2 row[8];
+      if (TMA) {
+        const int r = static_cast<int>(tl % NRAW);
+        mbar_wait(&raw_full[r], static_cast<uint32_t>((tl / NRAW) & 1));
+        const uint8_t* rs = raw + r * RAWB + (b >> 5) * 2048 + (b & 31) * 8;
+        if (b < nbt && x0 + 8 <= w && y0 + 8 <= h) {
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) row[rr] = *reinterpret_cast<const uint2*>(rs + rr * 256);
+        } else if (b < nbt) {  // ragged block: tile()'s edge replication inside the strip
+          const uint8_t* rb = raw + r * RAWB;
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            const int ry = min(rr, h - 1 - y0);
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const int cx = min(b * 8 + c, w - 1 - bx0 * 8);
+              const uint32_t v = rb[(cx >> 8) * 2048 + ry * 256 + (cx & 255)];
+              if (c < 4) lo |= v << (8 * c);
+              else hi |= v << (8 * (c - 4));
+            }
+            row[rr] = make_uint2(lo, hi);
+          }
+        }
+        mbar_arrive(&raw_empty[r]);
+      } else if (b < nbt) {  // direct loads (unaligned views, host-mapped input)
+        const uint8_t* ib = in + f * frame_stride;
+        const bool fast = x0 + 8 <= w && y0 + 8 <= h && ((reinterpret_cast<uintptr_t>(ib + x0) & 7) == 0) &&
+                          ((pitch & 7) == 0);
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int yy = min(y0 + rr, h - 1);
+          if (fast) {
+            row[rr] = __ldg(reinterpret_cast<const uint2*>(ib + static_cast<size_t>(yy) * pitch + x0));
+          } else {
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t v = ib[static_cast<size_t>(yy) * pitch + min(x0 + c, w - 1)];
+              if (c < 4) lo |= v << (8 * c);
+              else hi |= v << (8 * (c - 4));
+            }
+            row[rr] = make_uint2(lo, hi);
+          }
+        }
+      }
+      const int s = static_cast<int>(tl % NA);
+      mbar_wait(&a_empty[s], static_cast<uint32_t>(((tl / NA) & 1) ^ 1));
+      if (b < nbt) {
+        uint8_t* arow = asm_ + s * ABYTES + b * 64;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(arow + ((q ^ ((b >> 1) & 3)) << 4)) =
+              make_uint4(row[2 * q].x, row[2 * q].y, row[2 * q + 1].x, row[2 * q + 1].y);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a_full[s]);
+    }
+  } else if (warp < W_FB) {
+    // ---------------- epilogue: thread = block = TMEM lane
+    const int qd = warp & 3, half = (warp - W_EPI) >> 2, b = 32 * qd + lane;
+    const uint32_t tla = tmem_base + (static_cast<uint32_t>(32 * qd) << 16) + 128 * half;
+    long long tl = 0;
+    for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+      int f, by, bx0;
+      tile_at(ti, f, by, bx0);
+      const int pi = args.pof[f];
+      const uint32_t U = args.U[pi], c17 = args.c17[pi];
+      const int shS = args.shS[pi], shK = args.shK[pi];
+      const int buf = static_cast<int>(tl & 1);
+      mbar_wait(&acc_full[buf], static_cast<uint32_t>((tl >> 1) & 1));
+      tc_fence_after();
+      uint32_t words[8];
+      uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        int32_t v0[32], v1[32];
+        tmem_ld32(tla + 256 * buf + 64 * k2, v0);
+        tmem_ld32(tla + 256 * buf + 64 * k2 + 32, v1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int32_t* v = rr ? v1 : v0;
+          int qv[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int a0 = v[4 * c], a1 = v[4 * c + 1], a2 = v[4 * c + 2], a3 = v[4 * c + 3];
+            const int hh = a0 * 256 + a1;
+            const int l = a2 * 256 + a3;
+            const int S = hh + (l >> 16) + static_cast<int>(c17);
+            qv[c] = S >> shS;
+            const uint32_t key = __funnelshift_l(static_cast<uint32_t>(l) << 16, static_cast<uint32_t>(S), shK);
+            mn = min(mn, key + U);
+          }
+          words[4 * k2 + 2 * rr] = pack4_sat(qv[0], qv[1], qv[2], qv[3]);
+          words[4 * k2 + 2 * rr + 1] = pack4_sat(qv[4], qv[5], qv[6], qv[7]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+      // uncertain blocks: merged over both halves, then stored by nobody here
+      const int nbt = min(TILE, bw - bx0);
+      const bool valid = b < nbt;
+      const uint32_t mine = __ballot_sync(0xFFFFFFFFu, valid && mn < 2u * U);
+      if (lane == 0) flagw[buf][qd][half] = mine;
+      named_sync(1 + qd, 64);
+      const uint32_t flagged = flagw[buf][qd][0] | flagw[buf][qd][1];
+      const int y0 = by * 8 + 4 * half, x0 = (bx0 + b) * 8;
+      uint8_t* ob = out + f * frame_stride;
+      if (valid && !((flagged >> lane) & 1u)) {
+        if (fast_out && x0 + 8 <= w && y0 + 4 <= h) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<uint2*>(ob + static_cast<size_t>(y0 + k) * pitch + x0) =
+                make_uint2(words[2 * k], words[2 * k + 1]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (y0 + k >= h) break;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              if (x0 + c < w) ob[static_cast<size_t>(y0 + k) * pitch + x0 + c] =
+                                  static_cast<uint8_t>(words[2 * k + (c >> 2)] >> (8 * (c & 3)));
+          }
+        }
+      }
+      if (half == 0 && flagged) {  // enqueue (tile, block) for the fallback warp
+        const uint32_t nf = __popc(flagged);
+        uint32_t slot0 = 0;
+        if (lane == 0) slot0 = atomicAdd(&fq_tail, nf);
+        slot0 = __shfl_sync(0xFFFFFFFFu, slot0, 0);
+        if ((flagged >> lane) & 1u) {
+          const uint32_t slot = (slot0 + __popc(flagged & ((1u << lane) - 1u))) % FQ;
+          volatile unsigned long long* qs = &fq[slot];
+          while (*qs != 0ull) __nanosleep(64);  // ring full (pathological masks only)
+          *qs = (static_cast<unsigned long long>(ti) << 7 | static_cast<unsigned long long>(b)) + 1ull;
+        }
+      }
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (half == 0 && lane == 0) atomicAdd(&fq_done, 1u);
+  } else {
+    // ---------------- fallback warp: reference-order chain on queued blocks
+    uint32_t head = 0;
+    while (true) {
+      volatile unsigned long long* qs = &fq[head % FQ];
+      unsigned long long e = *qs;
+      if (e == 0ull) {
+        if (*reinterpret_cast<volatile uint32_t*>(&fq_done) == 4u) {
+          __threadfence_block();
+          e = *qs;
+          if (e == 0ull) break;
+        } else {
+          __nanosleep(256);
+          continue;
+        }
+      }
+      __syncwarp();
+      const long long ti = static_cast<long long>((e - 1ull) >> 7);
+      const int b = static_cast<int>((e - 1ull) & 127ull);
+      int f, by, bx0;
+      tile_at(ti, f, by, bx0);
+      const int y0 = by * 8, x0 = (bx0 + b) * 8;
+      const uint8_t* ib = in + f * frame_stride;
+      uint8_t* ob = out + f * frame_stride + static_cast<size_t>(y0) * pitch + x0;
+      fallback_block(args.ref[args.pof[f]], ib, pitch, w, h, y0, x0, ob, fast_out, fb_sm, nan_flag, lane);
+      __syncwarp();
+      if (lane == 0) *qs = 0ull;
+      ++head;
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == W_MMA)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+}  // namespace
+
+namespace dctf {
+
+dctf_status upload_kq_operator(dctf_plan* p) {
+  std::vector<int8_t> img;
+  KqInfo info;
+  if (p->n != 8 || !layout_kq8(*p, img, info)) return DCTF_OK;  // not eligible: FP64 kernels stay
+  std::vector<double> chain;
+  refchain_image(*p, chain, p->ref_mode, p->ref_npairs);
+  cudaError_t e = cudaMalloc(&p->d_kq, img.size());
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_kq, img.data(), img.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_refchain, chain.size() * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->d_refchain, chain.data(), chain.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("kq operator upload: ") + cudaGetErrorString(e));
+  p->kq = true;
+  p->kq_F = info.F;
+  p->kq_U = info.U;
+  p->kq_ebound = info.ebound;
+  p->kq_flag_rate = info.flag_rate;
+  return DCTF_OK;
+}
+
+dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int* plan_of_frame, const uint8_t* in,
+                            uint8_t* out, int w, int h, size_t pitch, long long frame_stride, int nframes,
+                            cudaStream_t st, bool host_mapped, int* d_nan_or_null) {
+  if (nplans < 1 || nplans > KQ_MAX_PLANS || nframes > KQ_MAX_FRAMES)
+    return set_error(DCTF_INVALID_ARGUMENT, "k_fused8_q: too many plans / frames for one launch");
+  const int bw = (w + 7) / 8, bh = (h + 7) / 8, ntx = (bw + q8::TILE - 1) / q8::TILE;
+  const long long ntiles = static_cast<long long>(bh) * ntx * nframes;
+  if (ntiles <= 0) return DCTF_OK;
+  if (ntiles >= (1LL << 31) / 128 || static_cast<long long>(bw) * bh * nframes >= (1LL << 31))
+    return set_error(DCTF_INVALID_ARGUMENT, "image batch too large (>= 2^31 blocks)");
+  QArgs args{};
+  args.nplans = nplans;
+  for (int i = 0; i < nplans; ++i) {
+    const dctf_plan* p = plans[i];
+    if (!p->kq) return set_error(DCTF_INVALID_ARGUMENT, "k_fused8_q: plan has no integer operator");
+    args.bimg[i] = static_cast<const int8_t*>(p->d_kq);
+    args.U[i] = p->kq_U;
+    args.c17[i] = 1u << (p->kq_F - 17);
+    args.shS[i] = p->kq_F - 16;
+    args.shK[i] = 48 - p->kq_F;
+    args.ref[i] = RefPlan{p->d_refchain, p->d_weights, p->ref_mode, p->ref_npairs, p->kr, p->kc, p->padding};
+  }
+  for (int f = 0; f < nframes; ++f) args.pof[f] = static_cast<uint8_t>(plan_of_frame ? plan_of_frame[f] : 0);
+  const bool tma = !host_mapped && (pitch & 15) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+                   (nframes == 1 || (frame_stride & 15) == 0) && pitch < (1ull << 40) && !std::getenv("DCTF_Q_NO_TMA");
+  const bool fast_out = (pitch & 7) == 0 && (reinterpret_cast<uintptr_t>(out) & 7) == 0 &&
+                        (nframes == 1 || (frame_stride & 7) == 0);
+  CUtensorMap imap{};
+  if (tma) {
+    const dctf_status s = make_imap(&imap, in, w, h, nframes, pitch, frame_stride, 256);
+    if (s != DCTF_OK) return s;
+  }
+  const void* fn = tma ? reinterpret_cast<const void*>(k_fused8_q<true>) : reinterpret_cast<const void*>(k_fused8_q<false>);
+  {
+    const dctf_status sa = ensure_dyn_smem(fn, q8::SMEM, tma ? "k_fused8_q<tma>" : "k_fused8_q<direct>");
+    if (sa != DCTF_OK) return sa;
+  }
+  const unsigned grid = static_cast<unsigned>(std::min<long long>(sm_count(plans[0]->device), ntiles));
+  const cudaError_t e =
+      tma ? launch_pdl(k_fused8_q<true>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
+                       frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null)
+          : launch_pdl(k_fused8_q<false>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
+                       frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null);
+  add_launches(1);
+  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_fused8_q: ") + cudaGetErrorString(e));
+  return DCTF_OK;
+}
+
+}  // namespace dctf

@@ -1,0 +1,125 @@
+"""k_fused8_q — the exact-integer composed-operator image kernel (csrc/quant.cu).
+
+Claim under test: for every pixel the u8 output equals the reference's
+filter_image (image.hpp:210-225) on the same input, with NO near-tie
+exemption: certain pixels round exactly like the reference by the plan's
+error bound (plan.cc: layout_kq8), and uncertain blocks are recomputed in
+the reference's own operation order by the fallback warp. Checked against
+oracle/_ref (the reference compiled in place) for square masks and against
+the restated convolve (oracle/dctf_oracle.c) for masks outside the
+reference's domain (1x9 on 8x8 blocks, rectangular masks).
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+from conftest import nthreads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P(cuda):
+    import paper_1710_07193_b200 as P
+    return P
+
+
+def _run(P, img, w, kr, kc, pad, prec=None):
+    import torch
+    m = P.Mask(kr, w) if kr == kc else P.Mask.rect(kr, kc, w)
+    kw = {} if prec is None else {"precision": prec}
+    plan = P.FilterPlan(m, 8, P.PaddingMode(pad), **kw)
+    d = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    out = plan.filter_image(d)
+    torch.cuda.synchronize()
+    return plan, out.cpu().numpy()
+
+
+def _reference(ref, oracle, img, w, kr, kc, pad):
+    if kr == kc and kr <= 8:
+        return ref.filter_image(img, w, kr, pad, 8, threads=nthreads())
+    r_out, _ = oracle.filter_image_spatial(img, w, kr, kc, pad, 8, prequant=True)
+    return r_out
+
+
+def _masks():
+    from paper_1710_07193_b200 import synth
+    r3, _ = synth.random_mask(1003, 3)
+    r5, _ = synth.random_mask(1005, 5)
+    r7, _ = synth.random_mask(77, 7)
+    return {
+        "box3": (synth.BOX3, 3, 3),
+        "gauss5": (synth.gaussian_mask(5, 1.0), 5, 5),
+        "gauss7": (synth.gaussian_mask(7, 2.0), 7, 7),
+        "laplacian3": (synth.LAPLACIAN3, 3, 3),
+        "random3": (r3, 3, 3),
+        "random5": (r5, 5, 5),
+        "random7": (r7, 7, 7),
+        "motion1x9": (synth.MOTION_1x9, 1, 9),
+        "identity": (np.array([1.0]), 1, 1),
+    }
+
+
+@pytest.mark.parametrize("name", list(_masks()))
+@pytest.mark.parametrize("pad", [0, 1])
+@pytest.mark.parametrize("shape", [(1024, 1024), (333, 517), (2160, 3840)])
+def test_kq_bit_exact(P, ref, oracle, name, pad, shape):
+    from paper_1710_07193_b200 import synth
+    w, kr, kc = _masks()[name]
+    h, wd = shape
+    img = synth.sinusoid_image(zlib.crc32(f"{name}/{pad}/{shape}".encode()) & 0xFFFF, wd, h)
+    plan, out = _run(P, img, w, kr, kc, pad)
+    assert plan.image_kernel == "k_fused8_q", plan.image_kernel
+    r = _reference(ref, oracle, img, w, kr, kc, pad)
+    mism = int(np.count_nonzero(out != r))
+    print(f"[{name} pad={pad} {wd}x{h}] mismatches {mism}")
+    assert mism == 0
+
+
+def test_kq_half_ties_take_fallback(P, ref):
+    """A 1x1 mask of weight 0.5: every odd pixel is an exact .5 tie in exact
+    arithmetic, so nearly every block is uncertain and goes through the
+    fallback warp's queue (ring wrap-around included); the result must still
+    be the reference's rounding of its own FP64 chain, pixel for pixel."""
+    from paper_1710_07193_b200 import synth
+    img = synth.uniform_image(5, 1024, 512)
+    w = np.array([0.5])
+    plan, out = _run(P, img, w, 1, 1, 1)
+    assert plan.image_kernel == "k_fused8_q"
+    r = ref.filter_image(img, w, 1, 1, 8, threads=nthreads())
+    assert int(np.count_nonzero(out != r)) == 0
+
+
+def test_kq_matches_fp64_kernels(P):
+    """Same u8 as the FP64 DMMA kernels (which match the reference except at
+    near-ties) on a config-2 sized image."""
+    from paper_1710_07193_b200 import synth
+    img = synth.sinusoid_image(2, 4096, 4096)
+    w = synth.gaussian_mask(5, 1.0)
+    _, a = _run(P, img, w, 5, 5, 1)
+    _, b = _run(P, img, w, 5, 5, 1, prec=P.Precision.kFp64Dense)
+    assert int(np.count_nonzero(a != b)) <= 64  # reference near-ties only (~1e-5 of pixels)
+
+
+def test_kq_frames_one_launch(P, ref, oracle):
+    """A 4-mask frame batch runs as one k_fused8_q launch and equals the
+    reference frame by frame."""
+    import torch
+    from paper_1710_07193_b200 import _lib, synth
+    r5, _ = synth.random_mask(1005, 5)
+    masks = [(synth.LAPLACIAN3, 3, 3), (synth.gaussian_mask(5, 1.0), 5, 5), (synth.MOTION_1x9, 1, 9),
+             (r5, 5, 5)]
+    plans = [P.FilterPlan(P.Mask(k, w) if k == kc else P.Mask.rect(k, kc, w), 8, P.PaddingMode.kReplicate)
+             for w, k, kc in masks]
+    F, H, W = 8, 216, 384
+    frames = np.stack([synth.sinusoid_image(f, W, H) for f in range(F)])
+    d = torch.from_numpy(frames).cuda()
+    out = P.filter_frames(d, plans, [f % 4 for f in range(F)])
+    torch.cuda.synchronize()
+    assert _lib.last_launch_count() == 1
+    out = out.cpu().numpy()
+    for f in range(F):
+        w, k, kc = masks[f % 4]
+        r = _reference(ref, oracle, frames[f], w, k, kc, 1)
+        assert int(np.count_nonzero(out[f] != r)) == 0, f
