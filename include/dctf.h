@@ -230,6 +230,12 @@ dctf_status dctf_plan_nan_check(const dctf_plan* plan, void* stream, int* nan_se
  * entry. */
 dctf_status dctf_measure_fp64_peak(int device, int mode, double* tflops);
 
+/* Diagnostics: blocks the k_fused8_q fallback warp recomputed in the
+ * reference's operation order since the last call (process-wide; needs
+ * DCTF_Q_COUNT=1 in the environment before the first filter call, else
+ * DCTF_UNSUPPORTED). Synchronises the current device. */
+dctf_status dctf_diag_fallback_blocks(unsigned long long* n);
+
 /* Number of kernels the last call on this host thread launched (bench
  * accounting of gpu_launches). */
 int dctf_last_launch_count(void);

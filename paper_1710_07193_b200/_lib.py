@@ -65,6 +65,7 @@ _SIGS = {
     "dctf_filter_image_spatial_host": (_st, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_size_t]),
     "dctf_measure_fp64_peak": (_st, [C.c_int, C.c_int, _d]),
     "dctf_last_launch_count": (C.c_int, []),
+    "dctf_diag_fallback_blocks": (_st, [C.POINTER(C.c_ulonglong)]),
     "dctf_last_error_message": (C.c_char_p, []),
     "dctf_version": (C.c_char_p, []),
 }

@@ -1029,9 +1029,10 @@ namespace dctf {
 // others (a ~1e-4 fraction of blocks at the BASELINE masks) are flagged and
 // recomputed in the reference's own operation order (k_fallback8).
 //
-// B-operand image: 256 rows x 64 bytes, K-major, 64-byte swizzle (UMMA
-// SWIZZLE_64B: 16-byte chunk c of row n stored at chunk c ^ ((n >> 1) & 3));
-// row n = 4 i + s holds digit s of output pixel i, so one 32-column
+// B-operand image: 256 rows x 128 bytes, K-major, 128-byte swizzle (UMMA
+// SWIZZLE_128B: 16-byte chunk c of row n stored at chunk c ^ (n & 7)); row
+// n = 4 i + s holds digit s of output pixel i (bytes 0-63: the 64 input
+// pixels; bytes 64-65: the rounding offset's digits), so one 32-column
 // tcgen05.ld returns 8 whole pixels.
 bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   info = KqInfo{};
@@ -1113,7 +1114,10 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   if (U >= std::ldexp(1.0L, 30)) return false;
   const double flag_rate = static_cast<double>(64.0L * 2.0L * T / scale);  // per block, uniform fractions
   if (flag_rate > 0.02) return false;
-  bimg.assign(size_t(256) * 64, 0);
+  bimg.assign(size_t(256) * 128, 0);
+  auto put = [&](int row, int k, int v) {
+    bimg[size_t(row) * 128 + ((((k >> 4) ^ (row & 7)) << 4) | (k & 15))] = static_cast<int8_t>(v);
+  };
   for (int i = 0; i < nn; ++i)
     for (int j = 0; j < nn; ++j) {
       long long v = Ki[size_t(i) * nn + j];
@@ -1124,11 +1128,17 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
       }
       if (v < -128 || v > 127) return false;
       d[0] = static_cast<int>(v);
-      for (int s = 0; s < 4; ++s) {
-        const int row = 4 * i + s;
-        bimg[size_t(row) * 64 + ((((j >> 4) ^ ((row >> 1) & 3)) << 4) | (j & 15))] = static_cast<int8_t>(d[s]);
-      }
+      for (int s = 0; s < 4; ++s) put(4 * i + s, j, d[s]);
     }
+  // The rounding offset 2^(F-1) as accumulator constants: the A rows carry
+  // [1, 1] at bytes 64-65, so digit s of every output gets B[.][64] + B[.][65].
+  // F - 1 >= 24: 2^(F-25) on digit 0; else 2^(F-17) on digit 1 (both <= 128).
+  const int cs = F - 1 >= 24 ? 0 : 1;
+  const int cv = 1 << (F - 1 - (cs == 0 ? 24 : 16));
+  for (int i = 0; i < nn; ++i) {
+    put(4 * i + cs, 64, (cv + 1) / 2);
+    put(4 * i + cs, 65, cv / 2);
+  }
   info.ok = true;
   info.F = F;
   info.U = static_cast<uint32_t>(U);

@@ -55,6 +55,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "device.cuh"
@@ -67,14 +68,45 @@ using dctf::set_error;
 
 namespace {
 
+#ifdef QDBG
+// [cta < 4][tile < 64][event < 8] clock64 stamps of tiles QDBG_T0.. (instrumented build only)
+#ifndef QDBG_T0
+#define QDBG_T0 0
+#endif
+__device__ long long g_qdbg[4][64][8];
+#define QSTAMP(tl, ev)                                                                                  \
+  do {                                                                                                  \
+    if (blockIdx.x < 4 && (tl) >= QDBG_T0 && (tl) < QDBG_T0 + 64) g_qdbg[blockIdx.x][(tl)-QDBG_T0][(ev)] = clock64(); \
+  } while (0)
+#define QSTAMP_EPI(tl, ev)                 \
+  do {                                     \
+    if (b == 0 && part == 0) QSTAMP(tl, ev); \
+  } while (0)
+#else
+#define QSTAMP_EPI(tl, ev) \
+  do {                     \
+  } while (0)
+#define QSTAMP(tl, ev) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace q8 {
 constexpr int TILE = 128;                  // blocks per tile = MMA M = TMEM lanes
 constexpr int NCOL = 256;                  // accumulator columns: 64 pixels x 4 digits
-constexpr int BBYTES = NCOL * 64;          // one plan's digit image
-constexpr int ABYTES = TILE * 64;          // one A stage
+constexpr int ROWB = 128;                  // operand row: 64 pixel bytes + the constant chunk
+constexpr int BBYTES = NCOL * ROWB;        // one plan's digit image
+constexpr int ABYTES = TILE * ROWB;        // one A stage
 constexpr int RAWB = 8 * TILE * 8;         // one raw stage: 8 rows x 1024 px
 constexpr int NRAW = 6, NA = 2;
-constexpr int W_TMA = 0, W_MMA = 1, W_CONV = 2, NCONV = 4, W_EPI = 6, NEPI = 8, W_FB = 14;
+#ifndef Q8_EXP
+#define Q8_EXP 0  // measurement variants: 1 = epilogue without the pixel math, 3 = without stores
+#endif
+#ifndef Q8_NPART
+#define Q8_NPART 2
+#endif
+constexpr int NPART = Q8_NPART;            // epilogue warps per TMEM lane quarter
+constexpr int W_TMA = 0, W_MMA = 1, W_CONV = 2, NCONV = 4, W_EPI = 6, NEPI = 4 * NPART, W_FB = W_EPI + NEPI;
 constexpr int THREADS = 32 * (W_FB + 1);
 constexpr int FQ = 256;                    // fallback queue slots
 constexpr int SMEM = 1024 + KQ_MAX_PLANS * BBYTES + NA * ABYTES + NRAW * RAWB;
@@ -88,22 +120,22 @@ struct RefPlan {
 
 struct QArgs {
   const int8_t* bimg[KQ_MAX_PLANS];
-  uint32_t U[KQ_MAX_PLANS], c17[KQ_MAX_PLANS];
-  int shS[KQ_MAX_PLANS], shK[KQ_MAX_PLANS];
+  uint32_t U[KQ_MAX_PLANS];
+  int shS[KQ_MAX_PLANS], shL[KQ_MAX_PLANS];  // F - 16, 32 - F
   RefPlan ref[KQ_MAX_PLANS];
   int nplans;
   uint8_t pof[KQ_MAX_FRAMES];  // plan of frame
 };
 
-// UMMA shared-memory descriptor, K-major, SWIZZLE_64B (8-row atoms of 64 B):
-// SBO = 512 B between 8-row groups, version 1 (sm_100).
-__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B (8-row atoms of 128 B):
+// SBO = 1024 B between 8-row groups, version 1 (sm_100).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
   d |= static_cast<uint64_t>(1u) << 16;
-  d |= static_cast<uint64_t>(512u >> 4) << 32;
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;
   d |= static_cast<uint64_t>(1u) << 46;
-  d |= static_cast<uint64_t>(4u) << 61;
+  d |= static_cast<uint64_t>(2u) << 61;
   return d;
 }
 // kind::i8 instruction descriptor: D s32, A u8 (pixels), B s8 (digits), both K-major.
@@ -150,8 +182,87 @@ __device__ __forceinline__ uint32_t pack4_sat(int x0, int x1, int x2, int x3) {
       : "r"(x0), "r"(x1), "r"(x2), "r"(x3));
   return r;
 }
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+
+// One pixel row of a block (8 pixels x 4 digit accumulators, TMEM columns
+// 4c + s) -> 8 u8 (two words) and the running uncertainty minimum. With
+// T1 = a0 256 + a1, T2 = a2 256 + a3 (the rounding offset already added to
+// a0 / a1 by the constant K chunk), v = T1 2^16 + T2 = z 2^F:
+//   q   = (T1 + (T2 >> 16)) >> (F - 16)      floor(z + 1/2)
+//   key = (T1 2^16 + T2) << (32 - F) mod 2^32 = (v mod 2^F) 2^(32-F)
+// (F32: F = 32, no shift).
+template <bool F32>
+__device__ __forceinline__ void q8_row(const int32_t (&v)[32], int shS, int shL, uint32_t U, uint32_t& mn0,
+                                       uint32_t& mn1, uint32_t& w0, uint32_t& w1) {
+  int qv[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int t1 = v[4 * c] * 256 + v[4 * c + 1];
+    const int t2 = v[4 * c + 2] * 256 + v[4 * c + 3];
+    uint32_t key = static_cast<uint32_t>(t1) * 65536u + static_cast<uint32_t>(t2);
+    if (!F32) key <<= shL;
+    qv[c] = (t1 + (t2 >> 16)) >> shS;
+    if (c & 1) mn1 = min(mn1, key + U);
+    else mn0 = min(mn0, key + U);
+  }
+  w0 = pack4_sat(qv[0], qv[1], qv[2], qv[3]);
+  w1 = pack4_sat(qv[4], qv[5], qv[6], qv[7]);
+}
+
+// The epilogue's ROWS pixel rows of one tile: row r's math overlaps the TMEM
+// load of row r + 1; the accumulator is released after the last load.
+template <int ROWS, bool F32>
+__device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32_t (&vb)[32], int shS, int shL,
+                                         uint32_t U, uint32_t& mn0, uint32_t& mn1, uint32_t (&words)[2 * ROWS],
+                                         uint64_t* acc_empty) {
+  tmem_ld32(col0, va);
+  tmem_wait_ld();
+  if (ROWS == 1) {
+    tc_fence_before();
+    mbar_arrive(acc_empty);
+  }
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    if (r + 1 < ROWS) tmem_ld32(col0 + 32 * (r + 1), (r & 1) ? va : vb);
+#if Q8_EXP == 1
+    words[2 * r] = ((r & 1) ? vb : va)[0];
+    words[2 * r + 1] = ((r & 1) ? vb : va)[31];
+#else
+    q8_row<F32>((r & 1) ? vb : va, shS, shL, U, mn0, mn1, words[2 * r], words[2 * r + 1]);
+#endif
+    if (r + 1 < ROWS) {
+      tmem_wait_ld();
+      if (r + 2 == ROWS) {
+        tc_fence_before();
+        mbar_arrive(acc_empty);  // accumulator drained: the MMA of tile tl+2 may start
+      }
+    }
+  }
+}
+
+// Cropped byte stores of ROWS rows (image edges, unaligned outputs).
+template <int ROWS>
+__device__ __forceinline__ void store_ragged(uint8_t* ob, size_t pitch, const uint32_t (&words)[2 * ROWS],
+                                             int rows_left, int cols_left) {
+#pragma unroll
+  for (int k = 0; k < ROWS; ++k)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (k < rows_left && c < cols_left)
+        ob[static_cast<size_t>(k) * pitch + c] = static_cast<uint8_t>(words[2 * k + (c >> 2)] >> (8 * (c & 3)));
+}
+
+// Appends the warp's flagged blocks (ballot `flagged`) to the fallback ring.
+__device__ __noinline__ void enqueue_fallback(unsigned long long* fq, uint32_t* tail, uint32_t flagged, bool mine,
+                                              int lane, long long ti, int b) {
+  uint32_t slot0 = 0;
+  if (lane == 0) slot0 = atomicAdd(tail, static_cast<uint32_t>(__popc(flagged)));
+  slot0 = __shfl_sync(0xFFFFFFFFu, slot0, 0);
+  if (mine) {
+    const uint32_t slot = (slot0 + __popc(flagged & ((1u << lane) - 1u))) % q8::FQ;
+    volatile unsigned long long* qs = &fq[slot];
+    while (*qs != 0ull) __nanosleep(64);  // ring full (pathological masks only)
+    *qs = (static_cast<unsigned long long>(ti) << 7 | static_cast<unsigned long long>(b)) + 1ull;
+  }
 }
 
 // The reference's per-block chain on one flagged block, one warp: lane owns
@@ -247,7 +358,8 @@ template <bool TMA>
 __global__ void __launch_bounds__(q8::THREADS, 1)
     k_fused8_q(const __grid_constant__ CUtensorMap imap, const __grid_constant__ QArgs args,
                const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
-               long long frame_stride, int nframes, int bw, int bh, int ntx, bool fast_out, int* nan_flag) {
+               long long frame_stride, int nframes, int bw, int bh, int ntx, bool fast_out, int* nan_flag,
+               unsigned long long* fb_count) {
   using namespace q8;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
@@ -256,7 +368,6 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   uint8_t* raw = asm_ + NA * ABYTES;                  // raw pixel stages
   __shared__ uint64_t raw_full[NRAW], raw_empty[NRAW], a_full[NA], a_empty[NA], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_s;
-  __shared__ uint32_t flagw[2][4][2];
   __shared__ unsigned long long fq[FQ];
   __shared__ uint32_t fq_tail, fq_done;
   __shared__ __align__(16) double fb_sm[256];
@@ -265,6 +376,14 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   pdl_trigger();
   for (int pi = 0; pi < args.nplans; ++pi) cta_copy_async(bsm + pi * BBYTES, args.bimg[pi], BBYTES);
   for (int i = threadIdx.x; i < FQ; i += blockDim.x) fq[i] = 0ull;
+  // A rows, bytes 64..127 (chunks 4-7, 128B-swizzled): the constant input
+  // [1, 1, 0, ...] that adds the digits of the rounding offset 2^(F-1)
+  // (plan.cc: layout_kq8, bytes 64-65 of the B rows) to the accumulators
+  for (int i = threadIdx.x; i < NA * TILE * 4; i += blockDim.x) {
+    const int st = i / (TILE * 4), b = (i >> 2) % TILE, c = 4 + (i & 3);
+    *reinterpret_cast<uint4*>(asm_ + st * ABYTES + b * ROWB + ((c ^ (b & 7)) << 4)) =
+        make_uint4(c == 4 ? 0x0101u : 0u, 0u, 0u, 0u);
+  }
   if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_s)),
@@ -319,6 +438,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
         const int r = static_cast<int>(tl % NRAW);
         const uint32_t k = static_cast<uint32_t>(tl / NRAW);
         mbar_wait(&raw_empty[r], (k & 1u) ^ 1u);
+        QSTAMP(tl, 0);
         const int nbt = min(TILE, bw - bx0);
         const int nbox = (nbt * 8 + 255) >> 8;
         mbar_expect_tx(&raw_full[r], static_cast<uint32_t>(nbox * 2048));
@@ -337,12 +457,14 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
         const int s = static_cast<int>(tl % NA);
         const int buf = static_cast<int>(tl & 1);
         mbar_wait(&a_full[s], static_cast<uint32_t>((tl / NA) & 1));
+        QSTAMP(tl, 3);
         mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
+        QSTAMP(tl, 4);
         tc_fence_after();
         const uint32_t sa = smem_u32(asm_ + s * ABYTES), sb = smem_u32(bsm + pi * BBYTES);
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
-          mma_u8s8(tmem_base + 256 * buf, desc_sw64(sa + 32 * ks), desc_sw64(sb + 32 * ks), idesc, ks);
+        for (int ks = 0; ks < 3; ++ks)  // K = 64 pixel bytes + 32 constant bytes
+          mma_u8s8(tmem_base + 256 * buf, desc_sw128(sa + 32 * ks), desc_sw128(sb + 32 * ks), idesc, ks);
         mma_commit(&acc_full[buf]);
         mma_commit(&a_empty[s]);
       }
@@ -361,6 +483,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       if (TMA) {
         const int r = static_cast<int>(tl % NRAW);
         mbar_wait(&raw_full[r], static_cast<uint32_t>((tl / NRAW) & 1));
+        if (b == 0) QSTAMP(tl, 1);
         const uint8_t* rs = raw + r * RAWB + (b >> 5) * 2048 + (b & 31) * 8;
         if (b < nbt && x0 + 8 <= w && y0 + 8 <= h) {
 #pragma unroll
@@ -405,100 +528,66 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       }
       const int s = static_cast<int>(tl % NA);
       mbar_wait(&a_empty[s], static_cast<uint32_t>(((tl / NA) & 1) ^ 1));
+      if (b == 0) QSTAMP(tl, 2);
       if (b < nbt) {
-        uint8_t* arow = asm_ + s * ABYTES + b * 64;
+        uint8_t* arow = asm_ + s * ABYTES + b * ROWB;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4*>(arow + ((q ^ ((b >> 1) & 3)) << 4)) =
+          *reinterpret_cast<uint4*>(arow + ((q ^ (b & 7)) << 4)) =
               make_uint4(row[2 * q].x, row[2 * q].y, row[2 * q + 1].x, row[2 * q + 1].y);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&a_full[s]);
     }
   } else if (warp < W_FB) {
-    // ---------------- epilogue: thread = block = TMEM lane
-    const int qd = warp & 3, half = (warp - W_EPI) >> 2, b = 32 * qd + lane;
-    const uint32_t tla = tmem_base + (static_cast<uint32_t>(32 * qd) << 16) + 128 * half;
+    // ---------------- epilogue: thread = block = TMEM lane; NPART warps per
+    // lane quarter, each 8 / NPART pixel rows (32 accumulator columns per row)
+    constexpr int ROWS = 8 / NPART;
+    const int qd = warp & 3, part = (warp - W_EPI) >> 2, b = 32 * qd + lane;
+    const uint32_t tla = tmem_base + (static_cast<uint32_t>(32 * qd) << 16) + 32 * ROWS * part;
     long long tl = 0;
     for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
       int f, by, bx0;
       tile_at(ti, f, by, bx0);
       const int pi = args.pof[f];
-      const uint32_t U = args.U[pi], c17 = args.c17[pi];
-      const int shS = args.shS[pi], shK = args.shK[pi];
+      const uint32_t U = args.U[pi];
+      const int shS = args.shS[pi], shL = args.shL[pi];
       const int buf = static_cast<int>(tl & 1);
+      const uint32_t col0 = tla + 256 * buf;
       mbar_wait(&acc_full[buf], static_cast<uint32_t>((tl >> 1) & 1));
+      QSTAMP_EPI(tl, 5);
       tc_fence_after();
-      uint32_t words[8];
-      uint32_t mn = 0xFFFFFFFFu;
-#pragma unroll
-      for (int k2 = 0; k2 < 2; ++k2) {
-        int32_t v0[32], v1[32];
-        tmem_ld32(tla + 256 * buf + 64 * k2, v0);
-        tmem_ld32(tla + 256 * buf + 64 * k2 + 32, v1);
-        tmem_wait_ld();
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int32_t* v = rr ? v1 : v0;
-          int qv[8];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int a0 = v[4 * c], a1 = v[4 * c + 1], a2 = v[4 * c + 2], a3 = v[4 * c + 3];
-            const int hh = a0 * 256 + a1;
-            const int l = a2 * 256 + a3;
-            const int S = hh + (l >> 16) + static_cast<int>(c17);
-            qv[c] = S >> shS;
-            const uint32_t key = __funnelshift_l(static_cast<uint32_t>(l) << 16, static_cast<uint32_t>(S), shK);
-            mn = min(mn, key + U);
-          }
-          words[4 * k2 + 2 * rr] = pack4_sat(qv[0], qv[1], qv[2], qv[3]);
-          words[4 * k2 + 2 * rr + 1] = pack4_sat(qv[4], qv[5], qv[6], qv[7]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[buf]);
-      // uncertain blocks: merged over both halves, then stored by nobody here
+      uint32_t words[2 * ROWS];
+      uint32_t mn0 = 0xFFFFFFFFu, mn1 = 0xFFFFFFFFu;
+      int32_t va[32], vb[32];
+      // row r is processed while row r + 1 streams in from TMEM
+      if (shL == 0) epi_rows<ROWS, true>(col0, va, vb, shS, 0, U, mn0, mn1, words, &acc_empty[buf]);
+      else epi_rows<ROWS, false>(col0, va, vb, shS, shL, U, mn0, mn1, words, &acc_empty[buf]);
+      QSTAMP_EPI(tl, 6);
+      // A block with an uncertain pixel in this warp's rows: those rows are
+      // left to the fallback warp (which rewrites the whole block; the other
+      // rows it writes carry the same bytes as the certain ones stored here).
       const int nbt = min(TILE, bw - bx0);
       const bool valid = b < nbt;
-      const uint32_t mine = __ballot_sync(0xFFFFFFFFu, valid && mn < 2u * U);
-      if (lane == 0) flagw[buf][qd][half] = mine;
-      named_sync(1 + qd, 64);
-      const uint32_t flagged = flagw[buf][qd][0] | flagw[buf][qd][1];
-      const int y0 = by * 8 + 4 * half, x0 = (bx0 + b) * 8;
-      uint8_t* ob = out + f * frame_stride;
-      if (valid && !((flagged >> lane) & 1u)) {
-        if (fast_out && x0 + 8 <= w && y0 + 4 <= h) {
+      const bool unsure = valid && min(mn0, mn1) < 2u * U;
+      const int y0 = by * 8 + ROWS * part, x0 = (bx0 + b) * 8;
+      uint8_t* ob = out + f * frame_stride + static_cast<size_t>(y0) * pitch + x0;
+      if (valid && !unsure && Q8_EXP != 3) {
+        if (fast_out && x0 + 8 <= w && y0 + ROWS <= h) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            *reinterpret_cast<uint2*>(ob + static_cast<size_t>(y0 + k) * pitch + x0) =
-                make_uint2(words[2 * k], words[2 * k + 1]);
+          for (int k = 0; k < ROWS; ++k)
+            *reinterpret_cast<uint2*>(ob + static_cast<size_t>(k) * pitch) = make_uint2(words[2 * k], words[2 * k + 1]);
         } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (y0 + k >= h) break;
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              if (x0 + c < w) ob[static_cast<size_t>(y0 + k) * pitch + x0 + c] =
-                                  static_cast<uint8_t>(words[2 * k + (c >> 2)] >> (8 * (c & 3)));
-          }
+          store_ragged<ROWS>(ob, pitch, words, h - y0, w - x0);
         }
       }
-      if (half == 0 && flagged) {  // enqueue (tile, block) for the fallback warp
-        const uint32_t nf = __popc(flagged);
-        uint32_t slot0 = 0;
-        if (lane == 0) slot0 = atomicAdd(&fq_tail, nf);
-        slot0 = __shfl_sync(0xFFFFFFFFu, slot0, 0);
-        if ((flagged >> lane) & 1u) {
-          const uint32_t slot = (slot0 + __popc(flagged & ((1u << lane) - 1u))) % FQ;
-          volatile unsigned long long* qs = &fq[slot];
-          while (*qs != 0ull) __nanosleep(64);  // ring full (pathological masks only)
-          *qs = (static_cast<unsigned long long>(ti) << 7 | static_cast<unsigned long long>(b)) + 1ull;
-        }
-      }
+      const uint32_t flagged = __ballot_sync(0xFFFFFFFFu, unsure);
+      if (flagged) enqueue_fallback(fq, &fq_tail, flagged, unsure, lane, ti, b);
     }
     __threadfence_block();
     __syncwarp();
-    if (half == 0 && lane == 0) atomicAdd(&fq_done, 1u);
+    if (lane == 0) atomicAdd(&fq_done, 1u);
+    QSTAMP_EPI(tl, 7);
   } else {
     // ---------------- fallback warp: reference-order chain on queued blocks
     uint32_t head = 0;
@@ -506,12 +595,12 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       volatile unsigned long long* qs = &fq[head % FQ];
       unsigned long long e = *qs;
       if (e == 0ull) {
-        if (*reinterpret_cast<volatile uint32_t*>(&fq_done) == 4u) {
+        if (*reinterpret_cast<volatile uint32_t*>(&fq_done) == static_cast<uint32_t>(NEPI)) {
           __threadfence_block();
           e = *qs;
           if (e == 0ull) break;
         } else {
-          __nanosleep(256);
+          __nanosleep(1024);
           continue;
         }
       }
@@ -525,7 +614,10 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       uint8_t* ob = out + f * frame_stride + static_cast<size_t>(y0) * pitch + x0;
       fallback_block(args.ref[args.pof[f]], ib, pitch, w, h, y0, x0, ob, fast_out, fb_sm, nan_flag, lane);
       __syncwarp();
-      if (lane == 0) *qs = 0ull;
+      if (lane == 0) {
+        *qs = 0ull;
+        if (fb_count) atomicAdd(fb_count, 1ull);
+      }
       ++head;
       __syncwarp();
     }
@@ -540,6 +632,17 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
 }  // namespace
 
 namespace dctf {
+
+// DCTF_Q_COUNT=1: a process-wide device counter of the blocks the fallback
+// warp recomputed (diagnostics; read with dctf_diag_fallback_blocks).
+static unsigned long long* fallback_counter() {
+  static unsigned long long* c = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (std::getenv("DCTF_Q_COUNT") && cudaMalloc(&c, 8) == cudaSuccess) cudaMemset(c, 0, 8);
+  });
+  return c;
+}
 
 dctf_status upload_kq_operator(dctf_plan* p) {
   std::vector<int8_t> img;
@@ -564,6 +667,7 @@ dctf_status upload_kq_operator(dctf_plan* p) {
 dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int* plan_of_frame, const uint8_t* in,
                             uint8_t* out, int w, int h, size_t pitch, long long frame_stride, int nframes,
                             cudaStream_t st, bool host_mapped, int* d_nan_or_null) {
+  unsigned long long* fb_count = fallback_counter();
   if (nplans < 1 || nplans > KQ_MAX_PLANS || nframes > KQ_MAX_FRAMES)
     return set_error(DCTF_INVALID_ARGUMENT, "k_fused8_q: too many plans / frames for one launch");
   const int bw = (w + 7) / 8, bh = (h + 7) / 8, ntx = (bw + q8::TILE - 1) / q8::TILE;
@@ -578,9 +682,8 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
     if (!p->kq) return set_error(DCTF_INVALID_ARGUMENT, "k_fused8_q: plan has no integer operator");
     args.bimg[i] = static_cast<const int8_t*>(p->d_kq);
     args.U[i] = p->kq_U;
-    args.c17[i] = 1u << (p->kq_F - 17);
     args.shS[i] = p->kq_F - 16;
-    args.shK[i] = 48 - p->kq_F;
+    args.shL[i] = 32 - p->kq_F;
     args.ref[i] = RefPlan{p->d_refchain, p->d_weights, p->ref_mode, p->ref_npairs, p->kr, p->kc, p->padding};
   }
   for (int f = 0; f < nframes; ++f) args.pof[f] = static_cast<uint8_t>(plan_of_frame ? plan_of_frame[f] : 0);
@@ -601,12 +704,29 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
   const unsigned grid = static_cast<unsigned>(std::min<long long>(sm_count(plans[0]->device), ntiles));
   const cudaError_t e =
       tma ? launch_pdl(k_fused8_q<true>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
-                       frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null)
+                       frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null, fb_count)
           : launch_pdl(k_fused8_q<false>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
-                       frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null);
+                       frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null, fb_count);
   add_launches(1);
   if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_fused8_q: ") + cudaGetErrorString(e));
   return DCTF_OK;
 }
 
 }  // namespace dctf
+
+extern "C" dctf_status dctf_diag_fallback_blocks(unsigned long long* n) {
+  if (!n) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  *n = 0;
+  unsigned long long* c = dctf::fallback_counter();
+  if (!c) return set_error(DCTF_UNSUPPORTED, "set DCTF_Q_COUNT=1 before the first filter call");
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(n, c, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemset(c, 0, 8) != cudaSuccess)
+    return set_error(DCTF_CUDA_ERROR, "fallback counter read failed");
+  return DCTF_OK;
+}
+
+#ifdef QDBG
+extern "C" int dctf_qdbg_read(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_qdbg, sizeof(g_qdbg)) == cudaSuccess ? 0 : 1;
+}
+#endif

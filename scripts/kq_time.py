@@ -4,12 +4,21 @@ import os
 import sys
 import time
 
+import ctypes as C
+
+os.environ.setdefault("DCTF_Q_COUNT", "1")
 import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1710_07193_b200 as P  # noqa: E402
-from paper_1710_07193_b200 import synth  # noqa: E402
+from paper_1710_07193_b200 import _lib, synth  # noqa: E402
+
+
+def fallbacks():
+    n = C.c_ulonglong(0)
+    _lib.lib.dctf_diag_fallback_blocks(C.byref(n))
+    return n.value
 
 
 def ring_time(launch, n, reps=200):
@@ -35,6 +44,10 @@ for label, kw in (("kq", {}), ("fp64", {"env": "DCTF_NO_Q"})):
     pl = P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate)
     os.environ.pop("DCTF_NO_Q", None)
     ms = ring_time(lambda i: pl.filter_image(ins[i % RING]), RING)
+    fallbacks()
+    pl.filter_image(ins[0])
+    nfb = fallbacks()
+    print(f"cfg2 {label:5s} fallback blocks per launch {nfb}")
     print(f"cfg2 {label:5s} {pl.image_kernel:14s} {ms*1e3:8.1f} us  {262144/ms/1e6:6.2f} G blk/s", flush=True)
 
 W, H, F = 3840, 2160, 64
@@ -63,6 +76,9 @@ for label in ("kq", "fp64"):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     ms = float(np.median(ts))
+    fallbacks()
+    P.filter_frames(d, plans, idx)
+    print(f"cfg5 {label} fallback blocks per call {fallbacks()}")
     res[label] = o
     print(f"cfg5 {label:5s} {[p.image_kernel for p in plans]} {ms:.3f} ms  {F*W*H/64/ms/1e6:6.2f} G blk/s", flush=True)
 diff = (res["kq"] != res["fp64"]).sum().item()
