@@ -10,7 +10,7 @@ all: $(PKG)/libdctf_b200.so $(PKG)/libdctf_synth.so oracle cpp-test cli
 
 # one object per translation unit (built in parallel under make -j), linked
 # into the product library; ptxas -v reports are concatenated in build_ptxas.log
-CU_SRCS := capi coef fused tc ozaki spatial quant
+CU_SRCS := capi coef fused tc ozaki spatial quant host
 CU_OBJS := $(patsubst %,build/%.o,$(CU_SRCS)) build/plan.o
 HDRS := $(CSRC)/internal.h $(CSRC)/device.cuh $(CSRC)/fastdiv.cuh include/dctf.h
 
@@ -23,7 +23,7 @@ build/plan.o: $(CSRC)/plan.cc $(HDRS)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 
 $(PKG)/libdctf_b200.so: $(CU_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -ldl
 	@cat build/*.ptxas.log > build_ptxas.log
 
 $(PKG)/libdctf_synth.so: $(CSRC)/synth.cc

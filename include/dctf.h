@@ -51,18 +51,26 @@ typedef enum {
 typedef enum { DCTF_PAD_ZERO = 0, DCTF_PAD_REPLICATE = 1 } dctf_padding; /* spatial.hpp:29-32 */
 
 typedef enum {
-  DCTF_PREC_FP64 = 0,    /* FP64 DMMA tensor pipe; coefficients within 1e-9 rel. */
+  DCTF_PREC_FP64 = 0,    /* FP64-exact: coefficients on the FP64 DMMA pipe within
+                            1e-9 rel.; the n = 8 u8 image path (no coefficient
+                            output) on k_fused8_q — the fused chain composed
+                            into one operator, exact int8 tcgen05 digit slices,
+                            u8 equal to the reference's on every pixel (error-
+                            bounded rounding, reference-order fallback)      */
   DCTF_PREC_TF32X3 = 1,  /* split-precision tcgen05 kind::tf32, 3 passes          */
   DCTF_PREC_BF16X3 = 2,  /* split-precision tcgen05 kind::f16 (bf16), 3 passes;
                             coefficients within ~1e-4 rel. (16-bit split)     */
   DCTF_PREC_INT8_EXACT = 3, /* n = 8 image path: DCT-domain contraction as exact INT8
                               tcgen05 slices (FP64-class accuracy); other entry
                               points of such a plan run the FP64 kernels        */
-  DCTF_PREC_FP64_DENSE = 4  /* as FP64, but never exploit operator structure: the
-                              n = 8 image path of a DCTF_PREC_FP64 plan whose H is
-                              block-diagonal in the (u mod 2, v mod 2) classes
-                              (masks symmetric in both axes) runs the parity-
-                              class kernel; this mode keeps the dense one     */
+  DCTF_PREC_FP64_DENSE = 4, /* as FP64_DMMA, but never exploit operator structure:
+                              the n = 8 image path runs the dense k_fused8 (a
+                              DMMA plan whose H is block-diagonal in the
+                              (u mod 2, v mod 2) classes runs the parity-class
+                              kernel, a low-rank mask the sandwich kernel)     */
+  DCTF_PREC_FP64_DMMA = 5   /* as FP64, but the n = 8 u8 image path stays on the
+                              FP64 DMMA kernels (k_fused8_sep / _sym / k_fused8)
+                              instead of the exact-integer k_fused8_q          */
 } dctf_precision;
 
 typedef struct dctf_plan dctf_plan;
@@ -196,6 +204,50 @@ dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
                                   const int* h_plan_of_frame, const uint8_t* d_in, uint8_t* d_out,
                                   int nframes, int width, int height, size_t pitch,
                                   size_t frame_stride, void* stream);
+
+/* Frame batch on HOST buffers (synchronous): filter_image (image.hpp:210-225)
+ * per frame, frame f with plans[plan_of_frame[f]]. Frames stream through a
+ * per-call 3-slot device ring in ~16 MiB chunks; the H2D copy, the batch
+ * kernel and the D2H copy of consecutive chunks overlap on three per-thread
+ * streams. Pinned (cudaHostAlloc'd) buffers run at PCIe speed. Concurrent
+ * calls from several host threads are allowed. */
+dctf_status dctf_filter_frames_host(const dctf_plan* const* plans, int nplans, const int* h_plan_of_frame,
+                                    const uint8_t* h_in, uint8_t* h_out, int nframes, int width, int height,
+                                    size_t pitch, size_t frame_stride);
+
+/* Multi-GPU (one process, one host thread and stream per device;
+ * SURVEY.md §8(e)). Blocks never exchange data (image.hpp:205-209), so a
+ * dctf_multi holds one replica of a plan per listed device (a device may be
+ * listed twice: two replicas on one GPU) and the entries shard contiguous
+ * block-row bands (one image) or contiguous frame ranges (a batch) over the
+ * replicas, shard r = [total*r/N, total*(r+1)/N), with no data-path
+ * collective. Results are byte-identical to the single-device entries. */
+typedef struct dctf_multi dctf_multi;
+dctf_status dctf_multi_create(const double* h_weights, int kr, int kc, int n, int padding, int precision,
+                              const int* devices, int ndevices, dctf_multi** out);
+dctf_status dctf_multi_destroy(dctf_multi* m);
+/* Replica count and replica 0 (for the per-plan queries above). */
+dctf_status dctf_multi_info(const dctf_multi* m, int* ndevices, const dctf_plan** replica0);
+dctf_status dctf_multi_replica(const dctf_multi* m, int r, const dctf_plan** out);
+/* filter_image on host buffers, block-row bands over the replicas. */
+dctf_status dctf_filter_image_host_multi(const dctf_multi* m, const uint8_t* h_in, uint8_t* h_out, int width,
+                                         int height, size_t pitch);
+/* dctf_filter_frames_host with frame ranges over the replicas (plans[i] are
+ * dctf_multi over the same device list). */
+dctf_status dctf_filter_frames_host_multi(const dctf_multi* const* plans, int nplans, const int* h_plan_of_frame,
+                                          const uint8_t* h_in, uint8_t* h_out, int nframes, int width, int height,
+                                          size_t pitch, size_t frame_stride);
+/* Device-resident batch: replica r filters its shard of frames
+ * [nframes*r/N, nframes*(r+1)/N) from d_in[r] into d_out[r] (both on its
+ * device, holding just that shard, frame_stride apart) on streams[r] (NULL
+ * list = default streams). With d_gather != NULL (and nframes % N == 0) the
+ * shards are all-gathered so d_gather[r] holds all nframes frames in order
+ * — NCCL (libnccl.so.2 loaded at run time; NVLink / NVSwitch), distinct
+ * devices only, else DCTF_UNSUPPORTED. Returns after the gather completes. */
+dctf_status dctf_filter_frames_u8_multi(const dctf_multi* const* plans, int nplans, const int* h_plan_of_frame,
+                                        const uint8_t* const* d_in, uint8_t* const* d_out, int nframes, int width,
+                                        int height, size_t pitch, size_t frame_stride, uint8_t* const* d_gather,
+                                        void* const* streams);
 
 /* End-to-end host-buffer entry (the reference's filter_image signature):
  * copies h_in to the device, filters, copies back into h_out, in chunks of

@@ -22,6 +22,7 @@
 #include <cctype>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <istream>
@@ -51,7 +52,8 @@ enum class Precision {
   kTf32x3 = DCTF_PREC_TF32X3,
   kBf16x3 = DCTF_PREC_BF16X3,
   kInt8Exact = DCTF_PREC_INT8_EXACT,
-  kFp64Dense = DCTF_PREC_FP64_DENSE
+  kFp64Dense = DCTF_PREC_FP64_DENSE,
+  kFp64Dmma = DCTF_PREC_FP64_DMMA
 };
 
 class BlockMatrix {
@@ -540,14 +542,75 @@ inline GrayImage filter_image(const FilterPlan& plan, const GrayImage& img) {
   return out;
 }
 
-// filter_image (image.hpp:210-225): the DCT path, fused on the device.
+// Devices the free-standing filter_image / filter_frames use (this build's
+// multi-GPU extension): set_devices({0, 1, ...}) or the
+// DCTF_DEVICES environment variable ("0,1,2,3"); default {0}. With more than
+// one device an image is split into block-row bands and a frame batch into
+// frame ranges, one replica and host thread per device (blocks are
+// independent, image.hpp:205-209); the output is byte-identical.
+namespace detail {
+inline std::vector<int>& device_list() {
+  static std::vector<int> devs = [] {
+    std::vector<int> d;
+    if (const char* e = std::getenv("DCTF_DEVICES")) {
+      std::stringstream ss(e);
+      std::string tok;
+      while (std::getline(ss, tok, ','))
+        if (!tok.empty()) d.push_back(std::stoi(tok));
+    }
+    if (d.empty()) d.push_back(0);
+    return d;
+  }();
+  return devs;
+}
+}  // namespace detail
+inline void set_devices(const std::vector<int>& devices) {
+  if (devices.empty()) throw std::invalid_argument("set_devices: empty device list");
+  detail::device_list() = devices;
+}
+inline const std::vector<int>& devices() { return detail::device_list(); }
+
+// One FilterPlan replica per device (dctf_multi): the multi-device host entries.
+class MultiFilterPlan {
+ public:
+  MultiFilterPlan(const Mask& mask, int n, PaddingMode padding, const std::vector<int>& devs,
+                  Precision precision = Precision::kFp64) {
+    if (mask.rows() == mask.cols() && mask.rows() > n)
+      throw std::invalid_argument("build_spatial_operator_set: mask larger than block");
+    dctf_multi* m = nullptr;
+    check(dctf_multi_create(mask.weights().data(), mask.rows(), mask.cols(), n, int(padding), int(precision),
+                            devs.data(), int(devs.size()), &m));
+    multi_ = std::shared_ptr<dctf_multi>(m, [](dctf_multi* q) { dctf_multi_destroy(q); });
+  }
+  const dctf_multi* handle() const { return multi_.get(); }
+  int replicas() const {
+    int r = 0;
+    check(dctf_multi_info(multi_.get(), &r, nullptr));
+    return r;
+  }
+
+ private:
+  std::shared_ptr<dctf_multi> multi_;
+};
+
+inline GrayImage filter_image(const MultiFilterPlan& plan, const GrayImage& img) {
+  if (img.samples.size() != size_t(img.width) * img.height)
+    throw std::invalid_argument("GrayImage: sample count must be width*height");
+  GrayImage out{img.width, img.height, std::vector<std::uint8_t>(img.samples.size())};
+  check(dctf_filter_image_host_multi(plan.handle(), img.samples.data(), out.samples.data(), img.width,
+                                     img.height, size_t(img.width)));
+  return out;
+}
+
+// filter_image (image.hpp:210-225): the DCT path, fused on the device(s).
 inline GrayImage filter_image(const GrayImage& img, const Mask& mask, PaddingMode padding,
                               Domain path = Domain::kDct, int n = 8) {
   if (mask.rows() == mask.cols() && mask.rows() > n)
     throw std::invalid_argument("filter_image: mask larger than block");
   if (img.samples.size() != size_t(img.width) * img.height)
     throw std::invalid_argument("GrayImage: sample count must be width*height");
-  const FilterPlan plan(mask, n, padding);
+  if (path == Domain::kDct && devices().size() > 1) return filter_image(MultiFilterPlan(mask, n, padding, devices()), img);
+  const FilterPlan plan(mask, n, padding, Precision::kFp64, devices()[0]);
   GrayImage out{img.width, img.height, std::vector<std::uint8_t>(img.samples.size())};
   if (path == Domain::kDct)
     check(dctf_filter_image_host(plan.handle(), img.samples.data(), out.samples.data(), img.width,
@@ -556,6 +619,43 @@ inline GrayImage filter_image(const GrayImage& img, const Mask& mask, PaddingMod
     check(dctf_filter_image_spatial_host(plan.handle(), img.samples.data(), out.samples.data(),
                                          img.width, img.height, size_t(img.width)));
   return out;
+}
+
+// A video batch (equal-size frames), frame f filtered with
+// masks[mask_of_frame[f]] — filter_image per frame, as one batched call on the
+// configured devices (frame ranges per device when there are several).
+inline std::vector<GrayImage> filter_frames(const std::vector<GrayImage>& frames, const std::vector<Mask>& masks,
+                                            const std::vector<int>& mask_of_frame, PaddingMode padding, int n = 8) {
+  if (frames.empty()) return {};
+  if (mask_of_frame.size() != frames.size())
+    throw std::invalid_argument("filter_frames: one mask index per frame");
+  const int w = frames[0].width, h = frames[0].height;
+  std::vector<std::uint8_t> in(size_t(w) * h * frames.size()), out(in.size());
+  for (size_t f = 0; f < frames.size(); ++f) {
+    if (frames[f].width != w || frames[f].height != h || frames[f].samples.size() != size_t(w) * h)
+      throw std::invalid_argument("filter_frames: frames must share one size");
+    std::copy(frames[f].samples.begin(), frames[f].samples.end(), in.begin() + f * size_t(w) * h);
+  }
+  const size_t fs = size_t(w) * h;
+  if (devices().size() > 1) {
+    std::vector<MultiFilterPlan> plans;
+    std::vector<const dctf_multi*> hs;
+    for (const Mask& m : masks) plans.emplace_back(m, n, padding, devices());
+    for (const auto& p : plans) hs.push_back(p.handle());
+    check(dctf_filter_frames_host_multi(hs.data(), int(hs.size()), mask_of_frame.data(), in.data(), out.data(),
+                                        int(frames.size()), w, h, size_t(w), fs));
+  } else {
+    std::vector<FilterPlan> plans;
+    std::vector<const dctf_plan*> hs;
+    for (const Mask& m : masks) plans.emplace_back(m, n, padding, Precision::kFp64, devices()[0]);
+    for (const auto& p : plans) hs.push_back(p.handle());
+    check(dctf_filter_frames_host(hs.data(), int(hs.size()), mask_of_frame.data(), in.data(), out.data(),
+                                  int(frames.size()), w, h, size_t(w), fs));
+  }
+  std::vector<GrayImage> res(frames.size());
+  for (size_t f = 0; f < frames.size(); ++f)
+    res[f] = GrayImage{w, h, std::vector<std::uint8_t>(out.begin() + f * fs, out.begin() + (f + 1) * fs)};
+  return res;
 }
 
 // tile / assemble (image.hpp:155-203), for callers of the per-block API: an

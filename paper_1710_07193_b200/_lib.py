@@ -22,7 +22,7 @@ lib = C.CDLL(LIB_PATH)
 
 OK, INVALID_ARGUMENT, CUDA_ERROR, NAN_ENCOUNTERED, UNSUPPORTED = range(5)
 PAD_ZERO, PAD_REPLICATE = 0, 1
-PREC_FP64, PREC_TF32X3, PREC_BF16X3, PREC_INT8_EXACT, PREC_FP64_DENSE = 0, 1, 2, 3, 4
+PREC_FP64, PREC_TF32X3, PREC_BF16X3, PREC_INT8_EXACT, PREC_FP64_DENSE, PREC_FP64_DMMA = 0, 1, 2, 3, 4, 5
 
 _d = C.POINTER(C.c_double)
 _u8 = C.POINTER(C.c_uint8)
@@ -66,6 +66,18 @@ _SIGS = {
     "dctf_measure_fp64_peak": (_st, [C.c_int, C.c_int, _d]),
     "dctf_last_launch_count": (C.c_int, []),
     "dctf_diag_fallback_blocks": (_st, [C.POINTER(C.c_ulonglong)]),
+    "dctf_filter_frames_host": (_st, [C.POINTER(_vp), C.c_int, _i, _vp, _vp, C.c_int, C.c_int, C.c_int,
+                                      C.c_size_t, C.c_size_t]),
+    "dctf_multi_create": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i, C.c_int, C.POINTER(_vp)]),
+    "dctf_multi_destroy": (_st, [_vp]),
+    "dctf_multi_info": (_st, [_vp, _i, C.POINTER(_vp)]),
+    "dctf_multi_replica": (_st, [_vp, C.c_int, C.POINTER(_vp)]),
+    "dctf_filter_image_host_multi": (_st, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_size_t]),
+    "dctf_filter_frames_host_multi": (_st, [C.POINTER(_vp), C.c_int, _i, _vp, _vp, C.c_int, C.c_int, C.c_int,
+                                            C.c_size_t, C.c_size_t]),
+    "dctf_filter_frames_u8_multi": (_st, [C.POINTER(_vp), C.c_int, _i, C.POINTER(_vp), C.POINTER(_vp), C.c_int,
+                                          C.c_int, C.c_int, C.c_size_t, C.c_size_t, C.POINTER(_vp),
+                                          C.POINTER(_vp)]),
     "dctf_last_error_message": (C.c_char_p, []),
     "dctf_version": (C.c_char_p, []),
 }

@@ -521,7 +521,8 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_hfused, hfused.data(), hfused.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
-  p->sym = precision == DCTF_PREC_FP64 && dctf::parity_block_diagonal(p->op, n);
+  const bool fp64 = precision == DCTF_PREC_FP64 || precision == DCTF_PREC_FP64_DMMA;
+  p->sym = fp64 && dctf::parity_block_diagonal(p->op, n);
   if (e == cudaSuccess && p->sym && n == 16) {
     std::vector<double> gsym;
     dctf::layout_gsym16(p->op, p->basis, gsym);
@@ -532,7 +533,7 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
   // n = 8 sandwich kernel: worth it where it runs fewer DMMA per block than
   // the alternative (4P + 4 against 8 parity-class / 20 dense): separable
   // masks, and rank <= 3 when the operator has no parity structure
-  if (e == cudaSuccess && n == 8 && (precision == DCTF_PREC_FP64) && !std::getenv("DCTF_NO_SEP")) {
+  if (e == cudaSuccess && n == 8 && fp64 && !std::getenv("DCTF_NO_SEP")) {
     std::vector<double> frag;
     const bool psym = dctf::parity_block_diagonal(p->op, 8);
     if (dctf::layout_sep8(*p, frag, p->sep_rank) && (!psym || p->sep_rank == 1)) {
@@ -623,6 +624,50 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
 }
 }  // namespace
 
+namespace dctf {
+// The batch dispatch of dctf_filter_frames_u8 (arguments validated by the
+// caller; the device is current): one k_fused8_q launch when every plan has
+// the integer operator, else one launch per plan for evenly spaced frames.
+dctf_status filter_frames_device(const dctf_plan* const* plans, int nplans, const int* h_plan_of_frame,
+                                 const uint8_t* d_in, uint8_t* d_out, int nframes, int w, int h, size_t pitch,
+                                 size_t frame_stride, cudaStream_t st) {
+  dctf_status s = DCTF_OK;
+  // Every plan on the exact-integer kernel: the whole batch is one launch
+  // (each plan's digit image resident in shared memory, per-frame selection).
+  bool all_kq = plans[0]->n == 8 && nplans <= dctf::KQ_MAX_PLANS && nframes <= dctf::KQ_MAX_FRAMES;
+  for (int i = 0; i < nplans && all_kq; ++i) all_kq = plans[i]->kq;
+  if (all_kq)
+    return dctf::launch_fused8_q(plans, nplans, h_plan_of_frame, d_in, d_out, w, h, pitch,
+                                 static_cast<long long>(frame_stride), nframes, st, false, nullptr);
+  // Frames sharing a plan and evenly spaced go in one launch (round-robin
+  // assignment -> one launch per plan); anything else falls back per frame.
+  for (int pi = 0; pi < nplans && s == DCTF_OK; ++pi) {
+    int first = -1, second = -1, count = 0;
+    bool arith = true;
+    for (int f = 0; f < nframes; ++f) {
+      if (h_plan_of_frame[f] != pi) continue;
+      if (first < 0) first = f;
+      else if (second < 0) second = f;
+      else if ((f - first) != count * (second - first)) arith = false;
+      ++count;
+    }
+    if (count == 0) continue;
+    if (arith) {
+      const long long step = count > 1 ? static_cast<long long>(second - first) : 1;
+      s = filter_image_device(plans[pi], d_in + first * frame_stride, d_out + first * frame_stride,
+                              w, h, pitch, step * static_cast<long long>(frame_stride), count,
+                              nullptr, st);
+    } else {
+      for (int f = 0; f < nframes && s == DCTF_OK; ++f)
+        if (h_plan_of_frame[f] == pi)
+          s = filter_image_device(plans[pi], d_in + f * frame_stride, d_out + f * frame_stride, w,
+                                  h, pitch, 0, 1, nullptr, st);
+    }
+  }
+  return s;
+}
+}  // namespace dctf
+
 extern "C" {
 
 dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int padding,
@@ -630,7 +675,7 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
   dctf::reset_launches();
   if (!out || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
-  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DENSE)
+  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DMMA)
     return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
   if (kr < 1 || kc < 1) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
   auto* p = new dctf_plan();
@@ -655,7 +700,7 @@ dctf_status dctf_plan_create_from_pairs(const double* h_lefts, const double* h_r
   dctf::reset_launches();
   if (!out || (npairs > 0 && (!h_lefts || !h_rights)) || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
-  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DENSE)
+  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DMMA)
     return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
   if (domain != 0 && domain != 1) return set_error(DCTF_INVALID_ARGUMENT, "domain must be 0 (spatial) or 1 (DCT)");
   if (k < 1 || (k % 2) == 0) return set_error(DCTF_INVALID_ARGUMENT, "Mask: side must be odd and >= 1");
@@ -679,7 +724,7 @@ dctf_status dctf_plan_create_from_dump(const char* text, size_t len, int precisi
   dctf::reset_launches();
   if (!out || !text) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
-  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DENSE)
+  if (precision < DCTF_PREC_FP64 || precision > DCTF_PREC_FP64_DMMA)
     return set_error(DCTF_INVALID_ARGUMENT, "unknown precision mode");
   auto* p = new dctf_plan();
   p->precision = precision;
@@ -969,40 +1014,8 @@ dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
     if (h_plan_of_frame[f] < 0 || h_plan_of_frame[f] >= nplans)
       return set_error(DCTF_INVALID_ARGUMENT, "plan_of_frame index out of range");
   DeviceGuard guard(plans[0]->device);
-  const cudaStream_t st = as_stream(stream);
-  // Every plan on the exact-integer kernel: the whole batch is one launch
-  // (each plan's digit image resident in shared memory, per-frame selection).
-  bool all_kq = plans[0]->n == 8 && nplans <= dctf::KQ_MAX_PLANS && nframes <= dctf::KQ_MAX_FRAMES;
-  for (int i = 0; i < nplans && all_kq; ++i) all_kq = plans[i]->kq;
-  if (all_kq)
-    return dctf::launch_fused8_q(plans, nplans, h_plan_of_frame, d_in, d_out, w, h, pitch,
-                                 static_cast<long long>(frame_stride), nframes, st, false, nullptr);
-  // Frames sharing a plan and evenly spaced go in one launch (round-robin
-  // assignment -> one launch per plan); anything else falls back per frame.
-  for (int pi = 0; pi < nplans && s == DCTF_OK; ++pi) {
-    int first = -1, second = -1, count = 0;
-    bool arith = true;
-    for (int f = 0; f < nframes; ++f) {
-      if (h_plan_of_frame[f] != pi) continue;
-      if (first < 0) first = f;
-      else if (second < 0) second = f;
-      else if ((f - first) != count * (second - first)) arith = false;
-      ++count;
-    }
-    if (count == 0) continue;
-    if (arith) {
-      const long long step = count > 1 ? static_cast<long long>(second - first) : 1;
-      s = filter_image_device(plans[pi], d_in + first * frame_stride, d_out + first * frame_stride,
-                              w, h, pitch, step * static_cast<long long>(frame_stride), count,
-                              nullptr, st);
-    } else {
-      for (int f = 0; f < nframes && s == DCTF_OK; ++f)
-        if (h_plan_of_frame[f] == pi)
-          s = filter_image_device(plans[pi], d_in + f * frame_stride, d_out + f * frame_stride, w,
-                                  h, pitch, 0, 1, nullptr, st);
-    }
-  }
-  return s;
+  return dctf::filter_frames_device(plans, nplans, h_plan_of_frame, d_in, d_out, nframes, w, h, pitch,
+                                    frame_stride, as_stream(stream));
 }
 
 dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w,
@@ -1014,6 +1027,17 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
   if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
+  // Plans on k_fused8_q (TMA-fed: no zero-copy reads of host memory) and
+  // split-precision plans (three kernels) go through the copy-engine band
+  // pipeline: per-call scratch, per-thread streams, no plan lock.
+  const char* mode_env = std::getenv("DCTF_E2E_MODE");
+  if (p->kq || p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3 ||
+      (mode_env && std::atoi(mode_env) == 0)) {
+    int launches = 0;
+    s = dctf::image_host_copy(p, h_in, h_out, w, h, pitch, &launches);
+    dctf::t_launches = launches;
+    return s;
+  }
   std::lock_guard<std::mutex> lock(p->io_mu);
   size_t dpitch = (static_cast<size_t>(w) + 15) & ~size_t(15);
   // mode 1 stages the input with the caller's pitch (the kernel then reads
@@ -1239,14 +1263,17 @@ dctf_status dctf_filter_image_spatial_host(const dctf_plan* p, const uint8_t* h_
   if (w == 0 || h == 0) return DCTF_OK;  // tile() of an empty image has no blocks
   if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
-  const size_t bytes = pitch * static_cast<size_t>(h);
+  // device copy at the width rounded to 16 bytes; only w bytes of each of the
+  // caller's rows are read and written (its row padding is not ours)
+  const size_t dpitch = (static_cast<size_t>(w) + 15) & ~size_t(15);
+  const size_t bytes = dpitch * static_cast<size_t>(h);
   uint8_t *din = nullptr, *dout = nullptr;
   CUDA_TRY(cudaMalloc(&din, bytes));
   cudaError_t e = cudaMalloc(&dout, bytes);
-  if (e == cudaSuccess) e = cudaMemcpy(din, h_in, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy2D(din, dpitch, h_in, pitch, w, h, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
-    s = dctf_filter_image_spatial_u8(p, din, dout, w, h, pitch, nullptr);
-    if (s == DCTF_OK) e = cudaMemcpy(h_out, dout, bytes, cudaMemcpyDeviceToHost);
+    s = dctf_filter_image_spatial_u8(p, din, dout, w, h, dpitch, nullptr);
+    if (s == DCTF_OK) e = cudaMemcpy2D(h_out, pitch, dout, dpitch, w, h, cudaMemcpyDeviceToHost);
   }
   cudaFree(din);
   cudaFree(dout);

@@ -100,6 +100,14 @@ dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* 
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
                                 cudaStream_t st, bool host_mapped = false);
 void reset_launches();
+// host.cu: one image from / to host buffers through the copy-engine pipeline
+// (per-call scratch, per-thread streams).
+dctf_status image_host_copy(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w, int h, size_t pitch,
+                            int* launches);
+// capi.cu: dctf_filter_frames_u8's dispatch (validated arguments, device current).
+dctf_status filter_frames_device(const dctf_plan* const* plans, int nplans, const int* h_plan_of_frame,
+                                 const uint8_t* d_in, uint8_t* d_out, int nframes, int w, int h, size_t pitch,
+                                 size_t frame_stride, cudaStream_t st);
 
 // Host operator compiler (plan.cc).
 // Builds C and the dense DCT-domain operator H for the mask.

@@ -32,7 +32,7 @@ from ._lib import InvalidArgument, Unsupported, check
 __all__ = [
     "PaddingMode", "Domain", "Precision", "Mask", "row_symmetric", "DctBasis", "FilterPlan",
     "forward_2d", "inverse_2d", "filter_image", "filter_frames", "InvalidArgument", "Unsupported",
-    "format_operator_dump", "operator_from_dump",
+    "format_operator_dump", "operator_from_dump", "filter_frames_host", "MultiPlan",
 ]
 
 
@@ -52,6 +52,7 @@ class Precision(enum.IntEnum):
     kBf16x3 = _lib.PREC_BF16X3
     kInt8Exact = _lib.PREC_INT8_EXACT
     kFp64Dense = _lib.PREC_FP64_DENSE
+    kFp64Dmma = _lib.PREC_FP64_DMMA
 
 
 class Mask:
@@ -521,3 +522,101 @@ def filter_frames(frames, plans: Sequence[FilterPlan], plan_of_frame: Sequence[i
     check(_lib.lib.dctf_filter_frames_u8(handles, len(plans), idx, _dptr(frames), _dptr(out), f, w,
                                          h, w, h * w, _stream(frames.device)))
     return out
+
+
+def _frames_args(frames: np.ndarray, plans, plan_of_frame):
+    frames = np.ascontiguousarray(frames, dtype=np.uint8)
+    if frames.ndim != 3:
+        raise InvalidArgument("expected (frames, height, width) uint8 frames")
+    f, h, w = frames.shape
+    if len(plan_of_frame) != f:
+        raise InvalidArgument("plan_of_frame must have one entry per frame")
+    handles = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+    idx = (C.c_int * max(f, 1))(*[int(i) for i in plan_of_frame])
+    return frames, f, h, w, handles, idx
+
+
+def filter_frames_host(frames: np.ndarray, plans: Sequence[FilterPlan], plan_of_frame: Sequence[int],
+                       out: np.ndarray | None = None) -> np.ndarray:
+    """Video batch on host memory (dctf_filter_frames_host): (F, h, w) uint8
+    numpy frames in, filtered frames out; the copies to and from the device
+    overlap the batch kernel. Pinned buffers (torch ``pin_memory``) run at
+    PCIe speed."""
+    frames, f, h, w, handles, idx = _frames_args(frames, plans, plan_of_frame)
+    if out is None:
+        out = np.empty_like(frames)
+    check(_lib.lib.dctf_filter_frames_host(handles, len(plans), idx, frames.ctypes.data, out.ctypes.data, f, w, h,
+                                           w, h * w))
+    return out
+
+
+class MultiPlan:
+    """One FilterPlan replica per device (dctf_multi, include/dctf.h): the
+    multi-GPU entries shard block-row bands / frame ranges over the replicas
+    (blocks are independent, image.hpp:205-209). A device may repeat (two
+    replicas on one GPU)."""
+
+    def __init__(self, mask: Mask, n: int, padding: PaddingMode, devices: Sequence[int],
+                 precision: Precision = Precision.kFp64):
+        h = C.c_void_p()
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        check(_lib.lib.dctf_multi_create(mask._w.ctypes.data_as(_lib._d), mask.kr, mask.kc, int(n), int(padding),
+                                         int(precision), devs, len(devices), C.byref(h)))
+        self._h, self.devices, self._n = h, list(devices), int(n)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None and getattr(_lib, "lib", None) is not None:
+            _lib.lib.dctf_multi_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def image_kernel(self) -> str:
+        r0 = C.c_void_p()
+        check(_lib.lib.dctf_multi_info(self._h, None, C.byref(r0)))
+        return _lib.lib.dctf_plan_image_kernel(r0).decode()
+
+    def filter_image_host(self, img: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        if img.ndim != 2:
+            raise InvalidArgument("expected a (height, width) uint8 image")
+        if out is None:
+            out = np.empty_like(img)
+        h, w = img.shape
+        check(_lib.lib.dctf_filter_image_host_multi(self._h, img.ctypes.data, out.ctypes.data, w, h,
+                                                    img.strides[0]))
+        return out
+
+    @staticmethod
+    def filter_frames_host(frames: np.ndarray, plans: Sequence["MultiPlan"], plan_of_frame: Sequence[int],
+                           out: np.ndarray | None = None) -> np.ndarray:
+        frames, f, h, w, handles, idx = _frames_args(frames, plans, plan_of_frame)
+        if out is None:
+            out = np.empty_like(frames)
+        check(_lib.lib.dctf_filter_frames_host_multi(handles, len(plans), idx, frames.ctypes.data,
+                                                     out.ctypes.data, f, w, h, w, h * w))
+        return out
+
+    @staticmethod
+    def filter_frames(shards, plans: Sequence["MultiPlan"], plan_of_frame: Sequence[int], gather=None):
+        """Device-resident batch: shards[r] is a contiguous (F_r, h, w) uint8
+        CUDA tensor on replica r's device holding its frame range; returns the
+        filtered shards. With gather=[t_r] (each (F, h, w) on device r) the
+        shards are NCCL all-gathered into every t_r."""
+        import torch
+        n = len(shards)
+        f = sum(int(t.shape[0]) for t in shards)
+        h, w = int(shards[0].shape[1]), int(shards[0].shape[2])
+        outs = [torch.empty_like(t) for t in shards]
+        handles = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+        idx = (C.c_int * max(f, 1))(*[int(i) for i in plan_of_frame])
+        din = (C.c_void_p * n)(*[t.data_ptr() for t in shards])
+        dout = (C.c_void_p * n)(*[t.data_ptr() for t in outs])
+        dg = None if gather is None else (C.c_void_p * n)(*[t.data_ptr() for t in gather])
+        sts = (C.c_void_p * n)(*[torch.cuda.current_stream(t.device).cuda_stream for t in shards])
+        check(_lib.lib.dctf_filter_frames_u8_multi(handles, len(plans), idx, din, dout, f, w, h, w, h * w, dg,
+                                                   sts))
+        return outs

@@ -3,6 +3,7 @@
 // image_test.cc, dct_test.cc), on the GPU. Built by `make cpp-test`, run by
 // tests/test_gpu_cpp.py. Prints one line per check, exits non-zero on failure.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <random>
 
@@ -108,11 +109,12 @@ int main() {
     GrayImage img{1000, 600, std::vector<std::uint8_t>(1000 * 600)};
     for (auto& s : img.samples) s = std::uint8_t(rng() & 255);
     const Mask g = Mask::gaussian3();
-    const FilterPlan sym(g, 8, PaddingMode::kReplicate);
+    const FilterPlan sym(g, 8, PaddingMode::kReplicate, Precision::kFp64Dmma);
     const FilterPlan dense(g, 8, PaddingMode::kReplicate, Precision::kFp64Dense);
     const FilterPlan i8(g, 8, PaddingMode::kReplicate, Precision::kInt8Exact);
+    const FilterPlan q(g, 8, PaddingMode::kReplicate);
     CHECK(sym.image_kernel() == "k_fused8_sep" && dense.image_kernel() == "k_fused8" &&
-              i8.image_kernel() == "k_fused8_i8",
+              i8.image_kernel() == "k_fused8_i8" && q.image_kernel() == "k_fused8_q",
           "image kernel selection by mask structure / precision");
     const GrayImage a = filter_image(sym, img), b = filter_image(dense, img), c = filter_image(i8, img);
     CHECK(a.samples == b.samples && a.samples == c.samples, "parity-class, dense and INT8-exact u8 identical");
@@ -201,6 +203,52 @@ int main() {
     CHECK(threw, "merge_symmetric of a merged set throws invalid_argument");
   }
   CHECK(quantize_sample(127.5) == 128 && quantize_sample(0.5) == 1 && quantize_sample(-3) == 0, "quantize KATs");
+  // multi-device path (dctf_multi): two replicas on device 0 — the 2-way
+  // sharding code path (block-row bands, frame ranges, one host thread per
+  // replica) — must be byte-identical to the single-device entries
+  {
+    GrayImage img{1000, 737, std::vector<std::uint8_t>(1000 * 737)};
+    std::uniform_int_distribution<int> d(0, 255);
+    for (auto& v : img.samples) v = std::uint8_t(d(rng));
+    std::vector<double> g5(25), r5(25);
+    double gs = 0, rs = 0;
+    std::uniform_real_distribution<double> u(-1, 1);
+    for (int i = 0; i < 25; ++i) {
+      const int y = i / 5 - 2, x = i % 5 - 2;
+      g5[i] = std::exp(-(x * x + y * y) / 2.0);
+      gs += g5[i];
+      r5[i] = u(rng);
+      rs += r5[i];
+    }
+    for (int i = 0; i < 25; ++i) {
+      g5[i] /= gs;
+      r5[i] /= rs;
+    }
+    const Mask mg(5, g5), mr(5, r5);
+    for (const Mask* m : {&mg, &mr}) {
+      const FilterPlan one(*m, 8, PaddingMode::kReplicate);
+      const MultiFilterPlan two(*m, 8, PaddingMode::kReplicate, {0, 0});
+      CHECK(two.replicas() == 2, "MultiFilterPlan on {0, 0} has two replicas");
+      CHECK(filter_image(two, img).samples == filter_image(one, img).samples,
+            "2-replica block-row bands == single device (ragged 1000x737)");
+    }
+    std::vector<GrayImage> frames(7, GrayImage{384, 216, std::vector<std::uint8_t>(384 * 216)});
+    for (auto& f : frames)
+      for (auto& v : f.samples) v = std::uint8_t(d(rng));
+    const std::vector<int> mof = {0, 1, 0, 1, 1, 0, 0};
+    set_devices({0});
+    const auto a = filter_frames(frames, {mg, mr}, mof, PaddingMode::kReplicate);
+    set_devices({0, 0});
+    const auto b = filter_frames(frames, {mg, mr}, mof, PaddingMode::kReplicate);
+    const auto c = filter_image(frames[3], mr, PaddingMode::kReplicate);  // 2 replicas, one image
+    set_devices({0});
+    bool same = a.size() == frames.size() && b.size() == frames.size();
+    for (size_t f = 0; same && f < frames.size(); ++f) same = a[f].samples == b[f].samples;
+    CHECK(same, "filter_frames: 2-replica frame ranges == single device (7 frames, 2 masks)");
+    const FilterPlan pr(mr, 8, PaddingMode::kReplicate);
+    CHECK(a[3].samples == filter_image(pr, frames[3]).samples, "filter_frames frame == filter_image of that frame");
+    CHECK(c.samples == a[3].samples, "filter_image with set_devices({0, 0}) == single device");
+  }
   std::printf("%s\n", failures ? "FAILED" : "ALL PASSED");
   return failures ? 1 : 0;
 }

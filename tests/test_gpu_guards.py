@@ -40,10 +40,10 @@ def _cases():
     out = []
     for n in (8, 16):
         for name in ("gaussian5", "laplacian", "random3", "random5", "symrank3", "motion1x9"):
-            for prec in ("kFp64", "kFp64Dense", "kInt8Exact", "kTf32x3", "kBf16x3"):
-                if prec == "kInt8Exact" and n != 8:
+            for prec in ("kFp64", "kFp64Dmma", "kFp64Dense", "kInt8Exact", "kTf32x3", "kBf16x3"):
+                if prec in ("kInt8Exact", "kFp64Dmma") and n != 8:
                     continue
-                if prec != "kFp64" and name not in ("gaussian5", "random5"):
+                if prec not in ("kFp64", "kFp64Dmma") and name not in ("gaussian5", "random5"):
                     continue
                 out.append((n, name, prec))
     return out
@@ -97,6 +97,9 @@ def test_entry_points_stay_in_bounds(cuda, n, name, prec, pad):
         _lib.check(lib.dctf_filter_image_u8(plan.handle, row1(src), row1(out), wd, h, pitch, blk1(co), sp))
         img_ok(out, ref_img, "filter_image_u8 + coefs")
         coef_ok(co, co_t.cpu().numpy(), "filter_image_u8 coefficient dump")
+        # without the dump (k_fused8_q for n = 8 FP64 plans: at exact .5 ties
+        # it rounds like the reference, where the FP64 dump kernels may not)
+        ref_img = plan.filter_image(tight).cpu().numpy()
         out = canvas()
         _lib.check(lib.dctf_filter_image_u8(plan.handle, row1(src), row1(out), wd, h, pitch, None, sp))
         img_ok(out, ref_img, "filter_image_u8")
@@ -149,6 +152,16 @@ def test_entry_points_stay_in_bounds(cuda, n, name, prec, pad):
                     assert (b[1:h + 1, wd:] == CANARY_U8).all(), f"{what}: bytes past the row end"
                     assert np.array_equal(b[1:h + 1, :wd], ref_img), f"{what}: differs from the device path"
                     assert np.array_equal(hsn, hsrc), f"{what}: wrote into its input"
+            # the spatial path's host entry on the same pitched buffers
+            ho = np.full((h + 3, hp), CANARY_U8, np.uint8)
+            hs = hsrc.copy()
+            _lib.check(lib.dctf_filter_image_spatial_host(plan.handle, hs.ctypes.data + hp, ho.ctypes.data + hp,
+                                                          wd, h, hp))
+            what = f"filter_image_spatial_host pitch={hp}"
+            assert (ho[0] == CANARY_U8).all() and (ho[h + 1:] == CANARY_U8).all(), f"{what}: rows outside"
+            assert (ho[1:h + 1, wd:] == CANARY_U8).all(), f"{what}: bytes past the row end"
+            assert np.array_equal(ho[1:h + 1, :wd], sp_t), f"{what}: differs from the device path"
+            assert np.array_equal(hs, hsrc), f"{what}: wrote into its input"
 
 
 @pytest.mark.parametrize("n", [8, 16])

@@ -1,5 +1,5 @@
 """Memory-layout edge cases of the image entry points, for every image kernel
-(k_fused8_sep, k_fused8_sym, k_fused8, k_fused16_sep, k_fused16_sym, k_fused16, k_fused8_i8, the
+(k_fused8_q, k_fused8_sep, k_fused8_sym, k_fused8, k_fused16_sep, k_fused16_sym, k_fused16, k_fused8_i8, the
 unfused 3xTF32 route): views whose base pointer or pitch is not 16-byte
 aligned (the kernels fall back from 16-byte vector loads to the clamped
 per-byte path), padded pitches, and the host-buffer entry on pinned and
@@ -17,10 +17,13 @@ pytestmark = pytest.mark.gpu
 def _plans():
     g5 = synth.gaussian_mask(5, 1.0)
     r5, _ = synth.random_mask(77, 5)
-    yield "k_fused8_sep", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate)
-    yield "k_fused8_sep", P.FilterPlan(P.Mask(3, synth.random_mask(3, 3)[0]), 8, P.PaddingMode.kZero)
-    yield "k_fused8_sym", P.FilterPlan(P.Mask(5, synth.symmetric_mask(5, 5)), 8, P.PaddingMode.kReplicate)
-    yield "k_fused8", P.FilterPlan(P.Mask(5, r5), 8, P.PaddingMode.kZero)
+    yield "k_fused8_sep", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
+    yield "k_fused8_sep", P.FilterPlan(P.Mask(3, synth.random_mask(3, 3)[0]), 8, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma)
+    yield "k_fused8_sym", P.FilterPlan(P.Mask(5, synth.symmetric_mask(5, 5)), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
+    yield "k_fused8", P.FilterPlan(P.Mask(5, r5), 8, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma)
+    yield "k_fused8_q", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate)
+    yield "k_fused8_q", P.FilterPlan(P.Mask(5, r5), 8, P.PaddingMode.kZero)
+    yield "k_fused8_q", P.FilterPlan(P.Mask.rect(1, 9, synth.MOTION_1x9), 8, P.PaddingMode.kReplicate)
     yield "k_fused16_sep", P.FilterPlan(P.Mask(5, g5), 16, P.PaddingMode.kZero)
     yield "k_fused16_sep", P.FilterPlan(P.Mask(3, synth.LAPLACIAN3), 16, P.PaddingMode.kReplicate)
     yield "k_fused16_sym", P.FilterPlan(P.Mask(5, synth.symmetric_mask(5, 5)), 16, P.PaddingMode.kZero)

@@ -20,16 +20,18 @@ ASYM3 = np.array([0.3, -0.2, 0.1, 0.25, 0.4, -0.05, 0.15, 0.1, -0.05])
 def _plans():
     g5 = synth.gaussian_mask(5, 1.0)
     return [
-        ("sym8", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate)),
-        ("dense8", P.FilterPlan(P.Mask(3, ASYM3 / ASYM3.sum()), 8, P.PaddingMode.kZero)),
+        ("sym8", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)),
+        ("dense8", P.FilterPlan(P.Mask(3, ASYM3 / ASYM3.sum()), 8, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma)),
         ("int8exact", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate,
                                    precision=P.Precision.kInt8Exact)),
         ("sym16", P.FilterPlan(P.Mask(7, synth.gaussian_mask(7, 2.0)), 16, P.PaddingMode.kReplicate)),
         ("dense16", P.FilterPlan(P.Mask(3, ASYM3 / ASYM3.sum()), 16, P.PaddingMode.kReplicate)),
+        ("q8", P.FilterPlan(P.Mask(5, g5), 8, P.PaddingMode.kReplicate)),
+        ("q8dense", P.FilterPlan(P.Mask(3, ASYM3 / ASYM3.sum()), 8, P.PaddingMode.kZero)),
     ]
 
 
-@pytest.mark.parametrize("idx", range(5))
+@pytest.mark.parametrize("idx", range(7))
 def test_image_chain_raw_and_war(cuda, idx):
     torch = cuda
     name, plan = _plans()[idx]
@@ -87,7 +89,7 @@ def test_coefficient_chain(cuda, n, precision, masksym):
 def test_torch_producer_then_filter(cuda):
     """A torch kernel (no PDL trigger) writing the input right before the launch."""
     torch = cuda
-    plan = P.FilterPlan(P.Mask(5, synth.gaussian_mask(5, 1.0)), 8, P.PaddingMode.kReplicate)
+    plan = P.FilterPlan(P.Mask(5, synth.gaussian_mask(5, 1.0)), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
     x = torch.from_numpy(synth.sinusoid_image(3, 2048, 2048)).cuda()
     y = torch.empty_like(x)
     for k in range(4):

@@ -26,7 +26,7 @@ def test_round_trip_full_size(cuda):
     torch = cuda
     for n in (8, 16):
         img = torch.from_numpy(synth.uniform_image(3, 8192, 8192)).cuda()
-        plan = P.FilterPlan(P.Mask(1, np.array([1.0])), n, P.PaddingMode.kZero)
+        plan = P.FilterPlan(P.Mask(1, np.array([1.0])), n, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma)
         x = plan.forward_image(img)
         back = plan.inverse_image_u8(x, 8192, 8192)
         assert torch.equal(back, img), n
@@ -41,7 +41,7 @@ def test_linearity_full_size(cuda, n):
     x2 = torch.randn((nb, n, n), dtype=torch.float64, device="cuda", generator=g) * 300
     a, b = 0.75, -1.5
     for w, k in ((synth.gaussian_mask(5, 1.0), 5), (synth.random_mask(3, 5)[0], 5)):
-        plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
         lhs = plan.filter_coeffs(a * x1 + b * x2)
         rhs = a * plan.filter_coeffs(x1) + b * plan.filter_coeffs(x2)
         assert (lhs - rhs).abs().max().item() <= 1e-12 * lhs.abs().max().item()
@@ -53,7 +53,7 @@ def test_block_order_independence(cuda):
     x = torch.randn((nb, 8, 8), dtype=torch.float64, device="cuda") * 200
     perm = torch.randperm(nb, device="cuda")
     for w, k in ((synth.gaussian_mask(5, 1.0), 5), (synth.random_mask(3, 3)[0], 3)):
-        plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero)
+        plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma)
         y = plan.filter_coeffs(x)
         yp = plan.filter_coeffs(x[perm].contiguous())
         assert torch.equal(yp, y[perm])
@@ -67,7 +67,7 @@ def test_parity_class_kernel_equals_dense_config3_size(cuda):
                          (synth.symmetric_mask(5, 5), 5, "k_fused8_sym"), (synth.LAPLACIAN3, 3, "k_fused8_sym"),
                          (synth.random_mask(1003, 3)[0], 3, "k_fused8_sep")):
         for pad in (P.PaddingMode.kZero, P.PaddingMode.kReplicate):
-            sym = P.FilterPlan(P.Mask(k, w), 8, pad)
+            sym = P.FilterPlan(P.Mask(k, w), 8, pad, precision=P.Precision.kFp64Dmma)
             dense = P.FilterPlan(P.Mask(k, w), 8, pad, precision=P.Precision.kFp64Dense)
             assert sym.image_kernel == kernel and dense.image_kernel == "k_fused8"
             cs = torch.empty((nb, 8, 8), dtype=torch.float64, device="cuda")

@@ -48,7 +48,7 @@ def test_fused8_sep_reference_parity(cuda, ref, name, w, k, kernel, wh):
     d = torch.from_numpy(img).cuda()
     nb = ((wd + 7) // 8) * ((h + 7) // 8)
     for pad in (0, 1):
-        plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad))
+        plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad), precision=P.Precision.kFp64Dmma)
         assert plan.image_kernel == kernel, name
         co = torch.empty((nb, 8, 8), dtype=torch.float64, device="cuda")
         out = plan.filter_image(d, co)
@@ -64,9 +64,9 @@ def test_fused8_sep_matches_replaced_kernels(cuda, name, w, k, kernel, monkeypat
     torch = cuda
     img = torch.from_numpy(synth.uniform_image(72, 2048, 512)).cuda()
     nb = 256 * 64
-    sep = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kReplicate)
+    sep = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
     monkeypatch.setenv("DCTF_NO_SEP", "1")
-    other = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kReplicate)
+    other = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
     monkeypatch.delenv("DCTF_NO_SEP")
     assert sep.image_kernel == "k_fused8_sep" and other.image_kernel in ("k_fused8_sym", "k_fused8")
     ca = torch.empty((nb, 8, 8), dtype=torch.float64, device="cuda")
@@ -84,7 +84,7 @@ def test_fused8_sep_motion_blur_frames(cuda, oracle):
     torch = cuda
     frames = np.stack([synth.sinusoid_image(80 + f, 272, 136) for f in range(3)])
     d = torch.from_numpy(frames).cuda()
-    plan = P.FilterPlan(P.Mask.rect(1, 9, synth.MOTION_1x9), 8, P.PaddingMode.kReplicate)
+    plan = P.FilterPlan(P.Mask.rect(1, 9, synth.MOTION_1x9), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
     assert plan.image_kernel == "k_fused8_sep"
     outs = P.filter_frames(d, [plan], [0, 0, 0])
     for f in range(3):
@@ -131,7 +131,7 @@ def test_coef8_sep_ragged_guarded(cuda, ref, nblocks):
     for seed, k, rank in ((11, 3, 1), (12, 3, 2), (13, 5, 3)):
         w = _rank_mask(seed, k, rank)
         for pad in (0, 1):
-            plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad))
+            plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad), precision=P.Precision.kFp64Dmma)
             dense = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad), precision=P.Precision.kFp64Dense)
             assert plan.coef_kernel == "k_coef8_sep" and dense.coef_kernel == "k_coef8", (rank, pad)
             guard = 40
@@ -154,7 +154,7 @@ def test_operator_set_round_trip_through_pairs(cuda, ref):
     torch = cuda
     w, k = ref.mask_preset("gaussian3")
     for n in (8, 16):
-        plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
         lefts, rights = plan.dct_set()
         rl, rr, merged = ref.plan_pairs(w, k, n, 1)
         assert merged and np.array_equal(lefts, rl) and np.array_equal(rights, rr), n

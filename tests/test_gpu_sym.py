@@ -51,17 +51,17 @@ def _masks(ref):
 @pytest.mark.gpu
 def test_kernel_selection(cuda, ref, monkeypatch):
     for name, w, k in _masks(ref):
-        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero).image_kernel == expected_n8_kernel(w, k), name
+        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma).image_kernel == expected_n8_kernel(w, k), name
         assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero,
                             precision=P.Precision.kFp64Dense).image_kernel == "k_fused8", name
         monkeypatch.setenv("DCTF_NO_SEP", "1")
-        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8_sym", name
+        assert P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma).image_kernel == "k_fused8_sym", name
         monkeypatch.delenv("DCTF_NO_SEP")
     w, _ = synth.random_mask(3, 3)   # rank 3, no parity structure: sandwich at n = 8, dense at 16
-    assert P.FilterPlan(P.Mask(3, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8_sep"
+    assert P.FilterPlan(P.Mask(3, w), 8, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma).image_kernel == "k_fused8_sep"
     assert P.FilterPlan(P.Mask(3, w), 16, P.PaddingMode.kZero).image_kernel == "k_fused16"
     w, _ = synth.random_mask(5, 5)   # rank 5: dense
-    assert P.FilterPlan(P.Mask(5, w), 8, P.PaddingMode.kZero).image_kernel == "k_fused8"
+    assert P.FilterPlan(P.Mask(5, w), 8, P.PaddingMode.kZero, precision=P.Precision.kFp64Dmma).image_kernel == "k_fused8"
 
 
 @pytest.mark.gpu
@@ -80,7 +80,7 @@ def test_sym_matches_reference_and_dense(cuda, ref, wh, nosep, monkeypatch):
     nb = ((wd + 7) // 8) * ((h + 7) // 8)
     for name, w, k in _masks(ref):
         for pad in (0, 1):
-            sym = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad))
+            sym = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad), precision=P.Precision.kFp64Dmma)
             dense = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode(pad), precision=P.Precision.kFp64Dense)
             cs = torch.empty((nb, 8, 8), dtype=torch.float64, device="cuda")
             cd = torch.empty_like(cs)
@@ -104,8 +104,8 @@ def test_sym_frames_and_pitch(cuda, ref):
     torch = cuda
     w, k = synth.gaussian_mask(5, 1.0), 5
     wr, _ = synth.random_mask(5, 5)
-    plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kReplicate)
-    plan_r = P.FilterPlan(P.Mask(5, wr), 8, P.PaddingMode.kReplicate)
+    plan = P.FilterPlan(P.Mask(k, w), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
+    plan_r = P.FilterPlan(P.Mask(5, wr), 8, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
     assert plan.image_kernel == "k_fused8_sep" and plan_r.image_kernel == "k_fused8"
     frames = np.stack([synth.sinusoid_image(40 + f, 264, 136) for f in range(4)])
     d = torch.from_numpy(frames).cuda()
@@ -143,7 +143,7 @@ def test_coef_sym_ragged_and_guarded(cuda, ref, n, nblocks):
     xh = rng.uniform(-500, 500, (nblocks, n, n))
     x = torch.from_numpy(xh).cuda()
     for w, k, kernel in cases:
-        plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        plan = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
         dense = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dense)
         assert plan.coef_kernel == kernel and dense.coef_kernel == f"k_coef{n}"
         guard = 40
@@ -226,9 +226,9 @@ def test_sep16_matches_sym16(cuda, n, monkeypatch):
     img = torch.from_numpy(synth.uniform_image(4, 2048, 1024)).cuda()
     nb = (2048 // 16) * (1024 // 16)
     for k, w in ((7, synth.gaussian_mask(7, 2.0)), (9, synth.motion_9x9()), (3, synth.LAPLACIAN3)):
-        sep = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        sep = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
         monkeypatch.setenv("DCTF_NO_SEP", "1")
-        sym = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate)
+        sym = P.FilterPlan(P.Mask(k, w), n, P.PaddingMode.kReplicate, precision=P.Precision.kFp64Dmma)
         monkeypatch.delenv("DCTF_NO_SEP")
         assert sep.image_kernel == "k_fused16_sep" and sym.image_kernel == "k_fused16_sym", k
         ca = torch.empty((nb, n, n), dtype=torch.float64, device="cuda")
