@@ -288,6 +288,12 @@ dctf_status dctf_measure_fp64_peak(int device, int mode, double* tflops);
  * DCTF_UNSUPPORTED). Synchronises the current device. */
 dctf_status dctf_diag_fallback_blocks(unsigned long long* n);
 
+/* Diagnostics: this device's INT8 tensor-core throughput (tera-ops/s,
+ * 2 ops per MAC) with back-to-back tcgen05.mma kind::i8 M128 N256 K32 from
+ * shared memory — the roofline denominator of k_fused8_q's tensor side.
+ * Synchronous; ~10 ms. */
+dctf_status dctf_measure_int8_peak(int device, double* tops);
+
 /* Number of kernels the last call on this host thread launched (bench
  * accounting of gpu_launches). */
 int dctf_last_launch_count(void);

@@ -7,4 +7,4 @@ Two checkers, both loaded with ctypes:
 Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
 import this package. The product package never does.
 """
-from .oracle import Oracle, Reference, reference_available  # noqa: F401
+from .oracle import LAPLACIAN3, MOTION_1x9, Gen, Oracle, Reference, reference_available  # noqa: F401

@@ -276,3 +276,44 @@ class Reference:
         buf = C.create_string_buffer(ln.value)
         self._chk(self.L.ref_format_plan_sets(_p(w), k, n, padding, buf, C.byref(ln)))
         return buf.raw[: ln.value].decode()
+
+
+class Gen:
+    """The BASELINE configs' seeded inputs (libgen.so, gen.cc) for the CPU
+    checkers and bench.py --impl reference, which must not load the product
+    package; pinned to paper_1710_07193_b200/csrc/synth.cc by tests/test_oracle.py."""
+
+    def __init__(self):
+        so = os.path.join(HERE, "libgen.so")
+        if not os.path.exists(so):
+            raise RuntimeError(f"{so} missing: run `make -C oracle`")
+        L = self.L = C.CDLL(so)
+        L.og_uniform_image.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_void_p]
+        L.og_sinusoid_image.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_int]
+        L.og_gaussian_mask.argtypes = [C.c_int, C.c_double, C.c_void_p]
+        L.og_random_mask.argtypes = [C.c_uint64, C.c_int, C.c_void_p]
+        L.og_random_mask.restype = C.c_int
+
+    def uniform_image(self, seed, w, h):
+        img = np.empty((h, w), np.uint8)
+        self.L.og_uniform_image(seed, w, h, img.ctypes.data)
+        return img
+
+    def sinusoid_image(self, seed, w, h, threads=None, out=None):
+        img = np.empty((h, w), np.uint8) if out is None else out
+        self.L.og_sinusoid_image(seed, w, h, img.ctypes.data, threads or os.cpu_count() or 1)
+        return img
+
+    def gaussian_mask(self, k, sigma):
+        w = np.empty(k * k)
+        self.L.og_gaussian_mask(k, sigma, w.ctypes.data)
+        return w
+
+    def random_mask(self, seed, k):
+        w = np.empty(k * k)
+        r = self.L.og_random_mask(seed, k, w.ctypes.data)
+        return w, int(r)
+
+
+LAPLACIAN3 = np.array([0, -1, 0, -1, 5, -1, 0, -1, 0], np.float64)
+MOTION_1x9 = np.full(9, 1.0 / 9.0)  # kr = 1, kc = 9

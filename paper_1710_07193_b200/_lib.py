@@ -64,6 +64,7 @@ _SIGS = {
     "dctf_convolve_blocks_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
     "dctf_filter_image_spatial_host": (_st, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_size_t]),
     "dctf_measure_fp64_peak": (_st, [C.c_int, C.c_int, _d]),
+    "dctf_measure_int8_peak": (_st, [C.c_int, _d]),
     "dctf_last_launch_count": (C.c_int, []),
     "dctf_diag_fallback_blocks": (_st, [C.POINTER(C.c_ulonglong)]),
     "dctf_filter_frames_host": (_st, [C.POINTER(_vp), C.c_int, _i, _vp, _vp, C.c_int, C.c_int, C.c_int,

@@ -730,3 +730,86 @@ extern "C" int dctf_qdbg_read(long long* out) {
   return cudaMemcpyFromSymbol(out, g_qdbg, sizeof(g_qdbg)) == cudaSuccess ? 0 : 1;
 }
 #endif
+
+// ---------------------------------------------------------------------------
+// In-run INT8 tensor-core peak (the roofline denominator of k_fused8_q's
+// tensor side; MEASURED_PEAKS.json has bf16 only): one CTA per SM, one thread
+// issuing back-to-back tcgen05.mma kind::i8 M128 N256 K32 from shared memory
+// into TMEM, the shape and operand path k_fused8_q uses.
+namespace {
+__global__ void __launch_bounds__(128, 1) k_peak_i8(int iters, int* sink) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = align1024(smem_raw);
+  __shared__ uint64_t done;
+  __shared__ uint32_t tb;
+  for (int i = threadIdx.x; i < (q8::ABYTES + q8::BBYTES) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(0x01010101u, 0, 0x01010101u, 0);
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tb)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = idesc_u8s8(128, 256);
+    const uint32_t sa = smem_u32(base), sb = smem_u32(base + q8::ABYTES);
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        mma_u8s8(tb + 256 * (it & 1), desc_sw128(sa + 32 * (ks & 1)), desc_sw128(sb + 32 * (ks & 1)), idesc,
+                 it > 1 || ks > 0);
+    mma_commit(&done);
+    mbar_wait(&done, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x < 32) {
+    int32_t v[32];
+    tmem_ld32(tb, v);
+    tmem_wait_ld();
+    if (v[0] == 0x7fffffff) sink[0] = v[1];
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512));
+  }
+}
+}  // namespace
+
+extern "C" dctf_status dctf_measure_int8_peak(int device, double* tops) {
+  if (!tops) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  const int smem = 1024 + q8::ABYTES + q8::BBYTES;
+  dctf_status s = dctf::ensure_dyn_smem(reinterpret_cast<const void*>(k_peak_i8), smem, "k_peak_i8");
+  int* sink = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  float best = 1e30f;
+  const int iters = 4096, ctas = dctf::sm_count(device);
+  if (s == DCTF_OK && (cudaMalloc(&sink, 4) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
+                       cudaEventCreate(&e1) != cudaSuccess))
+    s = set_error(DCTF_CUDA_ERROR, "int8 peak probe setup");
+  for (int rep = 0; rep < 4 && s == DCTF_OK; ++rep) {
+    cudaEventRecord(e0);
+    k_peak_i8<<<ctas, 128, smem>>>(iters, sink);
+    cudaEventRecord(e1);
+    if (cudaEventSynchronize(e1) != cudaSuccess) {
+      s = set_error(DCTF_CUDA_ERROR, "int8 peak probe");
+      break;
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0) best = std::min(best, ms);
+  }
+  if (s == DCTF_OK) *tops = 2.0 * 128 * 256 * 32 * 4.0 * iters * ctas / (best * 1e-3) / 1e12;
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaFree(sink);
+  cudaSetDevice(prev);
+  return s;
+}

@@ -178,3 +178,21 @@ def test_golden_fixtures(oracle):
         assert hashlib.sha256(co.tobytes()).hexdigest() == case["sha256_coef_out"], case["name"]
         if case.get("stored"):
             assert np.array_equal(out, data[case["name"] + "_u8"]), case["name"]
+
+
+def test_oracle_generators_match_product_synth():
+    """oracle/gen.cc (the inputs of bench.py --impl reference, which must not
+    load the product package) is byte-for-byte the product's synth.cc."""
+    from oracle import LAPLACIAN3, MOTION_1x9, Gen
+    from paper_1710_07193_b200 import synth
+    g = Gen()
+    for seed, w, h in ((0, 3840, 24), (63, 517, 333), (2, 4096, 8), (5, 64, 64)):
+        assert np.array_equal(g.sinusoid_image(seed, w, h, threads=3), synth.sinusoid_image(seed, w, h)), seed
+        assert np.array_equal(g.uniform_image(seed, w, h), synth.uniform_image(seed, w, h)), seed
+    for k, s in ((3, 1.0), (5, 1.0), (7, 2.0)):
+        assert np.array_equal(g.gaussian_mask(k, s), synth.gaussian_mask(k, s))
+    for seed, k in ((1003, 3), (1005, 5), (77, 7)):
+        a, ra = g.random_mask(seed, k)
+        b, rb = synth.random_mask(seed, k)
+        assert np.array_equal(a, b) and ra == rb
+    assert np.array_equal(LAPLACIAN3, synth.LAPLACIAN3) and np.array_equal(MOTION_1x9, synth.MOTION_1x9)
