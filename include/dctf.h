@@ -128,14 +128,21 @@ dctf_status dctf_plan_pairs(const dctf_plan* plan, int domain, double* h_lefts, 
  * were merged (OperatorSet::pairs.size(), ::symmetric_merged). */
 dctf_status dctf_plan_info(const dctf_plan* plan, int* n, int* npairs, int* symmetric_merged);
 
-/* Name of the kernel dctf_filter_image_u8 runs for this plan: "k_fused8",
- * "k_fused8_sym" (parity-class structure), "k_fused8_i8", "k_fused16" or
- * "unfused" (forward -> filter_coeffs -> inverse). NULL for a NULL plan. */
+/* Name of the kernel dctf_filter_image_u8 runs for this plan:
+ *   n = 8:  "k_fused8_q" (DCTF_PREC_FP64 default: exact-integer tcgen05
+ *           composed operator + reference-order fallback), "k_fused8_sep"
+ *           (separable sandwich, DMMA), "k_fused8_sym" (parity classes,
+ *           DMMA), "k_fused8" (dense DMMA), "k_fused8_i8" (INT8-exact digit
+ *           slices, DCTF_PREC_INT8_EXACT);
+ *   n = 16: "k_fused16_sep", "k_fused16_sym", "k_fused16";
+ *   "unfused" (forward -> filter_coeffs -> inverse; the split-precision modes).
+ * NULL for a NULL plan. */
 const char* dctf_plan_image_kernel(const dctf_plan* plan);
 
-/* Name of the kernel dctf_filter_coeffs runs for this plan: "k_coef8",
- * "k_coef8_sym" (parity-class structure), "k_coef16" or "k_coef_tf32x3".
- * NULL for a NULL plan. */
+/* Name of the kernel dctf_filter_coeffs runs for this plan: "k_coef8_sep" /
+ * "k_coef16_sep" (separable sandwich), "k_coef8_sym" / "k_coef16_sym"
+ * (parity-class structure), "k_coef8" / "k_coef16" (dense), "k_coef_tf32x3"
+ * or "k_coef_bf16x3" (split precision on tcgen05). NULL for a NULL plan. */
 const char* dctf_plan_coef_kernel(const dctf_plan* plan);
 
 /* Host-only operator compile (no device needed): the same compile

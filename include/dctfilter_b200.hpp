@@ -16,6 +16,16 @@
 //
 // There is no CPU compute path here: DctBasis and every transform dispatch to
 // the device; without a CUDA device, construction throws.
+//
+// Attribution: the host-side one-time construction in this header (the Mask
+// class with its fingerprint and presets, build_shift_matrix,
+// build_band_matrix, build_spatial_operator_set, to_dct_domain,
+// merge_symmetric) follows the dctfilter reference (mask.hpp:27-108,
+// operators.hpp:61-169), Copyright (c) the dctfilter project authors,
+// licensed under the Apache License, Version 2.0
+// (http://www.apache.org/licenses/LICENSE-2.0). Bit-identical operator sets
+// and identical exception text are the drop-in contract, so these sections
+// keep the reference's arithmetic order and messages.
 #pragma once
 
 #include <algorithm>

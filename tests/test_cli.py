@@ -114,6 +114,14 @@ def test_filter_image_paths_agree(tmp_path, cuda, ref):
 def test_verify_and_corrupt(cuda):
     r = run("verify", "--trials", "3", "--seed", "7", check_rc=0)
     assert "VERIFIED" in r.stdout
+    # the reference's 8 filter suites + symmetric-merge (dctfilter_main.cc:297-317, 353),
+    # in its line format; the correction suite is reported as out of scope
+    lines = r.stdout.splitlines()
+    suites = [ln for ln in lines if "max_float_err=" in ln]
+    assert len(suites) == 9 and suites[-1].startswith("symmetric-merge ")
+    err = float(suites[-1].split("max_float_err=")[1].split()[0])
+    assert err < 1e-9 and suites[-1].endswith("u8_mismatches=0")
+    assert any(ln.startswith("correction-identity") and "out of scope" in ln for ln in lines)
     run("verify", "--trials", "3", "--seed", "7", "--corrupt", check_rc=1)
 
 
