@@ -289,10 +289,14 @@ dctf_status dctf_plan_nan_check(const dctf_plan* plan, void* stream, int* nan_se
  * entry. */
 dctf_status dctf_measure_fp64_peak(int device, int mode, double* tflops);
 
-/* Diagnostics: blocks the k_fused8_q fallback warp recomputed in the
- * reference's operation order since the last call (process-wide; needs
- * DCTF_Q_COUNT=1 in the environment before the first filter call, else
- * DCTF_UNSUPPORTED). Synchronises the current device. */
+/* Diagnostics: blocks k_fused8_q flagged as uncertain (a pixel within the
+ * integer path's error bound of a .5 boundary) since the last call, and of
+ * those the ones the fallback resolved with the reference-order chain (the
+ * rest settled by its FP64 first stage). Process-wide; needs DCTF_Q_COUNT=1
+ * in the environment before the first filter call, else DCTF_UNSUPPORTED.
+ * Synchronises the current device; resets both counters. chain may be NULL. */
+dctf_status dctf_diag_fallback_counts(unsigned long long* flagged, unsigned long long* chain);
+/* The flagged count alone (same counters). */
 dctf_status dctf_diag_fallback_blocks(unsigned long long* n);
 
 /* Diagnostics: this device's INT8 tensor-core throughput (tera-ops/s,

@@ -820,6 +820,7 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
     cudaFree(p->d_gscale);
     cudaFree(p->d_kq);
     cudaFree(p->d_refchain);
+    cudaFree(p->d_kqt);
     cudaFree(p->d_nan);
     cudaFree(p->d_weights);
     cudaFree(p->io_in);

@@ -51,6 +51,8 @@ struct dctf_plan {
   double kq_flag_rate = 0.0;     // expected flagged-block fraction (uniform fractions)
   void* d_kq = nullptr;          // 16 KB digit image (SW64 K-major)
   double* d_refchain = nullptr;  // C | C^t | lefts | rights (mode 1)
+  double* d_kqt = nullptr;       // K in FP64, transposed (the fallback's first stage)
+  double kq_margin = 0.0;        // first-stage tie window (pixel units)
   int ref_mode = 0, ref_npairs = 0;
 
   // Device staging of the host-buffer entry (copy mode), guarded by io_mu.
@@ -153,6 +155,8 @@ struct KqInfo {
   int F = 0;
   uint32_t U = 0;
   double ebound = 0.0, flag_rate = 0.0;
+  double margin = 0.0;       // second-stage window: reference FP64 deviation + our FP64 dot error
+  std::vector<double> kt;    // the composed operator K in FP64, transposed (kt[j * 64 + i] = K[i][j])
 };
 bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info);
 void refchain_image(const dctf_plan& p, std::vector<double>& out, int& mode, int& npairs);

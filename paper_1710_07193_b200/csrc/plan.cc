@@ -1139,6 +1139,22 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
     put(4 * i + cs, 64, (cv + 1) / 2);
     put(4 * i + cs, 65, cv / 2);
   }
+  // Second stage (the fallback warp's first step on a flagged block): z_i =
+  // sum_j K_ij p_j in FP64 from K rounded to double, sequential FMAs. Its
+  // error is <= (64 + 1) 2^-53 * 255 * sum_j |K_ij| (< 2^-46 * 255 * mag); a
+  // pixel farther than that plus the reference's own FP64 deviation (the M
+  // of the first window: 2^-30 + 2^-36 * 255 * mag) from a .5 boundary rounds
+  // as the reference does. The rest go through the reference-order chain.
+  long double magmax = 0.0L;
+  for (int i = 0; i < nn; ++i) {
+    long double mag = 0.0L;
+    for (int j = 0; j < nn; ++j) mag += std::fabs(K[size_t(i) * nn + j]);
+    magmax = std::max(magmax, mag);
+  }
+  info.margin = static_cast<double>(std::ldexp(1.0L, -30) + (std::ldexp(1.0L, -36) + std::ldexp(1.0L, -44)) * 255.0L * magmax);
+  info.kt.assign(size_t(nn) * nn, 0.0);
+  for (int i = 0; i < nn; ++i)
+    for (int j = 0; j < nn; ++j) info.kt[size_t(j) * nn + i] = static_cast<double>(K[size_t(i) * nn + j]);
   info.ok = true;
   info.F = F;
   info.U = static_cast<uint32_t>(U);

@@ -32,21 +32,24 @@
 // so the per-block test is a running unsigned min.
 //
 // CTA = 15 warps, one CTA per SM (TMEM: 2 x 256 columns), persistent over
-// tiles of up to 128 horizontally adjacent blocks (one block row, 8 x 1024 px):
-//   warp 0      TMA: 4 boxes [8 rows x 256 px] per tile into a 6-stage raw ring
+// tiles of up to 128 horizontally adjacent blocks (one block row, 8 x 1024 px).
+// Roles in issue-priority order (highest warp id first):
+//   warp 14     MMA issuer: 3 x tcgen05.mma (M 128, N 256, K 32) per tile into
+//               a double-buffered TMEM accumulator.
+//   warp 13     TMA: 4 boxes [8 rows x 256 px] per tile into a 6-stage raw ring
 //               (48 KB of pixels in flight per SM); a 3-D tensor map covers
 //               the whole frame batch, out-of-range rows/columns read as 0.
-//   warp 1      MMA issuer: 2 x tcgen05.mma (M 128, N 256, K 32) per tile into
-//               a double-buffered TMEM accumulator.
-//   warps 2-5   converters: thread = block; the block's 8 pixel rows from the
+//   warps 9-12  converters: thread = block; the block's 8 pixel rows from the
 //               raw stage (tile()'s edge replication for ragged blocks) into the
-//               K-major 64-byte-swizzled A operand.
-//   warps 6-13  epilogue: two warps per TMEM lane quarter (pixel rows 0-3 /
-//               4-7); tcgen05.ld 32 columns = 8 whole pixels, the integer
-//               rounding above, cvt.pack.sat, 8-byte coalesced row stores.
+//               K-major 128-byte-swizzled A operand.
+//   warps 1-8   epilogue: two groups of four warps (one per TMEM lane
+//               quarter), group g drains accumulator buffer g (every other
+//               tile); thread = block: tcgen05.ld 32 columns = 8 whole pixels
+//               per pixel row, the integer rounding above, cvt.pack.sat,
+//               8-byte coalesced row stores.
 //               Blocks with an uncertain pixel are not stored here; they go
 //               to the fallback queue.
-//   warp 14     fallback: the reference-order chain on queued blocks (FP64).
+//   warp 0      fallback: the reference-order chain on queued blocks (FP64).
 // The plans' digit images (16 KB each, up to 4 plans: one launch covers a
 // whole multi-mask frame batch) stay resident in shared memory.
 #include <cuda.h>
@@ -69,18 +72,18 @@ using dctf::set_error;
 namespace {
 
 #ifdef QDBG
-// [cta < 4][tile < 64][event < 8] clock64 stamps of tiles QDBG_T0.. (instrumented build only)
+// [cta < 4][tile < 64][event < 12] clock64 stamps of tiles QDBG_T0.. (instrumented build only)
 #ifndef QDBG_T0
 #define QDBG_T0 0
 #endif
-__device__ long long g_qdbg[4][64][8];
+__device__ long long g_qdbg[4][64][12];
 #define QSTAMP(tl, ev)                                                                                  \
   do {                                                                                                  \
     if (blockIdx.x < 4 && (tl) >= QDBG_T0 && (tl) < QDBG_T0 + 64) g_qdbg[blockIdx.x][(tl)-QDBG_T0][(ev)] = clock64(); \
   } while (0)
 #define QSTAMP_EPI(tl, ev)                 \
   do {                                     \
-    if (b == 0 && part == 0) QSTAMP(tl, ev); \
+    if (b == 0) QSTAMP(tl, ev);              \
   } while (0)
 #else
 #define QSTAMP_EPI(tl, ev) \
@@ -100,21 +103,41 @@ constexpr int ABYTES = TILE * ROWB;        // one A stage
 constexpr int RAWB = 8 * TILE * 8;         // one raw stage: 8 rows x 1024 px
 constexpr int NRAW = 6, NA = 2;
 #ifndef Q8_EXP
-#define Q8_EXP 0  // measurement variants: 1 = epilogue without the pixel math, 3 = without stores
+#define Q8_EXP 0  // measurement variants: 1 = epilogue without the pixel math, 3 = without stores,
+                  // 5 = converters without pixel loads / A writes, 6 = no MMA (commit only),
+                  // 7 = no constant K-step (2 MMAs per tile), 9 = fallback blocks dequeued, not recomputed
 #endif
-#ifndef Q8_NPART
-#define Q8_NPART 2
-#endif
-constexpr int NPART = Q8_NPART;            // epilogue warps per TMEM lane quarter
-constexpr int W_TMA = 0, W_MMA = 1, W_CONV = 2, NCONV = 4, W_EPI = 6, NEPI = 4 * NPART, W_FB = W_EPI + NEPI;
-constexpr int THREADS = 32 * (W_FB + 1);
+// epilogue: two groups of 4 warps (one per TMEM lane quarter); group g
+// drains accumulator buffer g, i.e. every other tile of the CTA
+constexpr int NGRP = 2;
+// Warp roles, ordered by issue priority: an SM sub-partition's scheduler
+// picks the highest eligible warp id first, so the short, latency-critical
+// roles (MMA issue, TMA, the converters that feed the MMA, the fallback warp
+// that keeps the flagged-block queue short) sit above the ALU-heavy epilogue.
+constexpr int W_EPI = 0, NEPI = 4 * NGRP, W_FB = W_EPI + NEPI, W_CONV = W_FB + 1, NCONV = 4,
+              W_TMA = W_CONV + NCONV, W_MMA = W_TMA + 1;
+constexpr int THREADS = 32 * (W_MMA + 1);
 constexpr int FQ = 256;                    // fallback queue slots
 constexpr int SMEM = 1024 + KQ_MAX_PLANS * BBYTES + NA * ABYTES + NRAW * RAWB;
 }  // namespace q8
 
+// wait flavour per role (measurement switches): sleeping waits by default
+#ifdef Q8_SPIN_ALL
+#define Q8_WAIT_MMA mbar_wait
+#define Q8_WAIT_OTHER mbar_wait
+#elif defined(Q8_SPIN_MMA)
+#define Q8_WAIT_MMA mbar_wait
+#define Q8_WAIT_OTHER mbar_wait_sleep
+#else
+#define Q8_WAIT_MMA mbar_wait_sleep
+#define Q8_WAIT_OTHER mbar_wait_sleep
+#endif
+
 struct RefPlan {
   const double* chain;    // C | C^t | lefts | rights (mode 1)
   const double* weights;  // kr x kc (mode 2)
+  const double* kt;       // composed operator K in FP64, transposed
+  double margin;          // tie window of the FP64 first stage
   int mode, npairs, kr, kc, padding;
 };
 
@@ -258,10 +281,14 @@ __device__ __noinline__ void enqueue_fallback(unsigned long long* fq, uint32_t* 
   if (lane == 0) slot0 = atomicAdd(tail, static_cast<uint32_t>(__popc(flagged)));
   slot0 = __shfl_sync(0xFFFFFFFFu, slot0, 0);
   if (mine) {
-    const uint32_t slot = (slot0 + __popc(flagged & ((1u << lane) - 1u))) % q8::FQ;
-    volatile unsigned long long* qs = &fq[slot];
+    // entry = claim sequence number (high word: consumers claim slots out of
+    // order, so a ring slot may still hold the entry FQ claims earlier) |
+    // (tile << 7 | block) + 1 (low word, never 0; tiles < 2^24)
+    const uint32_t seq = slot0 + __popc(flagged & ((1u << lane) - 1u));
+    volatile unsigned long long* qs = &fq[seq % q8::FQ];
     while (*qs != 0ull) __nanosleep(64);  // ring full (pathological masks only)
-    *qs = (static_cast<unsigned long long>(ti) << 7 | static_cast<unsigned long long>(b)) + 1ull;
+    *qs = static_cast<unsigned long long>(seq) << 32 |
+          ((static_cast<unsigned long long>(ti) << 7 | static_cast<unsigned long long>(b)) + 1ull);
   }
 }
 
@@ -280,7 +307,7 @@ __device__ __forceinline__ double ref_mm(const double* a, const double* b, int i
   return acc;
 }
 
-__device__ void fallback_block(const RefPlan& rp, const uint8_t* img, size_t pitch, int w, int h, int y0, int x0,
+__device__ bool fallback_block(const RefPlan& rp, const uint8_t* img, size_t pitch, int w, int h, int y0, int x0,
                                uint8_t* dst, bool fast_out, double* sm, int* nan_flag, int lane) {
   double* sx = sm;        // X (pixels, then forward coefficients)
   double* st = sm + 64;   // products
@@ -293,6 +320,31 @@ __device__ void fallback_block(const RefPlan& rp, const uint8_t* img, size_t pit
   }
   __syncwarp();
   double z[2];
+  // First stage: z = K p in FP64 (error far below the reference's own); a
+  // block with no pixel within rp.margin of a .5 boundary is final here.
+  {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < 64; ++j) {
+      const double pj = sx[j];
+      a0 = fma(__ldg(rp.kt + j * 64 + lane), pj, a0);
+      a1 = fma(__ldg(rp.kt + j * 64 + lane + 32), pj, a1);
+    }
+    const double t0 = a0 + 0.5, t1 = a1 + 0.5;
+    const double f0 = t0 - floor(t0), f1 = t1 - floor(t1);
+    const bool tie = f0 < rp.margin || f0 > 1.0 - rp.margin || f1 < rp.margin || f1 > 1.0 - rp.margin;
+    if (!__any_sync(0xFFFFFFFFu, tie)) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int e = lane + 32 * q, r = e >> 3, c = e & 7;
+        const double t = floor(q ? t1 : t0);
+        const uint32_t v = static_cast<uint32_t>(fmin(fmax(t, 0.0), 255.0));
+        if (y0 + r < h && x0 + c < w) dst[static_cast<size_t>(r) * pitch + c] = static_cast<uint8_t>(v);
+      }
+      __syncwarp();
+      return false;
+    }
+  }
   if (rp.mode == 1) {
     const double* C = rp.chain;
     const double* Ct = rp.chain + 64;
@@ -352,6 +404,7 @@ __device__ void fallback_block(const RefPlan& rp, const uint8_t* img, size_t pit
   }
   __syncwarp();
   (void)fast_out;
+  return true;
 }
 
 template <bool TMA>
@@ -369,13 +422,24 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   __shared__ uint64_t raw_full[NRAW], raw_empty[NRAW], a_full[NA], a_empty[NA], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long fq[FQ];
-  __shared__ uint32_t fq_tail, fq_done;
+  __shared__ uint32_t fq_tail, fq_head, fq_done;
   __shared__ __align__(16) double fb_sm[256];
+  // per-frame plan index and per-plan epilogue constants, staged from the
+  // parameter bank (dynamically indexed constant loads miss the constant cache)
+  __shared__ uint8_t pof_s[KQ_MAX_FRAMES];
+  __shared__ uint32_t U_s[KQ_MAX_PLANS];
+  __shared__ int shS_s[KQ_MAX_PLANS], shL_s[KQ_MAX_PLANS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   pdl_trigger();
   for (int pi = 0; pi < args.nplans; ++pi) cta_copy_async(bsm + pi * BBYTES, args.bimg[pi], BBYTES);
   for (int i = threadIdx.x; i < FQ; i += blockDim.x) fq[i] = 0ull;
+  for (int i = threadIdx.x; i < nframes; i += blockDim.x) pof_s[i] = args.pof[i];
+  if (threadIdx.x < KQ_MAX_PLANS) {
+    U_s[threadIdx.x] = args.U[threadIdx.x];
+    shS_s[threadIdx.x] = args.shS[threadIdx.x];
+    shL_s[threadIdx.x] = args.shL[threadIdx.x];
+  }
   // A rows, bytes 64..127 (chunks 4-7, 128B-swizzled): the constant input
   // [1, 1, 0, ...] that adds the digits of the rounding offset 2^(F-1)
   // (plan.cc: layout_kq8, bytes 64-65 of the B rows) to the accumulators
@@ -401,9 +465,10 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 32 * NEPI);
+      mbar_init(&acc_empty[i], 32 * 4);  // the four warps of epilogue group i
     }
     fq_tail = 0;
+    fq_head = 0;
     fq_done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -427,6 +492,54 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     bx0 = static_cast<int>(rem - static_cast<uint32_t>(by) * static_cast<uint32_t>(ntx)) * TILE;
   };
 
+  // Consumer side of the flagged-block queue: claim entries in order (one
+  // atomic per claim), recompute each claimed block in the reference's
+  // operation order. Returns once every epilogue warp has finished and no
+  // claimed entry remains. Run by the fallback warp from the start, and by
+  // every other warp once the CTA's tiles are done.
+  auto drain = [&](double* scratch) {
+    uint32_t nap = 64;
+    while (true) {
+      uint32_t slot = 0;
+      if (lane == 0) slot = atomicAdd(&fq_head, 1u);
+      slot = __shfl_sync(0xFFFFFFFFu, slot, 0);
+      volatile unsigned long long* qs = &fq[slot % FQ];
+      unsigned long long e;
+      auto mine = [&](unsigned long long v) { return v != 0ull && static_cast<uint32_t>(v >> 32) == slot; };
+      while (!mine(e = *qs)) {
+        if (*reinterpret_cast<volatile uint32_t*>(&fq_done) == static_cast<uint32_t>(NEPI)) {
+          __threadfence_block();
+          if (mine(e = *qs)) break;
+          if (slot >= *reinterpret_cast<volatile uint32_t*>(&fq_tail)) return;
+        }
+        __nanosleep(nap);
+        nap = min(nap * 2u, 2048u);
+      }
+      nap = 64;
+      __syncwarp();
+      const unsigned long long code = (e & 0xFFFFFFFFull) - 1ull;
+      const long long ti = static_cast<long long>(code >> 7);
+      const int b = static_cast<int>(code & 127ull);
+      int f, by, bx0;
+      tile_at(ti, f, by, bx0);
+      const int y0 = by * 8, x0 = (bx0 + b) * 8;
+      const uint8_t* ib = in + f * frame_stride;
+      uint8_t* ob = out + f * frame_stride + static_cast<size_t>(y0) * pitch + x0;
+      bool chain = false;
+      if (Q8_EXP != 9)
+        chain = fallback_block(args.ref[pof_s[f]], ib, pitch, w, h, y0, x0, ob, fast_out, scratch, nan_flag, lane);
+      __syncwarp();
+      if (lane == 0) {
+        *qs = 0ull;
+        if (fb_count) {
+          atomicAdd(fb_count, 1ull);
+          if (chain) atomicAdd(fb_count + 1, 1ull);
+        }
+      }
+      __syncwarp();
+    }
+  };
+
   if (warp == W_TMA) {
     // ---------------- TMA producer: raw strips into the ring
     if (TMA && lane == 0) {
@@ -437,7 +550,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
         tile_at(ti, f, by, bx0);
         const int r = static_cast<int>(tl % NRAW);
         const uint32_t k = static_cast<uint32_t>(tl / NRAW);
-        mbar_wait(&raw_empty[r], (k & 1u) ^ 1u);
+        Q8_WAIT_OTHER(&raw_empty[r], (k & 1u) ^ 1u);
         QSTAMP(tl, 0);
         const int nbt = min(TILE, bw - bx0);
         const int nbox = (nbt * 8 + 255) >> 8;
@@ -453,24 +566,26 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
         int f, by, bx0;
         tile_at(ti, f, by, bx0);
-        const int pi = args.pof[f];
+        const int pi = pof_s[f];
         const int s = static_cast<int>(tl % NA);
         const int buf = static_cast<int>(tl & 1);
-        mbar_wait(&a_full[s], static_cast<uint32_t>((tl / NA) & 1));
+        QSTAMP(tl, 10);
+        Q8_WAIT_MMA(&a_full[s], static_cast<uint32_t>((tl / NA) & 1));
         QSTAMP(tl, 3);
-        mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
+        Q8_WAIT_MMA(&acc_empty[buf], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
         QSTAMP(tl, 4);
         tc_fence_after();
         const uint32_t sa = smem_u32(asm_ + s * ABYTES), sb = smem_u32(bsm + pi * BBYTES);
 #pragma unroll
         for (int ks = 0; ks < 3; ++ks)  // K = 64 pixel bytes + 32 constant bytes
-          mma_u8s8(tmem_base + 256 * buf, desc_sw128(sa + 32 * ks), desc_sw128(sb + 32 * ks), idesc, ks);
+          if (Q8_EXP != 6 && (Q8_EXP != 7 || ks < 2)) mma_u8s8(tmem_base + 256 * buf, desc_sw128(sa + 32 * ks), desc_sw128(sb + 32 * ks), idesc, ks);
         mma_commit(&acc_full[buf]);
         mma_commit(&a_empty[s]);
+        QSTAMP(tl, 8);
       }
     }
     __syncwarp();
-  } else if (warp < W_EPI) {
+  } else if (warp >= W_CONV) {
     // ---------------- converters: thread = block b of the tile
     const int b = threadIdx.x - 32 * W_CONV;
     long long tl = 0;
@@ -482,10 +597,12 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       uint2 row[8];
       if (TMA) {
         const int r = static_cast<int>(tl % NRAW);
-        mbar_wait(&raw_full[r], static_cast<uint32_t>((tl / NRAW) & 1));
+        Q8_WAIT_OTHER(&raw_full[r], static_cast<uint32_t>((tl / NRAW) & 1));
         if (b == 0) QSTAMP(tl, 1);
         const uint8_t* rs = raw + r * RAWB + (b >> 5) * 2048 + (b & 31) * 8;
-        if (b < nbt && x0 + 8 <= w && y0 + 8 <= h) {
+        if (Q8_EXP == 5) {
+          row[0] = row[1] = row[2] = row[3] = row[4] = row[5] = row[6] = row[7] = make_uint2(b, r);
+        } else if (b < nbt && x0 + 8 <= w && y0 + 8 <= h) {
 #pragma unroll
           for (int rr = 0; rr < 8; ++rr) row[rr] = *reinterpret_cast<const uint2*>(rs + rr * 256);
         } else if (b < nbt) {  // ragged block: tile()'s edge replication inside the strip
@@ -527,9 +644,9 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
         }
       }
       const int s = static_cast<int>(tl % NA);
-      mbar_wait(&a_empty[s], static_cast<uint32_t>(((tl / NA) & 1) ^ 1));
+      Q8_WAIT_OTHER(&a_empty[s], static_cast<uint32_t>(((tl / NA) & 1) ^ 1));
       if (b == 0) QSTAMP(tl, 2);
-      if (b < nbt) {
+      if (b < nbt && Q8_EXP != 5) {
         uint8_t* arow = asm_ + s * ABYTES + b * ROWB;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -538,89 +655,67 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&a_full[s]);
+      if (b == 0) QSTAMP(tl, 9);
     }
   } else if (warp < W_FB) {
-    // ---------------- epilogue: thread = block = TMEM lane; NPART warps per
-    // lane quarter, each 8 / NPART pixel rows (32 accumulator columns per row)
-    constexpr int ROWS = 8 / NPART;
-    const int qd = warp & 3, part = (warp - W_EPI) >> 2, b = 32 * qd + lane;
-    const uint32_t tla = tmem_base + (static_cast<uint32_t>(32 * qd) << 16) + 32 * ROWS * part;
-    long long tl = 0;
-    for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+    // ---------------- epilogue: thread = block = TMEM lane; group g (warps
+    // W_EPI + 4g .. + 3, one per lane quarter) drains accumulator buffer g,
+    // i.e. the CTA's tiles tl = g, g + 2, ...
+    const int qd = warp & 3, grp = (warp - W_EPI) >> 2, b = 32 * qd + lane;
+    const uint32_t col0 = tmem_base + (static_cast<uint32_t>(32 * qd) << 16) + 256 * grp;
+    long long tl = grp;
+    for (long long ti = blockIdx.x + static_cast<long long>(grp) * gridDim.x; ti < ntiles;
+         ti += NGRP * static_cast<long long>(gridDim.x), tl += NGRP) {
       int f, by, bx0;
       tile_at(ti, f, by, bx0);
-      const int pi = args.pof[f];
-      const uint32_t U = args.U[pi];
-      const int shS = args.shS[pi], shL = args.shL[pi];
-      const int buf = static_cast<int>(tl & 1);
-      const uint32_t col0 = tla + 256 * buf;
-      mbar_wait(&acc_full[buf], static_cast<uint32_t>((tl >> 1) & 1));
+      const int pi = pof_s[f];
+      const uint32_t U = U_s[pi];
+      const int shS = shS_s[pi], shL = shL_s[pi];
+      Q8_WAIT_OTHER(&acc_full[grp], static_cast<uint32_t>((tl >> 1) & 1));
       QSTAMP_EPI(tl, 5);
       tc_fence_after();
-      uint32_t words[2 * ROWS];
+      uint32_t words[16];
       uint32_t mn0 = 0xFFFFFFFFu, mn1 = 0xFFFFFFFFu;
       int32_t va[32], vb[32];
       // row r is processed while row r + 1 streams in from TMEM
-      if (shL == 0) epi_rows<ROWS, true>(col0, va, vb, shS, 0, U, mn0, mn1, words, &acc_empty[buf]);
-      else epi_rows<ROWS, false>(col0, va, vb, shS, shL, U, mn0, mn1, words, &acc_empty[buf]);
+      if (shL == 0) epi_rows<8, true>(col0, va, vb, shS, 0, U, mn0, mn1, words, &acc_empty[grp]);
+      else epi_rows<8, false>(col0, va, vb, shS, shL, U, mn0, mn1, words, &acc_empty[grp]);
       QSTAMP_EPI(tl, 6);
-      // A block with an uncertain pixel in this warp's rows: those rows are
-      // left to the fallback warp (which rewrites the whole block; the other
-      // rows it writes carry the same bytes as the certain ones stored here).
+      // A block with an uncertain pixel is left to the fallback warp, which
+      // recomputes and writes the whole block.
       const int nbt = min(TILE, bw - bx0);
       const bool valid = b < nbt;
       const bool unsure = valid && min(mn0, mn1) < 2u * U;
-      const int y0 = by * 8 + ROWS * part, x0 = (bx0 + b) * 8;
+      const int y0 = by * 8, x0 = (bx0 + b) * 8;
       uint8_t* ob = out + f * frame_stride + static_cast<size_t>(y0) * pitch + x0;
       if (valid && !unsure && Q8_EXP != 3) {
-        if (fast_out && x0 + 8 <= w && y0 + ROWS <= h) {
+        if (fast_out && x0 + 8 <= w && y0 + 8 <= h) {
 #pragma unroll
-          for (int k = 0; k < ROWS; ++k)
+          for (int k = 0; k < 8; ++k)
             *reinterpret_cast<uint2*>(ob + static_cast<size_t>(k) * pitch) = make_uint2(words[2 * k], words[2 * k + 1]);
         } else {
-          store_ragged<ROWS>(ob, pitch, words, h - y0, w - x0);
+          store_ragged<8>(ob, pitch, words, h - y0, w - x0);
         }
       }
       const uint32_t flagged = __ballot_sync(0xFFFFFFFFu, unsure);
       if (flagged) enqueue_fallback(fq, &fq_tail, flagged, unsure, lane, ti, b);
+      QSTAMP_EPI(tl, 7);
     }
     __threadfence_block();
     __syncwarp();
     if (lane == 0) atomicAdd(&fq_done, 1u);
-    QSTAMP_EPI(tl, 7);
   } else {
     // ---------------- fallback warp: reference-order chain on queued blocks
-    uint32_t head = 0;
-    while (true) {
-      volatile unsigned long long* qs = &fq[head % FQ];
-      unsigned long long e = *qs;
-      if (e == 0ull) {
-        if (*reinterpret_cast<volatile uint32_t*>(&fq_done) == static_cast<uint32_t>(NEPI)) {
-          __threadfence_block();
-          e = *qs;
-          if (e == 0ull) break;
-        } else {
-          __nanosleep(1024);
-          continue;
-        }
-      }
-      __syncwarp();
-      const long long ti = static_cast<long long>((e - 1ull) >> 7);
-      const int b = static_cast<int>((e - 1ull) & 127ull);
-      int f, by, bx0;
-      tile_at(ti, f, by, bx0);
-      const int y0 = by * 8, x0 = (bx0 + b) * 8;
-      const uint8_t* ib = in + f * frame_stride;
-      uint8_t* ob = out + f * frame_stride + static_cast<size_t>(y0) * pitch + x0;
-      fallback_block(args.ref[args.pof[f]], ib, pitch, w, h, y0, x0, ob, fast_out, fb_sm, nan_flag, lane);
-      __syncwarp();
-      if (lane == 0) {
-        *qs = 0ull;
-        if (fb_count) atomicAdd(fb_count, 1ull);
-      }
-      ++head;
-      __syncwarp();
-    }
+    drain(fb_sm);
+  }
+  if (warp != W_FB) {
+    // Every tile of this CTA is done once all 14 other warps get here (the
+    // epilogue waited for the last MMA, the converters consumed every raw
+    // stage): the rest of the queue is drained by all warps in parallel, each
+    // with 2 KB of scratch in the now idle raw ring.
+    asm volatile("bar.sync 1, %0;" ::"n"(THREADS - 32) : "memory");
+    const int slot = warp < W_FB ? warp : warp - 1;
+    drain(reinterpret_cast<double*>(raw + slot * 2048));
   }
   tc_fence_before();
   __syncthreads();
@@ -639,7 +734,7 @@ static unsigned long long* fallback_counter() {
   static unsigned long long* c = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
-    if (std::getenv("DCTF_Q_COUNT") && cudaMalloc(&c, 8) == cudaSuccess) cudaMemset(c, 0, 8);
+    if (std::getenv("DCTF_Q_COUNT") && cudaMalloc(&c, 16) == cudaSuccess) cudaMemset(c, 0, 16);
   });
   return c;
 }
@@ -655,12 +750,16 @@ dctf_status upload_kq_operator(dctf_plan* p) {
   if (e == cudaSuccess) e = cudaMalloc(&p->d_refchain, chain.size() * sizeof(double));
   if (e == cudaSuccess)
     e = cudaMemcpy(p->d_refchain, chain.data(), chain.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_kqt, info.kt.size() * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->d_kqt, info.kt.data(), info.kt.size() * sizeof(double), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("kq operator upload: ") + cudaGetErrorString(e));
   p->kq = true;
   p->kq_F = info.F;
   p->kq_U = info.U;
   p->kq_ebound = info.ebound;
   p->kq_flag_rate = info.flag_rate;
+  p->kq_margin = info.margin;
   return DCTF_OK;
 }
 
@@ -684,7 +783,8 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
     args.U[i] = p->kq_U;
     args.shS[i] = p->kq_F - 16;
     args.shL[i] = 32 - p->kq_F;
-    args.ref[i] = RefPlan{p->d_refchain, p->d_weights, p->ref_mode, p->ref_npairs, p->kr, p->kc, p->padding};
+    args.ref[i] = RefPlan{p->d_refchain, p->d_weights, p->d_kqt, p->kq_margin, p->ref_mode, p->ref_npairs, p->kr,
+                          p->kc, p->padding};
   }
   for (int f = 0; f < nframes; ++f) args.pof[f] = static_cast<uint8_t>(plan_of_frame ? plan_of_frame[f] : 0);
   const bool tma = !host_mapped && (pitch & 15) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
@@ -714,16 +814,22 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
 
 }  // namespace dctf
 
-extern "C" dctf_status dctf_diag_fallback_blocks(unsigned long long* n) {
-  if (!n) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
-  *n = 0;
+extern "C" dctf_status dctf_diag_fallback_counts(unsigned long long* flagged, unsigned long long* chain) {
+  if (!flagged) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
+  *flagged = 0;
+  if (chain) *chain = 0;
   unsigned long long* c = dctf::fallback_counter();
   if (!c) return set_error(DCTF_UNSUPPORTED, "set DCTF_Q_COUNT=1 before the first filter call");
-  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(n, c, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
-      cudaMemset(c, 0, 8) != cudaSuccess)
+  unsigned long long v[2] = {0, 0};
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(v, c, 16, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemset(c, 0, 16) != cudaSuccess)
     return set_error(DCTF_CUDA_ERROR, "fallback counter read failed");
+  *flagged = v[0];
+  if (chain) *chain = v[1];
   return DCTF_OK;
 }
+
+extern "C" dctf_status dctf_diag_fallback_blocks(unsigned long long* n) { return dctf_diag_fallback_counts(n, nullptr); }
 
 #ifdef QDBG
 extern "C" int dctf_qdbg_read(long long* out) {

@@ -306,13 +306,21 @@ class FilterPlan:
         return h.reshape(nn, nn)
 
     # -- batched device entry points -------------------------------------
+    def _check_device(self, t):
+        """The C entry points switch to the plan's device and take the stream of
+        the tensor's device: a tensor on another GPU would be read there
+        without ordering, so it is rejected."""
+        if t.device.index != self._device:
+            raise InvalidArgument(f"tensor is on cuda:{t.device.index}, the plan on cuda:{self._device}")
+        return t
+
     def _check_blocks(self, t):
         import torch
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
             raise InvalidArgument("expected a CUDA float64 tensor of blocks")
         if t.dim() != 3 or t.shape[1] != self._n or t.shape[2] != self._n:
             raise InvalidArgument("apply: block side does not match operator set")
-        return t.contiguous()
+        return self._check_device(t).contiguous()
 
     def filter_coeffs(self, coeffs):
         """DCT coefficients in, filtered DCT coefficients out: (B, n, n) fp64."""
@@ -330,7 +338,7 @@ class FilterPlan:
     def forward_image(self, img):
         """tile() + forward_2d over a (h, w) uint8 CUDA tensor -> (B, n, n) fp64."""
         import torch
-        img = _check_image(img)
+        img = self._check_device(_check_image(img))
         h, w = img.shape
         n = self._n
         nb = ((w + n - 1) // n) * ((h + n - 1) // n)
@@ -368,16 +376,17 @@ class FilterPlan:
     def filter_image(self, img, coeffs_out=None):
         """Fused whole-image DCT path on a (h, w) uint8 CUDA tensor."""
         import torch
-        img = _check_image(img)
+        img = self._check_device(_check_image(img))
         h, w = img.shape
         out = _empty_pitched(img)
         cp = 0
         if coeffs_out is not None:
             n = self._n
             nb = ((w + n - 1) // n) * ((h + n - 1) // n)
-            if (coeffs_out.dtype != torch.float64 or not coeffs_out.is_contiguous()
-                    or coeffs_out.numel() != nb * n * n):
-                raise InvalidArgument("coeffs_out must be a contiguous fp64 (B, n, n) tensor")
+            if (not isinstance(coeffs_out, torch.Tensor) or coeffs_out.dtype != torch.float64
+                    or not coeffs_out.is_contiguous() or coeffs_out.numel() != nb * n * n
+                    or coeffs_out.device != img.device):
+                raise InvalidArgument("coeffs_out must be a contiguous fp64 (B, n, n) tensor on the image's device")
             cp = _dptr(coeffs_out)
         check(_lib.lib.dctf_filter_image_u8(self._h, _dptr(img), _dptr(out), w, h, img.stride(0),
                                             cp or None, _stream(img.device)))
@@ -387,7 +396,7 @@ class FilterPlan:
         """Spatial path (Domain::kSpatial): convolve per block, bit-identical to
         the reference's samples, then quantize (image.hpp:219-222)."""
         import torch
-        img = _check_image(img)
+        img = self._check_device(_check_image(img))
         h, w = img.shape
         out = _empty_pitched(img)
         check(_lib.lib.dctf_filter_image_spatial_u8(self._h, _dptr(img), _dptr(out), w, h,
@@ -506,9 +515,10 @@ def filter_image(img, mask: Mask, padding: PaddingMode, path: Domain = Domain.kD
     return plan.filter_image(img)
 
 
-def filter_frames(frames, plans: Sequence[FilterPlan], plan_of_frame: Sequence[int]):
+def filter_frames(frames, plans: Sequence[FilterPlan], plan_of_frame: Sequence[int], out=None):
     """Video batch: frames (F, h, w) uint8 CUDA tensor; frame f uses
-    plans[plan_of_frame[f]] (dctf_filter_frames_u8)."""
+    plans[plan_of_frame[f]] (dctf_filter_frames_u8). ``out``: optional
+    preallocated result of the same shape on the same device."""
     import torch
     if not (isinstance(frames, torch.Tensor) and frames.is_cuda and frames.dtype == torch.uint8
             and frames.dim() == 3 and frames.is_contiguous()):
@@ -516,7 +526,13 @@ def filter_frames(frames, plans: Sequence[FilterPlan], plan_of_frame: Sequence[i
     f, h, w = frames.shape
     if len(plan_of_frame) != f:
         raise InvalidArgument("plan_of_frame must have one entry per frame")
-    out = torch.empty_like(frames)
+    for p in plans:
+        p._check_device(frames)
+    if out is None:
+        out = torch.empty_like(frames)
+    elif not (isinstance(out, torch.Tensor) and out.shape == frames.shape and out.dtype == torch.uint8
+              and out.device == frames.device and out.is_contiguous()):
+        raise InvalidArgument("out must be a contiguous uint8 tensor shaped like frames, on their device")
     handles = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
     idx = (C.c_int * f)(*[int(i) for i in plan_of_frame])
     check(_lib.lib.dctf_filter_frames_u8(handles, len(plans), idx, _dptr(frames), _dptr(out), f, w,
