@@ -34,22 +34,24 @@
 // CTA = 15 warps, one CTA per SM (TMEM: 2 x 256 columns), persistent over
 // tiles of up to 128 horizontally adjacent blocks (one block row, 8 x 1024 px).
 // Roles in issue-priority order (highest warp id first):
-//   warp 14     MMA issuer: 3 x tcgen05.mma (M 128, N 256, K 32) per tile into
-//               a double-buffered TMEM accumulator.
+//   warp 14     MMA issuer: the whole warp runs the loop, one elected lane
+//               issues the tile's 3 x tcgen05.mma (M 128, N 256, K 32) and two
+//               commits in one asm block, into a double-buffered accumulator.
 //   warp 13     TMA: 4 boxes [8 rows x 256 px] per tile into a 6-stage raw ring
 //               (48 KB of pixels in flight per SM); a 3-D tensor map covers
 //               the whole frame batch, out-of-range rows/columns read as 0.
 //   warps 9-12  converters: thread = block; the block's 8 pixel rows from the
 //               raw stage (tile()'s edge replication for ragged blocks) into the
 //               K-major 128-byte-swizzled A operand.
-//   warps 1-8   epilogue: two groups of four warps (one per TMEM lane
+//   warp 8      fallback: flagged blocks from the CTA's queue (FP64 first
+//               stage, reference-order chain for near-ties); after the last
+//               tile every warp drains what is left.
+//   warps 0-7   epilogue: two groups of four warps (one per TMEM lane
 //               quarter), group g drains accumulator buffer g (every other
 //               tile); thread = block: tcgen05.ld 32 columns = 8 whole pixels
 //               per pixel row, the integer rounding above, cvt.pack.sat,
-//               8-byte coalesced row stores.
-//               Blocks with an uncertain pixel are not stored here; they go
-//               to the fallback queue.
-//   warp 0      fallback: the reference-order chain on queued blocks (FP64).
+//               8-byte coalesced row stores. Blocks with an uncertain pixel
+//               are not stored here; they go to the fallback queue.
 // The plans' digit images (16 KB each, up to 4 plans: one launch covers a
 // whole multi-mask frame batch) stay resident in shared memory.
 #include <cuda.h>
@@ -559,30 +561,33 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       }
     }
   } else if (warp == W_MMA) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_u8s8(128, 256);
-      long long tl = 0;
-      for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
-        int f, by, bx0;
-        tile_at(ti, f, by, bx0);
-        const int pi = pof_s[f];
-        const int s = static_cast<int>(tl % NA);
-        const int buf = static_cast<int>(tl & 1);
-        QSTAMP(tl, 10);
-        Q8_WAIT_MMA(&a_full[s], static_cast<uint32_t>((tl / NA) & 1));
-        QSTAMP(tl, 3);
-        Q8_WAIT_MMA(&acc_empty[buf], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
-        QSTAMP(tl, 4);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(asm_ + s * ABYTES), sb = smem_u32(bsm + pi * BBYTES);
-#pragma unroll
-        for (int ks = 0; ks < 3; ++ks)  // K = 64 pixel bytes + 32 constant bytes
-          if (Q8_EXP != 6 && (Q8_EXP != 7 || ks < 2)) mma_u8s8(tmem_base + 256 * buf, desc_sw128(sa + 32 * ks), desc_sw128(sb + 32 * ks), idesc, ks);
-        mma_commit(&acc_full[buf]);
-        mma_commit(&a_empty[s]);
-        QSTAMP(tl, 8);
-      }
+    constexpr uint32_t idesc = idesc_u8s8(128, 256);
+    const uint64_t da0 = desc_sw128(smem_u32(asm_)), db0 = desc_sw128(smem_u32(bsm));
+    constexpr uint64_t DA_STAGE = ABYTES >> 4, DB_PLAN = BBYTES >> 4;
+    const uint32_t acc_full0 = smem_u32(&acc_full[0]), a_empty0 = smem_u32(&a_empty[0]);
+    long long tl = 0;
+    for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+      int f, by, bx0;
+      tile_at(ti, f, by, bx0);
+      const int pi = pof_s[f];
+      const int s = static_cast<int>(tl % NA);
+      const int buf = static_cast<int>(tl & 1);
+      Q8_WAIT_MMA(&a_full[s], static_cast<uint32_t>((tl / NA) & 1));
+      Q8_WAIT_MMA(&acc_empty[buf], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
+      tc_fence_after();
+      const uint64_t da = da0 + DA_STAGE * s, db = db0 + DB_PLAN * pi;
+      const uint32_t dt = tmem_base + 256 * buf;
+      asm volatile(
+          "{\n\t.reg .pred e;\n\t"
+          "elect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %4, %5, %3, 1;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %6, %7, %3, 1;\n\t"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}"
+          ::"r"(dt), "l"(da), "l"(db), "r"(idesc), "l"(da + 2), "l"(db + 2), "l"(da + 4), "l"(db + 4),
+          "r"(acc_full0 + 8u * buf), "r"(a_empty0 + 8u * s)
+          : "memory");
     }
     __syncwarp();
   } else if (warp >= W_CONV) {
