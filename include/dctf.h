@@ -256,12 +256,16 @@ dctf_status dctf_filter_frames_u8_multi(const dctf_multi* const* plans, int npla
                                         int height, size_t pitch, size_t frame_stride, uint8_t* const* d_gather,
                                         void* const* streams);
 
-/* End-to-end host-buffer entry (the reference's filter_image signature):
- * copies h_in to the device, filters, copies back into h_out, in chunks of
- * block rows pipelined over two streams so PCIe transfers overlap the
- * kernel. Synchronous. Pinned (cudaHostAlloc'd) buffers run at full PCIe
- * speed; pageable ones work. Returns DCTF_NAN_ENCOUNTERED like
- * quantize_sample would throw. */
+/* End-to-end host-buffer entry (the reference's filter_image signature).
+ * Synchronous; returns DCTF_NAN_ENCOUNTERED where quantize_sample would
+ * throw. Plans on k_fused8_q (n = 8 FP64) and the split-precision plans:
+ * bands of whole block rows (~16 MiB) stream through a per-call 3-slot device
+ * ring, H2D copy / kernel / D2H copy of consecutive bands overlapped on the
+ * calling thread's three streams (no plan lock; concurrent callers overlap).
+ * Other plans: pinned (cudaHostAlloc'd, mapped) buffers are read and written
+ * by the fused kernel itself over PCIe (zero-copy); pageable buffers go
+ * through pinned bounce buffers filled and drained by host threads; these
+ * modes use plan-owned staging under a per-plan lock. */
 dctf_status dctf_filter_image_host(const dctf_plan* plan, const uint8_t* h_in, uint8_t* h_out,
                                    int width, int height, size_t pitch);
 
@@ -278,8 +282,20 @@ dctf_status dctf_filter_coeffs_host(const dctf_plan* plan, const double* h_in, d
 dctf_status dctf_convolve_blocks_host(const dctf_plan* plan, const double* h_blocks, double* h_out,
                                       size_t nblocks);
 
-/* Synchronises `stream`, reads and clears the plan's NaN flag; *nan_seen is
- * 1 if any quantised sample was NaN since the last check. */
+/* NaN reporting (quantize_sample throws on NaN, spatial.hpp:71-75). The
+ * device-buffer entries (dctf_filter_image_u8, dctf_filter_frames_u8,
+ * dctf_inverse_u8, dctf_filter_image_spatial_u8) run asynchronously and set
+ * the plan's NaN flag (a frame batch: its first plan's); this call
+ * synchronises `stream`, reads and clears that flag: *nan_seen is 1 if any
+ * quantised sample was NaN since the last check. The flag is one word per
+ * plan: concurrent device-entry callers on one plan share it. The host-buffer
+ * entries (dctf_filter_image_host, dctf_filter_frames_host, their _multi
+ * forms, dctf_filter_image_spatial_host) use a per-call flag instead and
+ * return DCTF_NAN_ENCOUNTERED themselves.
+ * A NaN can only arise for masks whose reference chain overflows FP64 (huge
+ * weights); such plans run the reference's own operation order on the image
+ * path (dctf_plan_image_kernel: "k_refchain8" at n = 8, "unfused" at n = 16),
+ * so NaN arises where the reference's does. */
 dctf_status dctf_plan_nan_check(const dctf_plan* plan, void* stream, int* nan_seen);
 
 /* Diagnostics: measures this device's FP64 peak with a throughput

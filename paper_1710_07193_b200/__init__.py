@@ -7,7 +7,8 @@ the Python mirror of the reference's C++ API over that ABI.
 """
 from . import _lib  # noqa: F401  (fails loudly if the CUDA library is missing)
 from .dctfilter import (  # noqa: F401
-    DctBasis, Domain, FilterPlan, InvalidArgument, Mask, MultiPlan, PaddingMode, Precision, Unsupported,
+    DctBasis, Domain, FilterPlan, InvalidArgument, Mask, MultiPlan, NanEncountered, PaddingMode, Precision,
+    Unsupported,
     filter_frames, filter_frames_host, filter_image, format_operator_dump, forward_2d, inverse_2d,
     operator_from_dump, row_symmetric)
 

@@ -42,6 +42,10 @@ dctf_status set_error(dctf_status s, const std::string& msg) {
   return s;
 }
 void add_launches(int k) { t_launches += k; }
+thread_local int* t_nan = nullptr;
+int* nan_flag(const dctf_plan* p) { return t_nan ? t_nan : p->d_nan; }
+NanScope::NanScope(int* f) : prev(t_nan) { t_nan = f; }
+NanScope::~NanScope() { t_nan = prev; }
 void reset_launches() { t_launches = 0; }
 }  // namespace dctf
 
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(256) k_spatial(const uint8_t* __restrict__ img
                                                  size_t pitch, int bw, const double* __restrict__ blocks,
                                                  uint8_t* __restrict__ out_img, double* __restrict__ out_blocks,
                                                  long long nblocks, int n, const double* __restrict__ wts,
-                                                 int kr, int kc, int replicate) {
+                                                 int kr, int kc, int replicate, int* nan_flag) {
   __shared__ double ws[1024];
   for (int i = threadIdx.x; i < kr * kc && i < 1024; i += blockDim.x) ws[i] = wts[i];
   __syncthreads();
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(256) k_spatial(const uint8_t* __restrict__ img
   }
   if (U8) {
     const int y = by * n + i, x = bx * n + j;
-    if (y < h && x < w) out_img[static_cast<size_t>(y) * pitch + x] = static_cast<uint8_t>(quantize(acc, nullptr));
+    if (y < h && x < w) out_img[static_cast<size_t>(y) * pitch + x] = static_cast<uint8_t>(quantize(acc, nan_flag));
   } else {
     out_blocks[blk * nn + i * n + j] = acc;
   }
@@ -438,7 +442,7 @@ dctf_status launch_transform_n(const dctf_plan* p, const uint8_t* img_in, uint8_
   BasisParam<N> bp;
   std::copy(p->basis.begin(), p->basis.begin() + N * N, bp.c);
   kernel<<<static_cast<unsigned>(grid), 256, TrCfg<N>::SMEM, st>>>(img_in, img_out, w, h, pitch, bw, bin,
-                                                                   bout, nb, bp, p->d_nan);
+                                                                   bout, nb, bp, nan_flag(p));
   add_launches(1);
   CUDA_TRY(cudaGetLastError());
   return DCTF_OK;
@@ -609,10 +613,20 @@ dctf_status finish_plan(dctf_plan* p, dctf_plan** out) {
       return s;
     }
   }
+  // Masks whose reference chain can overflow FP64 (chain_bounded): the image
+  // path runs the reference's own operation order instead (see dctf_plan).
+  p->unbounded = !dctf::chain_bounded(*p);
+  if (p->unbounded && n == 8) {
+    const dctf_status s = dctf::upload_refchain_only(p);
+    if (s != DCTF_OK) {
+      dctf_plan_destroy(p);
+      return s;
+    }
+  }
   // n = 8 FP64 plans: the exact-integer composed-operator kernel serves the
   // u8 image path (coefficient requests keep the FP64 kernels); DCTF_NO_Q=1
   // at plan creation opts out.
-  if (precision == DCTF_PREC_FP64 && n == 8 && !std::getenv("DCTF_NO_Q")) {
+  if (precision == DCTF_PREC_FP64 && n == 8 && !p->unbounded && !std::getenv("DCTF_NO_Q")) {
     const dctf_status s = dctf::upload_kq_operator(p);
     if (s != DCTF_OK) {
       dctf_plan_destroy(p);
@@ -638,7 +652,7 @@ dctf_status filter_frames_device(const dctf_plan* const* plans, int nplans, cons
   for (int i = 0; i < nplans && all_kq; ++i) all_kq = plans[i]->kq;
   if (all_kq)
     return dctf::launch_fused8_q(plans, nplans, h_plan_of_frame, d_in, d_out, w, h, pitch,
-                                 static_cast<long long>(frame_stride), nframes, st, false, nullptr);
+                                 static_cast<long long>(frame_stride), nframes, st, false, nan_flag(plans[0]));
   // Frames sharing a plan and evenly spaced go in one launch (round-robin
   // assignment -> one launch per plan); anything else falls back per frame.
   for (int pi = 0; pi < nplans && s == DCTF_OK; ++pi) {
@@ -855,6 +869,7 @@ const char* dctf_plan_coef_kernel(const dctf_plan* p) {
 
 const char* dctf_plan_image_kernel(const dctf_plan* p) {
   if (!p) return nullptr;
+  if (p->unbounded) return p->n == 8 ? "k_refchain8" : "unfused";
   if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT) return "k_fused8_i8";
   if (p->kq) return "k_fused8_q";
   if (p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3) return "unfused";
@@ -965,7 +980,7 @@ dctf_status dctf_filter_image_spatial_u8(const dctf_plan* p, const uint8_t* d_in
   if (!dctf::launch_spatial_rows(p, d_in, w, h, pitch, bw, nullptr, d_out, nullptr, nb, as_stream(stream))) {
     const unsigned grid = static_cast<unsigned>((nb * n * n + 255) / 256);
     k_spatial<true><<<grid, 256, 0, as_stream(stream)>>>(d_in, w, h, pitch, bw, nullptr, d_out, nullptr, nb, n,
-                                                         p->d_weights, p->kr, p->kc, p->padding);
+                                                         p->d_weights, p->kr, p->kc, p->padding, dctf::nan_flag(p));
   }
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
@@ -986,7 +1001,7 @@ dctf_status dctf_convolve_blocks(const dctf_plan* p, const double* d_blocks, dou
   if (!dctf::launch_spatial_rows(p, nullptr, 0, 0, 0, 1, d_blocks, nullptr, d_out, nb, as_stream(stream))) {
     const unsigned grid = static_cast<unsigned>((nb * n * n + 255) / 256);
     k_spatial<false><<<grid, 256, 0, as_stream(stream)>>>(nullptr, 0, 0, 0, 1, d_blocks, nullptr, d_out, nb, n,
-                                                          p->d_weights, p->kr, p->kc, p->padding);
+                                                          p->d_weights, p->kr, p->kc, p->padding, dctf::nan_flag(p));
   }
   dctf::add_launches(1);
   CUDA_TRY(cudaGetLastError());
@@ -1095,7 +1110,11 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
       mode = m;
   }
   if (mode == 1) dpitch = pitch;
-  if (p->n != 8) CUDA_TRY(cudaMemsetAsync(p->d_nan, 0, sizeof(int), s_run));
+  // per-call NaN flag (the plan's own flag belongs to the device entries)
+  int* d_flag = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_flag), sizeof(int), s_run));
+  CUDA_TRY(cudaMemsetAsync(d_flag, 0, sizeof(int), s_run));
+  dctf::NanScope nan_scope(d_flag);
   const int n = p->n, bh = (h + n - 1) / n;
   int launches = 0;
   if (mode == 2) {
@@ -1191,10 +1210,8 @@ dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint
     }
   }
   int nan_seen = 0;
-  if (s == DCTF_OK && p->n != 8) {
-    CUDA_TRY(cudaStreamSynchronize(s_run));
-    CUDA_TRY(cudaMemcpyAsync(&nan_seen, p->d_nan, sizeof(int), cudaMemcpyDeviceToHost, s_run));
-  }
+  CUDA_TRY(cudaMemcpyAsync(&nan_seen, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s_run));
+  cudaFreeAsync(d_flag, s_run);
   CUDA_TRY(cudaStreamSynchronize(s_in));
   CUDA_TRY(cudaStreamSynchronize(s_run));
   CUDA_TRY(cudaStreamSynchronize(s_out));
@@ -1269,16 +1286,24 @@ dctf_status dctf_filter_image_spatial_host(const dctf_plan* p, const uint8_t* h_
   const size_t dpitch = (static_cast<size_t>(w) + 15) & ~size_t(15);
   const size_t bytes = dpitch * static_cast<size_t>(h);
   uint8_t *din = nullptr, *dout = nullptr;
+  int* d_flag = nullptr;  // per-call NaN flag (quantize_sample's throw)
+  int nan_seen = 0;
   CUDA_TRY(cudaMalloc(&din, bytes));
   cudaError_t e = cudaMalloc(&dout, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&d_flag, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(d_flag, 0, sizeof(int));
   if (e == cudaSuccess) e = cudaMemcpy2D(din, dpitch, h_in, pitch, w, h, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
+    dctf::NanScope nan_scope(d_flag);
     s = dctf_filter_image_spatial_u8(p, din, dout, w, h, dpitch, nullptr);
     if (s == DCTF_OK) e = cudaMemcpy2D(h_out, pitch, dout, dpitch, w, h, cudaMemcpyDeviceToHost);
+    if (s == DCTF_OK && e == cudaSuccess) e = cudaMemcpy(&nan_seen, d_flag, sizeof(int), cudaMemcpyDeviceToHost);
   }
   cudaFree(din);
   cudaFree(dout);
+  cudaFree(d_flag);
   if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, cudaGetErrorString(e));
+  if (s == DCTF_OK && nan_seen) return set_error(DCTF_NAN_ENCOUNTERED, "quantize: NaN sample");
   return s;
 }
 

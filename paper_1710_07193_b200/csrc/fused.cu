@@ -1486,26 +1486,28 @@ namespace dctf {
 dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h,
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
                                 cudaStream_t st, bool host_mapped) {
+  if (p->unbounded && p->n == 8 && !coef_out)
+    return dctf::launch_refchain8(p, in, out, w, h, pitch, frame_stride, nframes, st);
   if (p->kq && !coef_out)
     return dctf::launch_fused8_q(&p, 1, nullptr, in, out, w, h, pitch, frame_stride, nframes, st, host_mapped,
-                                 p->d_nan);
-  if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT)
+                                 nan_flag(p));
+  if (p->n == 8 && p->precision == DCTF_PREC_INT8_EXACT && !p->unbounded)
     return dctf::launch_fused8_i8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st,
                                   sm_count(p->device));
-  const bool split = p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3;
-  if (p->n == 8 && p->sep_rank > 0 && !host_mapped) {
+  const bool split = p->precision == DCTF_PREC_TF32X3 || p->precision == DCTF_PREC_BF16X3 || p->unbounded;
+  if (p->n == 8 && p->sep_rank > 0 && !host_mapped && !p->unbounded) {
     if (p->sep_rank == 1) return launch_fused8_sep_p<1>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
     if (p->sep_rank == 2) return launch_fused8_sep_p<2>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
     return launch_fused8_sep_p<3>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   }
-  if (p->n == 8 && p->sym)
+  if (p->n == 8 && p->sym && !p->unbounded)
     return launch_fused8_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st, host_mapped);
   if (p->n == 8 && !split) return launch_fused8(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
-  if (p->n == 16 && p->sep_rank > 0 && !std::getenv("DCTF_N16_UNFUSED"))
+  if (p->n == 16 && p->sep_rank > 0 && !p->unbounded && !std::getenv("DCTF_N16_UNFUSED"))
     return p->sep_rank == 1
                ? launch_fused16_sep_p<1>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st)
                : launch_fused16_sep_p<2>(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
-  if (p->n == 16 && p->sym && !std::getenv("DCTF_N16_UNFUSED"))
+  if (p->n == 16 && p->sym && !p->unbounded && !std::getenv("DCTF_N16_UNFUSED"))
     return launch_fused16_sym(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);
   if (!split && !std::getenv("DCTF_N16_UNFUSED"))
     return launch_fused16(p, in, out, w, h, pitch, frame_stride, nframes, coef_out, st);

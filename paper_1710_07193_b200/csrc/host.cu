@@ -115,8 +115,15 @@ dctf_status host_pipeline(int dev, int nch, size_t slot_bytes, In copy_in, Run r
   const int slots = std::min(3, nch);
   uint8_t* dbuf = nullptr;
   cudaStream_t s_in = io->s[0], s_run = io->s[1], s_out = io->s[2];
-  if (cudaMallocAsync(reinterpret_cast<void**>(&dbuf), 2 * slots * slot_bytes, s_run) != cudaSuccess)
+  // the ring, then a per-call NaN flag (quantize_sample's throw, reported as
+  // DCTF_NAN_ENCOUNTERED; the plan's own flag belongs to the device entries)
+  const size_t ring = ((2 * slots * slot_bytes + 255) / 256) * 256;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&dbuf), ring + 256, s_run) != cudaSuccess)
     return set_error(DCTF_CUDA_ERROR, "host pipeline: device ring allocation failed");
+  int* d_nan = reinterpret_cast<int*>(dbuf + ring);
+  cudaMemsetAsync(d_nan, 0, sizeof(int), s_run);
+  dctf::NanScope nan_scope(d_nan);
+  int nan_seen = 0;
   cudaEventRecord(io->ev[31], s_run);
   cudaStreamWaitEvent(s_in, io->ev[31], 0);
   cudaEvent_t* ev_in = io->ev;        // [slot] input chunk landed
@@ -151,11 +158,13 @@ dctf_status host_pipeline(int dev, int nch, size_t slot_bytes, In copy_in, Run r
   cudaEventRecord(io->ev[30], s_out);
   cudaStreamWaitEvent(s_run, io->ev[29], 0);
   cudaStreamWaitEvent(s_run, io->ev[30], 0);
+  cudaMemcpyAsync(&nan_seen, d_nan, sizeof(int), cudaMemcpyDeviceToHost, s_run);
   cudaFreeAsync(dbuf, s_run);
   const cudaError_t e = cudaStreamSynchronize(s_run);
   cudaStreamSynchronize(s_in);
   cudaStreamSynchronize(s_out);
   if (s == DCTF_OK && e != cudaSuccess) s = set_error(DCTF_CUDA_ERROR, std::string("host pipeline: ") + cudaGetErrorString(e));
+  if (s == DCTF_OK && nan_seen) s = set_error(DCTF_NAN_ENCOUNTERED, "quantize: NaN sample");
   return s;
 }
 

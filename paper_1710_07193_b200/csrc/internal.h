@@ -54,6 +54,12 @@ struct dctf_plan {
   double* d_kqt = nullptr;       // K in FP64, transposed (the fallback's first stage)
   double kq_margin = 0.0;        // first-stage tie window (pixel units)
   int ref_mode = 0, ref_npairs = 0;
+  // The reference chain's intermediates can overflow FP64 for this mask
+  // (huge weights; chain_bounded false): the u8 image path then runs the
+  // reference's own operation order (n = 8: k_refchain8; n = 16: forward ->
+  // filter_coeffs -> inverse), so inf / NaN arise where they arise in the
+  // reference and NaN is reported like quantize_sample's throw.
+  bool unbounded = false;
 
   // Device staging of the host-buffer entry (copy mode), guarded by io_mu.
   mutable std::mutex io_mu;
@@ -102,6 +108,15 @@ dctf_status filter_image_device(const dctf_plan* p, const uint8_t* in, uint8_t* 
                                 size_t pitch, long long frame_stride, int nframes, double* coef_out,
                                 cudaStream_t st, bool host_mapped = false);
 void reset_launches();
+// NaN flag the launchers pass to the quantizing kernels: the calling thread's
+// per-call flag while a NanScope is alive (host-buffer entries), else the
+// plan's own flag (device entries; dctf_plan_nan_check reads it).
+int* nan_flag(const dctf_plan* p);
+struct NanScope {
+  explicit NanScope(int* f);
+  ~NanScope();
+  int* prev;
+};
 // host.cu: one image from / to host buffers through the copy-engine pipeline
 // (per-call scratch, per-thread streams).
 dctf_status image_host_copy(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w, int h, size_t pitch,
@@ -160,6 +175,13 @@ struct KqInfo {
 };
 bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info);
 void refchain_image(const dctf_plan& p, std::vector<double>& out, int& mode, int& npairs);
+// True when every intermediate of the reference chain (forward_2d, apply_pairs,
+// inverse_2d or convolve) stays below 1e300 in magnitude for u8 inputs, so no
+// inf / NaN can arise (plan.cc).
+bool chain_bounded(const dctf_plan& p);
+dctf_status upload_refchain_only(dctf_plan* p);  // quant.cu: data of k_refchain8
+dctf_status launch_refchain8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
+                             long long frame_stride, int nframes, cudaStream_t st);
 
 // TMA tensor map over block-major FP64 coefficients (capi.cu): 2-D
 // [nblocks rows x nn cols], box [box_rows x 16 cols], 128B swizzle.

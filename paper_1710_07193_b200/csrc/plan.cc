@@ -1166,6 +1166,67 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
 // Device data of the reference-order fallback (k_fallback8): C, C^t and the
 // DCT-domain pairs (mode 1), or nothing beyond the plan's weights (mode 2,
 // convolve formula).
+// Elementwise magnitude bounds of the reference chain on u8 blocks (every
+// product and partial sum of block_matrix.hpp:67-81's i-k-j loops is at most
+// |A| |B| in absolute-value arithmetic): X = C P C^t (forward_2d), per pair
+// (L X) R and the running sum (apply_pairs), (C^t Y) C (inverse_2d); or the
+// convolve sum 255 sum|w|. Any non-finite operator entry fails the test.
+bool chain_bounded(const dctf_plan& p) {
+  const int n = p.n, nn = n * n;
+  constexpr double LIM = 1e300;
+  auto finite_all = [](const std::vector<double>& v) {
+    for (double x : v)
+      if (!std::isfinite(x)) return false;
+    return true;
+  };
+  if (!finite_all(p.weights)) return false;
+  if (p.dct_left.empty() && !(p.reference_domain && p.npairs == 0)) {
+    double s = 0.0;
+    for (double x : p.weights) s += std::fabs(x);
+    return 255.0 * s < LIM;
+  }
+  if (!finite_all(p.dct_left) || !finite_all(p.dct_right) || !finite_all(p.basis)) return false;
+  // |A| |B| with the partial-sum bound (max over outputs); returns max entry
+  auto absmul = [&](const std::vector<long double>& a, const std::vector<long double>& b,
+                    std::vector<long double>& c) {
+    c.assign(size_t(nn), 0.0L);
+    long double mx = 0.0L;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        long double acc = 0.0L;
+        for (int k = 0; k < n; ++k) acc += a[size_t(i) * n + k] * b[size_t(k) * n + j];
+        c[size_t(i) * n + j] = acc;
+        mx = std::max(mx, acc);
+      }
+    return mx;
+  };
+  std::vector<long double> C(nn), Ct(nn), X(nn, 255.0L), T, F, U, V, Acc(nn, 0.0L), Y, Z;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      C[size_t(i) * n + j] = std::fabs(p.basis[size_t(i) * n + j]);
+      Ct[size_t(j) * n + i] = C[size_t(i) * n + j];
+    }
+  long double mx = absmul(C, X, T);
+  mx = std::max(mx, absmul(T, Ct, F));
+  const int np = static_cast<int>(p.dct_left.size() / nn);
+  for (int q = 0; q < np; ++q) {
+    std::vector<long double> L(nn), R(nn);
+    for (int e = 0; e < nn; ++e) {
+      L[size_t(e)] = std::fabs(p.dct_left[size_t(q) * nn + e]);
+      R[size_t(e)] = std::fabs(p.dct_right[size_t(q) * nn + e]);
+    }
+    mx = std::max(mx, absmul(L, F, U));
+    mx = std::max(mx, absmul(U, R, V));
+    for (int e = 0; e < nn; ++e) {
+      Acc[size_t(e)] += V[size_t(e)];
+      mx = std::max(mx, Acc[size_t(e)]);
+    }
+  }
+  mx = std::max(mx, absmul(Ct, Acc, Y));
+  mx = std::max(mx, absmul(Y, C, Z));
+  return mx < LIM;
+}
+
 void refchain_image(const dctf_plan& p, std::vector<double>& out, int& mode, int& npairs) {
   const int nn = p.n * p.n;
   out.assign(p.basis.begin(), p.basis.end());

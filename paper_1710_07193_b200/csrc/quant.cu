@@ -324,7 +324,8 @@ __device__ bool fallback_block(const RefPlan& rp, const uint8_t* img, size_t pit
   double z[2];
   // First stage: z = K p in FP64 (error far below the reference's own); a
   // block with no pixel within rp.margin of a .5 boundary is final here.
-  {
+  // (No first stage for unbounded plans, rp.kt == nullptr: k_refchain8.)
+  if (rp.kt) {
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll 8
     for (int j = 0; j < 64; ++j) {
@@ -729,9 +730,53 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
 
+// u8 image path of unbounded plans (chain_bounded false: the reference's
+// intermediates can overflow FP64): every block through the reference's own
+// operation order, one warp per block, so inf / NaN arise exactly where they
+// arise in the reference and NaN sets the flag like quantize_sample's throw.
+__global__ void __launch_bounds__(256) k_refchain8(const __grid_constant__ RefPlan rp, const uint8_t* in, uint8_t* out,
+                                                    int w, int h, size_t pitch, long long frame_stride, int nframes,
+                                                    int bw, int bh, int* nan_flag) {
+  __shared__ __align__(16) double sm[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long per = static_cast<long long>(bw) * bh, nb = per * nframes;
+  for (long long b = static_cast<long long>(blockIdx.x) * 8 + warp; b < nb; b += static_cast<long long>(gridDim.x) * 8) {
+    const long long f = b / per, r = b - f * per;
+    const int by = static_cast<int>(r / bw), bx = static_cast<int>(r - static_cast<long long>(by) * bw);
+    fallback_block(rp, in + f * frame_stride, pitch, w, h, by * 8, bx * 8,
+                   out + f * frame_stride + static_cast<size_t>(by) * 8 * pitch + bx * 8, false, sm[warp], nan_flag,
+                   lane);
+  }
+}
+
 }  // namespace
 
 namespace dctf {
+
+dctf_status upload_refchain_only(dctf_plan* p) {
+  std::vector<double> chain;
+  refchain_image(*p, chain, p->ref_mode, p->ref_npairs);
+  cudaError_t e = cudaMalloc(&p->d_refchain, chain.size() * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->d_refchain, chain.data(), chain.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("reference chain upload: ") + cudaGetErrorString(e));
+  return DCTF_OK;
+}
+
+dctf_status launch_refchain8(const dctf_plan* p, const uint8_t* in, uint8_t* out, int w, int h, size_t pitch,
+                             long long frame_stride, int nframes, cudaStream_t st) {
+  const int bw = (w + 7) / 8, bh = (h + 7) / 8;
+  const long long nb = static_cast<long long>(bw) * bh * nframes;
+  if (nb <= 0) return DCTF_OK;
+  const RefPlan rp{p->d_refchain, p->d_weights, nullptr, 0.0, p->ref_mode, p->ref_npairs, p->kr, p->kc, p->padding};
+  const long long grid = std::min<long long>((nb + 7) / 8, 16LL * sm_count(p->device));
+  k_refchain8<<<static_cast<unsigned>(grid), 256, 0, st>>>(rp, in, out, w, h, pitch, frame_stride, nframes, bw, bh,
+                                                           nan_flag(p));
+  add_launches(1);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_refchain8: ") + cudaGetErrorString(e));
+  return DCTF_OK;
+}
 
 // DCTF_Q_COUNT=1: a process-wide device counter of the blocks the fallback
 // warp recomputed (diagnostics; read with dctf_diag_fallback_blocks).

@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_spatial_rows(const uint8_t* __re
                                                              const double* __restrict__ blocks,
                                                              uint8_t* __restrict__ out_img,
                                                              double* __restrict__ out_blocks, long long nblocks,
-                                                             long long nbatches, const SpWeights<KR, KC> wt) {
+                                                             long long nbatches, const SpWeights<KR, KC> wt,
+                                                             int* nan_flag) {
   using C = SpCfg<N>;
   __shared__ __align__(16) double tile[C::BPC * C::BS];
   const int b = threadIdx.x >> C::LOGN, i = threadIdx.x & (N - 1);
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_spatial_rows(const uint8_t* __re
           uint8_t* dst = out_img + static_cast<size_t>(y) * pitch + c_x0;
           uint32_t q[N];
 #pragma unroll
-          for (int j = 0; j < N; ++j) q[j] = quantize(acc[j], nullptr);  // finite: weights are checked finite
+          for (int j = 0; j < N; ++j) q[j] = quantize(acc[j], nan_flag);  // huge weights can overflow to NaN
           if (c_x0 + N <= w && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
 #pragma unroll
             for (int j = 0; j < N; j += 8) {
@@ -202,7 +203,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_spatial_rows(const uint8_t* __re
 
 template <int N, int KR, int KC, bool REP, bool U8>
 void launch_one(const uint8_t* img, int w, int h, size_t pitch, int bw, const double* blocks, uint8_t* out_img,
-                double* out_blocks, long long nblocks, const SpWeights<KR, KC>& wt, int device, cudaStream_t st) {
+                double* out_blocks, long long nblocks, const SpWeights<KR, KC>& wt, int device, cudaStream_t st,
+                int* nan_flag) {
   static const int per_sm = [] {
     int v = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_spatial_rows<N, KR, KC, REP, U8>, SP_THREADS, 0);
@@ -212,7 +214,7 @@ void launch_one(const uint8_t* img, int w, int h, size_t pitch, int bw, const do
   const long long resident = static_cast<long long>(dctf::sm_count(device)) * per_sm;
   const unsigned grid = static_cast<unsigned>(nbatches < resident ? nbatches : resident);
   k_spatial_rows<N, KR, KC, REP, U8><<<grid, SP_THREADS, 0, st>>>(img, w, h, pitch, bw, blocks, out_img,
-                                                                  out_blocks, nblocks, nbatches, wt);
+                                                                  out_blocks, nblocks, nbatches, wt, nan_flag);
 }
 
 template <int N, int KR, int KC>
@@ -224,11 +226,11 @@ void launch_rows(const dctf_plan* p, const uint8_t* img, int w, int h, size_t pi
   const bool rep = p->padding == DCTF_PAD_REPLICATE;
   const int dev = p->device;
   if (img) {
-    if (rep) launch_one<N, KR, KC, true, true>(img, w, h, pitch, bw, nullptr, out_img, nullptr, nblocks, wt, dev, st);
-    else launch_one<N, KR, KC, false, true>(img, w, h, pitch, bw, nullptr, out_img, nullptr, nblocks, wt, dev, st);
+    if (rep) launch_one<N, KR, KC, true, true>(img, w, h, pitch, bw, nullptr, out_img, nullptr, nblocks, wt, dev, st, dctf::nan_flag(p));
+    else launch_one<N, KR, KC, false, true>(img, w, h, pitch, bw, nullptr, out_img, nullptr, nblocks, wt, dev, st, dctf::nan_flag(p));
   } else {
-    if (rep) launch_one<N, KR, KC, true, false>(nullptr, 0, 0, 0, 1, blocks, nullptr, out_blocks, nblocks, wt, dev, st);
-    else launch_one<N, KR, KC, false, false>(nullptr, 0, 0, 0, 1, blocks, nullptr, out_blocks, nblocks, wt, dev, st);
+    if (rep) launch_one<N, KR, KC, true, false>(nullptr, 0, 0, 0, 1, blocks, nullptr, out_blocks, nblocks, wt, dev, st, dctf::nan_flag(p));
+    else launch_one<N, KR, KC, false, false>(nullptr, 0, 0, 0, 1, blocks, nullptr, out_blocks, nblocks, wt, dev, st, dctf::nan_flag(p));
   }
 }
 

@@ -27,7 +27,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import InvalidArgument, Unsupported, check
+from ._lib import InvalidArgument, NanEncountered, Unsupported, check  # noqa: F401
 
 __all__ = [
     "PaddingMode", "Domain", "Precision", "Mask", "row_symmetric", "DctBasis", "FilterPlan",
@@ -411,6 +411,19 @@ class FilterPlan:
         check(_lib.lib.dctf_convolve_blocks(self._h, _dptr(x), _dptr(y), x.shape[0],
                                             _stream(x.device)))
         return y
+
+    def filter_image_spatial_host(self, img: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """Spatial path (Domain::kSpatial) on host buffers; NaN raises
+        NanEncountered like quantize_sample (dctf_filter_image_spatial_host)."""
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        if img.ndim != 2:
+            raise InvalidArgument("expected a (height, width) uint8 image")
+        if out is None:
+            out = np.empty_like(img)
+        h, w = img.shape
+        check(_lib.lib.dctf_filter_image_spatial_host(self._h, img.ctypes.data, out.ctypes.data, w, h,
+                                                      img.strides[0]))
+        return out
 
     def filter_image_host(self, img: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
         """End-to-end host-buffer filter (H2D, fused kernel, D2H)."""

@@ -87,12 +87,15 @@ def test_config4(P, ref):
     from paper_1710_07193_b200 import synth
     img = synth.uniform_image(4, 8192, 8192)
     _full_case(P, ref, img, synth.gaussian_mask(7, 2.0), 7, 1, 16, "cfg4 gauss7 s2 replicate")
-    plan9 = _full_case(P, ref, img, synth.motion_9x9(), 9, 1, 16, "cfg4 motion 9x9 replicate")
-    # the 1x9 mask itself (convolve-formula plan) gives the same image
+    _full_case(P, ref, img, synth.motion_9x9(), 9, 1, 16, "cfg4 motion 9x9 replicate")
+    # the 1x9 mask itself (convolve-formula plan): the reference's 9x9
+    # embedding's u8 output, bit-exact except at the reference's own near-ties
     plan1 = P.FilterPlan(P.Mask.rect(1, 9, synth.MOTION_1x9), 16, P.PaddingMode.kReplicate)
-    d = _dev(img)
-    a, b = _host(plan9.filter_image(d)), _host(plan1.filter_image(d))
-    assert np.count_nonzero(a != b) <= 16
+    r_out, _, _, r_pq = ref.filter_image(img, synth.motion_9x9(), 9, 1, 16, threads=nthreads(), side_outputs=True)
+    b = _host(plan1.filter_image(_dev(img)))
+    mism, excused, near = tie_report(b, r_out, blocks_to_image(r_pq, 8192, 8192))
+    print(f"[cfg4 1x9 plan vs reference 9x9] mismatches {mism} (near-ties {excused}/{near})")
+    assert mism == excused
 
 
 def test_config5_frames(P, ref, oracle):
@@ -127,4 +130,65 @@ def test_config5_frames(P, ref, oracle):
         single = _host(plans[f % 4].filter_image(d[f]))
         assert np.array_equal(single, out_h[f])
     del d, out
+    torch.cuda.empty_cache()
+
+
+def test_config5_all_frames(P, ref, oracle):
+    """Config 5 in full (SURVEY 8(d) "golden volume"): all 64 frames of the
+    batched call against the reference (square masks) / the restated convolve
+    oracle (1x9), every pixel, near-ties counted; FP64 coefficients of frames
+    0-3 (one per mask) in full and of every 97th block of all 64 frames
+    against the reference's (reference forward_2d of the restated convolve for
+    the 1x9 frames: filtering commutes with the transform, operators_test.cc:
+    223-233)."""
+    import torch
+    from paper_1710_07193_b200 import synth
+    W, H, F = 3840, 2160, 64
+    nb = (W // 8) * (H // 8)
+    rnd5, _ = synth.random_mask(1005, 5)
+    masks = [(synth.LAPLACIAN3, 3, 3), (synth.gaussian_mask(5, 1.0), 5, 5),
+             (synth.MOTION_1x9, 1, 9), (rnd5, 5, 5)]
+    plans = [P.FilterPlan(P.Mask(k, w) if k == kc else P.Mask.rect(k, kc, w), 8,
+                          P.PaddingMode.kReplicate) for w, k, kc in masks]
+    frames = np.empty((F, H, W), np.uint8)
+    for f in range(F):
+        synth.sinusoid_image(f, W, H, out=frames[f])
+    d = _dev(frames)
+    out_h = _host(P.filter_frames(d, plans, [f % 4 for f in range(F)]))
+    sample = np.arange(0, nb, 97)
+    tot_mism = tot_exc = 0
+    worst = 0.0
+    for f in range(F):
+        w, k, kc = masks[f % 4]
+        if k == kc:
+            r_out, _, r_co, r_pq = ref.filter_image(frames[f], w, k, 1, 8, threads=nthreads(), side_outputs=True)
+        else:
+            r_out, r_pq = oracle.filter_image_spatial(frames[f], w, k, kc, 1, 8, prequant=True)
+            r_co = None
+        mism, excused, _ = tie_report(out_h[f], r_out, blocks_to_image(r_pq, W, H))
+        tot_mism += mism
+        tot_exc += excused
+        assert mism == excused, f"frame {f}"
+        plan = plans[f % 4]
+        if f < 4:  # full coefficients through the fused entry's coefficient output
+            co = torch.empty((nb, 8, 8), dtype=torch.float64, device="cuda")
+            o1 = _host(plan.filter_image(d[f], co))
+            m1, e1, _ = tie_report(o1, r_out, blocks_to_image(r_pq, W, H))
+            assert m1 == e1, f"frame {f} (single-image entry with coefficient output)"
+            full = _host(co)
+            gold = r_co if r_co is not None else ref.forward_blocks(np.ascontiguousarray(r_pq), threads=nthreads())
+            err = np.abs(full - gold).max() / np.abs(gold).max()
+            assert err <= TOL, f"frame {f} coefficients {err:.2e}"
+            worst = max(worst, err)
+            del co
+        # every 97th block: the coefficient path (forward_2d -> filter_coeffs)
+        y = _host(plan.filter_coeffs(plan.forward_image(d[f])))[sample]
+        gold = r_co[sample] if r_co is not None else ref.forward_blocks(
+            np.ascontiguousarray(r_pq[sample]), threads=nthreads())
+        err = np.abs(y - gold).max() / np.abs(gold).max()
+        assert err <= TOL, f"frame {f} sampled coefficients {err:.2e}"
+        worst = max(worst, err)
+    print(f"[cfg5 all 64 frames] u8 mismatches {tot_mism} (all near-ties: {tot_exc}); "
+          f"worst coefficient rel err {worst:.2e} (frames 0-3 full, every 97th block of all frames)")
+    del d
     torch.cuda.empty_cache()
