@@ -281,6 +281,12 @@ dctf_status dctf_filter_coeffs_host(const dctf_plan* plan, const double* h_in, d
                                     size_t nblocks);
 dctf_status dctf_convolve_blocks_host(const dctf_plan* plan, const double* h_blocks, double* h_out,
                                       size_t nblocks);
+/* FilterPlan::filter_block (filter.hpp:71-73) over nblocks spatial FP64
+ * blocks: inverse_2d(filter_coeffs(forward_2d(x))), the three kernels on the
+ * calling thread's stream with one copy each way (reference operation order
+ * for the transforms). */
+dctf_status dctf_filter_blocks_host(const dctf_plan* plan, const double* h_blocks, double* h_out,
+                                    size_t nblocks);
 
 /* NaN reporting (quantize_sample throws on NaN, spatial.hpp:71-75). The
  * device-buffer entries (dctf_filter_image_u8, dctf_filter_frames_u8,

@@ -478,7 +478,7 @@ class FilterPlan {
     return filter_coeffs(std::vector<BlockMatrix>{coeffs})[0];
   }
   std::vector<BlockMatrix> filter_block(const std::vector<BlockMatrix>& blocks) const {
-    return inverse_2d(basis_, filter_coeffs(forward_2d(basis_, blocks)));
+    return detail::run(plan_, n_, blocks, dctf_filter_blocks_host);  // one device round trip
   }
   BlockMatrix filter_block(const BlockMatrix& block) const {
     return filter_block(std::vector<BlockMatrix>{block})[0];

@@ -1230,28 +1230,32 @@ static dctf_status run_host_blocks(const dctf_plan* p, const double* h_in, doubl
   if (!h_in || !h_out) return set_error(DCTF_INVALID_ARGUMENT, "NULL buffer");
   DeviceGuard guard(p->device);
   const size_t bytes = nblocks * static_cast<size_t>(p->n) * p->n * sizeof(double);
-  cudaStream_t st;
-  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  double *din = nullptr, *dout = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&din), bytes, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dout), bytes, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(din, h_in, bytes, cudaMemcpyHostToDevice, st);
+  // the thread's cached stream and scratch (input and output halves)
+  cudaStream_t st = nullptr;
+  void* scratch = nullptr;
+  s = dctf::thread_scratch(p->device, 2 * bytes, &st, &scratch);
+  if (s != DCTF_OK) return s;
+  double* din = static_cast<double*>(scratch);
+  double* dout = din + bytes / sizeof(double);
+  cudaError_t e = cudaMemcpyAsync(din, h_in, bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) s = set_error(DCTF_CUDA_ERROR, cudaGetErrorString(e));
   if (s == DCTF_OK) {
     if (op == 0) s = dctf_forward_blocks(p, din, dout, nblocks, st);
     else if (op == 1) s = dctf_inverse_blocks(p, din, dout, nblocks, st);
     else if (op == 2) s = dctf_filter_coeffs(p, din, dout, nblocks, st);
-    else s = dctf_convolve_blocks(p, din, dout, nblocks, st);
+    else if (op == 3) s = dctf_convolve_blocks(p, din, dout, nblocks, st);
+    else {  // filter_block: forward -> filter_coeffs -> inverse, one round trip
+      s = dctf_forward_blocks(p, din, dout, nblocks, st);
+      if (s == DCTF_OK) s = dctf_filter_coeffs(p, dout, din, nblocks, st);
+      if (s == DCTF_OK) s = dctf_inverse_blocks(p, din, dout, nblocks, st);
+    }
   }
   if (s == DCTF_OK) {
     e = cudaMemcpyAsync(h_out, dout, bytes, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) s = set_error(DCTF_CUDA_ERROR, cudaGetErrorString(e));
   }
-  cudaFreeAsync(din, st);
-  cudaFreeAsync(dout, st);
   e = cudaStreamSynchronize(st);
   if (s == DCTF_OK && e != cudaSuccess) s = set_error(DCTF_CUDA_ERROR, cudaGetErrorString(e));
-  cudaStreamDestroy(st);
   return s;
 }
 
@@ -1271,6 +1275,10 @@ dctf_status dctf_filter_coeffs_host(const dctf_plan* p, const double* h_in, doub
 dctf_status dctf_convolve_blocks_host(const dctf_plan* p, const double* h_in, double* h_out,
                                       size_t nblocks) {
   return run_host_blocks(p, h_in, h_out, nblocks, 3);
+}
+
+dctf_status dctf_filter_blocks_host(const dctf_plan* p, const double* h_in, double* h_out, size_t nblocks) {
+  return run_host_blocks(p, h_in, h_out, nblocks, 4);
 }
 
 dctf_status dctf_filter_image_spatial_host(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w,

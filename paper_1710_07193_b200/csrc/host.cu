@@ -216,6 +216,40 @@ dctf_status frames_host(const dctf_plan* const* plans, int nplans, const int* po
 }  // namespace
 
 namespace dctf {
+// The calling thread's compute stream on `device` (created once per thread
+// and device) and a grow-only device scratch buffer of this thread on it:
+// the per-block host entries (forward / inverse / filter_coeffs / convolve
+// on host BlockMatrix batches) reuse both instead of creating a stream and
+// allocating per call.
+dctf_status thread_scratch(int device, size_t bytes, cudaStream_t* st, void** buf) {
+  IoStreams* io = nullptr;
+  const dctf_status s = io_streams(device, io);
+  if (s != DCTF_OK) return s;
+  *st = io->s[1];
+  struct Scratch {
+    std::vector<std::pair<void*, size_t>> per_dev;
+    ~Scratch() {
+      for (auto& b : per_dev)
+        if (b.first) cudaFree(b.first);
+    }
+  };
+  thread_local Scratch scratch;
+  if (scratch.per_dev.size() <= static_cast<size_t>(device)) scratch.per_dev.resize(device + 1, {nullptr, 0});
+  auto& b = scratch.per_dev[device];
+  if (b.second < bytes) {
+    if (b.first) {
+      cudaStreamSynchronize(*st);
+      cudaFree(b.first);
+    }
+    b = {nullptr, 0};
+    const size_t want = std::max(bytes, size_t(1) << 20);
+    if (cudaMalloc(&b.first, want) != cudaSuccess) return set_error(DCTF_CUDA_ERROR, "host scratch allocation failed");
+    b.second = want;
+  }
+  *buf = b.first;
+  return DCTF_OK;
+}
+
 // One image from / to host buffers through the copy-engine pipeline: bands of
 // whole block rows (~16 MiB) are independent images (blocks never cross a
 // band; the ragged bottom band replicates the image's last row exactly as

@@ -121,6 +121,9 @@ struct NanScope {
 // (per-call scratch, per-thread streams).
 dctf_status image_host_copy(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w, int h, size_t pitch,
                             int* launches);
+// host.cu: the calling thread's compute stream on `device` and a grow-only
+// device scratch buffer of at least `bytes` (per thread and device).
+dctf_status thread_scratch(int device, size_t bytes, cudaStream_t* st, void** buf);
 // capi.cu: dctf_filter_frames_u8's dispatch (validated arguments, device current).
 dctf_status filter_frames_device(const dctf_plan* const* plans, int nplans, const int* h_plan_of_frame,
                                  const uint8_t* d_in, uint8_t* d_out, int nframes, int w, int h, size_t pitch,
