@@ -128,6 +128,11 @@ dctf_status dctf_plan_pairs(const dctf_plan* plan, int domain, double* h_lefts, 
  * were merged (OperatorSet::pairs.size(), ::symmetric_merged). */
 dctf_status dctf_plan_info(const dctf_plan* plan, int* n, int* npairs, int* symmetric_merged);
 
+/* The plan's mask (kr x kc weights, row-major; NULL h_weights to query the
+ * shape only) and padding — for plans read from an operator dump, the dump's
+ * mask and padding (operator_io.hpp: read_operator_sets). */
+dctf_status dctf_plan_mask(const dctf_plan* plan, double* h_weights, int* kr, int* kc, int* padding);
+
 /* Name of the kernel dctf_filter_image_u8 runs for this plan:
  *   n = 8:  "k_fused8_q" (DCTF_PREC_FP64 default: exact-integer tcgen05
  *           composed operator + reference-order fallback), "k_fused8_sep"

@@ -516,9 +516,23 @@ class FilterPlan {
 
  private:
   FilterPlan(detail::PlanPtr plan, int device)
-      : mask_(Mask::identity()), padding_(PaddingMode::kZero), basis_(plan_n(plan.get()), device),
+      : mask_(plan_mask(plan.get())), padding_(plan_padding(plan.get())), basis_(plan_n(plan.get()), device),
         plan_(std::move(plan)) {
     check(dctf_plan_info(plan_.get(), &n_, &npairs_, &merged_));
+  }
+  // the dump's mask and padding (dctf_plan_mask), so mask(), padding() and
+  // dct_set() describe the plan read back
+  static Mask plan_mask(const dctf_plan* p) {
+    int kr = 0, kc = 0;
+    check(dctf_plan_mask(p, nullptr, &kr, &kc, nullptr));
+    std::vector<double> w(size_t(kr) * kc);
+    check(dctf_plan_mask(p, w.data(), nullptr, nullptr, nullptr));
+    return Mask(kr, std::move(w));
+  }
+  static PaddingMode plan_padding(const dctf_plan* p) {
+    int pad = 0;
+    check(dctf_plan_mask(p, nullptr, nullptr, nullptr, &pad));
+    return PaddingMode(pad);
   }
   static int plan_n(const dctf_plan* p) {
     int n = 0;

@@ -850,6 +850,15 @@ dctf_status dctf_plan_destroy(dctf_plan* p) {
   return DCTF_OK;
 }
 
+dctf_status dctf_plan_mask(const dctf_plan* p, double* h_weights, int* kr, int* kc, int* padding) {
+  if (!p) return set_error(DCTF_INVALID_ARGUMENT, "plan is NULL");
+  if (kr) *kr = p->kr;
+  if (kc) *kc = p->kc;
+  if (padding) *padding = p->padding;
+  if (h_weights && !p->weights.empty()) std::memcpy(h_weights, p->weights.data(), p->weights.size() * sizeof(double));
+  return DCTF_OK;
+}
+
 dctf_status dctf_plan_info(const dctf_plan* p, int* n, int* npairs, int* merged) {
   if (!p) return set_error(DCTF_INVALID_ARGUMENT, "plan is NULL");
   if (n) *n = p->n;

@@ -60,6 +60,16 @@ for rep in sys.argv[3:]:
     m = {k: {"value": vals[hh.index(k)], "unit": units[hh.index(k)]} for k in KEYS if k in hh}
     json.dump({"report": os.path.basename(rep), "kernel": name, "metrics": m},
               open(os.path.join(out, f"ncu_{name}.json"), "w"), indent=1)
+    if base == "k_fused8_q":  # the config-5 bench headline kernel
+        def tob(e):
+            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[e["unit"]]
+            return float(e["value"].replace(",", "")) * sc
+        traffic = tob(m["dram__bytes_read.sum"]) + tob(m["dram__bytes_write.sum"])
+        json.dump({"kernel": base, "dram_bytes_per_launch": traffic,
+                   "read_bytes": tob(m["dram__bytes_read.sum"]), "write_bytes": tob(m["dram__bytes_write.sum"]),
+                   "source": f"profiles/{tag}/ncu_{name}.json (ncu --set full --clock-control none, bench "
+                             f"config 5 step: one launch over 64 frames, 8,294,400 blocks)"},
+                  open(os.path.join(ROOT, "profiles", "ncu_headline_config5.json"), "w"), indent=1)
     if base in ("k_fused8", "k_fused8_sym", "k_fused8_sep"):
         def tobytes(e):
             s = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[e["unit"]]

@@ -250,6 +250,14 @@ int main() {
     CHECK(a[3].samples == filter_image(pr, frames[3]).samples, "filter_frames frame == filter_image of that frame");
     CHECK(c.samples == a[3].samples, "filter_image with set_devices({0, 0}) == single device");
   }
+  // FilterPlan::from_dump carries the dump's mask and padding (read_operator_sets)
+  {
+    const FilterPlan a(Mask::gaussian3(), 8, PaddingMode::kReplicate);
+    const FilterPlan b = FilterPlan::from_dump(a.dump());
+    CHECK(b.padding() == PaddingMode::kReplicate && b.mask().weights() == a.mask().weights() &&
+              b.dump() == a.dump(),
+          "from_dump: mask, padding and the re-written dump equal the source plan's");
+  }
   // Per-block drop-in cost (the reference's FilterPlan::filter_block loop,
   // ~5 us per 8x8 block on one CPU thread): one block per call
   // (cached per-thread stream and scratch, one device round trip) against a
