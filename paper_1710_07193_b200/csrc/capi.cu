@@ -331,17 +331,20 @@ dctf_status make_xmap(void* vmap, const double* d, long long nblocks, int nn, in
 // bytes, both multiples of 16, base 16-byte aligned); box [1][8][box_w], no
 // swizzle, OOB -> 0.
 dctf_status make_imap(void* vmap, const uint8_t* d, int w, int h, int nframes, size_t pitch,
-                      long long frame_stride, int box_w) {
+                      long long frame_stride, int box_w, int elem_bytes) {
   CUtensorMap* map = static_cast<CUtensorMap*>(vmap);
   PFN_encodeTiled_t fn = encode_fn();
   if (!fn) return set_error(DCTF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+  // elem_bytes 8: the row viewed as w / 8 uint64 elements (w % 8 == 0), so
+  // one box [box_w elements x 8 rows] spans box_w * 8 pixels
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(elem_bytes == 8 ? w / 8 : w), static_cast<cuuint64_t>(h),
                               static_cast<cuuint64_t>(nframes)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch),
                                  static_cast<cuuint64_t>(nframes > 1 ? frame_stride : pitch * h)};
   const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), 8, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(d), dims, strides, box, estr,
+  const CUresult r = fn(map, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 3,
+                        const_cast<uint8_t*>(d), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)

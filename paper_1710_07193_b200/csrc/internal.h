@@ -192,7 +192,8 @@ dctf_status make_xmap(void* map, const double* d, long long nblocks, int nn, int
 // TMA tensor map over a u8 frame batch (capi.cu): 3-D [nframes][h][w], box
 // [1][8][box_w], no swizzle, OOB -> 0.
 dctf_status make_imap(void* map, const uint8_t* d, int w, int h, int nframes, size_t pitch,
-                      long long frame_stride, int box_w);
+                      long long frame_stride, int box_w,
+                      int elem_bytes = 1);
 
 // Exact-INT8 tcgen05 fused n=8 path (ozaki.cu).
 dctf_status upload_i8_operator(dctf_plan* p);

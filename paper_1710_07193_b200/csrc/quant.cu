@@ -74,11 +74,13 @@ using dctf::set_error;
 namespace {
 
 #ifdef QDBG
-// [cta < 4][tile < 64][event < 12] clock64 stamps of tiles QDBG_T0.. (instrumented build only)
+// [cta < 4][tile < 64][event < 32] clock64 stamps of tiles QDBG_T0.. (instrumented build only;
+// scripts/kq_trace3.py: 0/1 MMA issue start / done, 2+w wake and 10+w release of epilogue warp w,
+// 18 converters' a_full arrival, 19 MMA sees a_full)
 #ifndef QDBG_T0
 #define QDBG_T0 0
 #endif
-__device__ long long g_qdbg[4][64][12];
+__device__ long long g_qdbg[4][64][32];
 #define QSTAMP(tl, ev)                                                                                  \
   do {                                                                                                  \
     if (blockIdx.x < 4 && (tl) >= QDBG_T0 && (tl) < QDBG_T0 + 64) g_qdbg[blockIdx.x][(tl)-QDBG_T0][(ev)] = clock64(); \
@@ -238,7 +240,7 @@ __device__ __forceinline__ void q8_row(const int32_t (&v)[32], int shS, int shL,
 template <int ROWS, bool F32>
 __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32_t (&vb)[32], int shS, int shL,
                                          uint32_t U, uint32_t& mn0, uint32_t& mn1, uint32_t (&words)[2 * ROWS],
-                                         uint64_t* acc_empty) {
+                                         uint64_t* acc_empty, long long* stamp = nullptr) {
   tmem_ld32(col0, va);
   tmem_wait_ld();
   if (ROWS == 1) {
@@ -259,6 +261,9 @@ __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32
       if (r + 2 == ROWS) {
         tc_fence_before();
         mbar_arrive(acc_empty);  // accumulator drained: the MMA of tile tl+2 may start
+#ifdef QDBG
+        if (stamp && (threadIdx.x & 31) == 0) *stamp = clock64();
+#endif
       }
     }
   }
@@ -410,13 +415,17 @@ __device__ bool fallback_block(const RefPlan& rp, const uint8_t* img, size_t pit
   return true;
 }
 
-template <bool TMA>
+// TM: 0 = direct global loads (unaligned views, host-mapped input), 1 = four
+// TMA boxes [8 rows x 256 px] per tile (u8 elements), 2 = one TMA box
+// [8 rows x 128 uint64] = the whole 8 x 1024 px strip (width % 8 == 0).
+template <int TM>
 __global__ void __launch_bounds__(q8::THREADS, 1)
     k_fused8_q(const __grid_constant__ CUtensorMap imap, const __grid_constant__ QArgs args,
                const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int w, int h, size_t pitch,
                long long frame_stride, int nframes, int bw, int bh, int ntx, bool fast_out, int* nan_flag,
                unsigned long long* fb_count) {
   using namespace q8;
+  constexpr bool TMA = TM != 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
   uint8_t* bsm = base;                                // digit images
@@ -544,9 +553,15 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   };
 
   if (warp == W_TMA) {
-    // ---------------- TMA producer: raw strips into the ring
-    if (TMA && lane == 0) {
-      prefetch_tmap(&imap);
+    // ---------------- TMA producer: raw strips into the ring. Like the MMA
+    // issuer: the converged warp runs the loop and one elected lane issues the
+    // tile's expect_tx and (up to) four box loads in one asm block (a lone
+    // lane-0 loop wraps each bulk-tensor instruction in its own elect loop,
+    // which held this warp's SM sub-partition ~100 cycles per load).
+    if (TMA) {
+      if (lane == 0) prefetch_tmap(&imap);
+      __syncwarp();
+      const uint64_t map = reinterpret_cast<uint64_t>(&imap);
       long long tl = 0;
       for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
         int f, by, bx0;
@@ -554,11 +569,40 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
         const int r = static_cast<int>(tl % NRAW);
         const uint32_t k = static_cast<uint32_t>(tl / NRAW);
         Q8_WAIT_OTHER(&raw_empty[r], (k & 1u) ^ 1u);
-        QSTAMP(tl, 0);
+        if (lane == 0) QSTAMP(tl, 20);
+        const uint32_t dst = smem_u32(raw + r * RAWB), bar = smem_u32(&raw_full[r]);
+        if (TM == 2) {
+          asm volatile(
+              "{\n\t.reg .pred e;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n\t"
+              "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%3, {%4, %5, %6}], [%1];\n\t}"
+              ::"r"(dst), "r"(bar), "r"(static_cast<uint32_t>(RAWB)), "l"(map), "r"(bx0), "r"(by * 8), "r"(f)
+              : "memory");
+          continue;
+        }
         const int nbt = min(TILE, bw - bx0);
         const int nbox = (nbt * 8 + 255) >> 8;
-        mbar_expect_tx(&raw_full[r], static_cast<uint32_t>(nbox * 2048));
-        for (int j = 0; j < nbox; ++j) tma_load_3d(raw + r * RAWB + j * 2048, &imap, &raw_full[r], bx0 * 8 + 256 * j, by * 8, f);
+        const int x0 = bx0 * 8, y0 = by * 8;
+        asm volatile(
+            "{\n\t.reg .pred e, p1, p2, p3;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.gt.and.s32 p1, %3, 1, e;\n\t"
+            "setp.gt.and.s32 p2, %3, 2, e;\n\t"
+            "setp.gt.and.s32 p3, %3, 3, e;\n\t"
+            "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n\t"
+            "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%4, {%5, %6, %7}], [%1];\n\t"
+            "@p1 cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%8], [%4, {%9, %6, %7}], [%1];\n\t"
+            "@p2 cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%10], [%4, {%11, %6, %7}], [%1];\n\t"
+            "@p3 cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%12], [%4, {%13, %6, %7}], [%1];\n\t}"
+            ::"r"(dst), "r"(bar), "r"(static_cast<uint32_t>(nbox * 2048)), "r"(nbox), "l"(map), "r"(x0), "r"(y0),
+            "r"(f), "r"(dst + 2048), "r"(x0 + 256), "r"(dst + 4096), "r"(x0 + 512), "r"(dst + 6144), "r"(x0 + 768)
+            : "memory");
       }
     }
   } else if (warp == W_MMA) {
@@ -574,7 +618,9 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       const int s = static_cast<int>(tl % NA);
       const int buf = static_cast<int>(tl & 1);
       Q8_WAIT_MMA(&a_full[s], static_cast<uint32_t>((tl / NA) & 1));
+      if (lane == 0) QSTAMP(tl, 19);
       Q8_WAIT_MMA(&acc_empty[buf], static_cast<uint32_t>(((tl >> 1) & 1) ^ 1));
+      if (lane == 0) QSTAMP(tl, 0);
       tc_fence_after();
       const uint64_t da = da0 + DA_STAGE * s, db = db0 + DB_PLAN * pi;
       const uint32_t dt = tmem_base + 256 * buf;
@@ -589,6 +635,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
           ::"r"(dt), "l"(da), "l"(db), "r"(idesc), "l"(da + 2), "l"(db + 2), "l"(da + 4), "l"(db + 4),
           "r"(acc_full0 + 8u * buf), "r"(a_empty0 + 8u * s)
           : "memory");
+      if (lane == 0) QSTAMP(tl, 1);
     }
     __syncwarp();
   } else if (warp >= W_CONV) {
@@ -604,13 +651,16 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       if (TMA) {
         const int r = static_cast<int>(tl % NRAW);
         Q8_WAIT_OTHER(&raw_full[r], static_cast<uint32_t>((tl / NRAW) & 1));
-        if (b == 0) QSTAMP(tl, 1);
-        const uint8_t* rs = raw + r * RAWB + (b >> 5) * 2048 + (b & 31) * 8;
+        if (b == 0) QSTAMP(tl, 21);
+        // row rr of block b: four boxes [8 rows x 256 px] (TM 1) or one strip
+        // [8 rows x 1024 px] (TM 2)
+        const uint8_t* rs = TM == 2 ? raw + r * RAWB + b * 8 : raw + r * RAWB + (b >> 5) * 2048 + (b & 31) * 8;
+        constexpr int RSTRIDE = TM == 2 ? 1024 : 256;
         if (Q8_EXP == 5) {
           row[0] = row[1] = row[2] = row[3] = row[4] = row[5] = row[6] = row[7] = make_uint2(b, r);
         } else if (b < nbt && x0 + 8 <= w && y0 + 8 <= h) {
 #pragma unroll
-          for (int rr = 0; rr < 8; ++rr) row[rr] = *reinterpret_cast<const uint2*>(rs + rr * 256);
+          for (int rr = 0; rr < 8; ++rr) row[rr] = *reinterpret_cast<const uint2*>(rs + rr * RSTRIDE);
         } else if (b < nbt) {  // ragged block: tile()'s edge replication inside the strip
           const uint8_t* rb = raw + r * RAWB;
 #pragma unroll
@@ -620,7 +670,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const int cx = min(b * 8 + c, w - 1 - bx0 * 8);
-              const uint32_t v = rb[(cx >> 8) * 2048 + ry * 256 + (cx & 255)];
+              const uint32_t v = TM == 2 ? rb[ry * 1024 + cx] : rb[(cx >> 8) * 2048 + ry * 256 + (cx & 255)];
               if (c < 4) lo |= v << (8 * c);
               else hi |= v << (8 * (c - 4));
             }
@@ -651,7 +701,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       }
       const int s = static_cast<int>(tl % NA);
       Q8_WAIT_OTHER(&a_empty[s], static_cast<uint32_t>(((tl / NA) & 1) ^ 1));
-      if (b == 0) QSTAMP(tl, 2);
+      if (b == 0) QSTAMP(tl, 22);
       if (b < nbt && Q8_EXP != 5) {
         uint8_t* arow = asm_ + s * ABYTES + b * ROWB;
 #pragma unroll
@@ -661,7 +711,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&a_full[s]);
-      if (b == 0) QSTAMP(tl, 9);
+      if (b == 0) QSTAMP(tl, 18);
     }
   } else if (warp < W_FB) {
     // ---------------- epilogue: thread = block = TMEM lane; group g (warps
@@ -678,15 +728,20 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       const uint32_t U = U_s[pi];
       const int shS = shS_s[pi], shL = shL_s[pi];
       Q8_WAIT_OTHER(&acc_full[grp], static_cast<uint32_t>((tl >> 1) & 1));
-      QSTAMP_EPI(tl, 5);
       tc_fence_after();
+#ifdef QDBG
+      if (lane == 0) QSTAMP(tl, 2 + (warp - W_EPI));
+      long long* rel = (blockIdx.x < 4 && tl < 64) ? &g_qdbg[blockIdx.x][tl][10 + (warp - W_EPI)] : nullptr;
+#else
+      long long* rel = nullptr;
+#endif
       uint32_t words[16];
       uint32_t mn0 = 0xFFFFFFFFu, mn1 = 0xFFFFFFFFu;
       int32_t va[32], vb[32];
       // row r is processed while row r + 1 streams in from TMEM
-      if (shL == 0) epi_rows<8, true>(col0, va, vb, shS, 0, U, mn0, mn1, words, &acc_empty[grp]);
-      else epi_rows<8, false>(col0, va, vb, shS, shL, U, mn0, mn1, words, &acc_empty[grp]);
-      QSTAMP_EPI(tl, 6);
+      if (shL == 0) epi_rows<8, true>(col0, va, vb, shS, 0, U, mn0, mn1, words, &acc_empty[grp], rel);
+      else epi_rows<8, false>(col0, va, vb, shS, shL, U, mn0, mn1, words, &acc_empty[grp], rel);
+      QSTAMP_EPI(tl, 26);
       // A block with an uncertain pixel is left to the fallback warp, which
       // recomputes and writes the whole block.
       const int nbt = min(TILE, bw - bx0);
@@ -705,7 +760,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       }
       const uint32_t flagged = __ballot_sync(0xFFFFFFFFu, unsure);
       if (flagged) enqueue_fallback(fq, &fq_tail, flagged, unsure, lane, ti, b);
-      QSTAMP_EPI(tl, 7);
+      QSTAMP_EPI(tl, 27);
     }
     __threadfence_block();
     __syncwarp();
@@ -841,22 +896,30 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
                    (nframes == 1 || (frame_stride & 15) == 0) && pitch < (1ull << 40) && !std::getenv("DCTF_Q_NO_TMA");
   const bool fast_out = (pitch & 7) == 0 && (reinterpret_cast<uintptr_t>(out) & 7) == 0 &&
                         (nframes == 1 || (frame_stride & 7) == 0);
+  // one 8 KB box per tile when the width allows 8-byte elements (each TMA
+  // issue holds the issuing warp's sub-partition; four per tile set the pace)
+  const int tm = !tma ? 0 : ((w & 7) == 0 && !std::getenv("DCTF_Q_TMA4")) ? 2 : 1;
   CUtensorMap imap{};
   if (tma) {
-    const dctf_status s = make_imap(&imap, in, w, h, nframes, pitch, frame_stride, 256);
+    const dctf_status s = tm == 2 ? make_imap(&imap, in, w, h, nframes, pitch, frame_stride, 128, 8)
+                                  : make_imap(&imap, in, w, h, nframes, pitch, frame_stride, 256);
     if (s != DCTF_OK) return s;
   }
-  const void* fn = tma ? reinterpret_cast<const void*>(k_fused8_q<true>) : reinterpret_cast<const void*>(k_fused8_q<false>);
+  const void* fn = tm == 2   ? reinterpret_cast<const void*>(k_fused8_q<2>)
+                   : tm == 1 ? reinterpret_cast<const void*>(k_fused8_q<1>)
+                             : reinterpret_cast<const void*>(k_fused8_q<0>);
   {
-    const dctf_status sa = ensure_dyn_smem(fn, q8::SMEM, tma ? "k_fused8_q<tma>" : "k_fused8_q<direct>");
+    const dctf_status sa = ensure_dyn_smem(fn, q8::SMEM, tm == 2 ? "k_fused8_q<tma wide>" : tm == 1 ? "k_fused8_q<tma>" : "k_fused8_q<direct>");
     if (sa != DCTF_OK) return sa;
   }
   const unsigned grid = static_cast<unsigned>(std::min<long long>(sm_count(plans[0]->device), ntiles));
   const cudaError_t e =
-      tma ? launch_pdl(k_fused8_q<true>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
-                       frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null, fb_count)
-          : launch_pdl(k_fused8_q<false>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
-                       frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null, fb_count);
+      tm == 2   ? launch_pdl(k_fused8_q<2>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
+                             frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null, fb_count)
+      : tm == 1 ? launch_pdl(k_fused8_q<1>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
+                             frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null, fb_count)
+                : launch_pdl(k_fused8_q<0>, grid, q8::THREADS, q8::SMEM, st, imap, args, in, out, w, h, pitch,
+                             frame_stride, nframes, bw, bh, ntx, fast_out, d_nan_or_null, fb_count);
   add_launches(1);
   if (e != cudaSuccess) return set_error(DCTF_CUDA_ERROR, std::string("k_fused8_q: ") + cudaGetErrorString(e));
   return DCTF_OK;
@@ -884,6 +947,10 @@ extern "C" dctf_status dctf_diag_fallback_blocks(unsigned long long* n) { return
 #ifdef QDBG
 extern "C" int dctf_qdbg_read(long long* out) {
   return cudaMemcpyFromSymbol(out, g_qdbg, sizeof(g_qdbg)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int dctf_qdbg_clear() {
+  static long long zero[4 * 64 * 32] = {};
+  return cudaMemcpyToSymbol(g_qdbg, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
 }
 #endif
 
