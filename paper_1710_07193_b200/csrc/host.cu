@@ -183,7 +183,10 @@ cudaError_t copy_images(uint8_t* dst, size_t dst_stride, size_t dst_pitch, const
 }
 
 // Host frames [0, nframes) -> device ring -> batch kernel -> host, chunks of
-// whole frames (~16 MiB). Caller validated the arguments.
+// whole frames (~32 MiB: per-chunk host work is ~20 us, so config 5 runs at
+// 92 % of the concurrent H2D + D2H bound with 32 MiB chunks against 86 % with
+// 8 MiB; ramped chunk sizes and deeper rings measured no better,
+// scripts/e2e_chunks.py). Caller validated the arguments.
 dctf_status frames_host(const dctf_plan* const* plans, int nplans, const int* pof, const uint8_t* h_in,
                         uint8_t* h_out, int nframes, int w, int h, size_t pitch, size_t frame_stride,
                         int* launches) {
@@ -191,7 +194,7 @@ dctf_status frames_host(const dctf_plan* const* plans, int nplans, const int* po
   if (nframes == 0 || w == 0 || h == 0) return DCTF_OK;
   const size_t dpitch = (static_cast<size_t>(w) + 15) & ~size_t(15);
   const size_t fbytes = dpitch * static_cast<size_t>(h);
-  const int cf = static_cast<int>(std::max<size_t>(1, std::min<size_t>(nframes, (size_t(16) << 20) / fbytes)));
+  const int cf = static_cast<int>(std::max<size_t>(1, std::min<size_t>(nframes, (size_t(32) << 20) / fbytes)));
   const int nch = (nframes + cf - 1) / cf;
   auto count = [&](int c) { return std::min(cf, nframes - c * cf); };
   return host_pipeline(
