@@ -689,6 +689,7 @@ extern "C" {
 
 dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int padding,
                              int precision, int device, dctf_plan** out) {
+  dctf::NvtxRange nvtx_range("dctf_plan_create");
   dctf::reset_launches();
   if (!out || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
@@ -714,6 +715,7 @@ dctf_status dctf_plan_create(const double* h_weights, int kr, int kc, int n, int
 dctf_status dctf_plan_create_from_pairs(const double* h_lefts, const double* h_rights, int npairs, int n,
                                         int domain, const double* h_weights, int k, int padding, int precision,
                                         int device, dctf_plan** out) {
+  dctf::NvtxRange nvtx_range("dctf_plan_create_from_pairs");
   dctf::reset_launches();
   if (!out || (npairs > 0 && (!h_lefts || !h_rights)) || !h_weights) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
@@ -738,6 +740,7 @@ dctf_status dctf_plan_create_from_pairs(const double* h_lefts, const double* h_r
 
 dctf_status dctf_plan_create_from_dump(const char* text, size_t len, int precision, int device,
                                        dctf_plan** out) {
+  dctf::NvtxRange nvtx_range("dctf_plan_create_from_dump");
   dctf::reset_launches();
   if (!out || !text) return set_error(DCTF_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
@@ -905,6 +908,7 @@ dctf_status dctf_plan_operator(const dctf_plan* p, double* h_op) {
 
 dctf_status dctf_forward(const dctf_plan* p, const uint8_t* d_img, int w, int h, size_t pitch,
                          double* d_coeffs, void* stream) {
+  dctf::NvtxRange nvtx_range("dctf_forward");
   dctf::reset_launches();
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
@@ -917,6 +921,7 @@ dctf_status dctf_forward(const dctf_plan* p, const uint8_t* d_img, int w, int h,
 
 dctf_status dctf_forward_blocks(const dctf_plan* p, const double* d_blocks, double* d_coeffs,
                                 size_t nblocks, void* stream) {
+  dctf::NvtxRange nvtx_range("dctf_forward_blocks");
   dctf::reset_launches();
   dctf_status s = check_plan(p);
   if (s != DCTF_OK) return s;
@@ -930,6 +935,7 @@ dctf_status dctf_forward_blocks(const dctf_plan* p, const double* d_blocks, doub
 
 dctf_status dctf_inverse_blocks(const dctf_plan* p, const double* d_coeffs, double* d_blocks,
                                 size_t nblocks, void* stream) {
+  dctf::NvtxRange nvtx_range("dctf_inverse_blocks");
   dctf::reset_launches();
   dctf_status s = check_plan(p);
   if (s != DCTF_OK) return s;
@@ -943,6 +949,7 @@ dctf_status dctf_inverse_blocks(const dctf_plan* p, const double* d_coeffs, doub
 
 dctf_status dctf_filter_coeffs(const dctf_plan* p, const double* d_in, double* d_out,
                                size_t nblocks, void* stream) {
+  dctf::NvtxRange nvtx_range("dctf_filter_coeffs");
   dctf::reset_launches();
   dctf_status s = check_plan(p);
   if (s != DCTF_OK) return s;
@@ -954,6 +961,7 @@ dctf_status dctf_filter_coeffs(const dctf_plan* p, const double* d_in, double* d
 
 dctf_status dctf_inverse_u8(const dctf_plan* p, const double* d_coeffs, uint8_t* d_img, int w,
                             int h, size_t pitch, void* stream) {
+  dctf::NvtxRange nvtx_range("dctf_inverse_u8");
   dctf::reset_launches();
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
@@ -966,6 +974,7 @@ dctf_status dctf_inverse_u8(const dctf_plan* p, const double* d_coeffs, uint8_t*
 
 dctf_status dctf_filter_image_u8(const dctf_plan* p, const uint8_t* d_in, uint8_t* d_out, int w,
                                  int h, size_t pitch, double* d_coeffs_out, void* stream) {
+  dctf::NvtxRange nvtx_range("dctf_filter_image_u8");
   dctf::reset_launches();
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
@@ -979,6 +988,7 @@ dctf_status dctf_filter_image_u8(const dctf_plan* p, const uint8_t* d_in, uint8_
 
 dctf_status dctf_filter_image_spatial_u8(const dctf_plan* p, const uint8_t* d_in, uint8_t* d_out,
                                          int w, int h, size_t pitch, void* stream) {
+  dctf::NvtxRange nvtx_range("dctf_filter_image_spatial_u8");
   dctf::reset_launches();
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
@@ -1024,6 +1034,7 @@ dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
                                   const int* h_plan_of_frame, const uint8_t* d_in, uint8_t* d_out,
                                   int nframes, int w, int h, size_t pitch, size_t frame_stride,
                                   void* stream) {
+  dctf::NvtxRange nvtx_range("dctf_filter_frames_u8");
   dctf::reset_launches();
   if (!plans || nplans < 1 || !h_plan_of_frame || nframes < 0)
     return set_error(DCTF_INVALID_ARGUMENT, "bad plan list");
@@ -1048,6 +1059,7 @@ dctf_status dctf_filter_frames_u8(const dctf_plan* const* plans, int nplans,
 
 dctf_status dctf_filter_image_host(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w,
                                    int h, size_t pitch) {
+  dctf::NvtxRange nvtx_range("dctf_filter_image_host");
   dctf::reset_launches();
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
@@ -1295,6 +1307,7 @@ dctf_status dctf_filter_blocks_host(const dctf_plan* p, const double* h_in, doub
 
 dctf_status dctf_filter_image_spatial_host(const dctf_plan* p, const uint8_t* h_in, uint8_t* h_out, int w,
                                            int h, size_t pitch) {
+  dctf::NvtxRange nvtx_range("dctf_filter_image_spatial_host");
   dctf_status s = check_plan(p);
   if (s == DCTF_OK) s = check_image(w, h, pitch);
   if (s != DCTF_OK) return s;

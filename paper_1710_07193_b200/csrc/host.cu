@@ -364,6 +364,7 @@ extern "C" {
 dctf_status dctf_filter_frames_host(const dctf_plan* const* plans, int nplans, const int* h_plan_of_frame,
                                     const uint8_t* h_in, uint8_t* h_out, int nframes, int width, int height,
                                     size_t pitch, size_t frame_stride) {
+  dctf::NvtxRange nvtx_range("dctf_filter_frames_host");
   dctf::reset_launches();
   dctf_status s = check_frames(plans, nplans, h_plan_of_frame, nframes, width, height, pitch, frame_stride);
   if (s != DCTF_OK) return s;
@@ -379,6 +380,7 @@ dctf_status dctf_filter_frames_host(const dctf_plan* const* plans, int nplans, c
 
 dctf_status dctf_multi_create(const double* h_weights, int kr, int kc, int n, int padding, int precision,
                               const int* devices, int ndevices, dctf_multi** out) {
+  dctf::NvtxRange nvtx_range("dctf_multi_create");
   if (!out || !devices || ndevices < 1) return set_error(DCTF_INVALID_ARGUMENT, "bad device list");
   *out = nullptr;
   auto* m = new dctf_multi();
@@ -420,6 +422,7 @@ dctf_status dctf_multi_replica(const dctf_multi* m, int r, const dctf_plan** out
 
 dctf_status dctf_filter_image_host_multi(const dctf_multi* m, const uint8_t* h_in, uint8_t* h_out, int width,
                                          int height, size_t pitch) {
+  dctf::NvtxRange nvtx_range("dctf_filter_image_host_multi");
   dctf::reset_launches();
   if (!m) return set_error(DCTF_INVALID_ARGUMENT, "plan is NULL");
   if (width < 0 || height < 0) return set_error(DCTF_INVALID_ARGUMENT, "image dimensions must be >= 0");
@@ -449,6 +452,7 @@ dctf_status dctf_filter_image_host_multi(const dctf_multi* m, const uint8_t* h_i
 dctf_status dctf_filter_frames_host_multi(const dctf_multi* const* ms, int nplans, const int* h_plan_of_frame,
                                           const uint8_t* h_in, uint8_t* h_out, int nframes, int width, int height,
                                           size_t pitch, size_t frame_stride) {
+  dctf::NvtxRange nvtx_range("dctf_filter_frames_host_multi");
   dctf::reset_launches();
   dctf_status s = check_multi_list(ms, nplans);
   if (s != DCTF_OK) return s;
@@ -475,6 +479,7 @@ dctf_status dctf_filter_frames_u8_multi(const dctf_multi* const* ms, int nplans,
                                         const uint8_t* const* d_in, uint8_t* const* d_out, int nframes, int width,
                                         int height, size_t pitch, size_t frame_stride, uint8_t* const* d_gather,
                                         void* const* streams) {
+  dctf::NvtxRange nvtx_range("dctf_filter_frames_u8_multi");
   dctf::reset_launches();
   dctf_status s = check_multi_list(ms, nplans);
   if (s != DCTF_OK) return s;

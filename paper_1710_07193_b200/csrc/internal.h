@@ -12,6 +12,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost a few ns without a tool attached
 
 #include "../../include/dctf.h"
 
@@ -76,6 +77,15 @@ struct dctf_plan {
 };
 
 namespace dctf {
+
+// NVTX range over one C-ABI entry (nsys / ncu --nvtx show the host-side
+// structure: plan compile, host pipelines, device launches).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Thread-local error / launch bookkeeping (capi.cu).
 dctf_status set_error(dctf_status s, const std::string& msg);
