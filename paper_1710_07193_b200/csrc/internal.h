@@ -184,6 +184,7 @@ struct KqInfo {
   uint32_t U = 0;
   double ebound = 0.0, flag_rate = 0.0;
   double margin = 0.0;       // second-stage window: reference FP64 deviation + our FP64 dot error
+  double eref = 0.0;         // rigorous bound of the reference chain's FP64 deviation (pixel units)
   std::vector<double> kt;    // the composed operator K in FP64, transposed (kt[j * 64 + i] = K[i][j])
 };
 bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info);

@@ -1034,6 +1034,76 @@ namespace dctf {
 // n = 4 i + s holds digit s of output pixel i (bytes 0-63: the 64 input
 // pixels; bytes 64-65: the rounding offset's digits), so one 32-column
 // tcgen05.ld returns 8 whole pixels.
+// Rigorous forward error bound of the reference's FP64 chain on u8 blocks,
+// per output sample (max over the block), by the standard model
+// |fl(A B) - A B| <= gamma_n |A| |B| with gamma_n = n u / (1 - n u), u = 2^-53,
+// propagated through the stages with absolute-value matrices (long double):
+//   T = C X, F = T C^t (forward_2d, dct.hpp:59-62), per pair U = L F,
+//   V = U R, acc += V (apply_pairs, filter.hpp:30-38), W = C^t acc, Z = W C
+//   (inverse_2d, dct.hpp:65-68); |X| <= 255. The zero-skips of
+// block_matrix.hpp:67-81 only drop exact zero terms. Convolve-formula plans:
+// z = sum of kr kc products in tap order, |err| <= gamma_{kr kc} 255 sum|w|.
+// Plus 64 x 2^-1022 for gradual underflow.
+static long double reference_error_bound(const dctf_plan& p) {
+  const int n = p.n, nn = n * n;
+  const long double u = std::ldexp(1.0L, -53);
+  auto gamma = [&](int k) { return k * u / (1.0L - k * u); };
+  const long double tiny = 64.0L * std::ldexp(1.0L, -1022);
+  if (p.dct_left.empty() && !(p.reference_domain && p.npairs == 0)) {
+    long double s = 0.0L;
+    for (double w : p.weights) s += std::fabs(static_cast<long double>(w));
+    return gamma(p.kr * p.kc) * 255.0L * s + tiny;
+  }
+  using Mat = std::vector<long double>;
+  auto mul = [&](const Mat& a, const Mat& b) {  // |A| |B| of bound matrices
+    Mat c(size_t(nn), 0.0L);
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < n; ++k)
+        for (int j = 0; j < n; ++j) c[size_t(i) * n + j] += a[size_t(i) * n + k] * b[size_t(k) * n + j];
+    return c;
+  };
+  auto add = [&](const Mat& a, const Mat& b, long double sb = 1.0L) {
+    Mat c(a);
+    for (int e = 0; e < nn; ++e) c[size_t(e)] += sb * b[size_t(e)];
+    return c;
+  };
+  auto scale = [&](const Mat& a, long double f) {
+    Mat c(a);
+    for (long double& v : c) v *= f;
+    return c;
+  };
+  Mat C(nn), Ct(nn), X(size_t(nn), 255.0L);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      C[size_t(i) * n + j] = std::fabs(static_cast<long double>(p.basis[size_t(i) * n + j]));
+      Ct[size_t(j) * n + i] = C[size_t(i) * n + j];
+    }
+  const long double g = gamma(n);
+  // value bounds (V*) and error bounds (E*) per stage
+  Mat VT = mul(C, X), ET = scale(VT, g);
+  Mat VF = mul(VT, Ct), EF = add(mul(ET, Ct), scale(VF, g));
+  const int np = static_cast<int>(p.dct_left.size() / nn);
+  Mat Vacc(size_t(nn), 0.0L), Eacc(size_t(nn), 0.0L), sumV(size_t(nn), 0.0L);
+  for (int q = 0; q < np; ++q) {
+    Mat L(nn), R(nn);
+    for (int e = 0; e < nn; ++e) {
+      L[size_t(e)] = std::fabs(static_cast<long double>(p.dct_left[size_t(q) * nn + e]));
+      R[size_t(e)] = std::fabs(static_cast<long double>(p.dct_right[size_t(q) * nn + e]));
+    }
+    Mat VU = mul(L, VF), EU = add(mul(L, EF), scale(VU, g));
+    Mat VV = mul(VU, R), EV = add(mul(EU, R), scale(VV, g));
+    Eacc = add(Eacc, EV);
+    sumV = add(sumV, VV);
+  }
+  Eacc = add(Eacc, scale(sumV, gamma(std::max(1, np))));  // the running sum's own roundings
+  Vacc = sumV;
+  Mat VW = mul(Ct, Vacc), EW = add(mul(Ct, Eacc), scale(VW, g));
+  Mat VZ = mul(VW, C), EZ = add(mul(EW, C), scale(VZ, g));
+  long double mx = 0.0L;
+  for (long double v : EZ) mx = std::max(mx, v);
+  return mx + tiny;
+}
+
 bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   info = KqInfo{};
   if (p.n != 8) return false;
@@ -1096,6 +1166,8 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   if (F < 17) return false;
   const long double scale = std::ldexp(1.0L, F);
   std::vector<long long> Ki(K.size());
+  // the reference's own FP64 deviation from the exact chain (rigorous bound)
+  const long double eref = reference_error_bound(p);
   long double emax = 0.0L;
   for (int i = 0; i < nn; ++i) {
     long double err = 0.0L, mag = 0.0L;
@@ -1106,7 +1178,7 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
       err += std::fabs(v - static_cast<long double>(q));
       mag += std::fabs(K[size_t(i) * nn + j]);
     }
-    const long double e = 255.0L * err / scale + std::ldexp(1.0L, -30) + std::ldexp(1.0L, -36) * 255.0L * mag;
+    const long double e = 255.0L * err / scale + eref + std::ldexp(1.0L, -60) * 255.0L * mag;
     emax = std::max(emax, e);
   }
   const long double T = std::ceil(emax * scale) + 1.0L;
@@ -1142,16 +1214,18 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   // Second stage (the fallback warp's first step on a flagged block): z_i =
   // sum_j K_ij p_j in FP64 from K rounded to double, sequential FMAs. Its
   // error is <= (64 + 1) 2^-53 * 255 * sum_j |K_ij| (< 2^-46 * 255 * mag); a
-  // pixel farther than that plus the reference's own FP64 deviation (the M
-  // of the first window: 2^-30 + 2^-36 * 255 * mag) from a .5 boundary rounds
-  // as the reference does. The rest go through the reference-order chain.
+  // pixel farther than that plus the reference's own FP64 deviation (eref,
+  // reference_error_bound) plus K's long-double composition error from a .5
+  // boundary rounds as the reference does. The rest go through the
+  // reference-order chain.
   long double magmax = 0.0L;
   for (int i = 0; i < nn; ++i) {
     long double mag = 0.0L;
     for (int j = 0; j < nn; ++j) mag += std::fabs(K[size_t(i) * nn + j]);
     magmax = std::max(magmax, mag);
   }
-  info.margin = static_cast<double>(std::ldexp(1.0L, -30) + (std::ldexp(1.0L, -36) + std::ldexp(1.0L, -44)) * 255.0L * magmax);
+  info.margin = static_cast<double>(eref + (std::ldexp(1.0L, -46) + std::ldexp(1.0L, -60)) * 255.0L * magmax);
+  info.eref = static_cast<double>(eref);
   info.kt.assign(size_t(nn) * nn, 0.0);
   for (int i = 0; i < nn; ++i)
     for (int j = 0; j < nn; ++j) info.kt[size_t(j) * nn + i] = static_cast<double>(K[size_t(i) * nn + j]);

@@ -59,6 +59,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -865,6 +866,10 @@ dctf_status upload_kq_operator(dctf_plan* p) {
   p->kq_ebound = info.ebound;
   p->kq_flag_rate = info.flag_rate;
   p->kq_margin = info.margin;
+  if (std::getenv("DCTF_Q_DEBUG"))
+    std::fprintf(stderr, "[k_fused8_q plan] F=%d U=%u window=%.3e (reference FP64 bound %.3e) second-stage margin=%.3e "
+                         "expected flagged blocks %.2e\n", info.F, info.U, info.ebound, info.eref, info.margin,
+                 info.flag_rate);
   return DCTF_OK;
 }
 
