@@ -10,10 +10,14 @@ namespace dctf {
 struct FastDiv {
   uint32_t d, m, s;
 };
-__device__ __forceinline__ FastDiv make_fastdiv(uint32_t d) {
+__host__ __device__ __forceinline__ FastDiv make_fastdiv(uint32_t d) {
   FastDiv f{d, 0u, 0u};
   if (d > 1) {
+#ifdef __CUDA_ARCH__
     const uint32_t l = 32u - static_cast<uint32_t>(__clz(d - 1));  // ceil(log2 d)
+#else
+    const uint32_t l = 32u - static_cast<uint32_t>(__builtin_clz(d - 1));
+#endif
     const uint32_t p = 31u + l;
     f.m = static_cast<uint32_t>(((1ull << p) + d - 1) / d);
     f.s = p - 32u;

@@ -152,6 +152,7 @@ struct QArgs {
   int shS[KQ_MAX_PLANS], shL[KQ_MAX_PLANS];  // F - 16, 32 - F
   RefPlan ref[KQ_MAX_PLANS];
   int nplans;
+  dctf::FastDiv fd_tpf, fd_ntx;  // tile -> (frame, block row, tile column), made on the host
   uint8_t pof[KQ_MAX_FRAMES];  // plan of frame
 };
 
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   uint8_t* raw = asm_ + NA * ABYTES;                  // raw pixel stages
   __shared__ uint64_t raw_full[NRAW], raw_empty[NRAW], a_full[NA], a_empty[NA], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_s;
+  __shared__ uint64_t ops_full;  // the plans' digit images have landed
   __shared__ unsigned long long fq[FQ];
   __shared__ uint32_t fq_tail, fq_head, fq_done;
   __shared__ __align__(16) double fb_sm[256];
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   pdl_trigger();
-  for (int pi = 0; pi < args.nplans; ++pi) cta_copy_async(bsm + pi * BBYTES, args.bimg[pi], BBYTES);
+  if (threadIdx.x == 0) QSTAMP(0, 28);
   for (int i = threadIdx.x; i < FQ; i += blockDim.x) fq[i] = 0ull;
   for (int i = threadIdx.x; i < nframes; i += blockDim.x) pof_s[i] = args.pof[i];
   if (threadIdx.x < KQ_MAX_PLANS) {
@@ -480,23 +482,36 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 32 * 4);  // the four warps of epilogue group i
     }
+    mbar_init(&ops_full, 1);
     fq_tail = 0;
     fq_head = 0;
     fq_done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the plans' digit images (plan-owned, written only at plan creation, so
+    // safe before pdl_wait): one bulk copy each, completing on ops_full,
+    // which only the MMA warp waits for; the TMA loads and conversion of the
+    // first tiles proceed meanwhile
+    mbar_expect_tx(&ops_full, static_cast<uint32_t>(args.nplans * BBYTES));
+    for (int pi = 0; pi < args.nplans; ++pi)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(bsm + pi * BBYTES)),
+          "l"(reinterpret_cast<uint64_t>(args.bimg[pi])), "r"(static_cast<uint32_t>(BBYTES)), "r"(smem_u32(&ops_full))
+          : "memory");
   }
-  cp_async_wait_all();
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
   pdl_wait();
+  if (threadIdx.x == 0) QSTAMP(0, 29);
 
   const long long tpf = static_cast<long long>(bh) * ntx;  // tiles per frame
   const long long ntiles = tpf * nframes;                  // < 2^31 (launcher)
-  const dctf::FastDiv fd_tpf = dctf::make_fastdiv(static_cast<uint32_t>(tpf)),
-                      fd_ntx = dctf::make_fastdiv(static_cast<uint32_t>(ntx));
+  // the divisors' magic numbers come precomputed (a 64-bit division per thread here cost ~1,000 cycles of the
+  // prologue)
+  const dctf::FastDiv fd_tpf = args.fd_tpf, fd_ntx = args.fd_ntx;
   auto tile_at = [&](long long ti, int& f, int& by, int& bx0) {
     const uint32_t u = static_cast<uint32_t>(ti);
     f = static_cast<int>(dctf::fdiv(fd_tpf, u));
@@ -526,7 +541,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
           if (slot >= *reinterpret_cast<volatile uint32_t*>(&fq_tail)) return;
         }
         __nanosleep(nap);
-        nap = min(nap * 2u, 2048u);
+        nap = min(nap * 2u, 256u);  // short: the kernel cannot end while this warp sleeps
       }
       nap = 64;
       __syncwarp();
@@ -611,6 +626,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     const uint64_t da0 = desc_sw128(smem_u32(asm_)), db0 = desc_sw128(smem_u32(bsm));
     constexpr uint64_t DA_STAGE = ABYTES >> 4, DB_PLAN = BBYTES >> 4;
     const uint32_t acc_full0 = smem_u32(&acc_full[0]), a_empty0 = smem_u32(&a_empty[0]);
+    Q8_WAIT_MMA(&ops_full, 0u);
     long long tl = 0;
     for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
       int f, by, bx0;
@@ -769,19 +785,23 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   } else {
     // ---------------- fallback warp: reference-order chain on queued blocks
     drain(fb_sm);
+    if (lane == 0) QSTAMP(1, 28);
   }
   if (warp != W_FB) {
     // Every tile of this CTA is done once all 14 other warps get here (the
     // epilogue waited for the last MMA, the converters consumed every raw
     // stage): the rest of the queue is drained by all warps in parallel, each
     // with 2 KB of scratch in the now idle raw ring.
+    if (threadIdx.x == 0) QSTAMP(0, 30);
     asm volatile("bar.sync 1, %0;" ::"n"(THREADS - 32) : "memory");
+    if (threadIdx.x == 0) QSTAMP(1, 29);
     const int slot = warp < W_FB ? warp : warp - 1;
     drain(reinterpret_cast<double*>(raw + slot * 2048));
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) QSTAMP(0, 31);
   if (warp == W_MMA)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
@@ -897,6 +917,8 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
                           p->kc, p->padding};
   }
   for (int f = 0; f < nframes; ++f) args.pof[f] = static_cast<uint8_t>(plan_of_frame ? plan_of_frame[f] : 0);
+  args.fd_tpf = dctf::make_fastdiv(static_cast<uint32_t>(static_cast<long long>(bh) * ntx));
+  args.fd_ntx = dctf::make_fastdiv(static_cast<uint32_t>(ntx));
   const bool tma = !host_mapped && (pitch & 15) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
                    (nframes == 1 || (frame_stride & 15) == 0) && pitch < (1ull << 40) && !std::getenv("DCTF_Q_NO_TMA");
   const bool fast_out = (pitch & 7) == 0 && (reinterpret_cast<uintptr_t>(out) & 7) == 0 &&
