@@ -123,3 +123,20 @@ def test_kq_frames_one_launch(P, ref, oracle):
         w, k, kc = masks[f % 4]
         r = _reference(ref, oracle, frames[f], w, k, kc, 1)
         assert int(np.count_nonzero(out[f] != r)) == 0, f
+
+
+@pytest.mark.parametrize("pad", [0, 1])
+def test_kq_dyadic_ties(P, ref, pad):
+    """3x3 masks of weights k/8: outputs are multiples of 1/8 in exact
+    arithmetic, so about one pixel in eight sits exactly on a .5 boundary and
+    the reference's rounding there is decided by its own FP64 noise. Those
+    blocks must pass the integer window, the FP64 first stage (the rigorous
+    bound of the reference's deviation, plan.cc: reference_error_bound) and
+    be settled by the reference-order chain, pixel for pixel."""
+    from paper_1710_07193_b200 import synth
+    img = synth.uniform_image(11 + pad, 512, 384)
+    for w in (np.array([1, 1, 1, 1, 0, 1, 1, 1, 1]) / 8.0, np.array([0, 1, 0, 2, 3, 1, 0, 1, 0]) / 8.0):
+        plan, out = _run(P, img, w, 3, 3, pad)
+        assert plan.image_kernel == "k_fused8_q"
+        r = ref.filter_image(img, w, 3, pad, 8, threads=nthreads())
+        assert int(np.count_nonzero(out != r)) == 0
