@@ -119,7 +119,7 @@ constexpr int NGRP = 2;
 // picks the highest eligible warp id first, so the short, latency-critical
 // roles (MMA issue, TMA, the converters that feed the MMA, the fallback warp
 // that keeps the flagged-block queue short) sit above the ALU-heavy epilogue.
-constexpr int W_EPI = 0, NEPI = 4 * NGRP, W_FB = W_EPI + NEPI, W_CONV = W_FB + 1, NCONV = 4,
+constexpr int W_EPI = 0, NEPI = 4 * NGRP, W_FB = W_EPI + NEPI, W_CONV = W_FB + 1, NCONV = 2,
               W_TMA = W_CONV + NCONV, W_MMA = W_TMA + 1;
 constexpr int THREADS = 32 * (W_MMA + 1);
 constexpr int FQ = 256;                    // fallback queue slots
@@ -656,79 +656,95 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     }
     __syncwarp();
   } else if (warp >= W_CONV) {
-    // ---------------- converters: thread = block b of the tile
-    const int b = threadIdx.x - 32 * W_CONV;
+    // ---------------- converters: thread = the block pair (2 c2, 2 c2 + 1) of
+    // the tile: one 16-byte shared load per pixel row covers both blocks
+    // (adjacent 8-byte rows of the strip), four 16-byte A-operand stores each
+    const int c2 = threadIdx.x - 32 * W_CONV;
     long long tl = 0;
     for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
       int f, by, bx0;
       tile_at(ti, f, by, bx0);
       const int nbt = min(TILE, bw - bx0);
-      const int y0 = by * 8, x0 = (bx0 + b) * 8;
-      uint2 row[8];
+      const int y0 = by * 8;
+      // row[rr] = {block 2 c2 row rr (x, y), block 2 c2 + 1 row rr (z, w)}
+      uint4 row[8];
+      const bool full = 2 * c2 + 1 < nbt && (bx0 + 2 * c2 + 2) * 8 <= w && y0 + 8 <= h;
+      // one block of the pair through tile()'s edge replication (ragged
+      // edges), from the staged strip (TMA) or from global memory
+      auto ragged = [&](int bb, const uint8_t* rb, int half) {
+        const int x0 = (bx0 + bb) * 8;
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          uint32_t lo = 0, hi = 0;
+          if (bb < nbt) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              uint32_t v;
+              if (rb) {
+                const int ry = min(rr, h - 1 - y0), cx = min(bb * 8 + c, w - 1 - bx0 * 8);
+                v = TM == 2 ? rb[ry * 1024 + cx] : rb[(cx >> 8) * 2048 + ry * 256 + (cx & 255)];
+              } else {
+                v = in[f * frame_stride + static_cast<size_t>(min(y0 + rr, h - 1)) * pitch + min(x0 + c, w - 1)];
+              }
+              if (c < 4) lo |= v << (8 * c);
+              else hi |= v << (8 * (c - 4));
+            }
+          }
+          if (half == 0) {
+            row[rr].x = lo;
+            row[rr].y = hi;
+          } else {
+            row[rr].z = lo;
+            row[rr].w = hi;
+          }
+        }
+      };
       if (TMA) {
         const int r = static_cast<int>(tl % NRAW);
         Q8_WAIT_OTHER(&raw_full[r], static_cast<uint32_t>((tl / NRAW) & 1));
-        if (b == 0) QSTAMP(tl, 21);
-        // row rr of block b: four boxes [8 rows x 256 px] (TM 1) or one strip
-        // [8 rows x 1024 px] (TM 2)
+        if (c2 == 0) QSTAMP(tl, 21);
+        // row rr of blocks 2 c2, 2 c2 + 1: four boxes [8 rows x 256 px] (TM 1)
+        // or one strip [8 rows x 1024 px] (TM 2)
+        const int b = 2 * c2;
         const uint8_t* rs = TM == 2 ? raw + r * RAWB + b * 8 : raw + r * RAWB + (b >> 5) * 2048 + (b & 31) * 8;
         constexpr int RSTRIDE = TM == 2 ? 1024 : 256;
-        if (Q8_EXP == 5) {
-          row[0] = row[1] = row[2] = row[3] = row[4] = row[5] = row[6] = row[7] = make_uint2(b, r);
-        } else if (b < nbt && x0 + 8 <= w && y0 + 8 <= h) {
+        if (full) {
 #pragma unroll
-          for (int rr = 0; rr < 8; ++rr) row[rr] = *reinterpret_cast<const uint2*>(rs + rr * RSTRIDE);
-        } else if (b < nbt) {  // ragged block: tile()'s edge replication inside the strip
-          const uint8_t* rb = raw + r * RAWB;
-#pragma unroll
-          for (int rr = 0; rr < 8; ++rr) {
-            const int ry = min(rr, h - 1 - y0);
-            uint32_t lo = 0, hi = 0;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const int cx = min(b * 8 + c, w - 1 - bx0 * 8);
-              const uint32_t v = TM == 2 ? rb[ry * 1024 + cx] : rb[(cx >> 8) * 2048 + ry * 256 + (cx & 255)];
-              if (c < 4) lo |= v << (8 * c);
-              else hi |= v << (8 * (c - 4));
-            }
-            row[rr] = make_uint2(lo, hi);
-          }
+          for (int rr = 0; rr < 8; ++rr) row[rr] = *reinterpret_cast<const uint4*>(rs + rr * RSTRIDE);
+        } else if (2 * c2 < nbt) {
+          ragged(2 * c2, raw + r * RAWB, 0);
+          ragged(2 * c2 + 1, raw + r * RAWB, 1);
         }
         mbar_arrive(&raw_empty[r]);
-      } else if (b < nbt) {  // direct loads (unaligned views, host-mapped input)
-        const uint8_t* ib = in + f * frame_stride;
-        const bool fast = x0 + 8 <= w && y0 + 8 <= h && ((reinterpret_cast<uintptr_t>(ib + x0) & 7) == 0) &&
-                          ((pitch & 7) == 0);
+      } else if (2 * c2 < nbt) {  // direct loads (unaligned views, host-mapped input)
+        const uint8_t* ib = in + f * frame_stride + (bx0 + 2 * c2) * 8;
+        if (full && ((reinterpret_cast<uintptr_t>(ib) & 15) == 0) && ((pitch & 15) == 0)) {
 #pragma unroll
-        for (int rr = 0; rr < 8; ++rr) {
-          const int yy = min(y0 + rr, h - 1);
-          if (fast) {
-            row[rr] = __ldg(reinterpret_cast<const uint2*>(ib + static_cast<size_t>(yy) * pitch + x0));
-          } else {
-            uint32_t lo = 0, hi = 0;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const uint32_t v = ib[static_cast<size_t>(yy) * pitch + min(x0 + c, w - 1)];
-              if (c < 4) lo |= v << (8 * c);
-              else hi |= v << (8 * (c - 4));
-            }
-            row[rr] = make_uint2(lo, hi);
-          }
+          for (int rr = 0; rr < 8; ++rr)
+            row[rr] = __ldg(reinterpret_cast<const uint4*>(ib + static_cast<size_t>(y0 + rr) * pitch));
+        } else {
+          ragged(2 * c2, nullptr, 0);
+          ragged(2 * c2 + 1, nullptr, 1);
         }
       }
       const int s = static_cast<int>(tl % NA);
       Q8_WAIT_OTHER(&a_empty[s], static_cast<uint32_t>(((tl / NA) & 1) ^ 1));
-      if (b == 0) QSTAMP(tl, 22);
-      if (b < nbt && Q8_EXP != 5) {
-        uint8_t* arow = asm_ + s * ABYTES + b * ROWB;
+      if (c2 == 0) QSTAMP(tl, 22);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4*>(arow + ((q ^ (b & 7)) << 4)) =
-              make_uint4(row[2 * q].x, row[2 * q].y, row[2 * q + 1].x, row[2 * q + 1].y);
+      for (int hb = 0; hb < 2; ++hb) {
+        const int b = 2 * c2 + hb;
+        if (b < nbt && Q8_EXP != 5) {
+          uint8_t* arow = asm_ + s * ABYTES + b * ROWB;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(arow + ((q ^ (b & 7)) << 4)) =
+                hb == 0 ? make_uint4(row[2 * q].x, row[2 * q].y, row[2 * q + 1].x, row[2 * q + 1].y)
+                        : make_uint4(row[2 * q].z, row[2 * q].w, row[2 * q + 1].z, row[2 * q + 1].w);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&a_full[s]);
-      if (b == 0) QSTAMP(tl, 18);
+      if (c2 == 0) QSTAMP(tl, 18);
     }
   } else if (warp < W_FB) {
     // ---------------- epilogue: thread = block = TMEM lane; group g (warps
