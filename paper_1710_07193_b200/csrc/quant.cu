@@ -31,18 +31,20 @@
 //   uncertain  <=>  (key + U) mod 2^32 < 2U,  U = T 2^(32-F)
 // so the per-block test is a running unsigned min.
 //
-// CTA = 15 warps, one CTA per SM (TMEM: 2 x 256 columns), persistent over
+// CTA = 13 warps, one CTA per SM (TMEM: 2 x 256 columns), persistent over
 // tiles of up to 128 horizontally adjacent blocks (one block row, 8 x 1024 px).
 // Roles in issue-priority order (highest warp id first):
-//   warp 14     MMA issuer: the whole warp runs the loop, one elected lane
+//   warp 12     MMA issuer: the whole warp runs the loop, one elected lane
 //               issues the tile's 3 x tcgen05.mma (M 128, N 256, K 32) and two
 //               commits in one asm block, into a double-buffered accumulator.
-//   warp 13     TMA: 4 boxes [8 rows x 256 px] per tile into a 6-stage raw ring
-//               (48 KB of pixels in flight per SM); a 3-D tensor map covers
-//               the whole frame batch, out-of-range rows/columns read as 0.
-//   warps 9-12  converters: thread = block; the block's 8 pixel rows from the
-//               raw stage (tile()'s edge replication for ragged blocks) into the
-//               K-major 128-byte-swizzled A operand.
+//   warp 11     TMA: one 8 KB box [8 rows x 1024 px] per tile (4 boxes of
+//               256 px when the width is not a multiple of 8) into a 6-stage
+//               raw ring (48 KB of pixels in flight per SM); a 3-D tensor map
+//               covers the whole frame batch, out-of-range pixels read as 0.
+//   warps 9-10  converters: thread = a pair of adjacent blocks; one 16-byte
+//               shared load per pixel row covers both (tile()'s edge
+//               replication for ragged blocks), written into the K-major
+//               128-byte-swizzled A operand.
 //   warp 8      fallback: flagged blocks from the CTA's queue (FP64 first
 //               stage, reference-order chain for near-ties); after the last
 //               tile every warp drains what is left.
@@ -52,7 +54,7 @@
 //               per pixel row, the integer rounding above, cvt.pack.sat,
 //               8-byte coalesced row stores. Blocks with an uncertain pixel
 //               are not stored here; they go to the fallback queue.
-// The plans' digit images (16 KB each, up to 4 plans: one launch covers a
+// The plans' digit images (32 KB each, up to 4 plans: one launch covers a
 // whole multi-mask frame batch) stay resident in shared memory.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -270,6 +272,14 @@ __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32
     }
   }
 }
+
+// A-operand row (= MMA row = TMEM lane) of block b of the tile, an
+// involution: bit 0 flipped when bit 3 is set. A converter store instruction
+// writes blocks 2 c2 + hb of its 32 threads; with the identity map their rows
+// fell on 4 of the 8 128B-swizzle phases (2-way bank conflicts on every A
+// store), with this map on all 8. The epilogue's lanes see the same 32
+// blocks in a permuted order, so its row stores stay one 256-byte segment.
+__device__ __forceinline__ int a_row(int b) { return b ^ ((b >> 3) & 1); }
 
 // Cropped byte stores of ROWS rows (image edges, unaligned outputs).
 template <int ROWS>
@@ -732,12 +742,12 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       if (c2 == 0) QSTAMP(tl, 22);
 #pragma unroll
       for (int hb = 0; hb < 2; ++hb) {
-        const int b = 2 * c2 + hb;
+        const int b = 2 * c2 + hb, m = a_row(b);
         if (b < nbt && Q8_EXP != 5) {
-          uint8_t* arow = asm_ + s * ABYTES + b * ROWB;
+          uint8_t* arow = asm_ + s * ABYTES + m * ROWB;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<uint4*>(arow + ((q ^ (b & 7)) << 4)) =
+            *reinterpret_cast<uint4*>(arow + ((q ^ (m & 7)) << 4)) =
                 hb == 0 ? make_uint4(row[2 * q].x, row[2 * q].y, row[2 * q + 1].x, row[2 * q + 1].y)
                         : make_uint4(row[2 * q].z, row[2 * q].w, row[2 * q + 1].z, row[2 * q + 1].w);
         }
@@ -750,7 +760,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     // ---------------- epilogue: thread = block = TMEM lane; group g (warps
     // W_EPI + 4g .. + 3, one per lane quarter) drains accumulator buffer g,
     // i.e. the CTA's tiles tl = g, g + 2, ...
-    const int qd = warp & 3, grp = (warp - W_EPI) >> 2, b = 32 * qd + lane;
+    const int qd = warp & 3, grp = (warp - W_EPI) >> 2, b = a_row(32 * qd + lane);  // TMEM lane -> block
     const uint32_t col0 = tmem_base + (static_cast<uint32_t>(32 * qd) << 16) + 256 * grp;
     long long tl = grp;
     for (long long ti = blockIdx.x + static_cast<long long>(grp) * gridDim.x; ti < ntiles;
@@ -804,7 +814,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     if (lane == 0) QSTAMP(1, 28);
   }
   if (warp != W_FB) {
-    // Every tile of this CTA is done once all 14 other warps get here (the
+    // Every tile of this CTA is done once all 12 other warps get here (the
     // epilogue waited for the last MMA, the converters consumed every raw
     // stage): the rest of the queue is drained by all warps in parallel, each
     // with 2 KB of scratch in the now idle raw ring.
