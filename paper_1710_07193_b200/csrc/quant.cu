@@ -83,7 +83,7 @@ namespace {
 #ifndef QDBG_T0
 #define QDBG_T0 0
 #endif
-__device__ long long g_qdbg[4][64][32];
+__device__ long long g_qdbg[4][64][48];  // 32 + w: end of epilogue warp w's tile iteration
 #define QSTAMP(tl, ev)                                                                                  \
   do {                                                                                                  \
     if (blockIdx.x < 4 && (tl) >= QDBG_T0 && (tl) < QDBG_T0 + 64) g_qdbg[blockIdx.x][(tl)-QDBG_T0][(ev)] = clock64(); \
@@ -110,9 +110,9 @@ constexpr int ABYTES = TILE * ROWB;        // one A stage
 constexpr int RAWB = 8 * TILE * 8;         // one raw stage: 8 rows x 1024 px
 constexpr int NRAW = 6, NA = 2;
 #ifndef Q8_EXP
-#define Q8_EXP 0  // measurement variants: 1 = epilogue without the pixel math, 3 = without stores,
-                  // 5 = converters without pixel loads / A writes, 6 = no MMA (commit only),
-                  // 7 = no constant K-step (2 MMAs per tile), 9 = fallback blocks dequeued, not recomputed
+#define Q8_EXP 0  // measurement variants (bit flags, wrong output): 1 = epilogue without the pixel math,
+                  // 2 = without stores (the output bytes kept live), 4 = converters without pixel loads /
+                  // A writes, 16 = fallback blocks dequeued, not recomputed
 #endif
 // epilogue: two groups of 4 warps (one per TMEM lane quarter); group g
 // drains accumulator buffer g, i.e. every other tile of the CTA
@@ -254,7 +254,7 @@ __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {
     if (r + 1 < ROWS) tmem_ld32(col0 + 32 * (r + 1), (r & 1) ? va : vb);
-#if Q8_EXP == 1
+#if Q8_EXP & 1
     words[2 * r] = ((r & 1) ? vb : va)[0];
     words[2 * r + 1] = ((r & 1) ? vb : va)[31];
 #else
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       const uint8_t* ib = in + f * frame_stride;
       uint8_t* ob = out + f * frame_stride + static_cast<size_t>(y0) * pitch + x0;
       bool chain = false;
-      if (Q8_EXP != 9)
+      if (!(Q8_EXP & 16))
         chain = fallback_block(args.ref[pof_s[f]], ib, pitch, w, h, y0, x0, ob, fast_out, scratch, nan_flag, lane);
       __syncwarp();
       if (lane == 0) {
@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
 #pragma unroll
       for (int hb = 0; hb < 2; ++hb) {
         const int b = 2 * c2 + hb, m = a_row(b);
-        if (b < nbt && Q8_EXP != 5) {
+        if (b < nbt && !(Q8_EXP & 4)) {
           uint8_t* arow = asm_ + s * ABYTES + m * ROWB;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -792,7 +792,12 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       const bool unsure = valid && min(mn0, mn1) < 2u * U;
       const int y0 = by * 8, x0 = (bx0 + b) * 8;
       uint8_t* ob = out + f * frame_stride + static_cast<size_t>(y0) * pitch + x0;
-      if (valid && !unsure && Q8_EXP != 3) {
+      if (valid && !unsure && (Q8_EXP & 2)) {  // no stores, the bytes kept live
+        uint32_t x = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x ^= words[k];
+        if (x == 0x9e3779b9u) *ob = 1;
+      } else if (valid && !unsure) {
         if (fast_out && x0 + 8 <= w && y0 + 8 <= h) {
 #pragma unroll
           for (int k = 0; k < 8; ++k)
@@ -804,6 +809,9 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       const uint32_t flagged = __ballot_sync(0xFFFFFFFFu, unsure);
       if (flagged) enqueue_fallback(fq, &fq_tail, flagged, unsure, lane, ti, b);
       QSTAMP_EPI(tl, 27);
+#ifdef QDBG
+      if (lane == 0) QSTAMP(tl, 32 + (warp - W_EPI));
+#endif
     }
     __threadfence_block();
     __syncwarp();
@@ -1002,7 +1010,7 @@ extern "C" int dctf_qdbg_read(long long* out) {
   return cudaMemcpyFromSymbol(out, g_qdbg, sizeof(g_qdbg)) == cudaSuccess ? 0 : 1;
 }
 extern "C" int dctf_qdbg_clear() {
-  static long long zero[4 * 64 * 32] = {};
+  static long long zero[4 * 64 * 48] = {};
   return cudaMemcpyToSymbol(g_qdbg, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
 }
 #endif

@@ -31,7 +31,7 @@ torch.cuda.synchronize()
 _lib.lib.dctf_qdbg_clear()
 P.filter_frames(d, plans, idx)
 torch.cuda.synchronize()
-buf = np.zeros((4, 64, 32), np.int64)
+buf = np.zeros((4, 64, 48), np.int64)
 _lib.lib.dctf_qdbg_read(buf.ctypes.data_as(C.c_void_p))
 nw = int(os.environ.get("NEPI", "8"))
 for cta in range(2):
@@ -48,6 +48,8 @@ for cta in range(2):
           f"{m(t[sl, 19] - t[sl, 18])}")
     print("   wake - issue per epilogue warp:   ", [m(x) for x in wake])
     print("   release - issue per epilogue warp:", [m(x) for x in rel])
+    print("   tile end - issue per epilogue warp:", [m(t[sl, 32 + w] - iss) for w in range(nw)])
+    print("   iteration period per epilogue warp:", [m(np.diff(t[16:48:2, 32 + w] if w < 4 else t[17:49:2, 32 + w])) for w in range(nw)])
     relmax = np.max(np.stack([t[sl, 10 + w] for w in range(nw)]), axis=0)
     print(f"   converter (tile i) relative to MMA issue of tile i-2: raw seen {m(t[18:50, 21] - t[16:48, 0])}, "
           f"A stage {m(t[18:50, 22] - t[16:48, 0])}, a_full arrive {m(t[18:50, 18] - t[16:48, 0])}; "
