@@ -326,6 +326,15 @@ dctf_status dctf_diag_fallback_counts(unsigned long long* flagged, unsigned long
 /* The flagged count alone (same counters). */
 dctf_status dctf_diag_fallback_blocks(unsigned long long* n);
 
+/* Diagnostics: how k_fused8_q represents this plan's composed 64 x 64 pixel
+ * operator K. *denominator > 0: K = K' / denominator with integer K' (odd
+ * denominator; integer masks, odd box means, odd motion blurs) — one int8
+ * digit and one accumulator per pixel, exact rounding without a near-tie
+ * test. *denominator = 0: round(K 2^*fraction_bits) in four int8 digits with
+ * the uncertainty window and the reference-order fallback. DCTF_UNSUPPORTED
+ * when the plan does not run k_fused8_q. Either pointer may be NULL. */
+dctf_status dctf_plan_kq_form(const dctf_plan* plan, int* denominator, int* fraction_bits);
+
 /* Diagnostics: this device's INT8 tensor-core throughput (tera-ops/s,
  * 2 ops per MAC) with back-to-back tcgen05.mma kind::i8 M128 N256 K32 from
  * shared memory — the roofline denominator of k_fused8_q's tensor side.

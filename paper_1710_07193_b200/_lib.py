@@ -70,6 +70,7 @@ _SIGS = {
     "dctf_filter_blocks_host": (_st, [_vp, _vp, _vp, C.c_size_t]),
     "dctf_plan_mask": (_st, [_vp, _d, _i, _i, _i]),
     "dctf_diag_fallback_counts": (_st, [C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
+    "dctf_plan_kq_form": (_st, [_vp, _i, _i]),
     "dctf_filter_frames_host": (_st, [C.POINTER(_vp), C.c_int, _i, _vp, _vp, C.c_int, C.c_int, C.c_int,
                                       C.c_size_t, C.c_size_t]),
     "dctf_multi_create": (_st, [_d, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i, C.c_int, C.POINTER(_vp)]),

@@ -882,6 +882,14 @@ const char* dctf_plan_coef_kernel(const dctf_plan* p) {
   return p->sym ? "k_coef16_sym" : "k_coef16";
 }
 
+dctf_status dctf_plan_kq_form(const dctf_plan* p, int* denominator, int* fraction_bits) {
+  if (!p) return set_error(DCTF_INVALID_ARGUMENT, "NULL plan");
+  if (!p->kq) return set_error(DCTF_UNSUPPORTED, "the plan does not run k_fused8_q");
+  if (denominator) *denominator = p->kq_den;
+  if (fraction_bits) *fraction_bits = p->kq_F;
+  return DCTF_OK;
+}
+
 const char* dctf_plan_image_kernel(const dctf_plan* p) {
   if (!p) return nullptr;
   if (p->unbounded) return p->n == 8 ? "k_refchain8" : "unfused";

@@ -54,6 +54,9 @@ struct dctf_plan {
   double* d_refchain = nullptr;  // C | C^t | lefts | rights (mode 1)
   double* d_kqt = nullptr;       // K in FP64, transposed (the fallback's first stage)
   double kq_margin = 0.0;        // first-stage tie window (pixel units)
+  int kq_den = 0;                // > 0: rational operator K = K' / den (odd den), single-accumulator path
+  uint32_t kq_magic = 0;         // ceil(2^32 / den) (den > 1)
+  int kq_bias = 0;               // floor-division bias B (the accumulator carries + B den)
   int ref_mode = 0, ref_npairs = 0;
   // The reference chain's intermediates can overflow FP64 for this mask
   // (huge weights; chain_bounded false): the u8 image path then runs the
@@ -186,6 +189,9 @@ struct KqInfo {
   double margin = 0.0;       // second-stage window: reference FP64 deviation + our FP64 dot error
   double eref = 0.0;         // rigorous bound of the reference chain's FP64 deviation (pixel units)
   std::vector<double> kt;    // the composed operator K in FP64, transposed (kt[j * 64 + i] = K[i][j])
+  int den = 0;               // > 0: K = K' / den with integer K', odd den: exact single-accumulator path
+  uint32_t magic = 0;        // ceil(2^32 / den)
+  int bias = 0;              // B: the accumulator constant is (den - 1) / 2 + B den, q = floor(acc / den) - B
 };
 bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info);
 void refchain_image(const dctf_plan& p, std::vector<double>& out, int& mode, int& npairs);

@@ -1158,6 +1158,85 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
     if (!std::isfinite(static_cast<double>(v))) return false;
     kmax = std::max(kmax, std::fabs(v));
   }
+  // the reference's own FP64 deviation from the exact chain (rigorous bound)
+  const long double eref = reference_error_bound(p);
+  auto put = [&](int row, int k, int v) {
+    bimg[size_t(row) * 128 + ((((k >> 4) ^ (row & 7)) << 4) | (k & 15))] = static_cast<int8_t>(v);
+  };
+  // Rational operators with an odd denominator, K = K' / d with integer
+  // |K'| <= 127 (d = 1: integer masks — Laplacian, Sobel, identity; d = k^2 or
+  // k: odd box means and motion blurs): one int8 digit per entry, N = sum_j
+  // K'_ij p_j exact in one int32 accumulator, z = N / d. z + 1/2 = (2 N + d) /
+  // (2 d) has an odd numerator, so it is at least 1 / (2 d) away from every
+  // integer: no pixel can be a near-tie, and with the operator's deviation
+  // from K' / d (255 sum_j |K_ij - K'_ij / d|, ~1e-11) plus the reference's own
+  // FP64 deviation far below that distance the reference rounds to
+  //   q = floor((2 N + d) / (2 d)) = floor((N + (d - 1) / 2) / d)
+  // on every pixel. The accumulator constant (A bytes 64-95 = 1, 1, 255 x 30;
+  // B bytes 64-95) adds (d - 1) / 2 + B d, B d >= the most negative N, so the
+  // division is unsigned: q = mulhi(acc, ceil(2^32 / d)) - B (acc < 2^32 / d).
+  // B-operand image: 64 rows (row i = output pixel i), same K-major 128-byte-swizzled layout.
+  for (int d = 1; d <= 255 && kmax > 0.0L; d += 2) {
+    if (kmax * d > 127.0L + 1e-9L) break;
+    bool ok = true;
+    long double dev = 0.0L;
+    for (size_t e = 0; e < K.size() && ok; ++e) {
+      const long double v = K[e] * d;
+      ok = std::fabs(v - std::nearbyint(v)) <= 1e-9L * d;
+    }
+    if (!ok) continue;
+    std::vector<int> Kp(K.size());
+    long long negmax = 0;
+    long double magmax = 0.0L;
+    for (int i = 0; i < nn; ++i) {
+      long double err = 0.0L, mag = 0.0L;
+      long long neg = 0;
+      for (int j = 0; j < nn; ++j) {
+        const long double v = K[size_t(i) * nn + j];
+        const int q = static_cast<int>(std::llroundl(v * d));
+        if (q < -127 || q > 127) ok = false;
+        Kp[size_t(i) * nn + j] = q;
+        err += std::fabs(v - static_cast<long double>(q) / d);
+        mag += std::fabs(v);
+        if (q < 0) neg += 255LL * (-q);
+      }
+      dev = std::max(dev, 255.0L * err + eref + std::ldexp(1.0L, -60) * 255.0L * mag);
+      negmax = std::max(negmax, neg);
+      magmax = std::max(magmax, mag);
+    }
+    if (!ok || dev > 0.4L / d) break;  // not this form after all: the digit path decides
+    const int B = static_cast<int>((negmax + d - 1) / d);
+    const long long cst = (d - 1) / 2 + static_cast<long long>(B) * d;
+    // acc = N + cst in [0, 2^32 / d): mulhi by ceil(2^32 / d) is then the exact quotient
+    const long long accmax = 255LL * 64 * 127 + cst;
+    if (cst > 254 + 255LL * 30 * 127 || static_cast<long double>(accmax) * d >= std::ldexp(1.0L, 32)) break;
+    bimg.assign(size_t(256) * 128, 0);
+    for (int i = 0; i < nn; ++i) {
+      for (int j = 0; j < nn; ++j) put(i, j, Kp[size_t(i) * nn + j]);
+      long long hi = cst / 255, lo = cst % 255;  // cst = b64 + b65 + 255 (b66 + ... + b95)
+      put(i, 64, static_cast<int>((lo + 1) / 2));
+      put(i, 65, static_cast<int>(lo / 2));
+      for (int k = 66; k < 96; ++k) {
+        const int b = static_cast<int>(std::min<long long>(hi, 127));
+        put(i, k, b);
+        hi -= b;
+      }
+    }
+    info.den = d;
+    info.magic = d > 1 ? static_cast<uint32_t>((std::ldexp(1.0L, 32) + d - 1) / d) : 0u;
+    info.bias = B;
+    info.ok = true;
+    info.F = 0;
+    info.U = 0;
+    info.ebound = static_cast<double>(dev);
+    info.eref = static_cast<double>(eref);
+    info.flag_rate = 0.0;
+    info.margin = 0.0;
+    info.kt.assign(size_t(nn) * nn, 0.0);
+    for (int i = 0; i < nn; ++i)
+      for (int j = 0; j < nn; ++j) info.kt[size_t(j) * nn + i] = static_cast<double>(K[size_t(i) * nn + j]);
+    return true;
+  }
   constexpr long double R = 16843009.0L;  // 256^3 + 256^2 + 256 + 1
   const long double lim = 127.0L * R - 1.0L;
   int F = 32;
@@ -1166,8 +1245,6 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   if (F < 17) return false;
   const long double scale = std::ldexp(1.0L, F);
   std::vector<long long> Ki(K.size());
-  // the reference's own FP64 deviation from the exact chain (rigorous bound)
-  const long double eref = reference_error_bound(p);
   long double emax = 0.0L;
   for (int i = 0; i < nn; ++i) {
     long double err = 0.0L, mag = 0.0L;
@@ -1187,9 +1264,6 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   const double flag_rate = static_cast<double>(64.0L * 2.0L * T / scale);  // per block, uniform fractions
   if (flag_rate > 0.02) return false;
   bimg.assign(size_t(256) * 128, 0);
-  auto put = [&](int row, int k, int v) {
-    bimg[size_t(row) * 128 + ((((k >> 4) ^ (row & 7)) << 4) | (k & 15))] = static_cast<int8_t>(v);
-  };
   for (int i = 0; i < nn; ++i)
     for (int j = 0; j < nn; ++j) {
       long long v = Ki[size_t(i) * nn + j];

@@ -121,8 +121,15 @@ constexpr int NGRP = 2;
 // picks the highest eligible warp id first, so the short, latency-critical
 // roles (MMA issue, TMA, the converters that feed the MMA, the fallback warp
 // that keeps the flagged-block queue short) sit above the ALU-heavy epilogue.
-constexpr int W_EPI = 0, NEPI = 4 * NGRP, W_FB = W_EPI + NEPI, W_CONV = W_FB + 1, NCONV = 2,
+// Converter sets: each set (two warps) takes every CSETS-th tile of the CTA, so
+// a set has CSETS tile periods for its load - transpose - store round trip.
+#ifndef Q8_CSETS
+#define Q8_CSETS 1
+#endif
+constexpr int CSETS = Q8_CSETS;
+constexpr int W_EPI = 0, NEPI = 4 * NGRP, W_FB = W_EPI + NEPI, W_CONV = W_FB + 1, NCONV = 2 * CSETS,
               W_TMA = W_CONV + NCONV, W_MMA = W_TMA + 1;
+static_assert(CSETS == 1 || (NRAW % CSETS == 0 && NA % CSETS == 0), "a stage belongs to one converter set");
 constexpr int THREADS = 32 * (W_MMA + 1);
 constexpr int FQ = 256;                    // fallback queue slots
 constexpr int SMEM = 1024 + KQ_MAX_PLANS * BBYTES + NA * ABYTES + NRAW * RAWB;
@@ -152,6 +159,9 @@ struct QArgs {
   const int8_t* bimg[KQ_MAX_PLANS];
   uint32_t U[KQ_MAX_PLANS];
   int shS[KQ_MAX_PLANS], shL[KQ_MAX_PLANS];  // F - 16, 32 - F
+  // rational plans (K = K' / den, odd den; plan.cc: layout_kq8): den > 0, q = mulhi(acc, magic) - bias
+  int den[KQ_MAX_PLANS], bias[KQ_MAX_PLANS];
+  uint32_t magic[KQ_MAX_PLANS];
   RefPlan ref[KQ_MAX_PLANS];
   int nplans;
   dctf::FastDiv fd_tpf, fd_ntx;  // tile -> (frame, block row, tile column), made on the host
@@ -273,6 +283,37 @@ __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32
   }
 }
 
+// Rational plans (K = K' / den, odd den): the tile's 64 accumulator columns
+// (one per pixel: N + (den - 1) / 2 + bias den, exact) in two loads, released
+// at once; q = floor(acc / den) - bias by an exact multiply-high (den > 1).
+// No pixel of such a plan can be a near-tie (plan.cc: layout_kq8).
+__device__ __forceinline__ void epi_rational(uint32_t col0, int den, uint32_t magic, int bias, uint32_t (&words)[16],
+                                             uint64_t* acc_empty, long long* stamp = nullptr) {
+  int32_t va[32], vb[32];
+  tmem_ld32(col0, va);
+  tmem_ld32(col0 + 32, vb);
+  tmem_wait_ld();
+  tc_fence_before();
+  mbar_arrive(acc_empty);
+#ifdef QDBG
+  if (stamp && (threadIdx.x & 31) == 0) *stamp = clock64();
+#else
+  (void)stamp;
+#endif
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int32_t(&v)[32] = r < 4 ? va : vb;
+    int q[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t a = static_cast<uint32_t>(v[8 * (r & 3) + c]);
+      q[c] = static_cast<int>(den == 1 ? a : __umulhi(a, magic)) - bias;
+    }
+    words[2 * r] = pack4_sat(q[0], q[1], q[2], q[3]);
+    words[2 * r + 1] = pack4_sat(q[4], q[5], q[6], q[7]);
+  }
+}
+
 // A-operand row (= MMA row = TMEM lane) of block b of the tile, an
 // involution: bit 0 flipped when bit 3 is set. A converter store instruction
 // writes blocks 2 c2 + hb of its 32 threads; with the identity map their rows
@@ -283,7 +324,7 @@ __device__ __forceinline__ int a_row(int b) { return b ^ ((b >> 3) & 1); }
 
 // Cropped byte stores of ROWS rows (image edges, unaligned outputs).
 template <int ROWS>
-__device__ __forceinline__ void store_ragged(uint8_t* ob, size_t pitch, const uint32_t (&words)[2 * ROWS],
+__device__ __noinline__ void store_ragged(uint8_t* ob, size_t pitch, const uint32_t (&words)[2 * ROWS],
                                              int rows_left, int cols_left) {
 #pragma unroll
   for (int k = 0; k < ROWS; ++k)
@@ -326,7 +367,7 @@ __device__ __forceinline__ double ref_mm(const double* a, const double* b, int i
   return acc;
 }
 
-__device__ bool fallback_block(const RefPlan& rp, const uint8_t* img, size_t pitch, int w, int h, int y0, int x0,
+__device__ __noinline__ bool fallback_block(const RefPlan& rp, const uint8_t* img, size_t pitch, int w, int h, int y0, int x0,
                                uint8_t* dst, bool fast_out, double* sm, int* nan_flag, int lane) {
   double* sx = sm;        // X (pixels, then forward coefficients)
   double* st = sm + 64;   // products
@@ -453,7 +494,8 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   // parameter bank (dynamically indexed constant loads miss the constant cache)
   __shared__ uint8_t pof_s[KQ_MAX_FRAMES];
   __shared__ uint32_t U_s[KQ_MAX_PLANS];
-  __shared__ int shS_s[KQ_MAX_PLANS], shL_s[KQ_MAX_PLANS];
+  __shared__ int shS_s[KQ_MAX_PLANS], shL_s[KQ_MAX_PLANS], den_s[KQ_MAX_PLANS], bias_s[KQ_MAX_PLANS];
+  __shared__ uint32_t magic_s[KQ_MAX_PLANS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   pdl_trigger();
@@ -464,14 +506,20 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     U_s[threadIdx.x] = args.U[threadIdx.x];
     shS_s[threadIdx.x] = args.shS[threadIdx.x];
     shL_s[threadIdx.x] = args.shL[threadIdx.x];
+    den_s[threadIdx.x] = args.den[threadIdx.x];
+    bias_s[threadIdx.x] = args.bias[threadIdx.x];
+    magic_s[threadIdx.x] = args.magic[threadIdx.x];
   }
   // A rows, bytes 64..127 (chunks 4-7, 128B-swizzled): the constant input
-  // [1, 1, 0, ...] that adds the digits of the rounding offset 2^(F-1)
-  // (plan.cc: layout_kq8, bytes 64-65 of the B rows) to the accumulators
+  // [1, 1, 255 x 30, 0 ...] that adds the B rows' bytes 64-95 to the
+  // accumulators: the digits of the rounding offset 2^(F-1) (bytes 64-65) or a
+  // rational plan's division constant (plan.cc: layout_kq8)
   for (int i = threadIdx.x; i < NA * TILE * 4; i += blockDim.x) {
     const int st = i / (TILE * 4), b = (i >> 2) % TILE, c = 4 + (i & 3);
     *reinterpret_cast<uint4*>(asm_ + st * ABYTES + b * ROWB + ((c ^ (b & 7)) << 4)) =
-        make_uint4(c == 4 ? 0x0101u : 0u, 0u, 0u, 0u);
+        c == 4   ? make_uint4(0xFFFF0101u, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu)
+        : c == 5 ? make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu)
+                 : make_uint4(0u, 0u, 0u, 0u);
   }
   if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -482,10 +530,10 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < NRAW; ++i) {
       mbar_init(&raw_full[i], 1);
-      mbar_init(&raw_empty[i], 32 * NCONV);
+      mbar_init(&raw_empty[i], 64);  // the two warps of the tile's converter set
     }
     for (int i = 0; i < NA; ++i) {
-      mbar_init(&a_full[i], 32 * NCONV);
+      mbar_init(&a_full[i], 64);
       mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -632,7 +680,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       }
     }
   } else if (warp == W_MMA) {
-    constexpr uint32_t idesc = idesc_u8s8(128, 256);
+    constexpr uint32_t idesc256 = idesc_u8s8(128, 256), idesc64 = idesc_u8s8(128, 64);
     const uint64_t da0 = desc_sw128(smem_u32(asm_)), db0 = desc_sw128(smem_u32(bsm));
     constexpr uint64_t DA_STAGE = ABYTES >> 4, DB_PLAN = BBYTES >> 4;
     const uint32_t acc_full0 = smem_u32(&acc_full[0]), a_empty0 = smem_u32(&a_empty[0]);
@@ -650,6 +698,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       if (lane == 0) QSTAMP(tl, 0);
       tc_fence_after();
       const uint64_t da = da0 + DA_STAGE * s, db = db0 + DB_PLAN * pi;
+      const uint32_t idesc = den_s[pi] > 0 ? idesc64 : idesc256;  // rational plans: one accumulator column per pixel
       const uint32_t dt = tmem_base + 256 * buf;
       asm volatile(
           "{\n\t.reg .pred e;\n\t"
@@ -669,9 +718,10 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     // ---------------- converters: thread = the block pair (2 c2, 2 c2 + 1) of
     // the tile: one 16-byte shared load per pixel row covers both blocks
     // (adjacent 8-byte rows of the strip), four 16-byte A-operand stores each
-    const int c2 = threadIdx.x - 32 * W_CONV;
-    long long tl = 0;
-    for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tl) {
+    const int cset = (warp - W_CONV) >> 1, c2 = (threadIdx.x - 32 * W_CONV) & 63;
+    long long tl = cset;
+    for (long long ti = blockIdx.x + static_cast<long long>(cset) * gridDim.x; ti < ntiles;
+         ti += CSETS * static_cast<long long>(gridDim.x), tl += CSETS) {
       int f, by, bx0;
       tile_at(ti, f, by, bx0);
       const int nbt = min(TILE, bw - bx0);
@@ -782,7 +832,8 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       uint32_t mn0 = 0xFFFFFFFFu, mn1 = 0xFFFFFFFFu;
       int32_t va[32], vb[32];
       // row r is processed while row r + 1 streams in from TMEM
-      if (shL == 0) epi_rows<8, true>(col0, va, vb, shS, 0, U, mn0, mn1, words, &acc_empty[grp], rel);
+      if (den_s[pi] > 0) epi_rational(col0, den_s[pi], magic_s[pi], bias_s[pi], words, &acc_empty[grp], rel);
+      else if (shL == 0) epi_rows<8, true>(col0, va, vb, shS, 0, U, mn0, mn1, words, &acc_empty[grp], rel);
       else epi_rows<8, false>(col0, va, vb, shS, shL, U, mn0, mn1, words, &acc_empty[grp], rel);
       QSTAMP_EPI(tl, 26);
       // A block with an uncertain pixel is left to the fallback warp, which
@@ -822,7 +873,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
     if (lane == 0) QSTAMP(1, 28);
   }
   if (warp != W_FB) {
-    // Every tile of this CTA is done once all 12 other warps get here (the
+    // Every tile of this CTA is done once all other warps get here (the
     // epilogue waited for the last MMA, the converters consumed every raw
     // stage): the rest of the queue is drained by all warps in parallel, each
     // with 2 KB of scratch in the now idle raw ring.
@@ -920,7 +971,14 @@ dctf_status upload_kq_operator(dctf_plan* p) {
   p->kq_ebound = info.ebound;
   p->kq_flag_rate = info.flag_rate;
   p->kq_margin = info.margin;
-  if (std::getenv("DCTF_Q_DEBUG"))
+  p->kq_den = info.den;
+  p->kq_magic = info.magic;
+  p->kq_bias = info.bias;
+  if (std::getenv("DCTF_Q_DEBUG") && info.den > 0)
+    std::fprintf(stderr, "[k_fused8_q plan] rational operator K = K'/%d (bias %d): deviation %.3e (reference FP64 bound "
+                         "%.3e) against a boundary distance of %.3e\n", info.den, info.bias, info.ebound, info.eref,
+                 0.5 / info.den);
+  else if (std::getenv("DCTF_Q_DEBUG"))
     std::fprintf(stderr, "[k_fused8_q plan] F=%d U=%u window=%.3e (reference FP64 bound %.3e) second-stage margin=%.3e "
                          "expected flagged blocks %.2e\n", info.F, info.U, info.ebound, info.eref, info.margin,
                  info.flag_rate);
@@ -947,6 +1005,9 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
     args.U[i] = p->kq_U;
     args.shS[i] = p->kq_F - 16;
     args.shL[i] = 32 - p->kq_F;
+    args.den[i] = p->kq_den;
+    args.bias[i] = p->kq_bias;
+    args.magic[i] = p->kq_magic;
     args.ref[i] = RefPlan{p->d_refchain, p->d_weights, p->d_kqt, p->kq_margin, p->ref_mode, p->ref_npairs, p->kr,
                           p->kc, p->padding};
   }

@@ -369,6 +369,17 @@ class FilterPlan:
         return _lib.lib.dctf_plan_image_kernel(self._h).decode()
 
     @property
+    def kq_form(self):
+        """(denominator, fraction_bits) of k_fused8_q's operator for this plan
+        (dctf_plan_kq_form): denominator > 0 = rational single-digit form,
+        0 = four-digit fixed point with fraction_bits; None when the plan does
+        not run k_fused8_q."""
+        den, fb = C.c_int(), C.c_int()
+        if _lib.lib.dctf_plan_kq_form(self._h, C.byref(den), C.byref(fb)) != 0:
+            return None
+        return den.value, fb.value
+
+    @property
     def coef_kernel(self) -> str:
         """Kernel filter_coeffs runs for this plan (dctf_plan_coef_kernel)."""
         return _lib.lib.dctf_plan_coef_kernel(self._h).decode()

@@ -25,6 +25,8 @@ masks = [(synth.LAPLACIAN3, 3, 3), (synth.gaussian_mask(5, 1.0), 5, 5), (synth.M
 plans = [P.FilterPlan(P.Mask(k, w) if k == kc else P.Mask.rect(k, kc, w), 8, P.PaddingMode.kReplicate)
          for w, k, kc in masks]
 idx = [f % 4 for f in range(F)]
+if os.environ.get("KQ_IDX"):  # e.g. KQ_IDX=0: every frame on the first plan (Laplacian)
+    idx = [int(os.environ["KQ_IDX"])] * F
 for _ in range(3):
     P.filter_frames(d, plans, idx)
 torch.cuda.synchronize()

@@ -140,3 +140,54 @@ def test_kq_dyadic_ties(P, ref, pad):
         assert plan.image_kernel == "k_fused8_q"
         r = ref.filter_image(img, w, 3, pad, 8, threads=nthreads())
         assert int(np.count_nonzero(out != r)) == 0
+
+
+def _int_masks():
+    sobel = np.array([-1.0, 0, 1, -2, 0, 2, -1, 0, 1])
+    lap8 = np.array([-1.0, -1, -1, -1, 9, -1, -1, -1, -1])
+    emboss = np.array([-2.0, -1, 0, -1, 1, 1, 0, 1, 2])
+    return {
+        "sobel": (sobel, 3, 3, 1), "laplacian8": (lap8, 3, 3, 1), "emboss": (emboss, 3, 3, 1),
+        "box5": (np.full(25, 1.0 / 25.0), 5, 5, 25), "box7": (np.full(49, 1.0 / 49.0), 7, 7, 49),
+        "motion1x5": (np.full(5, 0.2), 1, 5, 5), "motion3x1": (np.full(3, 1.0 / 3.0), 3, 1, 3),
+        "thirds": (np.array([1.0, -2, 1, -2, 7, -2, 1, -2, 1]) / 3.0, 3, 3, 3),
+    }
+
+
+@pytest.mark.parametrize("name", list(_int_masks()))
+@pytest.mark.parametrize("pad", [0, 1])
+def test_kq_rational_form(P, ref, oracle, name, pad):
+    """Integer masks and odd-denominator rational masks (K = K' / d) take the
+    single-digit form of k_fused8_q (plan.cc: layout_kq8): no fallback block,
+    every pixel the reference's (negative sums, saturation at both ends,
+    ragged shape)."""
+    import ctypes as C
+    import os
+    from paper_1710_07193_b200 import _lib, synth
+    w, kr, kc, den = _int_masks()[name]
+    img = synth.uniform_image(31, 523, 349)
+    counting = bool(os.environ.get("DCTF_Q_COUNT"))
+    n = C.c_ulonglong(0)
+    if counting:
+        _lib.lib.dctf_diag_fallback_blocks(C.byref(n))
+    plan, out = _run(P, img, w, kr, kc, pad)
+    assert plan.image_kernel == "k_fused8_q"
+    assert plan.kq_form[0] == den, plan.kq_form
+    if counting:
+        _lib.lib.dctf_diag_fallback_blocks(C.byref(n))
+        assert n.value == 0
+    want = _reference(ref, oracle, img, w, kr, kc, pad)
+    assert np.array_equal(out, want), int(np.count_nonzero(out != want))
+
+
+def test_kq_form_of_config5_masks(P):
+    """Config 5: the Laplacian (integer) and the 1x9 motion blur (ninths) are
+    rational, the Gaussian and the random 5x5 take the four-digit form."""
+    from paper_1710_07193_b200 import synth
+    r5, _ = synth.random_mask(1005, 5)
+    forms = []
+    for w, kr, kc in [(synth.LAPLACIAN3, 3, 3), (synth.gaussian_mask(5, 1.0), 5, 5), (synth.MOTION_1x9, 1, 9), (r5, 5, 5)]:
+        m = P.Mask(kr, w) if kr == kc else P.Mask.rect(kr, kc, w)
+        forms.append(P.FilterPlan(m, 8, P.PaddingMode.kReplicate).kq_form)
+    assert [f[0] for f in forms] == [1, 0, 9, 0], forms
+    assert forms[1][1] == 32 and 17 <= forms[3][1] <= 32
