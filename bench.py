@@ -59,10 +59,11 @@ NBLOCKS = NF * BPF                            # 8,294,400
 BYTES_PER_BLOCK = 2 * N * N                   # u8 in + u8 out
 L2_BYTES = 126 * 1000 * 1000
 MASK_NAMES = ["laplacian3x3", "gaussian5x5_s1", "motion1x9", "random5x5_seed1005"]
-# k_fused8_q per block: MMA M=1 row of N = 256 columns (64 pixels x 4 digits)
-# over K = 96 (64 pixel bytes + the rounding-offset chunk); algorithmic K = 64
-I8_OPS_EXECUTED = 2 * 256 * 96
-I8_OPS_ALGORITHMIC = 2 * 256 * 64
+# k_fused8_q per block: MMA M=1 row of N columns over K = 96 (64 pixel bytes +
+# the constant chunk); algorithmic K = 64. N = 256 (64 pixels x 4 digits) for
+# the four-digit operator form, N = 64 for rational plans (K = K'/d, one digit).
+def i8_ops(form, k):
+    return 2 * (64 if form and form[0] > 0 else 256) * k
 CONFIG = {
     "workload": "config5: 64 x 3840x2160 u8 frames S(f), f = 0..63 (sinusoid+noise, csrc/synth.cc); "
                 "8x8 blocks (8,294,400); mask f mod 4 = laplacian 3x3 / gaussian 5x5 sigma 1 / 1x9 motion "
@@ -618,6 +619,9 @@ def main():
     pof = [f % 4 for f in range(f0, f1)]
     plans, masks = make_plans(P, synth)
     kernels = sorted({p.image_kernel for p in plans})
+    forms = [p.kq_form for p in plans]
+    form_names = {n: (f"rational K'/{f[0]}, one digit" if f and f[0] > 0 else f"four digits, F = {f[1]}" if f else None)
+                  for n, f in zip(MASK_NAMES, forms)}
     host = np.empty((nf, FH, FW), np.uint8)
     for i, f in enumerate(range(f0, f1)):
         synth.sinusoid_image(f, FW, FH, out=host[i])
@@ -697,7 +701,9 @@ def main():
     blocks_rank = nf * BPF
     gbs_kernel = blocks_rank * BYTES_PER_BLOCK / (ms_local / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic("k_fused8_q")
-    i8_tops = blocks_rank * I8_OPS_EXECUTED / (ms_local / 1e3) / 1e12
+    i8_exec = sum(i8_ops(forms[m], 96) for m in pof) / max(1, nf)   # per block, mean over the rank's frames
+    i8_alg = sum(i8_ops(forms[m], 64) for m in pof) / max(1, nf)
+    i8_tops = blocks_rank * i8_exec / (ms_local / 1e3) / 1e12
     roofline = {
         "bound": "hbm", "kernel": "k_fused8_q", "achieved": gbs_kernel, "peak": hbm_peak, "unit": "GB/s",
         "frac": gbs_kernel / hbm_peak if hbm_peak else None,
@@ -708,8 +714,9 @@ def main():
         "launch_ms": ms_local,
         "note": "one step = one k_fused8_q launch (the whole frame range, four plans), so the launch "
                 "duration is the step's CUDA-event time on the launching stream",
-        "tensor_pipe": {"unit": "TOP/s (int8)", "executed_ops_per_block": I8_OPS_EXECUTED,
-                        "algorithmic_ops_per_block": I8_OPS_ALGORITHMIC, "achieved": i8_tops,
+        "operator_forms": form_names,
+        "tensor_pipe": {"unit": "TOP/s (int8)", "executed_ops_per_block": i8_exec,
+                        "algorithmic_ops_per_block": i8_alg, "achieved": i8_tops,
                         "peak": peak_i8, "frac": i8_tops / peak_i8 if peak_i8 else None,
                         "peak_source": "measured in this run (dctf_measure_int8_peak: back-to-back "
                                        "tcgen05.mma kind::i8 M128 N256 K32)"},

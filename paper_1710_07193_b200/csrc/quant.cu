@@ -23,7 +23,14 @@
 // convolve-formula plans) by a fallback warp of the same CTA, so the u8
 // output is the reference's on every pixel, not only outside near-ties.
 //
-// Epilogue arithmetic (per pixel, 32-bit integer ops only): with
+// Rational operators: when K = K' / d with integer |K'| <= 127 and odd d
+// (integer masks, odd box means, odd motion blurs) one digit and ONE
+// accumulator per pixel carry N = sum_j K'_ij p_j exactly (MMA N = 64);
+// z + 1/2 = (2 N + d) / (2 d) has an odd numerator, so no pixel can be a
+// near-tie and q = floor((N + (d - 1) / 2) / d) is the reference's rounding
+// everywhere (epi_rational; plan.cc: layout_kq8 has the bound).
+//
+// Epilogue arithmetic of the four-digit form (per pixel, 32-bit integer ops only): with
 // h = a0*256 + a1, l = a2*256 + a3, the rounding offset 2^(F-1) folded in:
 //   S = h + (l >> 16) + 2^(F-17)          -> v = S*2^16 + (l & 0xffff)
 //   q = S >> (F-16)                        = floor(z + 0.5) (u8 after saturation)
