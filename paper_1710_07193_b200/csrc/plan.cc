@@ -1020,7 +1020,8 @@ namespace dctf {
 // u8, so the tensor cores' int32 partials a_s = sum_j d_s[i][j] p_j are exact
 // and so is z_int = sum_s a_s 256^(3-s) = sum_j K_int[i][j] p_j. Against the
 // exact composed value z* the only error is the operator quantisation,
-//   |z_int 2^-F - z*| <= E_i = 255 sum_j |K[i][j] - K_int[i][j] 2^-F|,
+//   |z_int 2^-F - z*| <= E_i = 127.5 sum_j |K[i][j] - K_int[i][j] 2^-F| + 2^-(F+1)
+// (pixels centred at 127.5, the row's constant part carried by the accumulators),
 // and against the reference's own FP64 result z_ref (rounding in its
 // forward / apply / inverse chain, ~1e-13 relative in practice) the kernel
 // allows M_i = 2^-30 + 2^-36 * 255 sum_j |K[i][j]|. A pixel whose fixed-point
@@ -1245,17 +1246,25 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   if (F < 17) return false;
   const long double scale = std::ldexp(1.0L, F);
   std::vector<long long> Ki(K.size());
+  // Operator quantisation with the pixels centred: sum_j e_ij p_j (e = K 2^F -
+  // K_int) = sum_j e_ij (p_j - 127.5) + 127.5 sum_j e_ij. The second term is a
+  // constant of the row; rounded to an integer (corr[i]) it rides in the
+  // accumulator constants of digits 2 and 3, which leaves
+  // |error| <= 127.5 sum_j |e_ij| + 0.5 — half of the uncentred 255 sum_j |e_ij|.
+  std::vector<long long> corr(nn, 0);
   long double emax = 0.0L;
   for (int i = 0; i < nn; ++i) {
-    long double err = 0.0L, mag = 0.0L;
+    long double err = 0.0L, serr = 0.0L, mag = 0.0L;
     for (int j = 0; j < nn; ++j) {
       const long double v = K[size_t(i) * nn + j] * scale;
       const long long q = std::llroundl(v);
       Ki[size_t(i) * nn + j] = q;
       err += std::fabs(v - static_cast<long double>(q));
+      serr += v - static_cast<long double>(q);
       mag += std::fabs(K[size_t(i) * nn + j]);
     }
-    const long double e = 255.0L * err / scale + eref + std::ldexp(1.0L, -60) * 255.0L * mag;
+    corr[size_t(i)] = std::llroundl(127.5L * serr);
+    const long double e = (127.5L * err + 0.5L) / scale + eref + std::ldexp(1.0L, -60) * 255.0L * mag;
     emax = std::max(emax, e);
   }
   const long double T = std::ceil(emax * scale) + 1.0L;
@@ -1284,6 +1293,13 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   for (int i = 0; i < nn; ++i) {
     put(4 * i + cs, 64, (cv + 1) / 2);
     put(4 * i + cs, 65, cv / 2);
+    // the row's centring constant corr[i] = c3 + 256 c2 (|corr| <= 4080) on digits 3 and 2
+    const long long c = corr[size_t(i)];
+    const int c3 = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(c & 255)));
+    const int c2 = static_cast<int>((c - c3) / 256);
+    put(4 * i + 3, 64, c3 / 2);
+    put(4 * i + 3, 65, c3 - c3 / 2);
+    put(4 * i + 2, 64, c2);
   }
   // Second stage (the fallback warp's first step on a flagged block): z_i =
   // sum_j K_ij p_j in FP64 from K rounded to double, sequential FMAs. Its
