@@ -86,7 +86,8 @@ namespace {
 #ifdef QDBG
 // [cta < 4][tile < 64][event < 32] clock64 stamps of tiles QDBG_T0.. (instrumented build only;
 // scripts/kq_trace3.py: 0/1 MMA issue start / done, 2+w wake and 10+w release of epilogue warp w,
-// 18 converters' a_full arrival, 19 MMA sees a_full)
+// 18 converters' a_full arrival, 19 MMA sees a_full, 21-25 converter: raw stage seen, A stage free,
+// rows loaded, A rows stored, proxy fence done)
 #ifndef QDBG_T0
 #define QDBG_T0 0
 #endif
@@ -783,6 +784,7 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
           ragged(2 * c2 + 1, raw + r * RAWB, 1);
         }
         mbar_arrive(&raw_empty[r]);
+        if (c2 == 0) QSTAMP(tl, 23);
       } else if (2 * c2 < nbt) {  // direct loads (unaligned views, host-mapped input)
         const uint8_t* ib = in + f * frame_stride + (bx0 + 2 * c2) * 8;
         if (full && ((reinterpret_cast<uintptr_t>(ib) & 15) == 0) && ((pitch & 15) == 0)) {
@@ -809,7 +811,9 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
                         : make_uint4(row[2 * q].z, row[2 * q].w, row[2 * q + 1].z, row[2 * q + 1].w);
         }
       }
+      if (c2 == 0) QSTAMP(tl, 24);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (c2 == 0) QSTAMP(tl, 25);
       mbar_arrive(&a_full[s]);
       if (c2 == 0) QSTAMP(tl, 18);
     }

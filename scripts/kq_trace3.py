@@ -56,6 +56,9 @@ for cta in range(2):
     print(f"   converter (tile i) relative to MMA issue of tile i-2: raw seen {m(t[18:50, 21] - t[16:48, 0])}, "
           f"A stage {m(t[18:50, 22] - t[16:48, 0])}, a_full arrive {m(t[18:50, 18] - t[16:48, 0])}; "
           f"MMA sees a_full {m(t[18:50, 19] - t[16:48, 0])}, issue start {m(t[18:50, 0] - t[16:48, 0])}")
-    print(f"   converter loop top {m(t[18:50, 23] - t[16:48, 0])}, after TMA issue {m(t[18:50, 24] - t[16:48, 0])}")
+    c = lambda ev: m(t[sl, ev] - t[sl, 21])
+    print(f"   converter, from raw stage seen (21): rows loaded + raw stage released {c(23)}, A stage free {c(22)}, "
+          f"A rows stored {c(24)}, proxy fence done {c(25)}, a_full arrive {c(18)}; next tile's raw stage seen "
+          f"{m(t[17:49, 21] - t[16:48, 21])}")
     step = int(os.environ.get("LOOP", "2"))
     print(f"   issue(i+{step}) - last release(i): {m(t[16 + step:48 + step, 0] - relmax)}")
