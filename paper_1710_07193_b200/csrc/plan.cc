@@ -1285,21 +1285,33 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
       d[0] = static_cast<int>(v);
       for (int s = 0; s < 4; ++s) put(4 * i + s, j, d[s]);
     }
-  // The rounding offset 2^(F-1) as accumulator constants: the A rows carry
-  // [1, 1] at bytes 64-65, so digit s of every output gets B[.][64] + B[.][65].
-  // F - 1 >= 24: 2^(F-25) on digit 0; else 2^(F-17) on digit 1 (both <= 128).
+  // Accumulator constants: the A rows carry [1, 1] at bytes 64-65, so digit s
+  // of every output gets B[.][64] + B[.][65]. Three terms per row:
+  //  * the rounding offset 2^(F-1): 2^(F-25) on digit 0 when F - 1 >= 24, else 2^(F-17) on digit 1;
+  //  * the row's centring constant corr[i] (above);
+  //  * the window half-width T itself, so the fixed-point value the epilogue
+  //    sees is v + T and its uncertainty test needs no add: a pixel is
+  //    uncertain iff ((v + T) mod 2^F) < 2 T (quant.cu folds pairs of pixels
+  //    into one three-input minimum). floor((v + T) / 2^F) differs from
+  //    floor(v / 2^F) only inside that window, where the block is recomputed.
   const int cs = F - 1 >= 24 ? 0 : 1;
   const int cv = 1 << (F - 1 - (cs == 0 ? 24 : 16));
   for (int i = 0; i < nn; ++i) {
-    put(4 * i + cs, 64, (cv + 1) / 2);
-    put(4 * i + cs, 65, cv / 2);
-    // the row's centring constant corr[i] = c3 + 256 c2 (|corr| <= 4080) on digits 3 and 2
-    const long long c = corr[size_t(i)];
-    const int c3 = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(c & 255)));
-    const int c2 = static_cast<int>((c - c3) / 256);
-    put(4 * i + 3, 64, c3 / 2);
-    put(4 * i + 3, 65, c3 - c3 / 2);
-    put(4 * i + 2, 64, c2);
+    long long cst[4] = {0, 0, 0, 0};
+    cst[cs] += cv;
+    long long c = corr[size_t(i)] + static_cast<long long>(T);  // balanced base-256 digits onto 3, 2, 1, (0)
+    for (int sdig = 3; sdig >= 1; --sdig) {
+      const int low = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(c & 255)));
+      cst[sdig] += low;
+      c = (c - low) / 256;
+    }
+    cst[0] += c;
+    for (int sdig = 0; sdig < 4; ++sdig) {
+      const long long a = cst[sdig] / 2, b = cst[sdig] - a;
+      if (a < -127 || a > 127 || b < -127 || b > 127) return false;
+      put(4 * i + sdig, 64, static_cast<int>(a));
+      put(4 * i + sdig, 65, static_cast<int>(b));
+    }
   }
   // Second stage (the fallback warp's first step on a flagged block): z_i =
   // sum_j K_ij p_j in FP64 from K rounded to double, sequential FMAs. Its

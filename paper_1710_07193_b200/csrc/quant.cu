@@ -34,9 +34,10 @@
 // h = a0*256 + a1, l = a2*256 + a3, the rounding offset 2^(F-1) folded in:
 //   S = h + (l >> 16) + 2^(F-17)          -> v = S*2^16 + (l & 0xffff)
 //   q = S >> (F-16)                        = floor(z + 0.5) (u8 after saturation)
-//   key = (v mod 2^F) << (32-F)            one funnel shift of (S : l << 16)
+//   key = (v mod 2^F) << (32-F)
 //   uncertain  <=>  (key + U) mod 2^32 < 2U,  U = T 2^(32-F)
-// so the per-block test is a running unsigned min.
+// The accumulator constants carry T as well, so key is already key + U and the
+// per-block test is a running unsigned minimum, two pixels per VIMNMX3.
 //
 // CTA = 13 warps, one CTA per SM (TMEM: 2 x 256 columns), persistent over
 // tiles of up to 128 horizontally adjacent blocks (one block row, 8 x 1024 px).
@@ -240,19 +241,24 @@ __device__ __forceinline__ uint32_t pack4_sat(int x0, int x1, int x2, int x3) {
 //   key = (T1 2^16 + T2) << (32 - F) mod 2^32 = (v mod 2^F) 2^(32-F)
 // (F32: F = 32, no shift).
 template <bool F32>
-__device__ __forceinline__ void q8_row(const int32_t (&v)[32], int shS, int shL, uint32_t U, uint32_t& mn0,
-                                       uint32_t& mn1, uint32_t& w0, uint32_t& w1) {
+__device__ __forceinline__ void q8_row(const int32_t (&v)[32], int shS, int shL, uint32_t& mn0, uint32_t& mn1,
+                                       uint32_t& w0, uint32_t& w1) {
   int qv[8];
+  uint32_t key[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const int t1 = v[4 * c] * 256 + v[4 * c + 1];
     const int t2 = v[4 * c + 2] * 256 + v[4 * c + 3];
-    uint32_t key = static_cast<uint32_t>(t1) * 65536u + static_cast<uint32_t>(t2);
-    if (!F32) key <<= shL;
+    key[c] = static_cast<uint32_t>(t1) * 65536u + static_cast<uint32_t>(t2);
+    if (!F32) key[c] <<= shL;
     qv[c] = (t1 + (t2 >> 16)) >> shS;
-    if (c & 1) mn1 = min(mn1, key + U);
-    else mn0 = min(mn0, key + U);
   }
+  // the accumulators carry the window half-width (plan.cc: layout_kq8), so
+  // key = frac + U already: uncertain iff key < 2 U; pairs of pixels per minimum
+  mn0 = __vimin3_u32(mn0, key[0], key[1]);
+  mn1 = __vimin3_u32(mn1, key[2], key[3]);
+  mn0 = __vimin3_u32(mn0, key[4], key[5]);
+  mn1 = __vimin3_u32(mn1, key[6], key[7]);
   w0 = pack4_sat(qv[0], qv[1], qv[2], qv[3]);
   w1 = pack4_sat(qv[4], qv[5], qv[6], qv[7]);
 }
@@ -261,7 +267,7 @@ __device__ __forceinline__ void q8_row(const int32_t (&v)[32], int shS, int shL,
 // load of row r + 1; the accumulator is released after the last load.
 template <int ROWS, bool F32>
 __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32_t (&vb)[32], int shS, int shL,
-                                         uint32_t U, uint32_t& mn0, uint32_t& mn1, uint32_t (&words)[2 * ROWS],
+                                         uint32_t& mn0, uint32_t& mn1, uint32_t (&words)[2 * ROWS],
                                          uint64_t* acc_empty, long long* stamp = nullptr) {
   tmem_ld32(col0, va);
   tmem_wait_ld();
@@ -276,7 +282,7 @@ __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32
     words[2 * r] = ((r & 1) ? vb : va)[0];
     words[2 * r + 1] = ((r & 1) ? vb : va)[31];
 #else
-    q8_row<F32>((r & 1) ? vb : va, shS, shL, U, mn0, mn1, words[2 * r], words[2 * r + 1]);
+    q8_row<F32>((r & 1) ? vb : va, shS, shL, mn0, mn1, words[2 * r], words[2 * r + 1]);
 #endif
     if (r + 1 < ROWS) {
       tmem_wait_ld();
@@ -844,8 +850,8 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       int32_t va[32], vb[32];
       // row r is processed while row r + 1 streams in from TMEM
       if (den_s[pi] > 0) epi_rational(col0, den_s[pi], magic_s[pi], bias_s[pi], words, &acc_empty[grp], rel);
-      else if (shL == 0) epi_rows<8, true>(col0, va, vb, shS, 0, U, mn0, mn1, words, &acc_empty[grp], rel);
-      else epi_rows<8, false>(col0, va, vb, shS, shL, U, mn0, mn1, words, &acc_empty[grp], rel);
+      else if (shL == 0) epi_rows<8, true>(col0, va, vb, shS, 0, mn0, mn1, words, &acc_empty[grp], rel);
+      else epi_rows<8, false>(col0, va, vb, shS, shL, mn0, mn1, words, &acc_empty[grp], rel);
       QSTAMP_EPI(tl, 26);
       // A block with an uncertain pixel is left to the fallback warp, which
       // recomputes and writes the whole block.
