@@ -1296,6 +1296,21 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   //    floor(v / 2^F) only inside that window, where the block is recomputed.
   const int cs = F - 1 >= 24 ? 0 : 1;
   const int cv = 1 << (F - 1 - (cs == 0 ? 24 : 16));
+  // Smoothing operators (every K_int >= 0, rows summing to <= 1) at F = 32
+  // cannot leave [0, 255]: the fixed-point value with all constants stays in
+  // [0, 256 * 2^32), so the epilogue may take the output byte straight from
+  // bits 32-39 without the saturating pack (quant.cu: q8_row<2>).
+  bool nosat = F == 32;
+  for (int i = 0; i < nn && nosat; ++i) {
+    long double sum = 0.0L;
+    for (int j = 0; j < nn; ++j) {
+      if (Ki[size_t(i) * nn + j] < 0) nosat = false;
+      sum += static_cast<long double>(Ki[size_t(i) * nn + j]);
+    }
+    const long double cst = scale / 2.0L + static_cast<long double>(corr[size_t(i)]) + T;
+    if (cst < 0.0L || 255.0L * sum + cst >= 256.0L * scale) nosat = false;
+  }
+  info.nosat = nosat;
   for (int i = 0; i < nn; ++i) {
     long long cst[4] = {0, 0, 0, 0};
     cst[cs] += cv;

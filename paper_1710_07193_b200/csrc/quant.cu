@@ -240,7 +240,11 @@ __device__ __forceinline__ uint32_t pack4_sat(int x0, int x1, int x2, int x3) {
 //   q   = (T1 + (T2 >> 16)) >> (F - 16)      floor(z + 1/2)
 //   key = (T1 2^16 + T2) << (32 - F) mod 2^32 = (v mod 2^F) 2^(32-F)
 // (F32: F = 32, no shift).
-template <bool F32>
+// MODE 0: F < 32 (key shifted by 32 - F); 1: F = 32; 2: F = 32 and the plan's
+// outputs provably in [0, 255] (plan.cc: nosat), so the output byte is bits
+// 16-23 of S and four pixels pack with three byte permutes instead of four
+// shifts and two saturating packs.
+template <int MODE>
 __device__ __forceinline__ void q8_row(const int32_t (&v)[32], int shS, int shL, uint32_t& mn0, uint32_t& mn1,
                                        uint32_t& w0, uint32_t& w1) {
   int qv[8];
@@ -250,8 +254,8 @@ __device__ __forceinline__ void q8_row(const int32_t (&v)[32], int shS, int shL,
     const int t1 = v[4 * c] * 256 + v[4 * c + 1];
     const int t2 = v[4 * c + 2] * 256 + v[4 * c + 3];
     key[c] = static_cast<uint32_t>(t1) * 65536u + static_cast<uint32_t>(t2);
-    if (!F32) key[c] <<= shL;
-    qv[c] = (t1 + (t2 >> 16)) >> shS;
+    if (MODE == 0) key[c] <<= shL;
+    qv[c] = MODE == 2 ? t1 + (t2 >> 16) : (t1 + (t2 >> 16)) >> shS;
   }
   // the accumulators carry the window half-width (plan.cc: layout_kq8), so
   // key = frac + U already: uncertain iff key < 2 U; pairs of pixels per minimum
@@ -259,13 +263,18 @@ __device__ __forceinline__ void q8_row(const int32_t (&v)[32], int shS, int shL,
   mn1 = __vimin3_u32(mn1, key[2], key[3]);
   mn0 = __vimin3_u32(mn0, key[4], key[5]);
   mn1 = __vimin3_u32(mn1, key[6], key[7]);
-  w0 = pack4_sat(qv[0], qv[1], qv[2], qv[3]);
-  w1 = pack4_sat(qv[4], qv[5], qv[6], qv[7]);
+  if (MODE == 2) {
+    w0 = __byte_perm(__byte_perm(qv[0], qv[1], 0x0062), __byte_perm(qv[2], qv[3], 0x0062), 0x5410);
+    w1 = __byte_perm(__byte_perm(qv[4], qv[5], 0x0062), __byte_perm(qv[6], qv[7], 0x0062), 0x5410);
+  } else {
+    w0 = pack4_sat(qv[0], qv[1], qv[2], qv[3]);
+    w1 = pack4_sat(qv[4], qv[5], qv[6], qv[7]);
+  }
 }
 
 // The epilogue's ROWS pixel rows of one tile: row r's math overlaps the TMEM
 // load of row r + 1; the accumulator is released after the last load.
-template <int ROWS, bool F32>
+template <int ROWS, int MODE>
 __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32_t (&vb)[32], int shS, int shL,
                                          uint32_t& mn0, uint32_t& mn1, uint32_t (&words)[2 * ROWS],
                                          uint64_t* acc_empty, long long* stamp = nullptr) {
@@ -282,7 +291,7 @@ __device__ __forceinline__ void epi_rows(uint32_t col0, int32_t (&va)[32], int32
     words[2 * r] = ((r & 1) ? vb : va)[0];
     words[2 * r + 1] = ((r & 1) ? vb : va)[31];
 #else
-    q8_row<F32>((r & 1) ? vb : va, shS, shL, mn0, mn1, words[2 * r], words[2 * r + 1]);
+    q8_row<MODE>((r & 1) ? vb : va, shS, shL, mn0, mn1, words[2 * r], words[2 * r + 1]);
 #endif
     if (r + 1 < ROWS) {
       tmem_wait_ld();
@@ -850,8 +859,9 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       int32_t va[32], vb[32];
       // row r is processed while row r + 1 streams in from TMEM
       if (den_s[pi] > 0) epi_rational(col0, den_s[pi], magic_s[pi], bias_s[pi], words, &acc_empty[grp], rel);
-      else if (shL == 0) epi_rows<8, true>(col0, va, vb, shS, 0, mn0, mn1, words, &acc_empty[grp], rel);
-      else epi_rows<8, false>(col0, va, vb, shS, shL, mn0, mn1, words, &acc_empty[grp], rel);
+      else if (shL < 0) epi_rows<8, 2>(col0, va, vb, shS, 0, mn0, mn1, words, &acc_empty[grp], rel);  // F = 32, no saturation
+      else if (shL == 0) epi_rows<8, 1>(col0, va, vb, shS, 0, mn0, mn1, words, &acc_empty[grp], rel);
+      else epi_rows<8, 0>(col0, va, vb, shS, shL, mn0, mn1, words, &acc_empty[grp], rel);
       QSTAMP_EPI(tl, 26);
       // A block with an uncertain pixel is left to the fallback warp, which
       // recomputes and writes the whole block.
@@ -991,6 +1001,7 @@ dctf_status upload_kq_operator(dctf_plan* p) {
   p->kq_den = info.den;
   p->kq_magic = info.magic;
   p->kq_bias = info.bias;
+  p->kq_nosat = info.nosat;
   if (std::getenv("DCTF_Q_DEBUG") && info.den > 0)
     std::fprintf(stderr, "[k_fused8_q plan] rational operator K = K'/%d (bias %d): deviation %.3e (reference FP64 bound "
                          "%.3e) against a boundary distance of %.3e\n", info.den, info.bias, info.ebound, info.eref,
@@ -1021,7 +1032,7 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
     args.bimg[i] = static_cast<const int8_t*>(p->d_kq);
     args.U[i] = p->kq_U;
     args.shS[i] = p->kq_F - 16;
-    args.shL[i] = 32 - p->kq_F;
+    args.shL[i] = p->kq_nosat ? -1 : 32 - p->kq_F;  // -1: F = 32 and outputs provably in [0, 255]
     args.den[i] = p->kq_den;
     args.bias[i] = p->kq_bias;
     args.magic[i] = p->kq_magic;
