@@ -191,3 +191,50 @@ def test_kq_form_of_config5_masks(P):
         forms.append(P.FilterPlan(m, 8, P.PaddingMode.kReplicate).kq_form)
     assert [f[0] for f in forms] == [1, 0, 9, 0], forms
     assert forms[1][1] == 32 and 17 <= forms[3][1] <= 32
+
+
+def _random_family(seed):
+    """A seeded mask of one of the forms layout_kq8 tells apart: integer,
+    odd-denominator rational, smoothing (non-negative, sum 1), signed real."""
+    rng = np.random.default_rng(seed)
+    k = int(rng.choice([3, 5, 7]))
+    kind = seed % 4
+    if kind == 0:
+        w = rng.integers(-3, 4, k * k).astype(np.float64)
+        w[k * k // 2] += 1.0
+    elif kind == 1:
+        d = int(rng.choice([3, 5, 7, 9, 11, 15, 25, 49]))
+        w = rng.integers(-2, 5, k * k).astype(np.float64) / d
+    elif kind == 2:
+        w = rng.uniform(0.0, 1.0, k * k)
+        w /= w.sum()
+    else:
+        w = rng.uniform(-1.0, 1.0, k * k)
+        s = w.sum()
+        w = w / s if abs(s) > 0.3 else w
+    return w, k
+
+
+@pytest.mark.parametrize("seed", list(range(24)))
+def test_kq_random_masks_match_reference(P, ref, seed):
+    """Seeded masks of every operator form (integer, odd-denominator rational,
+    smoothing F = 32 without saturation, signed four-digit) on a ragged image,
+    both paddings: every pixel the reference's."""
+    from paper_1710_07193_b200 import synth
+    w, k = _random_family(seed)
+    img = synth.uniform_image(100 + seed, 331, 203) if seed & 1 else synth.sinusoid_image(100 + seed, 331, 203)
+    for pad in (0, 1):
+        plan, out = _run(P, img, w, k, k, pad)
+        want = ref.filter_image(img, w, k, pad, 8, threads=nthreads())
+        bad = int(np.count_nonzero(out != want))
+        assert bad == 0, (seed, pad, plan.image_kernel, plan.kq_form, bad)
+        form = plan.kq_form
+        assert plan.image_kernel == "k_fused8_q" and form is not None, (seed, pad, plan.image_kernel)
+        if seed % 4 == 0:
+            assert form[0] == 1, form            # integer operator
+        elif seed % 4 == 1:
+            assert form[0] >= 1 and form[0] % 2 == 1, form  # K' / d, odd d (or integer after reduction)
+        elif seed % 4 == 2:
+            assert form[0] == 0 and form[1] >= 30, form  # smoothing: four digits, F = 32 unless replication piles weight up
+        else:
+            assert form[0] == 0 and 17 <= form[1] <= 32, form
