@@ -57,6 +57,7 @@ struct dctf_plan {
   int kq_den = 0;                // > 0: rational operator K = K' / den (odd den), single-accumulator path
   uint32_t kq_magic = 0;         // ceil(2^32 / den) (den > 1)
   int kq_bias = 0;               // floor-division bias B (the accumulator carries + B den)
+  bool kq_unsigned = false;      // the digit image holds unsigned bytes (MMA B format u8)
   bool kq_nosat = false;         // F = 32 and every output provably in [0, 255]: the epilogue packs bytes without saturation
   int ref_mode = 0, ref_npairs = 0;
   // The reference chain's intermediates can overflow FP64 for this mask
@@ -194,6 +195,7 @@ struct KqInfo {
   uint32_t magic = 0;        // ceil(2^32 / den)
   int bias = 0;              // B: the accumulator constant is (den - 1) / 2 + B den, q = floor(acc / den) - B
   bool nosat = false;        // four-digit form, F = 32, K_int >= 0 and 255 row sums + constants < 256 * 2^32
+  bool unsigned_digits = false;  // K >= 0 with entries past 1/2: plain base-256 digits 0..255, B operand read as u8
 };
 bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info);
 void refchain_image(const dctf_plan& p, std::vector<double>& out, int& mode, int& npairs);

@@ -1243,6 +1243,18 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
   int F = 32;
   if (kmax > 0.0L) F = std::min(32, static_cast<int>(std::floor(std::log2(lim / kmax))));
   while (F > 0 && kmax * std::ldexp(1.0L, F) > lim) --F;  // log2 rounding guard
+  // Non-negative operators (smoothing masks; border replication piles weight up
+  // past 1/2 at the block's corners) keep F = 32 with UNSIGNED base-256 digits
+  // (0..255, the MMA's B operand read as u8) when the balanced digits would
+  // have to give up fraction bits: K_int = round(K 2^32) in [0, 2^32).
+  bool uns = false;
+  if (F < 32 && kmax * std::ldexp(1.0L, 32) <= 4294967295.0L - 1.0L) {
+    uns = true;
+    for (long double v : K)
+      if (std::llroundl(v * std::ldexp(1.0L, 32)) < 0) uns = false;
+    if (uns) F = 32;
+  }
+  info.unsigned_digits = uns;
   if (F < 17) return false;
   const long double scale = std::ldexp(1.0L, F);
   std::vector<long long> Ki(K.size());
@@ -1278,10 +1290,10 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
       long long v = Ki[size_t(i) * nn + j];
       int d[4];
       for (int s = 3; s >= 1; --s) {
-        d[s] = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(v & 255)));
+        d[s] = uns ? static_cast<int>(v & 255) : static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(v & 255)));
         v = (v - d[s]) / 256;
       }
-      if (v < -128 || v > 127) return false;
+      if (uns ? (v < 0 || v > 255) : (v < -128 || v > 127)) return false;
       d[0] = static_cast<int>(v);
       for (int s = 0; s < 4; ++s) put(4 * i + s, j, d[s]);
     }
@@ -1315,15 +1327,19 @@ bool layout_kq8(const dctf_plan& p, std::vector<int8_t>& bimg, KqInfo& info) {
     long long cst[4] = {0, 0, 0, 0};
     cst[cs] += cv;
     long long c = corr[size_t(i)] + static_cast<long long>(T);  // balanced base-256 digits onto 3, 2, 1, (0)
+    if (uns) {  // unsigned B bytes: the whole constant 2^31 + corr + T (> 0) in plain base 256
+      c += static_cast<long long>(cv) << (cs == 0 ? 24 : 16);
+      cst[cs] = 0;
+    }
     for (int sdig = 3; sdig >= 1; --sdig) {
-      const int low = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(c & 255)));
+      const int low = uns ? static_cast<int>(c & 255) : static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(c & 255)));
       cst[sdig] += low;
       c = (c - low) / 256;
     }
     cst[0] += c;
     for (int sdig = 0; sdig < 4; ++sdig) {
       const long long a = cst[sdig] / 2, b = cst[sdig] - a;
-      if (a < -127 || a > 127 || b < -127 || b > 127) return false;
+      if (uns ? (a < 0 || b < 0 || a > 255 || b > 255) : (a < -127 || a > 127 || b < -127 || b > 127)) return false;
       put(4 * i + sdig, 64, static_cast<int>(a));
       put(4 * i + sdig, 65, static_cast<int>(b));
     }

@@ -169,7 +169,7 @@ struct QArgs {
   uint32_t U[KQ_MAX_PLANS];
   int shS[KQ_MAX_PLANS], shL[KQ_MAX_PLANS];  // F - 16, 32 - F
   // rational plans (K = K' / den, odd den; plan.cc: layout_kq8): den > 0, q = mulhi(acc, magic) - bias
-  int den[KQ_MAX_PLANS], bias[KQ_MAX_PLANS];
+  int den[KQ_MAX_PLANS], bias[KQ_MAX_PLANS];  // den = -1: four digits read as unsigned bytes
   uint32_t magic[KQ_MAX_PLANS];
   RefPlan ref[KQ_MAX_PLANS];
   int nplans;
@@ -188,9 +188,10 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   d |= static_cast<uint64_t>(2u) << 61;
   return d;
 }
-// kind::i8 instruction descriptor: D s32, A u8 (pixels), B s8 (digits), both K-major.
-__host__ __device__ constexpr uint32_t idesc_u8s8(int m, int n) {
-  return (2u << 4) | (0u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+// kind::i8 instruction descriptor: D s32, A u8 (pixels), B s8 (digits; u8 for
+// the unsigned digit images of non-negative operators), both K-major.
+__host__ __device__ constexpr uint32_t idesc_u8s8(int m, int n, bool b_unsigned = false) {
+  return (2u << 4) | (0u << 7) | ((b_unsigned ? 0u : 1u) << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
          (static_cast<uint32_t>(m >> 4) << 24);
 }
 __device__ __forceinline__ void mma_u8s8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -703,7 +704,8 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       }
     }
   } else if (warp == W_MMA) {
-    constexpr uint32_t idesc256 = idesc_u8s8(128, 256), idesc64 = idesc_u8s8(128, 64);
+    constexpr uint32_t idesc256 = idesc_u8s8(128, 256), idesc64 = idesc_u8s8(128, 64),
+                       idesc256u = idesc_u8s8(128, 256, true);
     const uint64_t da0 = desc_sw128(smem_u32(asm_)), db0 = desc_sw128(smem_u32(bsm));
     constexpr uint64_t DA_STAGE = ABYTES >> 4, DB_PLAN = BBYTES >> 4;
     const uint32_t acc_full0 = smem_u32(&acc_full[0]), a_empty0 = smem_u32(&a_empty[0]);
@@ -721,7 +723,8 @@ __global__ void __launch_bounds__(q8::THREADS, 1)
       if (lane == 0) QSTAMP(tl, 0);
       tc_fence_after();
       const uint64_t da = da0 + DA_STAGE * s, db = db0 + DB_PLAN * pi;
-      const uint32_t idesc = den_s[pi] > 0 ? idesc64 : idesc256;  // rational plans: one accumulator column per pixel
+      // rational plans: one accumulator column per pixel; den -1: unsigned digit bytes
+      const uint32_t idesc = den_s[pi] > 0 ? idesc64 : den_s[pi] < 0 ? idesc256u : idesc256;
       const uint32_t dt = tmem_base + 256 * buf;
       asm volatile(
           "{\n\t.reg .pred e;\n\t"
@@ -1002,6 +1005,7 @@ dctf_status upload_kq_operator(dctf_plan* p) {
   p->kq_magic = info.magic;
   p->kq_bias = info.bias;
   p->kq_nosat = info.nosat;
+  p->kq_unsigned = info.unsigned_digits;
   if (std::getenv("DCTF_Q_DEBUG") && info.den > 0)
     std::fprintf(stderr, "[k_fused8_q plan] rational operator K = K'/%d (bias %d): deviation %.3e (reference FP64 bound "
                          "%.3e) against a boundary distance of %.3e\n", info.den, info.bias, info.ebound, info.eref,
@@ -1033,7 +1037,7 @@ dctf_status launch_fused8_q(const dctf_plan* const* plans, int nplans, const int
     args.U[i] = p->kq_U;
     args.shS[i] = p->kq_F - 16;
     args.shL[i] = p->kq_nosat ? -1 : 32 - p->kq_F;  // -1: F = 32 and outputs provably in [0, 255]
-    args.den[i] = p->kq_den;
+    args.den[i] = p->kq_den > 0 ? p->kq_den : p->kq_unsigned ? -1 : 0;
     args.bias[i] = p->kq_bias;
     args.magic[i] = p->kq_magic;
     args.ref[i] = RefPlan{p->d_refchain, p->d_weights, p->d_kqt, p->kq_margin, p->ref_mode, p->ref_npairs, p->kr,

@@ -235,6 +235,20 @@ def test_kq_random_masks_match_reference(P, ref, seed):
         elif seed % 4 == 1:
             assert form[0] >= 1 and form[0] % 2 == 1, form  # K' / d, odd d (or integer after reduction)
         elif seed % 4 == 2:
-            assert form[0] == 0 and form[1] >= 30, form  # smoothing: four digits, F = 32 unless replication piles weight up
+            assert form == (0, 32), form         # smoothing: four digits at F = 32 (unsigned digits past 1/2)
         else:
             assert form[0] == 0 and 17 <= form[1] <= 32, form
+
+
+@pytest.mark.parametrize("pad", [0, 1])
+def test_kq_smoothing_masks_keep_32_fraction_bits(P, ref, pad):
+    """Non-negative masks whose replicated corners pile weight past 1/2
+    (the reference's gaussian3 preset: 0.527 at a block corner) keep F = 32
+    through unsigned digit bytes; output equal to the reference's."""
+    from paper_1710_07193_b200 import synth
+    g3 = P.Mask.gaussian3(1.0).weights()
+    img = synth.sinusoid_image(7, 517, 333)
+    plan, out = _run(P, img, np.asarray(g3, np.float64), 3, 3, pad)
+    assert plan.kq_form == (0, 32), plan.kq_form
+    want = ref.filter_image(img, np.asarray(g3, np.float64), 3, pad, 8, threads=nthreads())
+    assert np.array_equal(out, want), int(np.count_nonzero(out != want))
