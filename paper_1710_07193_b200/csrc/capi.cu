@@ -100,6 +100,10 @@ __global__ void __launch_bounds__(256) k_transform(const uint8_t* __restrict__ i
   double cv[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) cv[k] = FWD ? bp.c[r * N + k] : bp.c[k * N + r];
+  bool cv_nz = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) cv_nz = cv_nz && cv[k] != 0.0;
+  const bool cv_nonzero = __all_sync(0xFFFFFFFFu, cv_nz);
   const long long nbatch = (nblocks + BPC - 1) / BPC;
   constexpr bool U8IN = FWD && U8;
   const bool async_in = !U8IN && (reinterpret_cast<uintptr_t>(blocks_in) & 15) == 0;
@@ -170,22 +174,44 @@ __global__ void __launch_bounds__(256) k_transform(const uint8_t* __restrict__ i
     double trow[N], o[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) trow[j] = 0.0;
+    // matmul's a == 0 skip (block_matrix.hpp:71) only matters when the other
+    // factor is not finite (0 * inf) or for the sign of a zero sum; with no
+    // zero multiplier in the warp the skip-free loop gives the same bits and
+    // runs without the per-k branches
+    if (!U8 && cv_nonzero) {  // (the u8 variants measured slower with the second code path)
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const double a = cv[k];
-      if (a != 0.0) {
+      for (int k = 0; k < N; ++k)
 #pragma unroll
-        for (int j = 0; j < N; ++j) trow[j] = __dadd_rn(trow[j], __dmul_rn(a, x[k * N + j]));
+        for (int j = 0; j < N; ++j) trow[j] = __dadd_rn(trow[j], __dmul_rn(cv[k], x[k * N + j]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double a = cv[k];
+        if (a != 0.0) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) trow[j] = __dadd_rn(trow[j], __dmul_rn(a, x[k * N + j]));
+        }
       }
     }
 #pragma unroll
     for (int j = 0; j < N; ++j) o[j] = 0.0;
+    bool t_nonzero = true;
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const double a = trow[k];
-      if (a != 0.0) {
+    for (int k = 0; k < N; ++k) t_nonzero = t_nonzero && trow[k] != 0.0;
+    if (!U8 && __all_sync(0xFFFFFFFFu, t_nonzero)) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, FWD ? bp.c[j * N + k] : bp.c[k * N + j]));
+      for (int k = 0; k < N; ++k)
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+          o[j] = __dadd_rn(o[j], __dmul_rn(trow[k], FWD ? bp.c[j * N + k] : bp.c[k * N + j]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double a = trow[k];
+        if (a != 0.0) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) o[j] = __dadd_rn(o[j], __dmul_rn(a, FWD ? bp.c[j * N + k] : bp.c[k * N + j]));
+        }
       }
     }
     if (blk >= nblocks) continue;
